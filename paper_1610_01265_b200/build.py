@@ -1,0 +1,43 @@
+"""Build libsts_b200.so in-tree with nvcc for sm_100a (no torch types in the ABI)."""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC = [os.path.join(HERE, "csrc", f) for f in ("stencil.cu", "aux.cu", "capi.cu")]
+DEPS = SRC + [os.path.join(HERE, "csrc", "sts_common.cuh"), os.path.join(ROOT, "include", "sts_b200.h")]
+OUT = os.path.join(HERE, "libsts_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def nccl_flags():
+    # NCCL headers/libraries: system copy (same ABI as the torch-bundled one that
+    # is already loaded when the library is opened from Python)
+    inc, libdir = "/usr/include", "/usr/lib/x86_64-linux-gnu"
+    return [f"-I{inc}", f"-L{libdir}", "-lnccl"]
+
+
+def build(force=False, verbose=True):
+    if not force and os.path.exists(OUT):
+        t = os.path.getmtime(OUT)
+        if all(os.path.getmtime(d) <= t for d in DEPS):
+            return OUT
+    cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}",
+           *SRC, "-o", OUT + ".tmp", *nccl_flags()]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    log = os.path.join(HERE, "build_ptxas.log")
+    with open(log, "w") as f:
+        f.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stderr)
+        raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
+    os.replace(OUT + ".tmp", OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv))

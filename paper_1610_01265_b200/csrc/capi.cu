@@ -1,0 +1,904 @@
+// C ABI of libsts_b200 (include/sts_b200.h): grid handle + metrics, halo
+// exchange (virtual slabs / NCCL), and the host drivers of the RKL2 and
+// BE+Jacobi-PCG advances.  Every arithmetic step of the path runs in the
+// kernels of stencil.cu / aux.cu; the host only sequences launches, computes
+// the per-stage RKL2 scalars, and polls PCG convergence flags.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "sts_common.cuh"
+
+namespace sts {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return STS_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return STS_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return STS_ERR_STATE;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    STS_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) STS_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+Geo slab_geo(const sts_grid* g, const Slab& s) {
+  Geo G;
+  G.n1g = g->n1g;
+  G.n2 = g->n2;
+  G.n3 = g->n3;
+  G.periodic3 = g->periodic3;
+  G.i0 = s.i0;
+  G.nl = s.nl;
+  G.plane = g->plane;
+  G.cstride = (long long)g->nl * g->plane;
+  G.m = g->m;
+  return G;
+}
+
+static cudaEvent_t get_event(sts_grid* g) {
+  if (!g->free_events.empty()) {
+    cudaEvent_t e = g->free_events.back();
+    g->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  STS_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// brackets one launch (or exchange) with events when timing is enabled; counts launches
+struct Timed {
+  sts_grid* g;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  bool count;
+  Timed(sts_grid* g_, int kind_, cudaStream_t st_, bool count_ = true) : g(g_), kind(kind_), st(st_), count(count_) {
+    if (g->timing) {
+      a = get_event(g);
+      STS_CUDA(cudaEventRecord(a, st));
+    }
+  }
+  ~Timed() {
+    if (a) {
+      cudaEvent_t b = get_event(g);
+      cudaEventRecord(b, st);
+      g->pending.push_back({kind, a, b});
+    }
+    if (count) g->launches += 1;
+  }
+};
+
+static int stencil_kind(int mode, int epi) { return (mode == STS_MODE_ANISO ? STS_K_ANISO_F : STS_K_ISO_F) + epi; }
+
+static void collect_timing(sts_grid* g) {
+  for (auto& r : g->pending) {
+    STS_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    STS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    g->acc_ms[r.kind] += ms;
+    g->acc_n[r.kind] += 1;
+    g->free_events.push_back(r.a);
+    g->free_events.push_back(r.b);
+  }
+  g->pending.clear();
+}
+
+double* ws_get(sts_grid* g, size_t bytes) {
+  if (bytes <= g->ws.bytes) return g->ws.base;
+  if (g->ws.base) STS_CUDA(cudaFree(g->ws.base));
+  g->ws.base = nullptr;
+  g->ws.bytes = 0;
+  if (cudaMalloc(&g->ws.base, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{STS_ERR_ALLOC, "cudaMalloc of " + std::to_string(bytes) + " bytes of workspace failed"};
+  }
+  g->ws.bytes = bytes;
+  return g->ws.base;
+}
+
+static void ensure_red(sts_grid* g, size_t bytes) {
+  if (bytes <= g->red_bytes) return;
+  if (g->d_red) STS_CUDA(cudaFree(g->d_red));
+  g->d_red = nullptr;
+  g->red_bytes = 0;
+  if (cudaMalloc(&g->d_red, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{STS_ERR_ALLOC, "cudaMalloc of reduction buffer failed"};
+  }
+  g->red_bytes = bytes;
+}
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ----------------------------------------------------------------------------
+// halo buffers and exchange
+// ----------------------------------------------------------------------------
+static void ensure_halos(sts_grid* g) {
+  for (auto& s : g->slabs) {
+    if (!s.halo_lo.empty()) continue;
+    s.halo_lo.assign(H_NSLOTS, nullptr);
+    s.halo_hi.assign(H_NSLOTS, nullptr);
+    const size_t bytes = (size_t)MAXC * g->plane * sizeof(double);
+    for (int h = 0; h < H_NSLOTS; ++h) {
+      if (s.has_lo) {
+        STS_CUDA(cudaMalloc(&s.halo_lo[h], bytes));
+        g->halo_bytes += bytes;
+      }
+      if (s.has_hi) {
+        STS_CUDA(cudaMalloc(&s.halo_hi[h], bytes));
+        g->halo_bytes += bytes;
+      }
+    }
+  }
+}
+
+static bool needs_halos(const sts_grid* g) {
+  for (auto& s : g->slabs)
+    if (s.has_lo || s.has_hi) return true;
+  return false;
+}
+
+// Fill the `slot` halo planes of every slab from `arr` ([ncomp][nl][plane], device).
+//  * slabs of this process (virtual decomposition): device-to-device copies
+//  * neighbouring ranks: ncclSend / ncclRecv of one plane per component
+static void exchange(sts_grid* g, int slot, const double* arr, int ncomp, cudaStream_t st) {
+  if (!needs_halos(g)) return;
+  ensure_halos(g);
+  Timed t(g, STS_K_HALO, st, false);
+  const long long P = g->plane;
+  const long long cs = (long long)g->nl * P;
+  if (g->comm == nullptr) {
+    for (auto& s : g->slabs) {
+      if (s.has_lo)
+        STS_CUDA(cudaMemcpy2DAsync(s.halo_lo[slot], P * sizeof(double), arr + s.off - P, cs * sizeof(double),
+                                   P * sizeof(double), ncomp, cudaMemcpyDeviceToDevice, st));
+      if (s.has_hi)
+        STS_CUDA(cudaMemcpy2DAsync(s.halo_hi[slot], P * sizeof(double), arr + s.off + (long long)s.nl * P,
+                                   cs * sizeof(double), P * sizeof(double), ncomp, cudaMemcpyDeviceToDevice, st));
+    }
+    return;
+  }
+  Slab& s = g->slabs[0];
+  STS_NCCL(ncclGroupStart());
+  for (int c = 0; c < ncomp; ++c) {
+    if (s.has_lo) {
+      STS_NCCL(ncclRecv(s.halo_lo[slot] + c * P, P, ncclDouble, g->rank - 1, g->comm, st));
+      STS_NCCL(ncclSend(arr + c * cs, P, ncclDouble, g->rank - 1, g->comm, st));
+    }
+    if (s.has_hi) {
+      STS_NCCL(ncclRecv(s.halo_hi[slot] + c * P, P, ncclDouble, g->rank + 1, g->comm, st));
+      STS_NCCL(ncclSend(arr + c * cs + (long long)(s.nl - 1) * P, P, ncclDouble, g->rank + 1, g->comm, st));
+    }
+  }
+  STS_NCCL(ncclGroupEnd());
+}
+
+static FieldV view(const sts_grid* g, const Slab& s, int slot, const double* arr) {
+  FieldV f;
+  f.p = arr ? arr + s.off : nullptr;
+  f.lo = (arr && s.has_lo) ? s.halo_lo[slot] : nullptr;
+  f.hi = (arr && s.has_hi) ? s.halo_hi[slot] : nullptr;
+  return f;
+}
+
+// ----------------------------------------------------------------------------
+// argument staging (host pointers -> device scratch)
+// ----------------------------------------------------------------------------
+struct Stage {
+  sts_grid* g;
+  cudaStream_t st;
+  std::vector<std::pair<const double*, size_t>> in;  // host src, count
+  std::vector<double**> in_dst;
+  std::vector<std::pair<double*, size_t>> out;       // host dst, count
+  std::vector<double**> out_dev;
+  size_t total = 0;
+  bool any_host = false;
+
+  void input(const double*& p, size_t count) {
+    if (p && !is_device_ptr(p)) {
+      in.push_back({p, count});
+      in_dst.push_back(const_cast<double**>(&p));
+      total += count;
+      any_host = true;
+    }
+  }
+  // output (may alias an input: then the input's staged copy is used in place)
+  void output(double*& p, size_t count, const double* alias_in = nullptr, const double* alias_host = nullptr) {
+    if (p && !is_device_ptr(p)) {
+      out.push_back({p, count});
+      out_dev.push_back(&p);
+      total += count;
+      any_host = true;
+    }
+    (void)alias_in;
+    (void)alias_host;
+  }
+  // carve staging out of `base` (count doubles), issue H2D copies; rewrite pointers
+  void begin(double* base) {
+    size_t off = 0;
+    for (size_t i = 0; i < in.size(); ++i) {
+      double* d = base + off;
+      STS_CUDA(cudaMemcpyAsync(d, in[i].first, in[i].second * sizeof(double), cudaMemcpyHostToDevice, st));
+      *in_dst[i] = d;
+      off += in[i].second;
+    }
+    for (size_t i = 0; i < out.size(); ++i) {
+      double* d = base + off;
+      *out_dev[i] = d;
+      off += out[i].second;
+    }
+  }
+  void end(const std::vector<double*>& dev_out) {
+    for (size_t i = 0; i < out.size(); ++i)
+      STS_CUDA(cudaMemcpyAsync(out[i].first, dev_out[i], out[i].second * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (!out.empty()) STS_CUDA(cudaStreamSynchronize(st));
+  }
+};
+
+static void check_mode(int mode, int ncomp, const double* b) {
+  STS_REQUIRE(mode == STS_MODE_ISO || mode == STS_MODE_ANISO, "mode must be STS_MODE_ISO or STS_MODE_ANISO");
+  STS_REQUIRE(ncomp >= 1 && ncomp <= MAXC, "ncomp must be 1..3");
+  STS_REQUIRE(mode == STS_MODE_ISO || ncomp == 1, "STS_MODE_ANISO supports ncomp == 1");
+  STS_REQUIRE(mode == STS_MODE_ISO || b != nullptr, "STS_MODE_ANISO requires b");
+}
+
+// coefficient halos for the operator (once per call)
+static void exchange_coeffs(sts_grid* g, int mode, const double* k1, const double* k2, const double* k3,
+                            const double* b, cudaStream_t st) {
+  exchange(g, H_K1, k1, 1, st);
+  if (mode == STS_MODE_ANISO) {
+    exchange(g, H_K2, k2, 1, st);
+    exchange(g, H_K3, k3, 1, st);
+    exchange(g, H_B, b, 3, st);
+  }
+}
+
+static StencilCall make_call(sts_grid* g, const Slab& s, int mode, int ncomp, int epi, const double* u,
+                             const double* k1, const double* k2, const double* k3, const double* b,
+                             const double* w) {
+  StencilCall c{};
+  c.mode = mode;
+  c.ncomp = ncomp;
+  c.epi = epi;
+  c.geo = slab_geo(g, s);
+  c.u = view(g, s, H_U, u);
+  c.k1 = view(g, s, H_K1, k1);
+  c.k2 = view(g, s, H_K2, k2);
+  c.k3 = view(g, s, H_K3, k3);
+  c.b = view(g, s, H_B, b);
+  c.w = w ? w + s.off : nullptr;
+  c.ib = 0;
+  c.ie = s.nl;
+  return c;
+}
+
+static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
+static const double* off(const double* p, const Slab& s) { return p ? p + s.off : nullptr; }
+
+// RKL2 coefficients, PAPER.md:134-138 (gamma~ per DESIGN R6)
+struct Rkl2Coef {
+  std::vector<double> mu, nu, mut, gt;
+};
+static Rkl2Coef rkl2_coefs(int s) {
+  std::vector<double> bj(s + 1);
+  for (int j = 0; j <= s; ++j) bj[j] = (j <= 2) ? 1.0 / 3.0 : (double(j) * j + j - 2.0) / (2.0 * j * (j + 1.0));
+  Rkl2Coef c;
+  c.mu.assign(s + 1, 0.0);
+  c.nu.assign(s + 1, 0.0);
+  c.mut.assign(s + 1, 0.0);
+  c.gt.assign(s + 1, 0.0);
+  const double ss = double(s) * s + s - 2.0;
+  c.mut[1] = 4.0 / (3.0 * ss);
+  for (int j = 2; j <= s; ++j) {
+    c.mu[j] = (2.0 * j - 1.0) / j * bj[j] / bj[j - 1];
+    c.nu[j] = -(j - 1.0) / j * bj[j] / bj[j - 2];
+    c.mut[j] = 4.0 * (2.0 * j - 1.0) / (j * ss) * bj[j] / bj[j - 1];
+    c.gt[j] = (bj[j - 1] - 1.0) * c.mut[j];
+  }
+  return c;
+}
+
+static void build_metrics(sts_grid* g) {
+  const int n1 = g->n1g, n2 = g->n2, n3 = g->n3;
+  const bool sph = g->geom == STS_GEOM_SPHERICAL;
+  const auto& x1f = g->h_x1f;
+  const auto& x1c = g->h_x1c;
+  const auto& x2f = g->h_x2f;
+  const auto& x2c = g->h_x2c;
+  const auto& x3f = g->h_x3f;
+  const auto& x3c = g->h_x3c;
+  std::vector<double> F1r(n1, 0), F2r(n1), F3r(n1), Vr(n1), iH1(n1, 0), iG2(n1);
+  std::vector<double> F1t(n2), F2t(n2, 0), F3t(n2), Vt(n2), iH2(n2, 0), iG3(n2);
+  std::vector<double> F1p(n3), F2p(n3), F3p(n3, 0), Vp(n3), iH3(n3, 0);
+  for (int i = 0; i < n1; ++i) {
+    const double a = x1f[i], b = x1f[i + 1], dx = b - a;
+    if (i + 1 < n1) iH1[i] = 1.0 / (x1c[i + 1] - x1c[i]);
+    if (sph) {
+      if (i + 1 < n1) F1r[i] = b * b * iH1[i];
+      F2r[i] = F3r[i] = 0.5 * (b * b - a * a) / x1c[i];
+      Vr[i] = (b * b * b - a * a * a) / 3.0;
+      iG2[i] = 1.0 / x1c[i];
+    } else {
+      F1r[i] = iH1[i];
+      F2r[i] = F3r[i] = Vr[i] = dx;
+      iG2[i] = 1.0;
+    }
+  }
+  for (int j = 0; j < n2; ++j) {
+    const double a = x2f[j], b = x2f[j + 1], dy = b - a;
+    if (j + 1 < n2) iH2[j] = 1.0 / (x2c[j + 1] - x2c[j]);
+    if (sph) {
+      F1t[j] = Vt[j] = std::cos(a) - std::cos(b);
+      if (j + 1 < n2) F2t[j] = std::sin(b) * iH2[j];
+      F3t[j] = dy / std::sin(x2c[j]);
+      iG3[j] = 1.0 / std::sin(x2c[j]);
+    } else {
+      F1t[j] = F3t[j] = Vt[j] = dy;
+      F2t[j] = iH2[j];
+      iG3[j] = 1.0;
+    }
+  }
+  const double period = x3f[n3] - x3f[0];
+  for (int k = 0; k < n3; ++k) {
+    const double dz = x3f[k + 1] - x3f[k];
+    if (k + 1 < n3) iH3[k] = 1.0 / (x3c[k + 1] - x3c[k]);
+    else if (g->periodic3) iH3[k] = 1.0 / (x3c[0] + period - x3c[k]);
+    F1p[k] = F2p[k] = Vp[k] = dz;
+    F3p[k] = iH3[k];
+  }
+  std::vector<const std::vector<double>*> arrs = {&F1r, &F2r, &F3r, &Vr, &iH1, &iG2, &F1t, &F2t, &F3t,
+                                                   &Vt, &iH2, &iG3, &F1p, &F2p, &F3p, &Vp, &iH3};
+  std::vector<double> host;
+  std::vector<size_t> offs;
+  for (auto* a : arrs) {
+    offs.push_back(host.size());
+    host.insert(host.end(), a->begin(), a->end());
+  }
+  // device copies of x1f, x1c for the f_c(r) profile of the face diffusivity
+  offs.push_back(host.size());
+  host.insert(host.end(), x1f.begin(), x1f.end());
+  offs.push_back(host.size());
+  host.insert(host.end(), x1c.begin(), x1c.end());
+  STS_CUDA(cudaMalloc(&g->d_metrics, host.size() * sizeof(double)));
+  STS_CUDA(cudaMemcpy(g->d_metrics, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
+  const double* d = g->d_metrics;
+  Metrics& m = g->m;
+  m.F1r = d + offs[0]; m.F2r = d + offs[1]; m.F3r = d + offs[2]; m.Vr = d + offs[3]; m.iH1 = d + offs[4];
+  m.iG2 = d + offs[5]; m.F1t = d + offs[6]; m.F2t = d + offs[7]; m.F3t = d + offs[8]; m.Vt = d + offs[9];
+  m.iH2 = d + offs[10]; m.iG3 = d + offs[11]; m.F1p = d + offs[12]; m.F2p = d + offs[13]; m.F3p = d + offs[14];
+  m.Vp = d + offs[15]; m.iH3 = d + offs[16];
+}
+
+static const double* d_x1f(const sts_grid* g) {
+  const size_t n1 = g->n1g, n2 = g->n2, n3 = g->n3;
+  return g->d_metrics + 6 * n1 + 6 * n2 + 5 * n3;
+}
+static const double* d_x1c(const sts_grid* g) { return d_x1f(g) + g->n1g + 1; }
+
+}  // namespace sts
+
+using namespace sts;
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int sts_version(void) { return 100; }
+
+const char* sts_last_error(void) { return g_last_error.c_str(); }
+
+int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const double* x1f, const double* x1c,
+                    const double* x2f, const double* x2c, const double* x3f, const double* x3c, int periodic3,
+                    int i0, int nl, int n_virtual, int device) {
+  return guard([&] {
+    STS_REQUIRE(out != nullptr, "out is NULL");
+    *out = nullptr;
+    STS_REQUIRE(geom == STS_GEOM_CARTESIAN || geom == STS_GEOM_SPHERICAL, "bad geom");
+    STS_REQUIRE(n1 >= 1 && n2 >= 1 && n3 >= 1, "n1, n2, n3 must be >= 1");
+    STS_REQUIRE(x1f && x1c && x2f && x2c && x3f && x3c, "coordinate arrays must be non-NULL");
+    STS_REQUIRE(i0 >= 0 && nl >= 1 && i0 + nl <= n1, "slab [i0, i0+nl) outside [0, n1)");
+    STS_REQUIRE(n_virtual >= 1 && n_virtual <= nl, "n_virtual must be in [1, nl]");
+    STS_REQUIRE(n_virtual == 1 || (i0 == 0 && nl == n1), "virtual slabs need the whole grid");
+    auto mono = [](const double* f, const double* c, int n) {
+      for (int i = 0; i < n; ++i)
+        if (!(f[i] < f[i + 1]) || !(c[i] > f[i] && c[i] < f[i + 1])) return false;
+      return true;
+    };
+    STS_REQUIRE(mono(x1f, x1c, n1) && mono(x2f, x2c, n2) && mono(x3f, x3c, n3),
+                "faces must increase and centres lie strictly inside their cells");
+    if (geom == STS_GEOM_SPHERICAL) {
+      STS_REQUIRE(x1f[0] > 0.0, "spherical r must be > 0");
+      STS_REQUIRE(x2f[0] >= 0.0 && x2f[n2] <= M_PI + 1e-12, "spherical theta must lie in [0, pi]");
+    }
+    DeviceGuard dg(device);
+    auto* g = new sts_grid();
+    g->device = device;
+    g->geom = geom;
+    g->n1g = n1;
+    g->n2 = n2;
+    g->n3 = n3;
+    g->periodic3 = periodic3 ? 1 : 0;
+    g->i0 = i0;
+    g->nl = nl;
+    g->n_virtual = n_virtual;
+    g->plane = (long long)n2 * n3;
+    g->h_x1f.assign(x1f, x1f + n1 + 1);
+    g->h_x1c.assign(x1c, x1c + n1);
+    g->h_x2f.assign(x2f, x2f + n2 + 1);
+    g->h_x2c.assign(x2c, x2c + n2);
+    g->h_x3f.assign(x3f, x3f + n3 + 1);
+    g->h_x3c.assign(x3c, x3c + n3);
+    try {
+      build_metrics(g);
+      // slabs: contiguous, sizes differ by at most one plane
+      for (int s = 0; s < n_virtual; ++s) {
+        Slab sl;
+        const int base = nl / n_virtual, rem = nl % n_virtual;
+        sl.i0 = i0 + s * base + std::min(s, rem);
+        sl.nl = base + (s < rem ? 1 : 0);
+        sl.off = (long long)(sl.i0 - i0) * g->plane;
+        sl.has_lo = sl.i0 > 0;        // a neighbour below exists (virtual slab or rank)
+        sl.has_hi = sl.i0 + sl.nl < n1;
+        g->slabs.push_back(sl);
+      }
+      STS_CUDA(cudaMallocHost(&g->h_pinned, 4096));
+      STS_CUDA(cudaMalloc(&g->d_ticket, 64 * sizeof(unsigned int)));
+    } catch (...) {
+      sts_grid_destroy(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int sts_grid_destroy(sts_grid* g) {
+  if (!g) return STS_OK;
+  return guard([&] {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    for (auto& s : g->slabs) {
+      for (auto* p : s.halo_lo) if (p) cudaFree(p);
+      for (auto* p : s.halo_hi) if (p) cudaFree(p);
+    }
+    if (g->comm) ncclCommDestroy(g->comm);
+    if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+    if (g->ev_a) cudaEventDestroy(g->ev_a);
+    if (g->ev_b) cudaEventDestroy(g->ev_b);
+    for (auto& r : g->pending) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : g->free_events) cudaEventDestroy(e);
+    if (g->d_metrics) cudaFree(g->d_metrics);
+    if (g->ws.base) cudaFree(g->ws.base);
+    if (g->d_red) cudaFree(g->d_red);
+    if (g->d_ticket) cudaFree(g->d_ticket);
+    if (g->h_pinned) cudaFreeHost(g->h_pinned);
+    delete g;
+    if (prev >= 0) cudaSetDevice(prev);
+  });
+}
+
+int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes) {
+  return guard([&] {
+    STS_REQUIRE(g && bytes, "NULL argument");
+    *bytes = g->ws.bytes + g->red_bytes + g->halo_bytes;
+  });
+}
+
+int sts_grid_kernel_launches(const sts_grid* g, long long* count) {
+  return guard([&] {
+    STS_REQUIRE(g && count, "NULL argument");
+    *count = g->launches;
+  });
+}
+
+int sts_grid_set_timing(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->timing = enable != 0;
+  });
+}
+
+int sts_grid_timing_reset(sts_grid* g) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    DeviceGuard dg(g->device);
+    collect_timing(g);
+    for (int k = 0; k < STS_K_NCLASSES; ++k) {
+      g->acc_ms[k] = 0.0;
+      g->acc_n[k] = 0;
+    }
+  });
+}
+
+int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms) {
+  return guard([&] {
+    STS_REQUIRE(g && count && ms, "NULL argument");
+    STS_REQUIRE(kind >= 0 && kind < STS_K_NCLASSES, "bad kernel class");
+    DeviceGuard dg(g->device);
+    collect_timing(g);
+    *count = g->acc_n[kind];
+    *ms = g->acc_ms[kind];
+  });
+}
+
+int sts_nccl_unique_id(void* out, size_t nbytes) {
+  return guard([&] {
+    STS_REQUIRE(out && nbytes >= sizeof(ncclUniqueId), "buffer too small for an ncclUniqueId");
+    ncclUniqueId id;
+    STS_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int sts_comm_init(sts_grid* g, int nranks, int rank, const void* uid, size_t nbytes) {
+  return guard([&] {
+    STS_REQUIRE(g && uid && nbytes >= sizeof(ncclUniqueId), "bad arguments");
+    STS_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    STS_REQUIRE(g->n_virtual == 1, "virtual slabs and NCCL ranks cannot be combined");
+    STS_REQUIRE(g->comm == nullptr, "communicator already initialised");
+    STS_REQUIRE((rank == 0) == (g->i0 == 0) && (rank == nranks - 1) == (g->i0 + g->nl == g->n1g),
+                "rank order must match r-slab order");
+    DeviceGuard dg(g->device);
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    g->nranks = nranks;
+    g->rank = rank;
+    if (nranks > 1) {
+      STS_NCCL(ncclCommInitRank(&g->comm, nranks, id, rank));
+      STS_CUDA(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
+      STS_CUDA(cudaEventCreateWithFlags(&g->ev_a, cudaEventDisableTiming));
+      STS_CUDA(cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming));
+    }
+  });
+}
+
+int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2, double* k3, double kappa0,
+                           double T_cut, double fc_r0, double fc_w, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g && T && k1 && k2 && k3, "NULL argument");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    Stage sg{g, st};
+    sg.input(T, N);
+    sg.output(k1, N);
+    sg.output(k2, N);
+    sg.output(k3, N);
+    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
+    exchange(g, H_AUX, T, 1, st);
+    Slab whole;
+    whole.i0 = g->i0;
+    whole.nl = g->nl;
+    whole.off = 0;
+    Geo G = slab_geo(g, whole);
+    FieldV Tv;
+    Tv.p = T;
+    // with a real neighbour above, the last plane's r-face uses the received halo
+    Tv.hi = (g->comm && g->slabs[0].has_hi) ? g->slabs[0].halo_hi[H_AUX] : nullptr;
+    {
+      Timed t(g, STS_K_FACE_KAPPA, st);
+      launch_face_kappa(G, Tv, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, d_x1f(g), d_x1c(g), st);
+    }
+    sg.end({k1, k2, k3});
+  });
+}
+
+int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out, const double* k1,
+                 const double* k2, const double* k3, const double* b, const double* w, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g && u && out && k1 && k2 && k3, "NULL argument");
+    check_mode(mode, ncomp, b);
+    STS_REQUIRE((const void*)u != (const void*)out, "u and out must not alias");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    Stage sg{g, st};
+    sg.input(u, N * ncomp);
+    sg.input(k1, N);
+    sg.input(k2, N);
+    sg.input(k3, N);
+    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
+    sg.input(w, N);
+    sg.output(out, N * ncomp);
+    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    exchange(g, H_U, u, ncomp, st);
+    for (auto& s : g->slabs) {
+      StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
+      c.ea.out = off(out, s);
+      Timed t(g, stencil_kind(c.mode, c.epi), st);
+      launch_stencil(c, st);
+    }
+    sg.end({out});
+  });
+}
+
+int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, const double* k3, const double* b,
+                 const double* w, double* dt_out, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g && k1 && k2 && k3 && dt_out, "NULL argument");
+    check_mode(mode, 1, b);
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    Stage sg{g, st};
+    sg.input(k1, N);
+    sg.input(k2, N);
+    sg.input(k3, N);
+    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
+    sg.input(w, N);
+    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    ensure_red(g, 4096);
+    auto* dmax = reinterpret_cast<unsigned long long*>(g->d_red);
+    STS_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+    for (auto& s : g->slabs) {
+      StencilCall c = make_call(g, s, mode, 1, 0, nullptr, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
+      Timed t(g, mode == STS_MODE_ANISO ? STS_K_ANISO_GERSH : STS_K_ISO_GERSH, st);
+      launch_gershgorin(c, dmax, st);
+    }
+    if (g->comm) STS_NCCL(ncclAllReduce(g->d_red, g->d_red, 1, ncclDouble, ncclMax, g->comm, st));
+    STS_CUDA(cudaMemcpyAsync(g->h_pinned, g->d_red, sizeof(double), cudaMemcpyDeviceToHost, st));
+    STS_CUDA(cudaStreamSynchronize(st));
+    const double lam = g->h_pinned[0];
+    *dt_out = lam > 0.0 ? 2.0 / lam : std::numeric_limits<double>::infinity();
+  });
+}
+
+int rkl2_num_stages(double dt, double dt_exp, int force_odd) {
+  if (!(std::isfinite(dt) && std::isfinite(dt_exp)) || dt < 0.0 || dt_exp <= 0.0) {
+    set_error("rkl2_num_stages: need finite dt >= 0 and dt_exp > 0");
+    return STS_ERR_ARG;
+  }
+  const double ratio = dt / dt_exp;
+  const double x = std::ceil((std::sqrt(9.0 + 16.0 * ratio) - 1.0) / 2.0);
+  if (x > 1e8) {
+    set_error("rkl2_num_stages: stage count overflow");
+    return STS_ERR_ARG;
+  }
+  int s = std::max(2, (int)x);
+  if (force_odd && (s % 2 == 0)) s += 1;
+  return s;
+}
+
+int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1, const double* k1,
+                 const double* k2, const double* k3, const double* b, const double* w, double dt, int s,
+                 void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g && u0 && u1 && k1 && k2 && k3, "NULL argument");
+    check_mode(mode, ncomp, b);
+    STS_REQUIRE(s >= 2, "s must be >= 2");
+    STS_REQUIRE(std::isfinite(dt) && dt >= 0.0, "dt must be finite and >= 0");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    const size_t NF = N * ncomp;
+    Stage sg{g, st};
+    sg.input(u0, NF);
+    sg.input(k1, N);
+    sg.input(k2, N);
+    sg.input(k3, N);
+    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
+    sg.input(w, N);
+    // host arrays (even an in-place u0 == u1) are staged separately: the result
+    // goes to its own device buffer and back; a device in-place advance is safe
+    // because Y0 is only read pointwise after stage 1
+    sg.output(u1, NF);
+    double* base = ws_get(g, (sg.total + 3 * NF) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 3 * NF);
+    double* M0 = base;
+    double* A = base + NF;
+    double* B = base + 2 * NF;
+    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
+    const Rkl2Coef co = rkl2_coefs(s);
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
+    exchange(g, H_U, u0, ncomp, st);
+    for (auto& sl : g->slabs) {
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
+      c.ea.out = off(A, sl);
+      c.ea.out2 = off(M0, sl);
+      c.ea.c0 = co.mut[1] * dt;
+      Timed t(g, stencil_kind(c.mode, c.epi), st);
+      launch_stencil(c, st);
+    }
+    // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
+    const double* prev = u0;
+    double* cur = A;
+    for (int j = 2; j <= s; ++j) {
+      double* dst;
+      if (j == s) dst = u1;
+      else if (prev == u0) dst = B;                       // never overwrite Y0
+      else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
+      exchange(g, H_U, cur, ncomp, st);
+      for (auto& sl : g->slabs) {
+        StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
+        c.ea.out = off(dst, sl);
+        c.ea.ym2 = off(prev, sl);
+        c.ea.y0 = off(u0, sl);
+        c.ea.m0 = off(M0, sl);
+        c.ea.mu = co.mu[j];
+        c.ea.nu = co.nu[j];
+        c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
+        c.ea.c0 = co.mut[j] * dt;
+        c.ea.c1 = co.gt[j] * dt;
+        Timed t(g, stencil_kind(c.mode, c.epi), st);
+        launch_stencil(c, st);
+      }
+      prev = cur;
+      cur = dst;
+    }
+    sg.end({u1});
+  });
+}
+
+int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const double* k1,
+                 const double* k2, const double* k3, const double* b, const double* w, double dt, double rtol,
+                 int kmax, int* iters_out, void* stream) {
+  int status = STS_OK;
+  int rc = guard([&] {
+    STS_REQUIRE(g && un && un1 && k1 && k2 && k3, "NULL argument");
+    check_mode(mode, ncomp, b);
+    STS_REQUIRE(kmax >= 1, "kmax must be >= 1");
+    STS_REQUIRE(std::isfinite(dt) && dt >= 0.0 && std::isfinite(rtol) && rtol >= 0.0, "bad dt / rtol");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    const size_t NF = N * ncomp;
+    const bool alias = (const void*)un == (const void*)un1;
+    // same DEVICE array for un and un1: x0 is already in place; otherwise write it
+    const bool write_x0 = !(alias && is_device_ptr(un1));
+    Stage sg{g, st};
+    sg.input(un, NF);
+    sg.input(k1, N);
+    sg.input(k2, N);
+    sg.input(k3, N);
+    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
+    sg.input(w, N);
+    sg.output(un1, NF);
+    double* base = ws_get(g, (sg.total + 3 * NF + N) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 3 * NF + N);
+    double* r = base;
+    double* p = base + NF;
+    double* y = base + 2 * NF;
+    double* d = base + 3 * NF;
+    double* x = un1;
+    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
+    // reduction storage
+    int sb_total = 0;
+    for (auto& sl : g->slabs) sb_total += stencil_blocks(slab_geo(g, sl), 0, sl.nl, nullptr);
+    const long long pstride = std::max(sb_total, PW_BLOCKS);
+    const size_t red_doubles = (size_t)2 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
+    ensure_red(g, red_doubles * sizeof(double));
+    double* partials = g->d_red;
+    double* sums = partials + 2 * ncomp * pstride;
+    PcgScal* sc = reinterpret_cast<PcgScal*>(sums + 16);
+    const double rtol2 = rtol * rtol;
+    const long long cs = (long long)g->nl * g->plane;
+
+    auto reduce = [&](int nblocks, int nq, int phase) {
+      Timed t(g, STS_K_PCG_REDUCE, st);
+      if (g->comm) {
+        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, PH_NONE, sc, rtol2, st);
+        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * nq, ncclDouble, ncclSum, g->comm, st));
+        launch_pcg_scalar(sums, ncomp, nq, phase, sc, rtol2, st);
+        g->launches += 1;
+      } else {
+        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2, st);
+      }
+    };
+
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; p = z0 = r0 d
+    exchange(g, H_U, un, ncomp, st);
+    {
+      int pb = 0;
+      for (auto& sl : g->slabs) {
+        StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
+        c.ea.out = off(r, sl);
+        c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
+        c.ea.out3 = off(p, sl);
+        c.ea.out4 = off(d, sl);
+        c.ea.dt = dt;
+        c.ea.partials = partials;
+        c.ea.pstride = pstride;
+        c.ea.pbase = pb;
+        pb += stencil_blocks(c.geo, 0, sl.nl, nullptr);
+        Timed t(g, stencil_kind(c.mode, c.epi), st);
+        launch_stencil(c, st);
+      }
+      reduce(sb_total, 2, PH_R0);
+    }
+    auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
+    int launched = 0;
+    int batch = 4;
+    bool all_done = false;
+    while (true) {
+      STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, st));
+      STS_CUDA(cudaStreamSynchronize(st));
+      all_done = true;
+      for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
+      if (all_done || launched >= kmax) break;
+      const int nb = std::min(batch, kmax - launched);
+      for (int it = 0; it < nb; ++it) {
+        // y = A p, alpha = r.z / p.y
+        exchange(g, H_U, p, ncomp, st);
+        int pb = 0;
+        for (auto& sl : g->slabs) {
+          StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, p, k1, k2, k3, bb, w);
+          c.ea.out = off(y, sl);
+          c.ea.dt = dt;
+          c.ea.partials = partials;
+          c.ea.pstride = pstride;
+          c.ea.pbase = pb;
+          c.ea.sc = sc;
+          pb += stencil_blocks(c.geo, 0, sl.nl, nullptr);
+          Timed t(g, stencil_kind(c.mode, c.epi), st);
+          launch_stencil(c, st);
+        }
+        reduce(sb_total, 1, PH_AP);
+        // x += alpha p, r -= alpha y, z = r d, r.z -> beta
+        {
+          Timed t(g, STS_K_PCG_UPDATE, st);
+          launch_pcg_update(ncomp, (long long)N, cs, x, r, p, y, d, sc, partials, pstride, st);
+        }
+        reduce(PW_BLOCKS, 1, PH_RZ);
+        // p = z + beta p
+        {
+          Timed t(g, STS_K_PCG_PUPDATE, st);
+          launch_pcg_pupdate(ncomp, (long long)N, cs, p, r, d, sc, st);
+        }
+      }
+      launched += nb;
+      batch = std::min(batch * 2, 64);
+    }
+    if (iters_out)
+      for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;
+    sg.end({un1});
+    if (!all_done) {
+      status = STS_ERR_NOT_CONVERGED;
+      set_error("be_pcg_solve: kmax reached before convergence");
+    }
+  });
+  return rc != STS_OK ? rc : status;
+}
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+// Internal declarations of libsts_b200 (not part of the C ABI).
+// Product code: shares nothing with oracle/ (DESIGN.md "Boundary").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sts_b200.h"
+
+namespace sts {
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+void set_error(const std::string& msg);
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define STS_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::sts::Error{STS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                           " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+  } while (0)
+
+#define STS_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      throw ::sts::Error{STS_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+#define STS_REQUIRE(cond, msg)                                  \
+  do {                                                          \
+    if (!(cond)) throw ::sts::Error{STS_ERR_ARG, (msg)};        \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// tiling constants: a CTA owns a TJ x TK (theta x phi) tile of cell columns and
+// marches along r over a chunk of planes (2.5-D blocking, phi contiguous).
+// ----------------------------------------------------------------------------
+constexpr int TK = 32;            // phi cells per tile  (one warp row, 256 B of FP64)
+constexpr int TJ = 8;             // theta cells per tile
+constexpr int NT = TK * TJ;       // threads per CTA
+constexpr int RJ = TJ + 2;        // cell region rows incl. halo
+constexpr int RK = TK + 2;        // cell region cols incl. halo
+constexpr int RC = RJ * RK;       // cells in the region
+constexpr int VJ = TJ + 1;        // vertex rows
+constexpr int VK = TK + 1;        // vertex cols
+constexpr int VC = VJ * VK;
+constexpr int MAXC = 3;           // max components (velocity)
+
+// Device metric arrays, all indexed by GLOBAL cell index (R1, §5).
+//   face coefficient A/h = F{d}r[i] * F{d}t[j] * F{d}p[k]   (ISO operator)
+//   volume V            = Vr[i] * Vt[j] * Vp[k]
+//   centre distances     h_r = H1[i], h_th = G2[i'] H2[j], h_ph = G2[i'] G3[j'] H3[k]
+//   (the "inv" arrays hold reciprocals used by the vertex scheme)
+struct Metrics {
+  const double *F1r, *F2r, *F3r, *Vr, *iH1, *iG2;   // n1
+  const double *F1t, *F2t, *F3t, *Vt, *iH2, *iG3;   // n2
+  const double *F1p, *F2p, *F3p, *Vp, *iH3;         // n3
+};
+
+// A field as seen by one slab: local planes plus optional halo planes.
+struct FieldV {
+  const double* p = nullptr;   // [ncomp][nl][plane]
+  const double* lo = nullptr;  // [ncomp][plane] : plane il = -1 (nullptr at r_min)
+  const double* hi = nullptr;  // [ncomp][plane] : plane il = nl (nullptr at r_max)
+};
+
+struct Geo {
+  int n1g, n2, n3, periodic3;
+  int i0, nl;                  // slab: global planes [i0, i0+nl)
+  long long plane;             // n2*n3
+  long long cstride;           // nl*plane (component stride of local arrays)
+  Metrics m;
+};
+
+// ----------------------------------------------------------------------------
+// the grid handle
+// ----------------------------------------------------------------------------
+struct Slab {
+  int i0, nl;                  // global planes of this slab
+  long long off;               // element offset of the slab in the (virtual) whole array
+  // halo buffers owned by the library: [field slot][side][MAXC*plane]
+  std::vector<double*> halo_lo, halo_hi;
+  bool has_lo, has_hi;
+};
+
+enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_NSLOTS };
+
+struct Workspace {
+  double* base = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace sts
+
+struct sts_grid {
+  int device = 0;
+  int geom = 0;
+  int n1g = 0, n2 = 0, n3 = 0, periodic3 = 0;
+  int i0 = 0, nl = 0;
+  int n_virtual = 1;
+  long long plane = 0;
+  std::vector<double> h_x1f, h_x1c, h_x2f, h_x2c, h_x3f, h_x3c;
+  double* d_metrics = nullptr;          // one allocation for all metric arrays
+  sts::Metrics m{};
+  std::vector<sts::Slab> slabs;         // 1 (real) or n_virtual (emulation)
+  // workspace (scratch fields, staging) — grows on demand
+  sts::Workspace ws;
+  double* d_red = nullptr;              // reduction partials + scalars
+  size_t red_bytes = 0;
+  unsigned int* d_ticket = nullptr;     // last-block tickets
+  double* h_pinned = nullptr;           // small pinned host mailbox
+  // multi-GPU
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  long long launches = 0;
+  size_t halo_bytes = 0;
+  // per-kernel-class event timing (sts_grid_set_timing)
+  bool timing = false;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> free_events;
+  double acc_ms[STS_K_NCLASSES] = {};
+  long long acc_n[STS_K_NCLASSES] = {};
+};
+
+namespace sts {
+
+Geo slab_geo(const sts_grid* g, const Slab& s);
+double* ws_get(sts_grid* g, size_t bytes);  // scratch of at least `bytes`, reused across calls
+
+// ----------------------------------------------------------------------------
+// kernel launchers (stencil.cu)
+// ----------------------------------------------------------------------------
+// Epilogues of the fused stencil pass (one pass = operator + pointwise update)
+enum Epi : int {
+  EPI_F = 0,        // out = F(u)
+  EPI_RKL2_FIRST,   // M0 = F(u0); y1 = u0 + c0*M0          (c0 = mu~_1 dt)
+  EPI_RKL2_STAGE,   // yj = mu*u + nu*ym2 + (1-mu-nu)*y0 + c0*F(u) + c1*M0
+  EPI_PCG_R0,       // r = dt*L u; d = 1/(wV - dt L_ii); x = u; z = r d; p = z; partials r.z, b.b d
+  EPI_PCG_AP,       // y = wV p - dt L p; partial p.y
+};
+
+// PCG per-component scalars (device)
+struct PcgScal {
+  double rz, rz_old, pAp, alpha, beta, thresh;
+  int done, iters;
+};
+
+struct EpiArgs {
+  double* out = nullptr;       // primary output   [ncomp][nl][plane]
+  double* out2 = nullptr;      // secondary output (M0 / x / ...)
+  double* out3 = nullptr;      // (p)
+  double* out4 = nullptr;      // (dinv)
+  const double* ym2 = nullptr; // Y_{j-2}
+  const double* y0 = nullptr;  // Y_0
+  const double* m0 = nullptr;  // M0 = F(Y_0)
+  double mu = 0, nu = 0, c0 = 0, c1 = 0, c2 = 0, dt = 0;
+  double* partials = nullptr;  // [value q][pstride]: per-CTA partial sums
+  long long pstride = 0;       // stride between partial-value rows
+  long long pbase = 0;         // this launch's first CTA slot
+  const PcgScal* sc = nullptr; // per-component PCG scalars (skip components with done set)
+};
+
+struct StencilCall {
+  int mode;                    // STS_MODE_ISO / STS_MODE_ANISO
+  int ncomp;
+  int epi;
+  Geo geo;
+  FieldV u, k1, k2, k3, b;
+  const double* w;             // [nl][plane] or nullptr
+  EpiArgs ea;
+  int ib, ie;                  // local plane range [ib, ie)
+};
+
+// number of CTAs launch_stencil will use for a plane range (for partial buffers)
+int stencil_blocks(const Geo& geo, int ib, int ie, int* ic_out);
+void launch_stencil(const StencilCall& c, cudaStream_t st);
+
+void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStream_t st);
+
+// pointwise / auxiliary kernels (aux.cu)
+void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double* k3, double kappa0,
+                       double T_cut, double fc_r0, double fc_w, const double* x1f_d, const double* x1c_d,
+                       cudaStream_t st);
+
+enum PcgPhase { PH_NONE = 0, PH_R0 = 1, PH_AP = 2, PH_RZ = 3 };
+constexpr int PW_BLOCKS = 148 * 8;   // grid of the pointwise PCG kernels
+// sums[c*nq + q] = sum_b partials[(c*nq+q)*pstride + b], then the phase's scalar update
+void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, int ncomp, int nq,
+                       double* sums, int phase, PcgScal* sc, double rtol2, cudaStream_t st);
+void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal* sc, double rtol2,
+                       cudaStream_t st);
+// x += a p; r -= a y; z = r d; partial r.z      (all local cells, per component)
+void launch_pcg_update(int ncomp, long long n, long long cstride, double* x, double* r, const double* p,
+                       const double* y, const double* d, const PcgScal* sc, double* partials,
+                       long long pstride, cudaStream_t st);
+// p = r d + beta p
+void launch_pcg_pupdate(int ncomp, long long n, long long cstride, double* p, const double* r,
+                        const double* d, const PcgScal* sc, cudaStream_t st);
+
+}  // namespace sts

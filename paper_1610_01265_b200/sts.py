@@ -1,0 +1,218 @@
+"""Thin ctypes binding of libsts_b200.so (include/sts_b200.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  Arrays are torch tensors (float64, C-contiguous) on the grid's CUDA
+device — or on the host (pinned or pageable), in which case the library stages
+them (the end-to-end path timed by bench.py).  There is no CPU fallback: if the
+shared library is missing or no CUDA device is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch  # noqa: F401  (loads CUDA runtime + NCCL before the library)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsts_b200.so")
+
+STS_OK = 0
+STS_ERR_NOT_CONVERGED = -4
+GEOM = {"cartesian": 0, "spherical": 1}
+MODE = {"iso": 0, "aniso": 1}
+UID_BYTES = 128
+
+_lib = None
+
+
+class StsError(RuntimeError):
+    def __init__(self, fn, code, msg):
+        super().__init__(f"{fn} failed ({code}): {msg}")
+        self.code = code
+
+
+def lib():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P = ctypes.c_void_p
+    D = ctypes.c_double
+    I = ctypes.c_int
+    sig = {
+        "sts_version": (I, []),
+        "sts_last_error": (ctypes.c_char_p, []),
+        "sts_grid_create": (I, [ctypes.POINTER(P), I, I, I, I, P, P, P, P, P, P, I, I, I, I, I]),
+        "sts_grid_destroy": (I, [P]),
+        "sts_grid_workspace_bytes": (I, [P, ctypes.POINTER(ctypes.c_size_t)]),
+        "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
+        "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
+        "sts_comm_init": (I, [P, I, I, P, ctypes.c_size_t]),
+        "sts_face_kappa_spitzer": (I, [P, P, P, P, P, D, D, D, D, P]),
+        "sts_op_apply": (I, [P, I, I, P, P, P, P, P, P, P, P]),
+        "sts_dt_euler": (I, [P, I, P, P, P, P, P, ctypes.POINTER(D), P]),
+        "rkl2_num_stages": (I, [D, D, I]),
+        "rkl2_advance": (I, [P, I, I, P, P, P, P, P, P, P, D, I, P]),
+        "be_pcg_solve": (I, [P, I, I, P, P, P, P, P, P, P, D, D, I, ctypes.POINTER(I), P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(fn, code, allow=()):
+    if code != STS_OK and code not in allow:
+        raise StsError(fn, code, lib().sts_last_error().decode())
+    return code
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError("arrays must be contiguous float64 tensors")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _stream(stream):
+    if stream is None:
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return None
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def version():
+    return lib().sts_version()
+
+
+def rkl2_num_stages(dt, dt_exp, force_odd=False):
+    """PAPER.md:142 Eq. (5) (DESIGN R5) — computed by the library."""
+    s = lib().rkl2_num_stages(float(dt), float(dt_exp), int(bool(force_odd)))
+    _check("rkl2_num_stages", STS_OK if s >= 2 else s)
+    return s
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UID_BYTES)
+    _check("sts_nccl_unique_id", lib().sts_nccl_unique_id(buf, UID_BYTES))
+    return buf.raw
+
+
+class Grid:
+    """Handle to a (slab of a) logically rectangular grid living on one GPU."""
+
+    def __init__(self, geom, x1f, x1c, x2f, x2c, x3f, x3c, periodic3, i0=0, nl=None, n_virtual=1, device=0):
+        import numpy as np
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (x1f, x1c, x2f, x2c, x3f, x3c)]
+        self._keep = arrs
+        n1, n2, n3 = len(arrs[1]), len(arrs[3]), len(arrs[5])
+        nl = n1 - i0 if nl is None else nl
+        h = ctypes.c_void_p()
+        _check("sts_grid_create", lib().sts_grid_create(
+            ctypes.byref(h), GEOM[geom], n1, n2, n3, *[_np_ptr(a) for a in arrs],
+            int(bool(periodic3)), int(i0), int(nl), int(n_virtual), int(device)))
+        self._h = h
+        self.shape_global = (n1, n2, n3)
+        self.i0, self.nl = i0, nl
+        self.shape = (nl, n2, n3)
+        self.device = torch.device("cuda", device)
+
+    @classmethod
+    def from_grid(cls, g, i0=0, nl=None, n_virtual=1, device=0):
+        """Duck-typed: any object with geom, x1f..x3c, periodic3 attributes."""
+        return cls(g.geom, g.x1f, g.x1c, g.x2f, g.x2c, g.x3f, g.x3c, g.periodic3,
+                   i0=i0, nl=nl, n_virtual=n_virtual, device=device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sts_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ info
+    @property
+    def kernel_launches(self):
+        v = ctypes.c_longlong()
+        _check("sts_grid_kernel_launches", lib().sts_grid_kernel_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    @property
+    def workspace_bytes(self):
+        v = ctypes.c_size_t()
+        _check("sts_grid_workspace_bytes", lib().sts_grid_workspace_bytes(self._h, ctypes.byref(v)))
+        return v.value
+
+    def comm_init(self, nranks, rank, uid: bytes):
+        buf = ctypes.create_string_buffer(uid, UID_BYTES)
+        _check("sts_comm_init", lib().sts_comm_init(self._h, int(nranks), int(rank), buf, UID_BYTES))
+
+    # ------------------------------------------------------------------ ops
+    def _alloc(self, ncomp, like):
+        shape = self.shape if ncomp == 1 else (ncomp,) + self.shape
+        dev = like.device if like is not None else self.device
+        if dev.type == "cpu":
+            return torch.empty(shape, dtype=torch.float64, pin_memory=torch.cuda.is_available())
+        return torch.empty(shape, dtype=torch.float64, device=dev)
+
+    def face_kappa_spitzer(self, T, kappa0, T_cut, fc_r0=10.0, fc_w=0.0, out=None, stream=None):
+        out = out or tuple(self._alloc(1, T) for _ in range(3))
+        _check("sts_face_kappa_spitzer", lib().sts_face_kappa_spitzer(
+            self._h, _ptr(T), *[_ptr(o) for o in out], float(kappa0), float(T_cut), float(fc_r0),
+            float(fc_w), _stream(stream)))
+        return out
+
+    def op_apply(self, mode, u, k, b=None, w=None, out=None, stream=None):
+        ncomp = 1 if u.dim() == 3 else u.shape[0]
+        out = self._alloc(ncomp, u) if out is None else out
+        _check("sts_op_apply", lib().sts_op_apply(
+            self._h, MODE[mode], ncomp, _ptr(u), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            _stream(stream)))
+        return out
+
+    def dt_euler(self, mode, k, b=None, w=None, stream=None):
+        dt = ctypes.c_double()
+        _check("sts_dt_euler", lib().sts_dt_euler(
+            self._h, MODE[mode], *[_ptr(x) for x in k], _ptr(b), _ptr(w), ctypes.byref(dt), _stream(stream)))
+        return dt.value
+
+    def rkl2_advance(self, mode, u0, k, b=None, w=None, dt=0.0, s=2, out=None, stream=None):
+        ncomp = 1 if u0.dim() == 3 else u0.shape[0]
+        out = self._alloc(ncomp, u0) if out is None else out
+        _check("rkl2_advance", lib().rkl2_advance(
+            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            float(dt), int(s), _stream(stream)))
+        return out
+
+    def be_pcg_solve(self, mode, un, k, b=None, w=None, dt=0.0, rtol=1e-12, kmax=100000, out=None,
+                     stream=None, allow_not_converged=False):
+        ncomp = 1 if un.dim() == 3 else un.shape[0]
+        out = self._alloc(ncomp, un) if out is None else out
+        iters = (ctypes.c_int * ncomp)()
+        _check("be_pcg_solve", lib().be_pcg_solve(
+            self._h, MODE[mode], ncomp, _ptr(un), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            float(dt), float(rtol), int(kmax), iters, _stream(stream)),
+            allow=(STS_ERR_NOT_CONVERGED,) if allow_not_converged else ())
+        return out, list(iters)
+
+
+def inf():
+    return math.inf

@@ -1,0 +1,319 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on identical seeded inputs.
+
+Tolerances (BASELINE north_star, DESIGN.md §3 "Parity bar"):
+  * operator / face diffusivity / Gershgorin: FP64 rounding of a different
+    summation order -> relative L2 <= 1e-12, max-norm <= 1e-11 * max|ref|
+  * RKL2: relative L2 <= 1e-11 after one super-step, <= 1e-9 after 20
+  * BE+PCG (rtol 1e-12): relative L2 <= 1e-11 (one step), iteration counts
+    identical within +-1
+Sizes span several 32 x 8 (phi x theta) tiles and r-chunks with ragged tails,
+plus the degenerate shapes (single plane / row / column, periodic n3 = 1, 2).
+"""
+import math
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import core as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import __graft_entry__ as e
+    e.build()
+    return torch.device("cuda", 0)
+
+
+def sts():
+    from paper_1610_01265_b200 import sts as S
+    return S
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def max_rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def cpu(t):
+    return t.detach().cpu().numpy()
+
+
+def sph(shape, r1=20.0, dr0=0.005, periodic=True):
+    n1, n2, n3 = shape
+    g = W.spherical_grid(n1, n2, n3, r1=r1, dr0=dr0)
+    if not periodic:
+        g = W.Grid("spherical", g.x1f, np.linspace(0.3, 2.8, n2 + 1), np.linspace(0.0, 1.5, n3 + 1), False)
+    return g
+
+
+SHAPES = [(1, 1, 1), (1, 5, 7), (3, 1, 40), (5, 9, 1), (4, 3, 2), (20, 19, 70), (17, 9, 33)]
+
+
+def _inputs(g, rng, bkind):
+    shape = g.shape
+    u = torch.as_tensor(rng.normal(size=shape) + 3.0)
+    k = [torch.as_tensor(rng.uniform(0.5, 2.0, shape)) for _ in range(3)]
+    if bkind == "random":
+        b = W.random_unit_b(g, seed=int(rng.integers(1 << 30)))
+    else:
+        b = W.tilted_dipole_b(g, 30.0)
+    return u, k, b
+
+
+# ---------------------------------------------------------------- A3
+@pytest.mark.parametrize("recipe", ["corona", "tr", "tr_fc"])
+def test_face_kappa_parity(dev, recipe):
+    g = sph((20, 19, 70))
+    T = W.corona_T(g, seed=3) if recipe == "corona" else W.tr_corona_T(g, seed=3)
+    fc_w = 0.5 if recipe == "tr_fc" else 0.0
+    G = sts().Grid.from_grid(g)
+    k = G.face_kappa_spitzer(T.to(dev), 1e-9, 5e5, 10.0, fc_w)
+    ref = O.spitzer_face_kappa(g, T.numpy(), 1e-9, 5e5, 10.0, fc_w)
+    for d in range(3):
+        assert max_rel(cpu(k[d]), ref[d]) <= 1e-13, d
+
+
+# ---------------------------------------------------------------- A1 / A2
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("kind", ["aniso_random", "aniso_dipole", "iso", "iso3_weighted", "cart_iso"])
+def test_op_apply_parity(dev, shape, kind):
+    rng = np.random.default_rng(zlib.crc32(repr((shape, kind)).encode()))
+    if kind == "cart_iso":
+        n1, n2, n3 = shape
+        g = W.Grid("cartesian", np.cumsum(np.r_[0, rng.uniform(0.5, 1.5, n1)]),
+                   np.cumsum(np.r_[0, rng.uniform(0.5, 1.5, n2)]), np.arange(n3 + 1) * 0.7, False)
+    else:
+        g = sph(shape, periodic=(shape[2] != 33))
+    u, k, b = _inputs(g, rng, "random" if kind == "aniso_random" else "dipole")
+    w = None
+    mode = "aniso" if kind.startswith("aniso") else "iso"
+    if kind == "iso3_weighted":
+        u = torch.as_tensor(rng.normal(size=(3,) + g.shape))
+        w = torch.as_tensor(rng.uniform(0.2, 5.0, g.shape))
+    G = sts().Grid.from_grid(g)
+    F = G.op_apply(mode, u.to(dev), [x.to(dev) for x in k], b.to(dev) if mode == "aniso" else None,
+                   None if w is None else w.to(dev))
+    op = O.Operator(g, [x.numpy() for x in k], b.numpy() if mode == "aniso" else None,
+                    None if w is None else w.numpy())
+    ref = op.apply(u.numpy())
+    if np.max(np.abs(ref)) == 0.0:
+        assert np.max(np.abs(cpu(F))) == 0.0
+        return
+    assert rel_l2(cpu(F), ref) <= 1e-12
+    assert max_rel(cpu(F), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 1, 40), (5, 9, 1), (4, 3, 2), (20, 19, 70), (17, 9, 33)])
+@pytest.mark.parametrize("mode", ["aniso", "iso"])
+def test_dt_euler_parity(dev, shape, mode):
+    rng = np.random.default_rng(7)
+    g = sph(shape, periodic=(shape[2] != 33))
+    u, k, b = _inputs(g, rng, "random")
+    w = torch.as_tensor(rng.uniform(0.2, 5.0, g.shape)) if mode == "iso" else None
+    G = sts().Grid.from_grid(g)
+    dt = G.dt_euler(mode, [x.to(dev) for x in k], b.to(dev) if mode == "aniso" else None,
+                    None if w is None else w.to(dev))
+    op = O.Operator(g, [x.numpy() for x in k], b.numpy() if mode == "aniso" else None,
+                    None if w is None else w.numpy())
+    ref = O.dt_euler(op)
+    if math.isinf(ref):
+        assert math.isinf(dt)
+    else:
+        assert abs(dt - ref) <= 1e-13 * ref
+
+
+# ---------------------------------------------------------------- A6
+def _oracle_rkl2_run(g, T0, cfg, ratio, nsteps, b):
+    """Lagged-diffusivity loop: refresh kappa, dt_exp, s every step."""
+    T = T0.copy()
+    dt = None
+    ss = []
+    for _ in range(nsteps):
+        kap = O.spitzer_face_kappa(g, T, cfg["kappa0"], cfg["T_cut"])
+        op = O.Operator(g, kap, b)
+        dte = O.dt_euler(op)
+        dt = ratio * dte if dt is None else dt
+        s = O.rkl2_num_stages(dt, dte)
+        ss.append(s)
+        T = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), T, dt, s)
+    return T, ss
+
+
+def _gpu_rkl2_run(G, T0, cfg, ratio, nsteps, b, inplace=False):
+    S = sts()
+    T = T0.clone()
+    dt = None
+    ss = []
+    for _ in range(nsteps):
+        k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+        dte = G.dt_euler("aniso", k, b)
+        dt = ratio * dte if dt is None else dt
+        s = S.rkl2_num_stages(dt, dte)
+        ss.append(s)
+        T = G.rkl2_advance("aniso", T, k, b, None, dt, s, out=T if inplace else None)
+    return T, ss
+
+
+@pytest.mark.parametrize("nsteps,tol", [(1, 1e-11), (20, 1e-9)])
+def test_rkl2_spitzer_parity(dev, nsteps, tol):
+    cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
+    g = cfg["grid"]
+    ref, s_ref = _oracle_rkl2_run(g, cfg["T"].numpy(), cfg, 100.0, nsteps, cfg["b"].numpy())
+    G = sts().Grid.from_grid(g)
+    out, s_gpu = _gpu_rkl2_run(G, cfg["T"].to(dev), cfg, 100.0, nsteps, cfg["b"].to(dev))
+    assert s_gpu == s_ref
+    assert rel_l2(cpu(out), ref) <= tol
+
+
+def test_rkl2_config0_parity(dev):
+    cfg = W.make_config("c0_heat32")
+    g = cfg["grid"]
+    k = [f.numpy() for f in cfg["faces"]]
+    op = O.Operator(g, k)
+    dte = O.dt_euler(op)
+    dt = 50.0 * dte
+    s = O.rkl2_num_stages(dt, dte)
+    G = sts().Grid.from_grid(g)
+    kd = [f.to(dev) for f in cfg["faces"]]
+    assert abs(G.dt_euler("iso", kd) - dte) <= 1e-15 * dte
+    u_ref = cfg["u"].numpy()
+    u = cfg["u"].to(dev)
+    for n in range(10):
+        u_ref = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), u_ref, dt, s)
+        u = G.rkl2_advance("iso", u, kd, None, None, dt, s)
+        if n == 0:
+            assert rel_l2(cpu(u), u_ref) <= 1e-11
+    assert rel_l2(cpu(u), u_ref) <= 1e-9
+    # conservation of the volume-weighted total (zero-flux walls): uniform V -> plain sum
+    assert abs(float(u.sum()) - float(cfg["u"].sum())) <= 1e-12 * float(cfg["u"].abs().sum())
+
+
+def test_rkl2_viscosity_parity(dev):
+    cfg = W.make_config("c2_visc64", shape=(20, 19, 70))
+    g = cfg["grid"]
+    k = [f.numpy() for f in cfg["visc_faces"]]
+    op = O.Operator(g, k, None, cfg["rho"].numpy())
+    dte = O.dt_euler(op)
+    dt = 500.0 * dte
+    s = O.rkl2_num_stages(dt, dte)
+    ref = O.rkl2_advance(lambda x: op.apply(x), cfg["v"].numpy(), dt, s)
+    G = sts().Grid.from_grid(g)
+    kd = [f.to(dev) for f in cfg["visc_faces"]]
+    rho = cfg["rho"].to(dev)
+    assert abs(G.dt_euler("iso", kd, None, rho) - dte) <= 1e-13 * dte
+    out = G.rkl2_advance("iso", cfg["v"].to(dev), kd, None, rho, dt, s)
+    assert rel_l2(cpu(out), ref) <= 1e-11
+
+
+def test_rkl2_inplace_and_host_pointers(dev):
+    cfg = W.make_config("c1_spitzer64", shape=(9, 17, 40))
+    g = cfg["grid"]
+    G = sts().Grid.from_grid(g)
+    T = cfg["T"].to(dev)
+    b = cfg["b"].to(dev)
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G.dt_euler("aniso", k, b)
+    s = sts().rkl2_num_stages(30 * dte, dte)
+    ref = G.rkl2_advance("aniso", T, k, b, None, 30 * dte, s)
+    T2 = T.clone()
+    G.rkl2_advance("aniso", T2, k, b, None, 30 * dte, s, out=T2)           # device in place
+    assert torch.equal(T2, ref)
+    Th = cfg["T"].clone().pin_memory()
+    kh = [x.cpu() for x in k]
+    out = G.rkl2_advance("aniso", Th, kh, b.cpu(), None, 30 * dte, s)       # host arrays (e2e path)
+    assert torch.equal(out, ref.cpu())
+    Th2 = cfg["T"].clone()                                                  # pageable, in place
+    G.rkl2_advance("aniso", Th2, kh, b.cpu(), None, 30 * dte, s, out=Th2)
+    assert torch.equal(Th2, ref.cpu())
+
+
+# ---------------------------------------------------------------- A7
+@pytest.mark.parametrize("case", ["c0", "c1", "c2"])
+def test_be_pcg_parity(dev, case):
+    if case == "c0":
+        cfg = W.make_config("c0_heat32")
+        g = cfg["grid"]
+        k, b, w, u, mode, ratio = cfg["faces"], None, None, cfg["u"], "iso", 50.0
+    elif case == "c1":
+        cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
+        g = cfg["grid"]
+        k = [torch.as_tensor(x) for x in O.spitzer_face_kappa(g, cfg["T"].numpy(), cfg["kappa0"], cfg["T_cut"])]
+        b, w, u, mode, ratio = cfg["b"], None, cfg["T"], "aniso", 100.0
+    else:
+        cfg = W.make_config("c2_visc64", shape=(20, 19, 70))
+        g = cfg["grid"]
+        k, b, w, u, mode, ratio = cfg["visc_faces"], None, cfg["rho"], cfg["v"], "iso", 500.0
+    op = O.Operator(g, [x.numpy() for x in k], None if b is None else b.numpy(), None if w is None else w.numpy())
+    dt = ratio * O.dt_euler(op)
+    ref, it_ref = O.be_pcg_solve(op, u.numpy(), dt, rtol=1e-12)
+    G = sts().Grid.from_grid(g)
+    out, it = G.be_pcg_solve(mode, u.to(dev), [x.to(dev) for x in k], None if b is None else b.to(dev),
+                             None if w is None else w.to(dev), dt, 1e-12, 100000)
+    assert all(abs(a - c) <= 1 for a, c in zip(it, it_ref)), (it, it_ref)
+    assert rel_l2(cpu(out), ref) <= 1e-11
+
+
+def test_be_pcg_degenerate(dev):
+    cfg = W.make_config("c1_spitzer64", shape=(6, 5, 8))
+    g = cfg["grid"]
+    G = sts().Grid.from_grid(g)
+    b = cfg["b"].to(dev)
+    k = G.face_kappa_spitzer(cfg["T"].to(dev), cfg["kappa0"], cfg["T_cut"])
+    c = torch.full(g.shape, 3.0, dtype=torch.float64, device=dev)     # L c = 0 -> 0 iterations
+    out, it = G.be_pcg_solve("aniso", c, k, b, None, 1e-3, 1e-12, 100)
+    assert it == [0] and torch.equal(out, c)
+    out, it = G.be_pcg_solve("aniso", cfg["T"].to(dev), k, b, None, 0.0, 1e-12, 100)   # dt = 0
+    assert it == [0] and torch.equal(out, cfg["T"].to(dev))
+    T = cfg["T"].to(dev)
+    out, it = G.be_pcg_solve("aniso", T, k, b, None, 1.0, 1e-12, 2, allow_not_converged=True)
+    assert it == [2]
+
+
+# ---------------------------------------------------------------- decomposition emulation
+@pytest.mark.parametrize("nv", [2, 3, 7])
+def test_virtual_slabs_match_single_domain(dev, nv):
+    """n_virtual r-slabs exchange boundary planes through halo buffers exactly
+    like the multi-GPU path; per-cell arithmetic is identical -> bitwise equal
+    operator / RKL2, PCG within rounding of its dot products."""
+    cfg = W.make_config("c1_spitzer64", shape=(21, 19, 70))
+    g = cfg["grid"]
+    G1 = sts().Grid.from_grid(g)
+    Gv = sts().Grid.from_grid(g, n_virtual=nv)
+    T = cfg["T"].to(dev)
+    b = cfg["b"].to(dev)
+    k = G1.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    assert all(torch.equal(x, y) for x, y in zip(k, Gv.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])))
+    assert torch.equal(G1.op_apply("aniso", T, k, b), Gv.op_apply("aniso", T, k, b))
+    d1, dv = G1.dt_euler("aniso", k, b), Gv.dt_euler("aniso", k, b)
+    assert d1 == dv
+    s = sts().rkl2_num_stages(100 * d1, d1)
+    assert torch.equal(G1.rkl2_advance("aniso", T, k, b, None, 100 * d1, s),
+                       Gv.rkl2_advance("aniso", T, k, b, None, 100 * d1, s))
+    x1, i1 = G1.be_pcg_solve("aniso", T, k, b, None, 100 * d1, 1e-12, 10000)
+    xv, iv = Gv.be_pcg_solve("aniso", T, k, b, None, 100 * d1, 1e-12, 10000)
+    assert abs(i1[0] - iv[0]) <= 1 and rel_l2(cpu(xv), cpu(x1)) <= 1e-12
+    # viscosity (3 components, weighted)
+    cv = W.make_config("c2_visc64", shape=(21, 19, 70))
+    kv = [f.to(dev) for f in cv["visc_faces"]]
+    rho, v = cv["rho"].to(dev), cv["v"].to(dev)
+    assert torch.equal(G1.op_apply("iso", v, kv, None, rho), Gv.op_apply("iso", v, kv, None, rho))
+
+
+def test_smoke_entry(dev):
+    import __graft_entry__ as e
+    e.smoke()
