@@ -1,0 +1,475 @@
+#!/usr/bin/env python3
+"""bench.py — Gcell-updates/s of the B200 RKL2 / BE+Jacobi-PCG parabolic advance.
+
+One *step* = one pass of the whole hot path (DESIGN.md §0 rows A1-A7) over the
+BASELINE.json configs[4] workload (Spitzer conduction + viscosity on the
+512 x 512 x 1024 spherical grid, FP64, dt = 300 dt_exp):
+  conduction: lagged face kappa -> Gershgorin dt_exp -> s -> RKL2 super-step,
+              and BE solved by Jacobi-PCG (rtol 1e-12)
+  viscosity : Gershgorin dt_exp -> s -> RKL2 super-step (3 components),
+              and BE solved by Jacobi-PCG (3 components)
+every step advancing the same resident inputs (deterministic work per step).
+A cell-update is one cell advanced by one RKL2 stage or one PCG iteration
+(a 3-component velocity cell counts once; the vector PCG counts its slowest
+component).  value = total cell-updates of all ranks / max-over-ranks device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (r-slab decomposition, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+METRIC = "Gcell-updates/s per RKL2 stage and PCG iter (1/2/4/8 B200), % HBM roofline"
+UNIT = "Gcell-updates/s"
+RATIO = {"c1_spitzer64": 100.0, "c2_visc64": 500.0, "c3_spitzer256": 100.0, "c4_scale512": 300.0}
+RTOL = 1e-12
+KMAX = 50000
+# bounded CPU sample of the same workload for the oracle baseline (cells of the box)
+CPU_BOX = (16, 48, 96)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# algorithmic HBM bytes per cell for each kernel class: every
+# field read or written exactly once, FP64
+# ----------------------------------------------------------------------------
+def bytes_per_cell(kind, ncomp=1, active=None):
+    c = ncomp if active is None else active
+    table = {
+        "face_kappa": 8 + 24,
+        "aniso_F": 8 + 48 + 8,
+        "aniso_rkl2_first": 8 + 48 + 16,
+        "aniso_rkl2_stage": 8 + 48 + 24 + 8,
+        "aniso_pcg_r0": 8 + 48 + 32,
+        "aniso_pcg_ap": 8 + 48 + 8,
+        "aniso_gersh": 48,
+        "iso_rkl2_first": 8 * c + 32 + 16 * c,
+        "iso_rkl2_stage": 32 * c + 32 + 8 * c,
+        "iso_pcg_r0": 8 * c + 32 + 24 * c + 8,
+        "iso_pcg_ap": 16 * c + 32,
+        "iso_gersh": 32,
+        "pcg_update": 48 * c + 8,
+        "pcg_pupdate": 24 * c + 8,
+    }
+    return table[kind]
+
+
+def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v):
+    """Total algorithmic bytes per class for one step on `ncells` local cells."""
+    B = {}
+    add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
+    if s_c:
+        _cond_bytes(add, s_c, it_c)
+    if s_v:
+        _visc_bytes(add, s_v, it_v)
+    return B
+
+
+def _cond_bytes(add, s_c, it_c):
+    add("face_kappa", bytes_per_cell("face_kappa"))
+    add("aniso_gersh", bytes_per_cell("aniso_gersh"))
+    add("aniso_rkl2_first", bytes_per_cell("aniso_rkl2_first"))
+    add("aniso_rkl2_stage", (s_c - 1) * bytes_per_cell("aniso_rkl2_stage"))
+    add("aniso_pcg_r0", bytes_per_cell("aniso_pcg_r0"))
+    add("aniso_pcg_ap", it_c * bytes_per_cell("aniso_pcg_ap"))
+    add("pcg_update", it_c * bytes_per_cell("pcg_update", 1))
+    add("pcg_pupdate", max(it_c - 1, 0) * bytes_per_cell("pcg_pupdate", 1))
+
+
+def _visc_bytes(add, s_v, it_v):
+    add("iso_gersh", bytes_per_cell("iso_gersh"))
+    add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
+    add("iso_rkl2_stage", (s_v - 1) * bytes_per_cell("iso_rkl2_stage", 3))
+    add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0", 3))
+    for k in range(1, max(it_v) + 1):
+        act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
+        add("iso_pcg_ap", bytes_per_cell("iso_pcg_ap", active=act))
+        add("pcg_update", bytes_per_cell("pcg_update", active=act))
+        act_p = sum(1 for i in it_v if i > k)
+        if act_p:
+            add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act_p))
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append({"sm": float(p[0]), "max": float(p[1]), "util": float(p[3]),
+                             "hw": p[5], "hw_th": p[6], "sw_th": p[7], "pcap": p[8]})
+            except ValueError:
+                continue
+        load = [r for r in rows if r["util"] >= 50] or rows
+        if not load:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        reasons = set()
+        for r in load:
+            for key, name in (("hw", "hw_slowdown"), ("hw_th", "hw_thermal_slowdown"),
+                              ("sw_th", "sw_thermal_slowdown"), ("pcap", "sw_power_cap")):
+                if r[key].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in load), "sm_max_mhz": max(r["max"] for r in load),
+                "reasons": sorted(reasons), "samples": len(load)}
+
+
+# ----------------------------------------------------------------------------
+# the GPU step
+# ----------------------------------------------------------------------------
+class Step:
+    def __init__(self, G, inp, ratio, dev, host=False):
+        self.G, self.inp, self.ratio, self.host = G, inp, ratio, host
+        shape = G.shape
+        alloc = (lambda *s: torch.empty(s, dtype=torch.float64, pin_memory=True)) if host else \
+            (lambda *s: torch.empty(s, dtype=torch.float64, device=dev))
+        self.k = tuple(torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(3))
+        self.T_rk, self.T_be = alloc(*shape), alloc(*shape)
+        self.v_rk, self.v_be = alloc(3, *shape), alloc(3, *shape)
+        self.h2d = self.d2h = 0
+
+    def __call__(self):
+        from paper_1610_01265_b200 import sts
+        G, I = self.G, self.inp
+        nb = lambda t: t.numel() * 8 if t.device.type == "cpu" else 0  # noqa: E731
+        s_c = it_c = s_v = 0
+        it_v = [0]
+        self.h2d = self.d2h = 0
+        if "T" in I:
+            # conduction (anisotropic Spitzer, lagged kappa)
+            T, b = I["T"], I["b"]
+            G.face_kappa_spitzer(T, I["kappa0"], I["T_cut"], out=self.k)
+            dte = G.dt_euler("aniso", self.k, b)
+            dt = self.ratio * dte
+            s_c = sts.rkl2_num_stages(dt, dte)
+            G.rkl2_advance("aniso", T, self.k, b, None, dt, s_c, out=self.T_rk)
+            _, (it_c,) = G.be_pcg_solve("aniso", T, self.k, b, None, dt, RTOL, KMAX, out=self.T_be)
+            # bytes each C-ABI call staged (inputs H2D, outputs D2H); 0 for device arrays
+            self.h2d += 3 * nb(T) + 3 * nb(b)
+            self.d2h += nb(self.T_rk) + nb(self.T_be)
+        if "v" in I:
+            # viscosity (isotropic, weighted by rho, 3 components)
+            kv, rho, v = I["visc_faces"], I["rho"], I["v"]
+            dtev = G.dt_euler("iso", kv, None, rho)
+            dtv = self.ratio * dtev
+            s_v = sts.rkl2_num_stages(dtv, dtev)
+            G.rkl2_advance("iso", v, kv, None, rho, dtv, s_v, out=self.v_rk)
+            _, it_v = G.be_pcg_solve("iso", v, kv, None, rho, dtv, RTOL, KMAX, out=self.v_be)
+            self.h2d += 3 * sum(nb(x) for x in kv) + 3 * nb(rho) + 2 * nb(v)
+            self.d2h += nb(self.v_rk) + nb(self.v_be)
+        return {"s_cond": s_c, "it_cond": it_c, "s_visc": s_v, "it_visc": it_v,
+                "units": s_c + it_c + s_v + max(it_v)}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+def allreduce_max(x, dev, ws):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws, dev):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[dev.index])
+
+
+# ----------------------------------------------------------------------------
+# oracle CPU sample (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------
+def cpu_box_config(name):
+    """BASELINE config `name`'s recipe restricted to a CPU_BOX block at the
+    stiff inner boundary (r planes 0.., equatorial theta band, phi 0..)."""
+    _, shape, _ = W.CONFIGS[name]
+    g = W.spherical_grid(*shape)
+    n1, n2, n3 = CPU_BOX
+    j0 = shape[1] // 2 - n2 // 2
+    box = W.Grid("spherical", g.x1f[:n1 + 1], g.x2f[j0:j0 + n2 + 1], g.x3f[:n3 + 1], periodic3=False,
+                 x1c=g.x1c[:n1], x2c=g.x2c[j0:j0 + n2], x3c=g.x3c[:n3], x1_span=g.span1)
+    cfg = {"grid": box, **W.SPITZER}
+    cfg["T"] = W.tr_corona_T(box, seed=2)
+    cfg["b"] = W.multipole_b(box, seed=3)
+    cfg["rho"], cfg["visc_faces"], cfg["v"] = W.viscosity_inputs(box, seed=4)
+    return cfg
+
+
+def oracle_step(cfg, ratio):
+    from oracle import core as O
+    g = cfg["grid"]
+    T = cfg["T"].numpy()
+    kap = O.spitzer_face_kappa(g, T, cfg["kappa0"], cfg["T_cut"])
+    op = O.Operator(g, kap, cfg["b"].numpy())
+    dte = O.dt_euler(op)
+    dt = ratio * dte
+    s_c = O.rkl2_num_stages(dt, dte)
+    O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), T, dt, s_c)
+    _, it_c = O.be_pcg_solve(op, T, dt, rtol=RTOL)
+    opv = O.Operator(g, [f.numpy() for f in cfg["visc_faces"]], None, cfg["rho"].numpy())
+    dtev = O.dt_euler(opv)
+    s_v = O.rkl2_num_stages(ratio * dtev, dtev)
+    O.rkl2_advance(opv.apply, cfg["v"].numpy(), ratio * dtev, s_v)
+    _, it_v = O.be_pcg_solve(opv, cfg["v"].numpy(), ratio * dtev, rtol=RTOL)
+    return s_c + it_c[0] + s_v + max(it_v)
+
+
+def time_oracle(name, ratio, steps=1, warmup=0):
+    from threadpoolctl import threadpool_limits
+    cfg = cpu_box_config(name)
+    ncells = cfg["grid"].ncells
+    with threadpool_limits(limits=1):
+        torch.set_num_threads(1)
+        for _ in range(warmup):
+            oracle_step(cfg, ratio)
+        t0 = time.perf_counter()
+        units = 0
+        for _ in range(steps):
+            units += oracle_step(cfg, ratio)
+        dt = time.perf_counter() - t0
+    return {"value": ncells * units / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle (numpy/scipy, 1 thread) full step of {name}'s recipe on a "
+                      f"{'x'.join(map(str, CPU_BOX))} block at r_min ({ncells} cells), dt = {ratio:g} dt_exp of "
+                      f"the block, {steps} step(s): {units} cell-updates per cell in {dt:.1f} s"}, dt / steps
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return 0
+    ratio = RATIO[args.config]
+    base, sec = time_oracle(args.config, ratio, steps=args.steps, warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config + " (bounded oracle sample)",
+                                            "sample": base["sample"]},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4_scale512", choices=list(RATIO))
+    ap.add_argument("--impl", default="sts", choices=["sts", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shape", default=None, help="override n1,n2,n3 (debug)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    ws, rank, lrank = dist_info()
+    assert ws == args.gpus or ws == 1, "launch N>1 with torchrun --nproc-per-node N"
+    dev = torch.device("cuda", lrank)
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    barrier(ws, dev)
+    from paper_1610_01265_b200 import sts
+
+    shape = tuple(int(x) for x in args.shape.split(",")) if args.shape else None
+    n1 = (shape or W.CONFIGS[args.config][1])[0]
+    i0, nl = W.split_planes(n1, ws)[rank]
+    cfg = W.make_config(args.config, device=dev, shape=shape, slab=(i0, nl) if ws > 1 else None)
+    gg = cfg["global_grid"]
+    G = sts.Grid.from_grid(gg, i0=i0, nl=nl, device=lrank)
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [sts.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        G.comm_init(ws, rank, obj[0])
+    ncells_local = nl * gg.shape[1] * gg.shape[2]
+    ncells_total = gg.ncells
+    ratio = RATIO[args.config]
+    inp = {k: cfg[k] for k in ("T", "b", "rho", "visc_faces", "v", "kappa0", "T_cut") if k in cfg}
+    step = Step(G, inp, ratio, dev)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- warm-up + timed region (device-resident inputs)
+    for _ in range(max(args.warmup, 0)):
+        info = step()
+    G.set_timing(True)
+    G.timing_reset()
+    launches0 = G.kernel_launches
+    sampler = ClockSampler(lrank)
+    sampler.start()
+    barrier(ws, dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    infos = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws, dev)
+    clocks = sampler.stop()
+    ms_local = e0.elapsed_time(e1)
+    ms = allreduce_max(ms_local, dev, ws)
+    launches = G.kernel_launches - launches0
+    timing = G.timing()
+    G.set_timing(False)
+    units = sum(i["units"] for i in infos)
+    value = ncells_total * units / (ms * 1e-3) / 1e9
+
+    # ---------------- roofline of the dominant kernel (rank 0's device timing)
+    peak, peak_kind = peaks()
+    Bytes = {}
+    for i in infos:
+        for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"]).items():
+            Bytes[k] = Bytes.get(k, 0.0) + v
+    kernels = {}
+    for k, (n, kms) in timing.items():
+        if n == 0:
+            continue
+        ent = {"launches": n, "ms": round(kms, 3), "share": round(kms / ms_local, 4)}
+        if k in Bytes and kms > 0:
+            ent["achieved_gbs"] = round(Bytes[k] / (kms * 1e-3) / 1e9, 1)
+            ent["frac"] = round(ent["achieved_gbs"] / peak, 4)
+        kernels[k] = ent
+    dom = max((k for k in kernels if "achieved_gbs" in kernels[k]), key=lambda k: kernels[k]["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if dom in tr.get("dram_bytes_per_cell", {}):
+            traffic = tr["dram_bytes_per_cell"][dom] * ncells_local
+    except Exception:
+        pass
+    eff = [k for k in kernels if "achieved_gbs" in kernels[k]]
+    launches_dom = infos[0]
+    n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"]}.get(dom)
+    bpl = (Bytes[dom] / len(infos) / n_eff) if n_eff else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
+                "algorithmic_bytes_per_launch": bpl}
+
+    # ---------------- end-to-end through the C ABI with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        host_inp = dict(inp)
+        for key in ("T", "b", "rho", "v"):
+            host_inp[key] = inp[key].cpu().pin_memory()
+        host_inp["visc_faces"] = tuple(x.cpu().pin_memory() for x in inp["visc_faces"])
+        hstep = Step(G, host_inp, ratio, dev, host=True)
+        hstep()  # warm-up (staging workspace)
+        barrier(ws, dev)
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        hinfos = [hstep() for _ in range(args.e2e_steps)]
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws, dev)
+        hms = allreduce_max(t0.elapsed_time(t1), dev, ws)
+        hunits = sum(i["units"] for i in hinfos)
+        e2e = {"value": ncells_total * hunits / (hms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": hstep.h2d * ws, "d2h_bytes_per_step": hstep.d2h * ws,
+               "steps": args.e2e_steps, "ms_per_step": hms / args.e2e_steps}
+        del host_inp, hstep
+
+    cpu_base = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu_base, _ = time_oracle(args.config, ratio, steps=1, warmup=0)
+
+    if rank == 0:
+        i0f = infos[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "shape": list(gg.shape), "cells": ncells_total,
+                       "dt_over_dt_exp": ratio, "pcg_rtol": RTOL, "parallelism": f"r-slab x{ws}",
+                       "l2": f"inputs larger than L2 ({ncells_total * 8 / 1e9:.2f} GB per field)" if
+                       ncells_total * 8 > 126e6 else "inputs fit L2 (no flush)",
+                       "stages_cond": i0f["s_cond"], "pcg_iters_cond": i0f["it_cond"],
+                       "stages_visc": i0f["s_visc"], "pcg_iters_visc": i0f["it_visc"]},
+            "roofline": roofline, "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

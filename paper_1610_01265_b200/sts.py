@@ -22,6 +22,10 @@ STS_ERR_NOT_CONVERGED = -4
 GEOM = {"cartesian": 0, "spherical": 1}
 MODE = {"iso": 0, "aniso": 1}
 UID_BYTES = 128
+# kernel classes of sts_grid_timing (include/sts_b200.h STS_K_*)
+KERNEL_CLASSES = ["face_kappa", "aniso_F", "aniso_rkl2_first", "aniso_rkl2_stage", "aniso_pcg_r0",
+                  "aniso_pcg_ap", "aniso_gersh", "iso_F", "iso_rkl2_first", "iso_rkl2_stage", "iso_pcg_r0",
+                  "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo"]
 
 _lib = None
 
@@ -50,6 +54,9 @@ def lib():
         "sts_grid_destroy": (I, [P]),
         "sts_grid_workspace_bytes": (I, [P, ctypes.POINTER(ctypes.c_size_t)]),
         "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
+        "sts_grid_set_timing": (I, [P, I]),
+        "sts_grid_timing_reset": (I, [P]),
+        "sts_grid_timing": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
         "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
         "sts_comm_init": (I, [P, I, I, P, ctypes.c_size_t]),
         "sts_face_kappa_spitzer": (I, [P, P, P, P, P, D, D, D, D, P]),
@@ -160,6 +167,22 @@ class Grid:
         v = ctypes.c_size_t()
         _check("sts_grid_workspace_bytes", lib().sts_grid_workspace_bytes(self._h, ctypes.byref(v)))
         return v.value
+
+    def set_timing(self, enable=True):
+        _check("sts_grid_set_timing", lib().sts_grid_set_timing(self._h, int(bool(enable))))
+
+    def timing_reset(self):
+        _check("sts_grid_timing_reset", lib().sts_grid_timing_reset(self._h))
+
+    def timing(self):
+        """{class name: (launches, device ms)} since the last timing_reset()."""
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            n = ctypes.c_longlong()
+            ms = ctypes.c_double()
+            _check("sts_grid_timing", lib().sts_grid_timing(self._h, i, ctypes.byref(n), ctypes.byref(ms)))
+            out[name] = (n.value, ms.value)
+        return out
 
     def comm_init(self, nranks, rank, uid: bytes):
         buf = ctypes.create_string_buffer(uid, UID_BYTES)

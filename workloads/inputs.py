@@ -25,10 +25,10 @@ import numpy as np
 import torch
 
 __all__ = [
-    "Grid", "uniform_cartesian", "spherical_grid", "geometric_faces", "subgrid",
+    "Grid", "uniform_cartesian", "spherical_grid", "geometric_faces", "subgrid", "r_slab", "split_planes",
     "gaussian_bump", "tilted_dipole_b", "multipole_b", "smooth_modes",
     "corona_T", "tr_corona_T", "viscosity_inputs", "constant_faces",
-    "CONFIGS", "make_config", "cartesian_mesh", "random_unit_b",
+    "CONFIGS", "SPITZER", "make_config", "cartesian_mesh", "random_unit_b",
 ]
 
 
@@ -43,6 +43,7 @@ class Grid:
     x1c: np.ndarray = field(default=None)
     x2c: np.ndarray = field(default=None)
     x3c: np.ndarray = field(default=None)
+    x1_span: tuple = None      # (x1 min, x1 max) of the GLOBAL grid when this is an r-slab
 
     def __post_init__(self):
         self.x1f = np.ascontiguousarray(self.x1f, dtype=np.float64)
@@ -55,6 +56,10 @@ class Grid:
             self.x2c = 0.5 * (self.x2f[1:] + self.x2f[:-1])
         if self.x3c is None:
             self.x3c = 0.5 * (self.x3f[1:] + self.x3f[:-1])
+
+    @property
+    def span1(self):
+        return self.x1_span if self.x1_span is not None else (float(self.x1f[0]), float(self.x1f[-1]))
 
     @property
     def shape(self):
@@ -111,6 +116,24 @@ def spherical_grid(nr, nt, nphi, r0=1.0, r1=20.0, dr0=0.005) -> Grid:
                 np.linspace(0.0, 2.0 * math.pi, nphi + 1), periodic3=True)
 
 
+def r_slab(grid: Grid, i0: int, nl: int) -> Grid:
+    """The r-planes [i0, i0+nl) of `grid` (fields evaluated on it equal the
+    corresponding planes of the global fields)."""
+    return Grid(grid.geom, grid.x1f[i0:i0 + nl + 1], grid.x2f, grid.x3f, periodic3=grid.periodic3,
+                x1c=grid.x1c[i0:i0 + nl], x2c=grid.x2c, x3c=grid.x3c, x1_span=grid.span1)
+
+
+def split_planes(n1: int, nparts: int):
+    """Balanced contiguous split of n1 planes: [(i0, nl)] (sizes differ by <= 1)."""
+    base, rem = divmod(n1, nparts)
+    out, i0 = [], 0
+    for p in range(nparts):
+        nl = base + (1 if p < rem else 0)
+        out.append((i0, nl))
+        i0 += nl
+    return out
+
+
 def subgrid(grid: Grid, c, radius: int):
     """Index box of half-width `radius` around cell c=(i,j,k).
 
@@ -141,7 +164,7 @@ def subgrid(grid: Grid, c, radius: int):
         x3f = grid.x3f[Kw[0]:Kw[-1] + 2]
         per, kloc = False, k - Kw[0]
     sub = Grid(grid.geom, grid.x1f[I[0]:I[-1] + 2], grid.x2f[J[0]:J[-1] + 2], x3f,
-               periodic3=per, x1c=grid.x1c[I], x2c=grid.x2c[J], x3c=x3c)
+               periodic3=per, x1c=grid.x1c[I], x2c=grid.x2c[J], x3c=x3c, x1_span=grid.span1)
     return sub, (I, J, Kw), (i - I[0], j - J[0], kloc)
 
 
@@ -252,11 +275,12 @@ def smooth_modes(grid: Grid, seed=1, nmodes=8, device="cpu"):
     """
     rng = np.random.default_rng(seed)
     r, t, p = _mesh(grid, device)
+    r_lo, r_hi = grid.span1
     if grid.geom == "spherical":
-        rho = torch.log(r / grid.x1f[0]) / math.log(grid.x1f[-1] / grid.x1f[0])
+        rho = torch.log(r / r_lo) / math.log(r_hi / r_lo)
         tt, pp = t, p
     else:
-        rho = (r - grid.x1f[0]) / (grid.x1f[-1] - grid.x1f[0])
+        rho = (r - r_lo) / (r_hi - r_lo)
         tt = math.pi * (t - grid.x2f[0]) / (grid.x2f[-1] - grid.x2f[0])
         pp = 2 * math.pi * (p - grid.x3f[0]) / (grid.x3f[-1] - grid.x3f[0])
     amps = rng.uniform(-1, 1, nmodes)
@@ -285,7 +309,7 @@ def tr_corona_T(grid: Grid, seed=2, T_ch=2.0e4, r_tr=1.01, w_tr=0.002, device="c
 def viscosity_inputs(grid: Grid, seed=4, nu=1.0, amp=1e-2, nmodes=6, device="cpu"):
     """Config 2: rho ~ r^-4 at cells, nu*rho evaluated at face positions, and a
     solenoidal velocity v = curl(Psi) (Cartesian components), Psi = sum of seeded
-    Fourier modes, scaled so max|v| = amp.
+    Fourier modes, scaled so |v| <= amp (sum of the mode amplitudes = amp).
 
     Returns (rho, (f1, f2, f3), v[3, n1, n2, n3]).
     """
@@ -293,21 +317,23 @@ def viscosity_inputs(grid: Grid, seed=4, nu=1.0, amp=1e-2, nmodes=6, device="cpu
     rc, _, _ = _mesh(grid, device)
     rf, _, _ = _mesh(grid, device, which=("f", "c", "c"))
     shape = grid.shape
-    rho = torch.broadcast_to(rc ** -4.0, shape).contiguous()
-    f1 = torch.broadcast_to(nu * rf ** -4.0, shape).contiguous()
-    f2 = torch.broadcast_to(nu * rc ** -4.0, shape).contiguous()
+    rho = torch.broadcast_to(1.0 / ((rc * rc) * (rc * rc)), shape).contiguous()
+    f1 = torch.broadcast_to(nu / ((rf * rf) * (rf * rf)), shape).contiguous()
+    f2 = torch.broadcast_to(nu / ((rc * rc) * (rc * rc)), shape).contiguous()
     f3 = f2.clone()
     x, y, z = cartesian_mesh(grid, device)
     v = torch.zeros((3,) + shape, dtype=torch.float64, device=device)
+    bound = 0.0
     for _ in range(nmodes):
         k = rng.normal(size=3) * 1.5
         c = rng.normal(size=3)
         ph = rng.uniform(0, 2 * math.pi)
         kxc = np.cross(k, c)
+        bound += float(np.linalg.norm(kxc))
         arg = torch.cos(k[0] * x + k[1] * y + k[2] * z + ph)
         for d in range(3):
             v[d] += kxc[d] * arg
-    v = v * (amp / v.abs().max())
+    v = v * (amp / bound)    # |v| <= amp everywhere; independent of the slab evaluated
     return rho, (f1, f2, f3), v.contiguous()
 
 
@@ -326,9 +352,10 @@ CONFIGS = {
 SPITZER = dict(kappa0=1.0e-9, T_cut=5.0e5)  # kappa0 scale is irrelevant: dt is set in units of dt_exp
 
 
-def make_config(name: str, device="cpu", shape=None, seed=0):
+def make_config(name: str, device="cpu", shape=None, seed=0, slab=None):
     """Build every input of a BASELINE.json config.  `shape` overrides the size
-    (for scaled-down parity runs of the same recipe)."""
+    (for scaled-down parity runs of the same recipe); `slab=(i0, nl)` builds
+    only those r-planes of the global fields (one rank's share)."""
     kind, default_shape, ratios = CONFIGS[name]
     n1, n2, n3 = shape or default_shape
     out = {"name": name, "kind": kind, "dt_ratios": ratios}
@@ -338,6 +365,9 @@ def make_config(name: str, device="cpu", shape=None, seed=0):
                    faces=constant_faces(g, 1.0, device), b=None, w=None, mode="iso")
         return out
     g = spherical_grid(n1, n2, n3)
+    out["global_grid"] = g
+    if slab is not None:
+        g = r_slab(g, *slab)
     out["grid"] = g
     if kind == "spitzer":
         out.update(T=corona_T(g, seed=seed + 1, device=device),
