@@ -62,11 +62,13 @@ def bytes_per_cell(kind, ncomp=1, active=None):
     c = ncomp if active is None else active
     table = {
         "face_kappa": 8 + 24,
-        "aniso_F": 8 + 48 + 8,
-        "aniso_rkl2_first": 8 + 48 + 16,
-        "aniso_rkl2_stage": 8 + 48 + 24 + 8,
+        # fast anisotropic path streams u + the 3 frozen vertex coefficients e
+        "vertex_coef": 48 + 24,
+        "aniso_F": 8 + 24 + 8,
+        "aniso_rkl2_first": 8 + 24 + 16,
+        "aniso_rkl2_stage": 8 + 24 + 24 + 8,
         "aniso_pcg_r0": 8 + 48 + 32,
-        "aniso_pcg_ap": 8 + 48 + 8,
+        "aniso_pcg_ap": 8 + 24 + 8,
         "aniso_gersh": 48,
         "iso_rkl2_first": 8 * c + 32 + 16 * c,
         "iso_rkl2_stage": 32 * c + 32 + 8 * c,
@@ -92,6 +94,7 @@ def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v):
 
 def _cond_bytes(add, s_c, it_c):
     add("face_kappa", bytes_per_cell("face_kappa"))
+    add("vertex_coef", 2 * bytes_per_cell("vertex_coef"))   # once per RKL2 advance and per PCG solve
     add("aniso_gersh", bytes_per_cell("aniso_gersh"))
     add("aniso_rkl2_first", bytes_per_cell("aniso_rkl2_first"))
     add("aniso_rkl2_stage", (s_c - 1) * bytes_per_cell("aniso_rkl2_stage"))

@@ -131,7 +131,8 @@ int sts_grid_kernel_launches(const sts_grid* g, long long* count);
 #define STS_K_PCG_PUPDATE 14
 #define STS_K_PCG_REDUCE 15
 #define STS_K_HALO 16
-#define STS_K_NCLASSES 17
+#define STS_K_VERTEX_COEF 17
+#define STS_K_NCLASSES 18
 int sts_grid_set_timing(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);

@@ -306,6 +306,31 @@ static StencilCall make_call(sts_grid* g, const Slab& s, int mode, int ncomp, in
   return c;
 }
 
+static size_t vertex_coef_doubles(const sts_grid* g, int mode) {
+  if (mode != STS_MODE_ANISO) return 0;
+  size_t n = 0;
+  for (auto& s : g->slabs) n += (size_t)3 * (s.nl + 1) * g->plane;
+  return n;
+}
+
+// per-advance precompute of the frozen vertex coefficients (after exchange_coeffs)
+static std::vector<const double*> build_vertex_coefs(sts_grid* g, int mode, double* base, const double* k1,
+                                                     const double* k2, const double* k3, const double* b,
+                                                     cudaStream_t st) {
+  std::vector<const double*> out(g->slabs.size(), nullptr);
+  if (mode != STS_MODE_ANISO) return out;
+  size_t o = 0;
+  for (size_t i = 0; i < g->slabs.size(); ++i) {
+    const Slab& s = g->slabs[i];
+    out[i] = base + o;
+    Timed t(g, STS_K_VERTEX_COEF, st);
+    launch_vertex_coef(slab_geo(g, s), view(g, s, H_B, b), view(g, s, H_K1, k1), view(g, s, H_K2, k2),
+                       view(g, s, H_K3, k3), base + o, st);
+    o += (size_t)3 * (s.nl + 1) * g->plane;
+  }
+  return out;
+}
+
 static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 static const double* off(const double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 
@@ -638,11 +663,16 @@ int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out,
     if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
     sg.input(w, N);
     sg.output(out, N * ncomp);
-    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
+    const size_t evn = vertex_coef_doubles(g, mode);
+    double* base = ws_get(g, (sg.total + evn) * sizeof(double));
+    if (sg.any_host) sg.begin(base + evn);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, base, k1, k2, k3, b, st);
     exchange(g, H_U, u, ncomp, st);
-    for (auto& s : g->slabs) {
+    for (size_t si = 0; si < g->slabs.size(); ++si) {
+      const Slab& s = g->slabs[si];
       StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
+      c.ev = ev[si];
       c.ea.out = off(out, s);
       Timed t(g, stencil_kind(c.mode, c.epi), st);
       launch_stencil(c, st);
@@ -722,18 +752,22 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
     // goes to its own device buffer and back; a device in-place advance is safe
     // because Y0 is only read pointwise after stage 1
     sg.output(u1, NF);
-    double* base = ws_get(g, (sg.total + 3 * NF) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 3 * NF);
+    const size_t evn = vertex_coef_doubles(g, mode);
+    double* base = ws_get(g, (sg.total + 3 * NF + evn) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 3 * NF + evn);
     double* M0 = base;
     double* A = base + NF;
     double* B = base + 2 * NF;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
     const Rkl2Coef co = rkl2_coefs(s);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, base + 3 * NF, k1, k2, k3, b, st);
     // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
     exchange(g, H_U, u0, ncomp, st);
-    for (auto& sl : g->slabs) {
+    for (size_t si = 0; si < g->slabs.size(); ++si) {
+      const Slab& sl = g->slabs[si];
       StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
+      c.ev = ev[si];
       c.ea.out = off(A, sl);
       c.ea.out2 = off(M0, sl);
       c.ea.c0 = co.mut[1] * dt;
@@ -749,8 +783,10 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
       else if (prev == u0) dst = B;                       // never overwrite Y0
       else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
       exchange(g, H_U, cur, ncomp, st);
-      for (auto& sl : g->slabs) {
+      for (size_t si = 0; si < g->slabs.size(); ++si) {
+        const Slab& sl = g->slabs[si];
         StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
+        c.ev = ev[si];
         c.ea.out = off(dst, sl);
         c.ea.ym2 = off(prev, sl);
         c.ea.y0 = off(u0, sl);
@@ -794,8 +830,10 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
     sg.input(w, N);
     sg.output(un1, NF);
-    double* base = ws_get(g, (sg.total + 3 * NF + N) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 3 * NF + N);
+    const size_t evn = vertex_coef_doubles(g, mode);
+    double* base = ws_get(g, (sg.total + 3 * NF + N + evn) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 3 * NF + N + evn);
+    double* evbase = base + 3 * NF + N;
     double* r = base;
     double* p = base + NF;
     double* y = base + 2 * NF;
@@ -803,9 +841,12 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     double* x = un1;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
     // reduction storage
-    int sb_total = 0;
-    for (auto& sl : g->slabs) sb_total += stencil_blocks(slab_geo(g, sl), 0, sl.nl, nullptr);
-    const long long pstride = std::max(sb_total, PW_BLOCKS);
+    int sb_r0 = 0, sb_ap = 0;
+    for (auto& sl : g->slabs) {
+      sb_r0 += stencil_blocks(mode, EPI_PCG_R0, slab_geo(g, sl), 0, sl.nl);
+      sb_ap += stencil_blocks(mode, EPI_PCG_AP, slab_geo(g, sl), 0, sl.nl);
+    }
+    const long long pstride = std::max(std::max(sb_r0, sb_ap), PW_BLOCKS);
     const size_t red_doubles = (size_t)2 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
     ensure_red(g, red_doubles * sizeof(double));
     double* partials = g->d_red;
@@ -827,6 +868,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     };
 
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, evbase, k1, k2, k3, b, st);
     // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; p = z0 = r0 d
     exchange(g, H_U, un, ncomp, st);
     {
@@ -841,11 +883,11 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
         c.ea.partials = partials;
         c.ea.pstride = pstride;
         c.ea.pbase = pb;
-        pb += stencil_blocks(c.geo, 0, sl.nl, nullptr);
+        pb += stencil_blocks(mode, EPI_PCG_R0, c.geo, 0, sl.nl);
         Timed t(g, stencil_kind(c.mode, c.epi), st);
         launch_stencil(c, st);
       }
-      reduce(sb_total, 2, PH_R0);
+      reduce(sb_r0, 2, PH_R0);
     }
     auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
     int launched = 0;
@@ -862,19 +904,21 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
         // y = A p, alpha = r.z / p.y
         exchange(g, H_U, p, ncomp, st);
         int pb = 0;
-        for (auto& sl : g->slabs) {
+        for (size_t si = 0; si < g->slabs.size(); ++si) {
+          const Slab& sl = g->slabs[si];
           StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, p, k1, k2, k3, bb, w);
+          c.ev = ev[si];
           c.ea.out = off(y, sl);
           c.ea.dt = dt;
           c.ea.partials = partials;
           c.ea.pstride = pstride;
           c.ea.pbase = pb;
           c.ea.sc = sc;
-          pb += stencil_blocks(c.geo, 0, sl.nl, nullptr);
+          pb += stencil_blocks(mode, EPI_PCG_AP, c.geo, 0, sl.nl);
           Timed t(g, stencil_kind(c.mode, c.epi), st);
           launch_stencil(c, st);
         }
-        reduce(sb_total, 1, PH_AP);
+        reduce(sb_ap, 1, PH_AP);
         // x += alpha p, r -= alpha y, z = r d, r.z -> beta
         {
           Timed t(g, STS_K_PCG_UPDATE, st);

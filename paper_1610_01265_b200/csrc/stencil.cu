@@ -317,6 +317,287 @@ __global__ void __launch_bounds__(NT, 3) aniso_kernel(StencilCall c, int ic, uns
   }
 }
 
+
+// ============================================================================
+// anisotropic operator, fast path (F / RKL2 stages / PCG A p)
+// ----------------------------------------------------------------------------
+// The vertex coefficients are frozen over an advance (lagged diffusivity,
+// PAPER.md:33), so vertex_coef_kernel folds b, kappa and the metrics into three
+// numbers per vertex ONCE per advance:  e_a = sqrt(V_v kappa_v) * b_{v,a} / (4 h_a)
+// (h_th, h_ph without their cell-dependent r / sin(theta) factors).  Then
+//   Q_v D_a = (e_v . d_v) e_{v,a},   d_v = the 4-difference sums of u,
+// and a stage / matvec pass streams only u, e (and the epilogue fields):
+// 64 B per cell per RKL2 stage instead of 88, 40 B per PCG matvec instead of 64.
+//
+// Thread (vj = warp, vk = lane) owns vertex column (j0-1+vj, k0-1+vk) and output
+// cell (j0+vj, k0+vk) (vj < 7, vk < 31): 7 x 31 outputs, 8 x 32 vertices, 9 x 33
+// staged u cells.  Per r-plane each thread reduces its 2x2 in-plane u box once
+// (3 sums kept in registers for the next vertex plane) and each cell reduces its
+// 2x2 in-plane vertex box once (3 sums kept for the next cell plane).  u planes
+// are staged with cp.async one plane ahead of use.
+// ============================================================================
+constexpr int FJ = 8, FK = 32;              // vertex rows / cols = warps / lanes
+constexpr int FOJ = FJ - 1, FOK = FK - 1;   // output rows / cols
+constexpr int FRJ = FJ + 1, FRK = FK + 1;   // staged cell rows / cols
+constexpr int FRC = FRJ * FRK;              // 297 staged cells per plane
+constexpr int FNT = FJ * FK;                // 256 threads
+constexpr size_t FAST_SMEM = (size_t)(2 * FRC + 3 * FNT) * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = ok ? 8 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// e for every vertex plane il = -1 .. nl-1 of a slab (vertex between cell planes
+// il and il+1): ev[a][(il+1)*plane + jv*n3 + kv], zero where the vertex has a
+// missing cell.  One thread per vertex; b / kappa gathered through L1/L2.
+__global__ void __launch_bounds__(256) vertex_coef_kernel(Geo G, FieldV b, FieldV k1, FieldV k2, FieldV k3,
+                                                          double* __restrict__ ev) {
+  const Metrics& M = G.m;
+  const long long nv = (long long)(G.nl + 1) * G.plane;
+  const long long es = nv;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nv; e += (long long)gridDim.x * blockDim.x) {
+    const int il = (int)(e / G.plane) - 1;
+    const long long rem = e - (long long)(il + 1) * G.plane;
+    const int jv = (int)(rem / G.n3);
+    const int kv = (int)(rem - (long long)jv * G.n3);
+    const int iv = G.i0 + il;
+    bool ok = iv >= 0 && iv + 1 < G.n1g && jv + 1 < G.n2 && (G.periodic3 || kv + 1 < G.n3);
+    double er = 0.0, et = 0.0, ep = 0.0;
+    if (ok) {
+      const int kv1 = (kv + 1 < G.n3) ? kv + 1 : 0;
+      const long long o00 = (long long)jv * G.n3 + kv, o01 = (long long)jv * G.n3 + kv1;
+      const long long o10 = o00 + G.n3, o11 = o01 + G.n3;
+      const double* bl0 = plane_ptr(b, G, il, 0); const double* bh0 = plane_ptr(b, G, il + 1, 0);
+      const double* bl1 = plane_ptr(b, G, il, 1); const double* bh1 = plane_ptr(b, G, il + 1, 1);
+      const double* bl2 = plane_ptr(b, G, il, 2); const double* bh2 = plane_ptr(b, G, il + 1, 2);
+      const double br = 0.125 * ((bl0[o00] + bl0[o01]) + (bl0[o10] + bl0[o11]) + ((bh0[o00] + bh0[o01]) + (bh0[o10] + bh0[o11])));
+      const double bt = 0.125 * ((bl1[o00] + bl1[o01]) + (bl1[o10] + bl1[o11]) + ((bh1[o00] + bh1[o01]) + (bh1[o10] + bh1[o11])));
+      const double bp = 0.125 * ((bl2[o00] + bl2[o01]) + (bl2[o10] + bl2[o11]) + ((bh2[o00] + bh2[o01]) + (bh2[o10] + bh2[o11])));
+      const double* K1l = plane_ptr(k1, G, il, 0);
+      const double* K2l = plane_ptr(k2, G, il, 0); const double* K2h = plane_ptr(k2, G, il + 1, 0);
+      const double* K3l = plane_ptr(k3, G, il, 0); const double* K3h = plane_ptr(k3, G, il + 1, 0);
+      const double kap = (1.0 / 12.0) * (((K1l[o00] + K1l[o01]) + (K1l[o10] + K1l[o11])) +
+                                         ((K2l[o00] + K2l[o01]) + (K3l[o00] + K3l[o10])) +
+                                         ((K2h[o00] + K2h[o01]) + (K3h[o00] + K3h[o10])));
+      const double C = 0.125 * (M.Vr[iv] + M.Vr[iv + 1]) * (M.Vt[jv] + M.Vt[jv + 1]) * (M.Vp[kv] + M.Vp[kv1]) * kap;
+      const double sq = sqrt(C);
+      er = sq * 0.25 * br * M.iH1[iv];
+      et = sq * 0.25 * bt * M.iH2[jv];
+      ep = sq * 0.25 * bp * M.iH3[kv];
+    }
+    ev[e] = er;
+    ev[es + e] = et;
+    ev[2 * es + e] = ep;
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fast_kernel(StencilCall c, int ic) {
+  extern __shared__ double sm[];
+  double* us = sm;                          // [2][FRC] staged u planes
+  double* vA = sm + 2 * FRC;                // [FNT] vertex A = Q Dr
+  double* vB = vA + FNT;                    //        B = Q Dt
+  double* vC = vB + FNT;                    //        C = Q Dp
+  const Geo& G = c.geo;
+  const Metrics& M = G.m;
+  const int tid = threadIdx.x;
+  const int vj = tid >> 5, vk = tid & 31;
+  const int j0 = blockIdx.y * FOJ, k0 = blockIdx.x * FOK;
+  const int ib = c.ib + blockIdx.z * ic;
+  const int ie = min(ib + ic, c.ie);
+  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+
+  if constexpr (EPI == EPI_PCG_AP) {
+    if (c.ea.sc && c.ea.sc[0].done) return;
+  }
+
+  // ---- staging assignments (fixed for the whole march) ----
+  int soff[2];
+  bool sok[2];
+  bool shas[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = tid + q * FNT;
+    shas[q] = e < FRC;
+    const int row = e / FRK, col = e - (e / FRK) * FRK;
+    const int j = j0 - 1 + row;
+    int k = k0 - 1 + col;
+    bool ok = shas[q] && j >= 0 && j < G.n2;
+    if (G.periodic3) k = wrapk(k, G.n3);
+    else ok = ok && k >= 0 && k < G.n3;
+    sok[q] = ok;
+    soff[q] = ok ? j * G.n3 + k : 0;
+  }
+  auto stage = [&](int il, int slot) {
+    const double* src = plane_ptr(c.u, G, il, 0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!shas[q]) continue;
+      const bool ok = sok[q] && src != nullptr;
+      cp_async8(us + slot * FRC + tid + q * FNT, ok ? src + soff[q] : c.ev, ok);
+    }
+    cp_async_commit();
+  };
+
+  // ---- per-thread vertex column ----
+  const int jv = j0 - 1 + vj;
+  int kv = k0 - 1 + vk;
+  bool vok = jv >= 0 && jv + 1 < G.n2;
+  if (G.periodic3) kv = wrapk(kv, G.n3);
+  else vok = vok && kv >= 0 && kv + 1 < G.n3;
+  const double ig3a = vok ? M.iG3[jv] : 0.0, ig3b = vok ? M.iG3[jv + 1] : 0.0;
+  const long long eoff = vok ? (long long)jv * G.n3 + kv : 0;
+  const long long es = (long long)(G.nl + 1) * G.plane;
+  const int j = j0 + vj, k = k0 + vk;
+  const bool own = vj < FOJ && vk < FOK && j < G.n2 && k < G.n3;
+  const long long coff = own ? (long long)j * G.n3 + k : 0;
+  const double ig3c = own ? M.iG3[j] : 0.0;
+  const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
+
+  const int c00 = vj * FRK + vk, c01 = c00 + 1, c10 = c00 + FRK, c11 = c10 + 1;
+  // in-plane 2x2 u box: sum, theta differences, phi differences (theta-metric weighted)
+  auto usums = [&](int slot, double& Su, double& Tu, double& Fu) {
+    const double* U = us + slot * FRC;
+    const double u00 = U[c00], u01 = U[c01], u10 = U[c10], u11 = U[c11];
+    Su = (u00 + u01) + (u10 + u11);
+    Tu = (u10 - u00) + (u11 - u01);
+    Fu = ig3a * (u01 - u00) + ig3b * (u11 - u10);
+  };
+  // frozen vertex coefficients of vertex plane il+1/2 (zero if the vertex is missing)
+  auto load_e = [&](int il, double& er, double& et, double& ep) {
+    const int iv = G.i0 + il;
+    er = et = ep = 0.0;
+    if (vok && iv >= 0 && iv + 1 < G.n1g && il < ie) {
+      const long long o = (long long)(il + 1) * G.plane + eoff;
+      er = __ldg(c.ev + o);
+      et = __ldg(c.ev + es + o);
+      ep = __ldg(c.ev + 2 * es + o);
+    }
+  };
+  // vertex between cell planes il and il+1
+  auto vertex = [&](int il, double er, double et, double ep, double SuL, double TuL, double FuL, double SuH,
+                    double TuH, double FuH) {
+    const int iv = G.i0 + il;
+    double A = 0.0, B = 0.0, C = 0.0;
+    if (vok && iv >= 0 && iv + 1 < G.n1g) {
+      const double ig2l = M.iG2[iv], ig2h = M.iG2[iv + 1];
+      const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
+      A = q * er;
+      B = q * et;
+      C = q * ep;
+    }
+    vA[tid] = A;
+    vB[tid] = B;
+    vC[tid] = C;
+  };
+  // pointwise epilogue operands of cell plane il (RKL2 stage only)
+  auto load_epi = [&](int il, double& ym2, double& y0, double& m0) {
+    if constexpr (EPI == EPI_RKL2_STAGE) {
+      if (own && il < ie) {
+        const long long gi = (long long)il * G.plane + coff;
+        ym2 = c.ea.ym2[gi];
+        y0 = c.ea.y0[gi];
+        m0 = c.ea.m0[gi];
+      }
+    }
+  };
+  auto vbox = [&](double& SA, double& DB, double& DC) {
+    if (!own) return;
+    const double a00 = vA[tid], a01 = vA[tid + 1], a10 = vA[tid + 32], a11 = vA[tid + 33];
+    const double b00 = vB[tid], b01 = vB[tid + 1], b10 = vB[tid + 32], b11 = vB[tid + 33];
+    const double d00 = vC[tid], d01 = vC[tid + 1], d10 = vC[tid + 32], d11 = vC[tid + 33];
+    SA = (a00 + a01) + (a10 + a11);
+    DB = (b00 + b01) - (b10 + b11);
+    DC = (d00 + d10) - (d01 + d11);
+  };
+
+  // ---- prologue: cell planes ib-1, ib -> vertex plane ib-1/2 ----
+  double SuL, TuL, FuL, SuH, TuH, FuH;
+  double SAl = 0, DBl = 0, DCl = 0;
+  double er, et, ep;
+  stage(ib - 1, (ib - 1) & 1);
+  stage(ib, ib & 1);
+  load_e(ib - 1, er, et, ep);
+  cp_async_wait_all();
+  __syncthreads();
+  usums((ib - 1) & 1, SuL, TuL, FuL);
+  usums(ib & 1, SuH, TuH, FuH);
+  double uc = us[(ib & 1) * FRC + c11];
+  vertex(ib - 1, er, et, ep, SuL, TuL, FuL, SuH, TuH, FuH);
+  __syncthreads();
+  vbox(SAl, DBl, DCl);
+  SuL = SuH;
+  TuL = TuH;
+  FuL = FuH;
+  if (ib + 1 <= ie) stage(ib + 1, (ib + 1) & 1);   // overwrites plane ib-1 (all reads done)
+  // register prefetch, one plane ahead: e of vertex plane ib+1/2, epilogue operands of cell plane ib
+  load_e(ib, er, et, ep);
+  double ym2 = 0, y0 = 0, m0 = 0;
+  load_epi(ib, ym2, y0, m0);
+
+  double part = 0.0;
+  for (int il = ib; il < ie; ++il) {
+    const double erc = er, etc = et, epc = ep;
+    const double ym2c = ym2, y0c = y0, m0c = m0;
+    load_e(il + 1, er, et, ep);                       // in flight during this plane
+    load_epi(il + 1, ym2, y0, m0);
+    cp_async_wait_all();
+    __syncthreads();                                  // plane il+1 staged; vertex smem free
+    if (il + 2 <= ie) stage(il + 2, il & 1);          // prefetch: overwrites plane il (in registers)
+    usums((il + 1) & 1, SuH, TuH, FuH);
+    const double un = us[((il + 1) & 1) * FRC + c11];
+    vertex(il, erc, etc, epc, SuL, TuL, FuL, SuH, TuH, FuH);
+    __syncthreads();
+    double SAh = 0, DBh = 0, DCh = 0;
+    vbox(SAh, DBh, DCh);
+    if (own) {
+      const int ig = G.i0 + il;
+      const double ig2c = M.iG2[ig];
+      const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
+      const double WV = (c.w ? __ldg(c.w + (long long)il * G.plane + coff) : 1.0) * M.Vr[ig] * vtpc;
+      const long long gi = (long long)il * G.plane + coff;
+      if constexpr (EPI == EPI_F) {
+        c.ea.out[gi] = Lu / WV;
+      } else if constexpr (EPI == EPI_RKL2_FIRST) {
+        const double F = Lu / WV;
+        c.ea.out2[gi] = F;
+        c.ea.out[gi] = uc + c.ea.c0 * F;
+      } else if constexpr (EPI == EPI_RKL2_STAGE) {
+        const double F = Lu / WV;
+        c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * ym2c + c.ea.c2 * y0c + c.ea.c0 * F + c.ea.c1 * m0c;
+      } else if constexpr (EPI == EPI_PCG_AP) {
+        const double y = WV * uc - c.ea.dt * Lu;
+        c.ea.out[gi] = y;
+        part += uc * y;
+      }
+    }
+    SAl = SAh;
+    DBl = DBh;
+    DCl = DCh;
+    SuL = SuH;
+    TuL = TuH;
+    FuL = FuH;
+    uc = un;
+  }
+  if constexpr (EPI == EPI_PCG_AP) {
+    double v[1] = {part};
+    block_partials<1>(v, c.ea.partials, c.ea.pstride, c.ea.pbase + blk);
+  }
+}
+
+void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st) {
+  const long long nv = (long long)(G.nl + 1) * G.plane;
+  if (nv == 0) return;
+  long long nb = (nv + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  vertex_coef_kernel<<<(int)nb, 256, 0, st>>>(G, b, k1, k2, k3, ev);
+  STS_CUDA(cudaGetLastError());
+}
+
 // ============================================================================
 // isotropic 7-point kernel (ncomp components)
 // ============================================================================
@@ -470,47 +751,292 @@ __global__ void __launch_bounds__(NT, 4) iso_kernel(StencilCall c, int ic, unsig
 }
 
 // ============================================================================
+// isotropic 7-point kernel, fast path (F / RKL2 stages / PCG A p), ncomp <= 3
+// ----------------------------------------------------------------------------
+// CTA = 8 x 32 (theta x phi) cell columns marching along r.  The u planes (all
+// components) and the theta / phi face diffusivities are staged in shared memory
+// with cp.async TWO planes ahead (3-slot ring), so the up-neighbour plane is
+// resident when a plane is processed and its successor is in flight; the r-face
+// diffusivity and w of the own column are register-prefetched one plane ahead.
+// ============================================================================
+constexpr int IRC = RC;   // (TJ+2) x (TK+2) staged region per field
+
+template <int NC>
+struct IsoSmem {
+  static constexpr int NF = NC + 2;                       // u comps + k2 + k3
+  static constexpr size_t bytes = (size_t)3 * NF * IRC * sizeof(double);
+};
+
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+template <int EPI, int NC>
+__global__ void __launch_bounds__(NT, (NC >= 3 ? 2 : 3)) iso_fast_kernel(StencilCall c, int ic) {
+  constexpr int NF = NC + 2;
+  extern __shared__ double sm[];
+  const Geo& G = c.geo;
+  const Metrics& M = G.m;
+  const int tid = threadIdx.x;
+  const int tk = tid % TK, tj = tid / TK;
+  const int j0 = blockIdx.y * TJ, k0 = blockIdx.x * TK;
+  const int ib = c.ib + blockIdx.z * ic;
+  const int ie = min(ib + ic, c.ie);
+  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  bool skip[NC];
+  bool all = true;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    skip[q] = (EPI == EPI_PCG_AP) && c.ea.sc && c.ea.sc[q].done;
+    all = all && skip[q];
+  }
+  if (EPI == EPI_PCG_AP && all) return;
+
+  // staging assignments (fixed)
+  int soff[2];
+  bool sok[2], shas[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = tid + q * NT;
+    shas[q] = e < IRC;
+    const int row = e / RK, col = e - (e / RK) * RK;
+    const int j = j0 - 1 + row;
+    int k = k0 - 1 + col;
+    bool ok = shas[q] && j >= 0 && j < G.n2;
+    if (G.periodic3) k = wrapk(k, G.n3);
+    else ok = ok && k >= 0 && k < G.n3;
+    sok[q] = ok;
+    soff[q] = ok ? j * G.n3 + k : 0;
+  }
+  auto slot_ptr = [&](int plane, int f) { return sm + ((plane % 3 + 3) % 3 * NF + f) * IRC; };
+  auto stage = [&](int il) {   // plane il in [-1, nl] (absent planes -> zeros)
+    const double* src[NF];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) src[q] = plane_ptr(c.u, G, il, q);
+    src[NC] = plane_ptr(c.k2, G, il, 0);
+    src[NC + 1] = plane_ptr(c.k3, G, il, 0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (!shas[q]) continue;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const bool ok = sok[q] && src[f] != nullptr;
+        cp_async8(slot_ptr(il, f) + tid + q * NT, ok ? src[f] + soff[q] : c.k1.p, ok);
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int j = j0 + tj, k = k0 + tk;
+  const bool own = (j < G.n2) && (k < G.n3);
+  const long long coff = own ? (long long)j * G.n3 + k : 0;
+  const bool jm = j >= 1, jp = j + 1 < G.n2;
+  const bool kself = G.periodic3 && G.n3 == 1;
+  const bool km = !kself && (G.periodic3 || k >= 1), kp = !kself && (G.periodic3 || k + 1 < G.n3);
+  const int kmw = G.periodic3 ? wrapk(k - 1, G.n3) : k - 1;
+  double f1tp = 0, f2p = 0, f2m = 0, f3p = 0, f3m = 0, vtp = 0;
+  if (own) {
+    f1tp = M.F1t[j] * M.F1p[k];
+    f2p = jp ? M.F2t[j] * M.F2p[k] : 0.0;
+    f2m = jm ? M.F2t[j - 1] * M.F2p[k] : 0.0;
+    f3p = kp ? M.F3t[j] * M.F3p[k] : 0.0;
+    f3m = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
+    vtp = M.Vt[j] * M.Vp[k];
+  }
+  const int r0 = (tj + 1) * RK + tk + 1;   // own cell in the staged region
+
+  // prologue: stage planes ib, ib+1 (ib-1 only needed for the own-column u_dn)
+  stage(ib);
+  stage(ib + 1);
+  double udn[NC], uc[NC];
+  const int ig0 = G.i0 + ib;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double* pd = (own && ig0 >= 1) ? plane_ptr(c.u, G, ib - 1, q) : nullptr;
+    udn[q] = pd ? __ldg(pd + coff) : 0.0;
+  }
+  double kdn = 0.0;
+  if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
+  // register prefetch of the own column's r-face diffusivity and w (plane ib)
+  double k1n = (own && ig0 + 1 < G.n1g) ? __ldg(plane_ptr(c.k1, G, ib, 0) + coff) : 0.0;
+  double wn = (own && c.w) ? __ldg(c.w + (long long)ib * G.plane + coff) : 1.0;
+  double part[NC];
+  double ym2n[NC], y0n[NC], m0n[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    part[q] = 0.0;
+    ym2n[q] = y0n[q] = m0n[q] = 0.0;
+    if (EPI == EPI_RKL2_STAGE && own) {
+      const long long go = (long long)ib * G.plane + coff + (long long)q * G.cstride;
+      ym2n[q] = c.ea.ym2[go];
+      y0n[q] = c.ea.y0[go];
+      m0n[q] = c.ea.m0[go];
+    }
+  }
+  bool first = true;
+
+  for (int il = ib; il < ie; ++il) {
+    const int ig = G.i0 + il;
+    const bool ip = ig + 1 < G.n1g;
+    if (il + 2 <= ie) stage(il + 2);   // slot of plane il-1 (finished last step)
+    else cp_async_commit();            // keep the group count uniform
+    const double k1c = k1n, wc = wn;
+    if (own && il + 1 < ie) {          // prefetch next plane's column values
+      k1n = (ig + 2 < G.n1g) ? __ldg(plane_ptr(c.k1, G, il + 1, 0) + coff) : 0.0;
+      wn = c.w ? __ldg(c.w + (long long)(il + 1) * G.plane + coff) : 1.0;
+    }
+    // epilogue operands: use the ones prefetched last step, prefetch the next plane's
+    double ym2[NC], y0v[NC], m0v[NC];
+    const long long gi = (long long)il * G.plane + coff;
+    if constexpr (EPI == EPI_RKL2_STAGE) {
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        ym2[q] = ym2n[q];
+        y0v[q] = y0n[q];
+        m0v[q] = m0n[q];
+        if (own && il + 1 < ie) {
+          const long long go = gi + G.plane + (long long)q * G.cstride;
+          ym2n[q] = c.ea.ym2[go];
+          y0n[q] = c.ea.y0[go];
+          m0n[q] = c.ea.m0[go];
+        }
+      }
+    }
+    cp_async_wait_1();                 // planes il and il+1 have landed (own copies)
+    __syncthreads();                   // ... and everybody's
+    if (own) {
+      if (first) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q) uc[q] = slot_ptr(il, q)[r0];
+        first = false;
+      }
+      const double f23r = M.F2r[ig], f3r = M.F3r[ig];
+      const double* K2 = slot_ptr(il, NC);
+      const double* K3 = slot_ptr(il, NC + 1);
+      const double Kup = ip ? k1c * M.F1r[ig] * f1tp : 0.0;
+      const double Kjp = jp ? K2[r0] * f23r * f2p : 0.0;
+      const double Kjm = jm ? K2[r0 - RK] * f23r * f2m : 0.0;
+      const double Kkp = kp ? K3[r0] * f3r * f3p : 0.0;
+      const double Kkm = km ? K3[r0 - 1] * f3r * f3m : 0.0;
+      const double WV = wc * M.Vr[ig] * vtp;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        const double* U = slot_ptr(il, q);
+        const double uup = ip ? slot_ptr(il + 1, q)[r0] : 0.0;
+        const double u0 = uc[q];
+        const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (U[r0 - RK] - u0) +
+                          Kjp * (U[r0 + RK] - u0) + Kkm * (U[r0 - 1] - u0) + Kkp * (U[r0 + 1] - u0);
+        const long long go = gi + (long long)q * G.cstride;
+        if (!skip[q]) {
+          if constexpr (EPI == EPI_F) {
+            c.ea.out[go] = Lu / WV;
+          } else if constexpr (EPI == EPI_RKL2_FIRST) {
+            const double F = Lu / WV;
+            c.ea.out2[go] = F;
+            c.ea.out[go] = u0 + c.ea.c0 * F;
+          } else if constexpr (EPI == EPI_RKL2_STAGE) {
+            const double F = Lu / WV;
+            c.ea.out[go] = c.ea.mu * u0 + c.ea.nu * ym2[q] + c.ea.c2 * y0v[q] + c.ea.c0 * F + c.ea.c1 * m0v[q];
+          } else if constexpr (EPI == EPI_PCG_AP) {
+            const double y = WV * u0 - c.ea.dt * Lu;
+            c.ea.out[go] = y;
+            part[q] += u0 * y;
+          }
+        }
+        udn[q] = u0;
+        uc[q] = uup;
+      }
+      kdn = Kup;
+    }
+    __syncthreads();                   // slot of plane il is restaged next step
+  }
+  cp_async_wait_all();
+  if constexpr (EPI == EPI_PCG_AP) block_partials<NC>(part, c.ea.partials, c.ea.pstride, c.ea.pbase + blk);
+}
+
+// ============================================================================
 // launch plumbing
 // ============================================================================
-int stencil_blocks(const Geo& G, int ib, int ie, int* ic_out) {
-  const int nbx = (G.n3 + TK - 1) / TK, nby = (G.n2 + TJ - 1) / TJ;
+static bool use_fast(int mode, int epi) {
+  return mode == STS_MODE_ANISO &&
+         (epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_AP);
+}
+bool stencil_uses_vertex_coef(int mode, int epi) { return use_fast(mode, epi); }
+
+// grid of the kernel launch_stencil uses for (mode, epi) on local planes [ib, ie)
+static dim3 stencil_grid(int mode, int epi, const Geo& G, int ib, int ie, int* ic_out) {
+  const bool fast = use_fast(mode, epi);
+  const int tk = fast ? FOK : TK, tj = fast ? FOJ : TJ;
+  const int nbx = (G.n3 + tk - 1) / tk, nby = (G.n2 + tj - 1) / tj;
   const int np = ie - ib;
   if (np <= 0) {
     if (ic_out) *ic_out = 1;
-    return 0;
+    return dim3(0, 0, 0);
   }
-  // enough CTAs for ~4 waves of 148 SMs x 3 resident, but >= 8 planes per chunk
+  // ~4 waves of 148 SMs x 3 resident CTAs, but >= 8 planes per chunk (each chunk
+  // re-stages one extra plane)
   const long long tiles = (long long)nbx * nby;
   const long long want = 148LL * 3 * 4;
   int ic = (int)((np * tiles + want - 1) / want);
   ic = ic < 8 ? 8 : ic;
   if (ic > np) ic = np;
-  const int nbz = (np + ic - 1) / ic;
   if (ic_out) *ic_out = ic;
-  return nbx * nby * nbz;
+  return dim3(nbx, nby, (np + ic - 1) / ic);
+}
+
+int stencil_blocks(int mode, int epi, const Geo& G, int ib, int ie) {
+  const dim3 g = stencil_grid(mode, epi, G, ib, ie, nullptr);
+  return (int)(g.x * g.y * g.z);
+}
+
+template <int EPI, int NC>
+static void launch_iso_fast(const StencilCall& c, dim3 grid, int ic, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    STS_CUDA(cudaFuncSetAttribute(iso_fast_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)IsoSmem<NC>::bytes));
+    attr = true;
+  }
+  iso_fast_kernel<EPI, NC><<<grid, NT, IsoSmem<NC>::bytes, st>>>(c, ic);
 }
 
 template <int EPI>
 static void launch_epi(const StencilCall& c, cudaStream_t st, unsigned long long* dmax) {
   int ic = 1;
-  stencil_blocks(c.geo, c.ib, c.ie, &ic);
-  const int np = c.ie - c.ib;
-  if (np <= 0) return;
-  dim3 grid((c.geo.n3 + TK - 1) / TK, (c.geo.n2 + TJ - 1) / TJ, (np + ic - 1) / ic);
+  const dim3 grid = stencil_grid(c.mode, EPI, c.geo, c.ib, c.ie, &ic);
+  if (grid.x == 0) return;
   if (c.mode == STS_MODE_ANISO) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      STS_CUDA(cudaFuncSetAttribute(aniso_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)ANISO_SMEM));
-      attr_set = true;
+    if constexpr (EPI == EPI_F || EPI == EPI_RKL2_FIRST || EPI == EPI_RKL2_STAGE || EPI == EPI_PCG_AP) {
+      static bool attr_fast = false;
+      if (!attr_fast) {
+        STS_CUDA(cudaFuncSetAttribute(aniso_fast_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)FAST_SMEM));
+        attr_fast = true;
+      }
+      if (!c.ev) throw Error{STS_ERR_STATE, "vertex coefficients missing for the anisotropic fast path"};
+      aniso_fast_kernel<EPI><<<grid, FNT, FAST_SMEM, st>>>(c, ic);
+    } else {
+      static bool attr_set = false;
+      if (!attr_set) {
+        STS_CUDA(cudaFuncSetAttribute(aniso_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ANISO_SMEM));
+        attr_set = true;
+      }
+      aniso_kernel<EPI><<<grid, NT, ANISO_SMEM, st>>>(c, ic, dmax);
     }
-    aniso_kernel<EPI><<<grid, NT, ANISO_SMEM, st>>>(c, ic, dmax);
   } else {
-    switch (c.ncomp) {
-      case 1: iso_kernel<EPI, 1><<<grid, NT, 0, st>>>(c, ic, dmax); break;
-      case 2: iso_kernel<EPI, 2><<<grid, NT, 0, st>>>(c, ic, dmax); break;
-      case 3: iso_kernel<EPI, 3><<<grid, NT, 0, st>>>(c, ic, dmax); break;
-      default: throw Error{STS_ERR_ARG, "ncomp must be 1..3"};
+    if constexpr (EPI == EPI_F || EPI == EPI_RKL2_FIRST || EPI == EPI_RKL2_STAGE || EPI == EPI_PCG_AP) {
+      switch (c.ncomp) {
+        case 1: launch_iso_fast<EPI, 1>(c, grid, ic, st); break;
+        case 2: launch_iso_fast<EPI, 2>(c, grid, ic, st); break;
+        case 3: launch_iso_fast<EPI, 3>(c, grid, ic, st); break;
+        default: throw Error{STS_ERR_ARG, "ncomp must be 1..3"};
+      }
+    } else {
+      switch (c.ncomp) {
+        case 1: iso_kernel<EPI, 1><<<grid, NT, 0, st>>>(c, ic, dmax); break;
+        case 2: iso_kernel<EPI, 2><<<grid, NT, 0, st>>>(c, ic, dmax); break;
+        case 3: iso_kernel<EPI, 3><<<grid, NT, 0, st>>>(c, ic, dmax); break;
+        default: throw Error{STS_ERR_ARG, "ncomp must be 1..3"};
+      }
     }
   }
   STS_CUDA(cudaGetLastError());

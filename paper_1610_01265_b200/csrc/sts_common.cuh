@@ -183,15 +183,20 @@ struct StencilCall {
   Geo geo;
   FieldV u, k1, k2, k3, b;
   const double* w;             // [nl][plane] or nullptr
+  const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][plane]
   EpiArgs ea;
   int ib, ie;                  // local plane range [ib, ie)
 };
 
-// number of CTAs launch_stencil will use for a plane range (for partial buffers)
-int stencil_blocks(const Geo& geo, int ib, int ie, int* ic_out);
+// number of CTAs launch_stencil will use for (mode, epilogue) on a plane range
+// (sizes the per-CTA partial-sum buffers)
+int stencil_blocks(int mode, int epi, const Geo& geo, int ib, int ie);
 void launch_stencil(const StencilCall& c, cudaStream_t st);
 
 void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStream_t st);
+// e_a = sqrt(V_v kappa_v) b_{v,a} / (4 h_a) for vertex planes -1 .. nl-1 of a slab
+void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st);
+bool stencil_uses_vertex_coef(int mode, int epi);
 
 // pointwise / auxiliary kernels (aux.cu)
 void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double* k3, double kappa0,

@@ -25,7 +25,8 @@ UID_BYTES = 128
 # kernel classes of sts_grid_timing (include/sts_b200.h STS_K_*)
 KERNEL_CLASSES = ["face_kappa", "aniso_F", "aniso_rkl2_first", "aniso_rkl2_stage", "aniso_pcg_r0",
                   "aniso_pcg_ap", "aniso_gersh", "iso_F", "iso_rkl2_first", "iso_rkl2_stage", "iso_pcg_r0",
-                  "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo"]
+                  "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo",
+                  "vertex_coef"]
 
 _lib = None
 
