@@ -51,9 +51,10 @@ def stall_reasons(path, top=6):
     vals = rows[2]
     st = []
     for i, h in enumerate(hdr):
-        if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio"):
+        if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
             try:
-                st.append((float(vals[i].replace(",", "")), h.split("stalled_")[1].replace(".ratio", "")))
+                st.append((float(vals[i].replace(",", "")),
+                           h.split("stalled_")[1].replace("_per_issue_active.ratio", "")))
             except ValueError:
                 pass
     return [f"{n}:{v:.2f}" for v, n in sorted(st, reverse=True)[:top]]
@@ -70,9 +71,8 @@ def main(paths):
             try:
                 rd = float(g("dram_read").replace(",", ""))
                 wr = float(g("dram_write").replace(",", ""))
-                unit = d["dram_read"][1]
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-                tot = (rd + wr) * scale
+                sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                tot = rd * sc.get(d["dram_read"][1], 1) + wr * sc.get(d["dram_write"][1], 1)
             except Exception:
                 tot = float("nan")
             st = stall_reasons(p)
