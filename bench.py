@@ -58,50 +58,61 @@ def peaks():
 # algorithmic HBM bytes per cell for each kernel class: every
 # field read or written exactly once, FP64
 # ----------------------------------------------------------------------------
-def bytes_per_cell(kind, ncomp=1, active=None):
+def bytes_per_cell(kind, ncomp=1, active=None, first=False):
     c = ncomp if active is None else active
     table = {
         "face_kappa": 8 + 24,
-        # fast anisotropic path streams u + the 3 frozen vertex coefficients e
+        # anisotropic passes stream u + the 3 frozen vertex coefficients e
         "vertex_coef": 48 + 24,
         "aniso_F": 8 + 24 + 8,
         "aniso_rkl2_first": 8 + 24 + 16,
         "aniso_rkl2_stage": 8 + 24 + 24 + 8,
         "aniso_pcg_r0": 8 + 48 + 32,
         "aniso_pcg_ap": 8 + 24 + 8,
+        # fused S-pass: z, pold, x, e in; p, y, x out (first iteration: z, e in; p, y out)
+        "aniso_pcg_s": (8 + 24 + 16) if first else (24 + 24 + 24),
         "aniso_gersh": 48,
         "iso_rkl2_first": 8 * c + 32 + 16 * c,
         "iso_rkl2_stage": 32 * c + 32 + 8 * c,
         "iso_pcg_r0": 8 * c + 32 + 24 * c + 8,
         "iso_pcg_ap": 16 * c + 32,
         "iso_gersh": 32,
-        "pcg_update": 48 * c + 8,
-        "pcg_pupdate": 24 * c + 8,
+        # U-pass: r, y, d in; r, z out
+        "pcg_update": 32 * c + 8,
+        # p pass of the unfused S-pass: z, pold, x in; p, x out (first: z in, p out)
+        "pcg_pupdate": 16 * c if first else 40 * c,
+        "pcg_xfinal": 24 * c,
     }
     return table[kind]
 
 
-def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v):
+def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True):
     """Total algorithmic bytes per class for one step on `ncells` local cells."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
-        _cond_bytes(add, s_c, it_c)
+        _cond_bytes(add, s_c, it_c, fused_c)
     if s_v:
         _visc_bytes(add, s_v, it_v)
     return B
 
 
-def _cond_bytes(add, s_c, it_c):
+def _cond_bytes(add, s_c, it_c, fused):
     add("face_kappa", bytes_per_cell("face_kappa"))
     add("vertex_coef", 2 * bytes_per_cell("vertex_coef"))   # once per RKL2 advance and per PCG solve
     add("aniso_gersh", bytes_per_cell("aniso_gersh"))
     add("aniso_rkl2_first", bytes_per_cell("aniso_rkl2_first"))
     add("aniso_rkl2_stage", (s_c - 1) * bytes_per_cell("aniso_rkl2_stage"))
     add("aniso_pcg_r0", bytes_per_cell("aniso_pcg_r0"))
-    add("aniso_pcg_ap", it_c * bytes_per_cell("aniso_pcg_ap"))
-    add("pcg_update", it_c * bytes_per_cell("pcg_update", 1))
-    add("pcg_pupdate", max(it_c - 1, 0) * bytes_per_cell("pcg_pupdate", 1))
+    for k in range(1, it_c + 1):
+        if fused:
+            add("aniso_pcg_s", bytes_per_cell("aniso_pcg_s", first=k == 1))
+        else:
+            add("pcg_pupdate", bytes_per_cell("pcg_pupdate", 1, first=k == 1))
+            add("aniso_pcg_ap", bytes_per_cell("aniso_pcg_ap"))
+        add("pcg_update", bytes_per_cell("pcg_update", 1))
+    if it_c:
+        add("pcg_xfinal", bytes_per_cell("pcg_xfinal", 1))
 
 
 def _visc_bytes(add, s_v, it_v):
@@ -111,11 +122,12 @@ def _visc_bytes(add, s_v, it_v):
     add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0", 3))
     for k in range(1, max(it_v) + 1):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
+        add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act, first=k == 1))
         add("iso_pcg_ap", bytes_per_cell("iso_pcg_ap", active=act))
         add("pcg_update", bytes_per_cell("pcg_update", active=act))
-        act_p = sum(1 for i in it_v if i > k)
-        if act_p:
-            add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act_p))
+    n_fin = sum(1 for i in it_v if i > 0)
+    if n_fin:
+        add("pcg_xfinal", bytes_per_cell("pcg_xfinal", active=n_fin))
 
 
 # ----------------------------------------------------------------------------
@@ -393,8 +405,10 @@ def main():
     # ---------------- roofline of the dominant kernel (rank 0's device timing)
     peak, peak_kind = peaks()
     Bytes = {}
+    fused_c = timing.get("aniso_pcg_s", (0, 0.0))[0] > 0
     for i in infos:
-        for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"]).items():
+        for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
+                                      fused_c).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
     kernels = {}
     for k, (n, kms) in timing.items():
@@ -416,7 +430,9 @@ def main():
         pass
     eff = [k for k in kernels if "achieved_gbs" in kernels[k]]
     launches_dom = infos[0]
-    n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"]}.get(dom)
+    n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
+             "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
+             "iso_pcg_ap": max(launches_dom["it_visc"])}.get(dom)
     bpl = (Bytes[dom] / len(infos) / n_eff) if n_eff else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,

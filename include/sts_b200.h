@@ -132,8 +132,18 @@ int sts_grid_kernel_launches(const sts_grid* g, long long* count);
 #define STS_K_PCG_REDUCE 15
 #define STS_K_HALO 16
 #define STS_K_VERTEX_COEF 17
-#define STS_K_NCLASSES 18
+#define STS_K_ANISO_PCG_S 18     /* fused PCG S-pass (p update + x update + A p), TMA path   */
+#define STS_K_PCG_XFINAL 19      /* final deferred x += alpha p after convergence            */
+#define STS_K_NCLASSES 20
 int sts_grid_set_timing(sts_grid* g, int enable);
+
+/*
+ * Kernel-path selection (testing / A-B measurement): enable != 0 (the default)
+ * lets the anisotropic RKL2 stages and PCG S-passes use the TMA + mbarrier
+ * pipelined kernels where eligible (n3 even, 16 B aligned arrays); 0 forces the
+ * cp.async kernels everywhere.  Results agree to rounding either way.
+ */
+int sts_grid_set_tma(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
 

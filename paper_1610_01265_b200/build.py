@@ -5,7 +5,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", f) for f in ("stencil.cu", "aux.cu", "capi.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("stencil.cu", "stencil_tma.cu", "aux.cu", "capi.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "sts_common.cuh"), os.path.join(ROOT, "include", "sts_b200.h")]
 OUT = os.path.join(HERE, "libsts_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

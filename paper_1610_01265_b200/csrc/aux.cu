@@ -143,6 +143,143 @@ __global__ void __launch_bounds__(256) pcg_pupdate_kernel(long long n, long long
   }
 }
 
+// ---- restructured iteration (DESIGN.md §5 "PCG passes"): the x update of Fig. 1
+// is deferred to the next p pass, so one iteration is
+//   S-pass (stencil): p_k = z_k + beta p_{k-1};  x += alpha_{k-1} p_{k-1};  y = A p_k;  p_k.y
+//   U-pass (pointwise): r -= alpha_k y;  z = r d;  r.z
+// and one final x += alpha p after convergence.  The kernels below are the
+// pointwise pieces (pcg_pnew is the S-pass's pointwise half when the stencil
+// has no fused variant).
+template <int NC>
+__global__ void __launch_bounds__(256) pcg_pnew_kernel(long long n, long long cs, double* __restrict__ pnew,
+                                                       const double* __restrict__ z, const double* __restrict__ pold,
+                                                       double* __restrict__ x, const PcgScal* __restrict__ sc,
+                                                       int first) {
+  double beta[NC], ax[NC];
+  bool act[NC];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    act[q] = !sc[q].done;
+    beta[q] = first ? 0.0 : sc[q].beta;
+    ax[q] = first ? 0.0 : sc[q].ax;
+    any = any || act[q];
+  }
+  if (!any) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      if (!act[q]) continue;
+      const long long o = e + q * cs;
+      if (first) {
+        pnew[o] = z[o];
+      } else {
+        const double po = pold[o];
+        pnew[o] = fma(beta[q], po, z[o]);
+        x[o] = fma(ax[q], po, x[o]);
+      }
+    }
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long cs, double* __restrict__ r,
+                                                          double* __restrict__ z, const double* __restrict__ y,
+                                                          const double* __restrict__ d, const PcgScal* __restrict__ sc,
+                                                          double* __restrict__ partials, long long pstride) {
+  double alpha[NC];
+  bool act[NC];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    act[q] = !sc[q].done;
+    alpha[q] = sc[q].alpha;
+    any = any || act[q];
+  }
+  if (!any) return;
+  double acc[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const double de = d[e];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      if (!act[q]) continue;
+      const long long o = e + q * cs;
+      const double rn = r[o] - alpha[q] * y[o];
+      const double zn = rn * de;
+      r[o] = rn;
+      z[o] = zn;
+      acc[q] += rn * zn;
+    }
+  }
+  __shared__ double red[NC][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum_d(acc[q]);
+    if (lane == 0) red[q][wid] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NC) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
+    partials[threadIdx.x * pstride + blockIdx.x] = s;
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long cs, double* __restrict__ x,
+                                                         const double* __restrict__ p0, const double* __restrict__ p1,
+                                                         const PcgScal* __restrict__ sc) {
+  double ax[NC];
+  const double* pp[NC];
+  bool act[NC];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    act[q] = sc[q].iters > 0;
+    ax[q] = sc[q].ax;
+    pp[q] = (sc[q].iters & 1) ? p1 : p0;
+    any = any || act[q];
+  }
+  if (!any) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      if (!act[q]) continue;
+      const long long o = e + q * cs;
+      x[o] = fma(ax[q], pp[q][o], x[o]);
+    }
+  }
+}
+
+#define STS_NC_SWITCH(ncomp, KER, ...)                                                  \
+  switch (ncomp) {                                                                   \
+    case 1: KER<1><<<PW_BLOCKS, 256, 0, st>>>(__VA_ARGS__); break;                   \
+    case 2: KER<2><<<PW_BLOCKS, 256, 0, st>>>(__VA_ARGS__); break;                   \
+    case 3: KER<3><<<PW_BLOCKS, 256, 0, st>>>(__VA_ARGS__); break;                   \
+    default: throw Error{STS_ERR_ARG, "ncomp"};                                      \
+  }
+
+void launch_pcg_pnew(int ncomp, long long n, long long cs, double* pnew, const double* z, const double* pold,
+                     double* x, const PcgScal* sc, int first, cudaStream_t st) {
+  STS_NC_SWITCH(ncomp, pcg_pnew_kernel, n, cs, pnew, z, pold, x, sc, first);
+  STS_CUDA(cudaGetLastError());
+}
+
+void launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* z, const double* y, const double* d,
+                        const PcgScal* sc, double* partials, long long pstride, cudaStream_t st) {
+  STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride);
+  STS_CUDA(cudaGetLastError());
+}
+
+void launch_pcg_xfinal(int ncomp, long long n, long long cs, double* x, const double* p0, const double* p1,
+                       const PcgScal* sc, cudaStream_t st) {
+  STS_NC_SWITCH(ncomp, pcg_xfinal_kernel, n, cs, x, p0, p1, sc);
+  STS_CUDA(cudaGetLastError());
+}
+
 void launch_pcg_update(int ncomp, long long n, long long cs, double* x, double* r, const double* p,
                        const double* y, const double* d, const PcgScal* sc, double* partials,
                        long long pstride, cudaStream_t st) {
@@ -175,6 +312,7 @@ __device__ void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal*
     s.iters = 0;
     s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
     s.beta = 0.0;
+    s.ax = 0.0;
   } else if (phase == PH_AP) {
     if (s.done) return;
     s.pAp = sums[c * nq];
@@ -184,6 +322,7 @@ __device__ void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal*
     s.rz_old = s.rz;
     s.rz = sums[c * nq];                   // r_r = r_{k+1} . z_{k+1}
     s.iters += 1;
+    s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k, applied by the next p pass / final pass
     if (s.rz <= s.thresh) s.done = 1;      // check r_r for convergence
     else s.beta = s.rz / s.rz_old;         // beta_k = r_r / r_old
   }

@@ -152,16 +152,15 @@ static void ensure_halos(sts_grid* g) {
     if (!s.halo_lo.empty()) continue;
     s.halo_lo.assign(H_NSLOTS, nullptr);
     s.halo_hi.assign(H_NSLOTS, nullptr);
-    const size_t bytes = (size_t)MAXC * g->plane * sizeof(double);
+    if (!s.has_lo && !s.has_hi) continue;
+    const size_t side = (size_t)MAXC * g->plane;
     for (int h = 0; h < H_NSLOTS; ++h) {
-      if (s.has_lo) {
-        STS_CUDA(cudaMalloc(&s.halo_lo[h], bytes));
-        g->halo_bytes += bytes;
-      }
-      if (s.has_hi) {
-        STS_CUDA(cudaMalloc(&s.halo_hi[h], bytes));
-        g->halo_bytes += bytes;
-      }
+      double* base = nullptr;
+      STS_CUDA(cudaMalloc(&base, 2 * side * sizeof(double)));
+      STS_CUDA(cudaMemset(base, 0, 2 * side * sizeof(double)));
+      g->halo_bytes += 2 * side * sizeof(double);
+      s.halo_lo[h] = base;          // freed through halo_lo
+      s.halo_hi[h] = base + side;
     }
   }
 }
@@ -232,7 +231,7 @@ struct Stage {
     if (p && !is_device_ptr(p)) {
       in.push_back({p, count});
       in_dst.push_back(const_cast<double**>(&p));
-      total += count;
+      total += (count + 31) / 32 * 32;
       any_host = true;
     }
   }
@@ -241,7 +240,7 @@ struct Stage {
     if (p && !is_device_ptr(p)) {
       out.push_back({p, count});
       out_dev.push_back(&p);
-      total += count;
+      total += (count + 31) / 32 * 32;
       any_host = true;
     }
     (void)alias_in;
@@ -254,12 +253,12 @@ struct Stage {
       double* d = base + off;
       STS_CUDA(cudaMemcpyAsync(d, in[i].first, in[i].second * sizeof(double), cudaMemcpyHostToDevice, st));
       *in_dst[i] = d;
-      off += in[i].second;
+      off += (in[i].second + 31) / 32 * 32;
     }
     for (size_t i = 0; i < out.size(); ++i) {
       double* d = base + off;
       *out_dev[i] = d;
-      off += out[i].second;
+      off += (out[i].second + 31) / 32 * 32;
     }
   }
   void end(const std::vector<double*>& dev_out) {
@@ -306,10 +305,13 @@ static StencilCall make_call(sts_grid* g, const Slab& s, int mode, int ncomp, in
   return c;
 }
 
+// workspace carving unit: every scratch field starts on a 256 B boundary (TMA needs 16 B)
+static size_t rnd(size_t n) { return (n + 31) / 32 * 32; }
+
 static size_t vertex_coef_doubles(const sts_grid* g, int mode) {
   if (mode != STS_MODE_ANISO) return 0;
   size_t n = 0;
-  for (auto& s : g->slabs) n += (size_t)3 * (s.nl + 1) * g->plane;
+  for (auto& s : g->slabs) n += rnd(3 * (size_t)ev_cstride(s.nl, g->n2, g->n3));
   return n;
 }
 
@@ -326,9 +328,18 @@ static std::vector<const double*> build_vertex_coefs(sts_grid* g, int mode, doub
     Timed t(g, STS_K_VERTEX_COEF, st);
     launch_vertex_coef(slab_geo(g, s), view(g, s, H_B, b), view(g, s, H_K1, k1), view(g, s, H_K2, k2),
                        view(g, s, H_K3, k3), base + o, st);
-    o += (size_t)3 * (s.nl + 1) * g->plane;
+    o += rnd(3 * (size_t)ev_cstride(s.nl, g->n2, g->n3));
   }
   return out;
+}
+
+// one stencil pass: the TMA pipelined kernel where eligible, else the cp.async kernels
+static void launch_pass(sts_grid* g, const StencilCall& c, cudaStream_t st) {
+  const int kind = (c.epi == EPI_PCG_S) ? STS_K_ANISO_PCG_S : stencil_kind(c.mode, c.epi);
+  Timed t(g, kind, st);
+  if (g->tma && launch_aniso_tma(c, st)) return;
+  if (c.epi == EPI_PCG_S) throw Error{STS_ERR_STATE, "fused PCG S-pass launched without a TMA-eligible call"};
+  launch_stencil(c, st);
 }
 
 static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
@@ -518,8 +529,7 @@ int sts_grid_destroy(sts_grid* g) {
     cudaGetDevice(&prev);
     cudaSetDevice(g->device);
     for (auto& s : g->slabs) {
-      for (auto* p : s.halo_lo) if (p) cudaFree(p);
-      for (auto* p : s.halo_hi) if (p) cudaFree(p);
+      for (auto* p : s.halo_lo) if (p) cudaFree(p);   // halo_hi points into the same allocation
     }
     if (g->comm) ncclCommDestroy(g->comm);
     if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
@@ -558,6 +568,13 @@ int sts_grid_set_timing(sts_grid* g, int enable) {
   return guard([&] {
     STS_REQUIRE(g, "NULL grid");
     g->timing = enable != 0;
+  });
+}
+
+int sts_grid_set_tma(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->tma = enable != 0;
   });
 }
 
@@ -664,7 +681,7 @@ int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out,
     sg.input(w, N);
     sg.output(out, N * ncomp);
     const size_t evn = vertex_coef_doubles(g, mode);
-    double* base = ws_get(g, (sg.total + evn) * sizeof(double));
+    double* base = ws_get(g, (rnd(sg.total) + evn) * sizeof(double));
     if (sg.any_host) sg.begin(base + evn);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
     const auto ev = build_vertex_coefs(g, mode, base, k1, k2, k3, b, st);
@@ -674,8 +691,7 @@ int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out,
       StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
       c.ev = ev[si];
       c.ea.out = off(out, s);
-      Timed t(g, stencil_kind(c.mode, c.epi), st);
-      launch_stencil(c, st);
+      launch_pass(g, c, st);
     }
     sg.end({out});
   });
@@ -753,15 +769,16 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
     // because Y0 is only read pointwise after stage 1
     sg.output(u1, NF);
     const size_t evn = vertex_coef_doubles(g, mode);
-    double* base = ws_get(g, (sg.total + 3 * NF + evn) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 3 * NF + evn);
+    const size_t NFr = rnd(NF);
+    double* base = ws_get(g, (rnd(sg.total) + 3 * NFr + evn) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 3 * NFr + evn);
     double* M0 = base;
-    double* A = base + NF;
-    double* B = base + 2 * NF;
+    double* A = base + NFr;
+    double* B = base + 2 * NFr;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
     const Rkl2Coef co = rkl2_coefs(s);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, base + 3 * NF, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, base + 3 * NFr, k1, k2, k3, b, st);
     // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
     exchange(g, H_U, u0, ncomp, st);
     for (size_t si = 0; si < g->slabs.size(); ++si) {
@@ -771,8 +788,7 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
       c.ea.out = off(A, sl);
       c.ea.out2 = off(M0, sl);
       c.ea.c0 = co.mut[1] * dt;
-      Timed t(g, stencil_kind(c.mode, c.epi), st);
-      launch_stencil(c, st);
+      launch_pass(g, c, st);
     }
     // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
     const double* prev = u0;
@@ -796,8 +812,7 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
         c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
         c.ea.c0 = co.mut[j] * dt;
         c.ea.c1 = co.gt[j] * dt;
-        Timed t(g, stencil_kind(c.mode, c.epi), st);
-        launch_stencil(c, st);
+        launch_pass(g, c, st);
       }
       prev = cur;
       cur = dst;
@@ -831,29 +846,47 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     sg.input(w, N);
     sg.output(un1, NF);
     const size_t evn = vertex_coef_doubles(g, mode);
-    double* base = ws_get(g, (sg.total + 3 * NF + N + evn) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 3 * NF + N + evn);
-    double* evbase = base + 3 * NF + N;
+    const size_t NFr = rnd(NF), Nr = rnd(N);
+    // scratch: r, z, y, p0, p1 [ncomp][nl][plane]; d [nl][plane]; vertex coefficients
+    double* base = ws_get(g, (5 * NFr + Nr + evn + rnd(sg.total)) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 5 * NFr + Nr + evn);
     double* r = base;
-    double* p = base + NF;
-    double* y = base + 2 * NF;
-    double* d = base + 3 * NF;
+    double* z = base + NFr;
+    double* y = base + 2 * NFr;
+    double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
+    double* d = base + 5 * NFr;
+    double* evbase = base + 5 * NFr + Nr;
     double* x = un1;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
-    // reduction storage
-    int sb_r0 = 0, sb_ap = 0;
-    for (auto& sl : g->slabs) {
-      sb_r0 += stencil_blocks(mode, EPI_PCG_R0, slab_geo(g, sl), 0, sl.nl);
-      sb_ap += stencil_blocks(mode, EPI_PCG_AP, slab_geo(g, sl), 0, sl.nl);
+    const double rtol2 = rtol * rtol;
+    const long long cs = (long long)g->nl * g->plane;
+
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, evbase, k1, k2, k3, b, st);
+    // the S-pass (p update + x update + A p) is ONE fused TMA kernel where eligible
+    bool fused = false;
+    if (g->tma && mode == STS_MODE_ANISO && ncomp == 1) {
+      StencilCall c = make_call(g, g->slabs[0], mode, 1, EPI_PCG_S, z, k1, k2, k3, bb, w);
+      c.u2 = view(g, g->slabs[0], H_P, pb[0]);
+      c.ev = ev[0];
+      c.ea.out = off(y, g->slabs[0]);
+      c.ea.out2 = off(pb[1], g->slabs[0]);
+      c.ea.x = off(x, g->slabs[0]);
+      fused = aniso_tma_eligible(c);
     }
-    const long long pstride = std::max(std::max(sb_r0, sb_ap), PW_BLOCKS);
+    // reduction storage (per-CTA partials of every pass)
+    int sb_r0 = 0, sb_s = 0;
+    for (auto& sl : g->slabs) {
+      const Geo G = slab_geo(g, sl);
+      sb_r0 += stencil_blocks(mode, EPI_PCG_R0, G, 0, sl.nl);
+      sb_s += fused ? aniso_tma_blocks(G, 0, sl.nl) : stencil_blocks(mode, EPI_PCG_AP, G, 0, sl.nl);
+    }
+    const long long pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
     const size_t red_doubles = (size_t)2 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
     ensure_red(g, red_doubles * sizeof(double));
     double* partials = g->d_red;
     double* sums = partials + 2 * ncomp * pstride;
     PcgScal* sc = reinterpret_cast<PcgScal*>(sums + 16);
-    const double rtol2 = rtol * rtol;
-    const long long cs = (long long)g->nl * g->plane;
 
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
@@ -867,28 +900,28 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       }
     };
 
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, evbase, k1, k2, k3, b, st);
-    // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; p = z0 = r0 d
+    // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
     exchange(g, H_U, un, ncomp, st);
     {
-      int pb = 0;
+      int pb0 = 0;
       for (auto& sl : g->slabs) {
         StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
         c.ea.out = off(r, sl);
         c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-        c.ea.out3 = off(p, sl);
+        c.ea.out3 = off(z, sl);
         c.ea.out4 = off(d, sl);
         c.ea.dt = dt;
         c.ea.partials = partials;
         c.ea.pstride = pstride;
-        c.ea.pbase = pb;
-        pb += stencil_blocks(mode, EPI_PCG_R0, c.geo, 0, sl.nl);
-        Timed t(g, stencil_kind(c.mode, c.epi), st);
-        launch_stencil(c, st);
+        c.ea.pbase = pb0;
+        pb0 += stencil_blocks(mode, EPI_PCG_R0, c.geo, 0, sl.nl);
+        launch_pass(g, c, st);
       }
       reduce(sb_r0, 2, PH_R0);
     }
+    // iteration k (Fig. 1 with the x update deferred one iteration):
+    //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
+    //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
     auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
     int launched = 0;
     int batch = 4;
@@ -901,39 +934,68 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       if (all_done || launched >= kmax) break;
       const int nb = std::min(batch, kmax - launched);
       for (int it = 0; it < nb; ++it) {
-        // y = A p, alpha = r.z / p.y
-        exchange(g, H_U, p, ncomp, st);
-        int pb = 0;
-        for (size_t si = 0; si < g->slabs.size(); ++si) {
-          const Slab& sl = g->slabs[si];
-          StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, p, k1, k2, k3, bb, w);
-          c.ev = ev[si];
-          c.ea.out = off(y, sl);
-          c.ea.dt = dt;
-          c.ea.partials = partials;
-          c.ea.pstride = pstride;
-          c.ea.pbase = pb;
-          c.ea.sc = sc;
-          pb += stencil_blocks(mode, EPI_PCG_AP, c.geo, 0, sl.nl);
-          Timed t(g, stencil_kind(c.mode, c.epi), st);
-          launch_stencil(c, st);
+        const int k = launched + it + 1;
+        const int first = (k == 1);
+        double* pold = pb[(k - 1) & 1];
+        double* pnew = pb[k & 1];
+        int pbs = 0;
+        if (fused) {
+          exchange(g, H_Z, z, ncomp, st);
+          if (!first) exchange(g, H_P, pold, ncomp, st);
+          for (size_t si = 0; si < g->slabs.size(); ++si) {
+            const Slab& sl = g->slabs[si];
+            StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
+            c.u = view(g, sl, H_Z, z);
+            c.u2 = first ? FieldV{} : view(g, sl, H_P, pold);
+            c.ev = ev[si];
+            c.ea.out = off(y, sl);
+            c.ea.out2 = off(pnew, sl);
+            c.ea.x = off(x, sl);
+            c.ea.first = first;
+            c.ea.dt = dt;
+            c.ea.partials = partials;
+            c.ea.pstride = pstride;
+            c.ea.pbase = pbs;
+            c.ea.sc = sc;
+            pbs += aniso_tma_blocks(c.geo, 0, sl.nl);
+            launch_pass(g, c, st);
+          }
+        } else {
+          {
+            Timed t(g, STS_K_PCG_PUPDATE, st);
+            launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, first, st);
+          }
+          exchange(g, H_U, pnew, ncomp, st);
+          for (size_t si = 0; si < g->slabs.size(); ++si) {
+            const Slab& sl = g->slabs[si];
+            StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, pnew, k1, k2, k3, bb, w);
+            c.ev = ev[si];
+            c.ea.out = off(y, sl);
+            c.ea.dt = dt;
+            c.ea.partials = partials;
+            c.ea.pstride = pstride;
+            c.ea.pbase = pbs;
+            c.ea.sc = sc;
+            pbs += stencil_blocks(mode, EPI_PCG_AP, c.geo, 0, sl.nl);
+            launch_pass(g, c, st);
+          }
         }
-        reduce(sb_ap, 1, PH_AP);
-        // x += alpha p, r -= alpha y, z = r d, r.z -> beta
+        reduce(sb_s, 1, PH_AP);
         {
           Timed t(g, STS_K_PCG_UPDATE, st);
-          launch_pcg_update(ncomp, (long long)N, cs, x, r, p, y, d, sc, partials, pstride, st);
+          launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride, st);
         }
         reduce(PW_BLOCKS, 1, PH_RZ);
-        // p = z + beta p
-        {
-          Timed t(g, STS_K_PCG_PUPDATE, st);
-          launch_pcg_pupdate(ncomp, (long long)N, cs, p, r, d, sc, st);
-        }
       }
       launched += nb;
       batch = std::min(batch * 2, 64);
     }
+    {
+      Timed t(g, STS_K_PCG_XFINAL, st);
+      launch_pcg_xfinal(ncomp, (long long)N, cs, x, pb[0], pb[1], sc, st);
+    }
+    STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, st));
+    STS_CUDA(cudaStreamSynchronize(st));
     if (iters_out)
       for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;
     sg.end({un1});

@@ -352,20 +352,24 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // e for every vertex plane il = -1 .. nl-1 of a slab (vertex between cell planes
-// il and il+1): ev[a][(il+1)*plane + jv*n3 + kv], zero where the vertex has a
-// missing cell.  One thread per vertex; b / kappa gathered through L1/L2.
+// il and il+1), in the padded layout of ev_row/ev_plane (sts_common.cuh): column
+// kv+1 holds vertex kv, column 0 the periodic wrap copy of kv = n3-1, zero where
+// the vertex has a missing cell.  One thread per padded entry; b / kappa gathered
+// through L1/L2.
 __global__ void __launch_bounds__(256) vertex_coef_kernel(Geo G, FieldV b, FieldV k1, FieldV k2, FieldV k3,
                                                           double* __restrict__ ev) {
   const Metrics& M = G.m;
-  const long long nv = (long long)(G.nl + 1) * G.plane;
+  const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3);
+  const long long nv = (long long)(G.nl + 1) * pp;
   const long long es = nv;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nv; e += (long long)gridDim.x * blockDim.x) {
-    const int il = (int)(e / G.plane) - 1;
-    const long long rem = e - (long long)(il + 1) * G.plane;
-    const int jv = (int)(rem / G.n3);
-    const int kv = (int)(rem - (long long)jv * G.n3);
+    const int il = (int)(e / pp) - 1;
+    const long long rem = e - (long long)(il + 1) * pp;
+    const int jv = (int)(rem / row);
+    int kv = (int)(rem - (long long)jv * row) - 1;
+    if (kv == -1 && G.periodic3) kv = G.n3 - 1;
     const int iv = G.i0 + il;
-    bool ok = iv >= 0 && iv + 1 < G.n1g && jv + 1 < G.n2 && (G.periodic3 || kv + 1 < G.n3);
+    bool ok = kv >= 0 && kv < G.n3 && iv >= 0 && iv + 1 < G.n1g && jv + 1 < G.n2 && (G.periodic3 || kv + 1 < G.n3);
     double er = 0.0, et = 0.0, ep = 0.0;
     if (ok) {
       const int kv1 = (kv + 1 < G.n3) ? kv + 1 : 0;
@@ -450,8 +454,9 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
   if (G.periodic3) kv = wrapk(kv, G.n3);
   else vok = vok && kv >= 0 && kv + 1 < G.n3;
   const double ig3a = vok ? M.iG3[jv] : 0.0, ig3b = vok ? M.iG3[jv + 1] : 0.0;
-  const long long eoff = vok ? (long long)jv * G.n3 + kv : 0;
-  const long long es = (long long)(G.nl + 1) * G.plane;
+  const long long eoff = vok ? (long long)jv * ev_row(G.n3) + kv + 1 : 0;
+  const long long epp = ev_plane(G.n2, G.n3);
+  const long long es = (long long)(G.nl + 1) * epp;
   const int j = j0 + vj, k = k0 + vk;
   const bool own = vj < FOJ && vk < FOK && j < G.n2 && k < G.n3;
   const long long coff = own ? (long long)j * G.n3 + k : 0;
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
     const int iv = G.i0 + il;
     er = et = ep = 0.0;
     if (vok && iv >= 0 && iv + 1 < G.n1g && il < ie) {
-      const long long o = (long long)(il + 1) * G.plane + eoff;
+      const long long o = (long long)(il + 1) * epp + eoff;
       er = __ldg(c.ev + o);
       et = __ldg(c.ev + es + o);
       ep = __ldg(c.ev + 2 * es + o);
@@ -590,7 +595,7 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
 }
 
 void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st) {
-  const long long nv = (long long)(G.nl + 1) * G.plane;
+  const long long nv = (long long)(G.nl + 1) * ev_plane(G.n2, G.n3);
   if (nv == 0) return;
   long long nb = (nv + 255) / 256;
   if (nb > 148 * 16) nb = 148 * 16;

@@ -1,0 +1,437 @@
+// TMA + mbarrier pipelined anisotropic stencil pass (sm_100a).
+//
+// Same arithmetic as aniso_fast_kernel (stencil.cu: vertex-centred symmetric
+// scheme of DESIGN.md R2 / PAPER.md:173 boxed term, with the frozen per-vertex
+// coefficients e of the lagged diffusivity), but every operand a CTA
+// needs for one r-plane -- the staged source plane(s) with their theta/phi halo,
+// the three vertex coefficients, and the pointwise epilogue operands -- arrives
+// as ONE "package" of cp.async.bulk.tensor (TMA) boxes completing on one
+// mbarrier.  A 3-slot ring keeps two packages in flight while the CTA computes
+// on the third, so the bytes in flight per SM no longer depend on registers or
+// on how far each thread can prefetch (the limit ncu showed for the cp.async
+// fast path: 27-29 % of DRAM peak, long-scoreboard bound).
+//
+// CTA = 8 warps x 32 lanes = 8 x 32 vertex columns -> 7 x 31 output cells.
+// Boxes per package Q(p) (cell plane p, global coordinates, OOB -> zeros):
+//   staged source f   : 34 cols x 9 rows  from (k0-1, j0-1)  of plane p
+//                       (p = -1 / nl: the library's halo planes of the neighbour slab)
+//   wrap columns      : 2 x 9 from (n3-2, j0-1) and (0, j0-1) (periodic phi, edge tiles only)
+//   vertex coeffs e   : 32 x 8 x 3 comps, vertex plane p-1 (padded e layout: no wrap)
+//   epilogue operands : 32 x 7 from (k0, j0), cell plane p-1
+// Epilogues: RKL2 first stage / stage recurrence (Fig. 2) and the fused
+// PCG S-pass  p = z + beta pold, x += ax pold, y = A p, partial p.y  (Fig. 1).
+#include <cudaTypedefs.h>
+
+#include "sts_common.cuh"
+
+namespace sts {
+
+namespace {
+
+constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= warps / lanes)
+constexpr int XOJ = XJ - 1, XOK = XK - 1;   // output rows / cols
+constexpr int XNT = XJ * XK;
+constexpr int XTS = 3;                      // ring slots (packages in flight = XTS - 1)
+constexpr int UBW = 34, UBH = 9;            // staged-source box (cols x rows)
+constexpr int MAXSRC = 2;                   // staged sources (PCG S-pass: z, pold)
+constexpr int MAXOWN = 4;                   // epilogue operand boxes
+// slot layout (doubles); every part starts on a 128 B boundary
+constexpr int U_MAIN = 320;                 // 9 x 34 = 306 -> 320
+constexpr int U_WL = 32, U_WR = 32;         // 9 x 2 = 18 -> 32
+constexpr int U_FIELD = U_MAIN + U_WL + U_WR;
+constexpr int E_PART = 3 * XJ * XK;         // 768
+constexpr int O_PART = XOJ * XK;            // 7 x 32 = 224
+constexpr int SLOT = MAXSRC * U_FIELD + E_PART + MAXOWN * O_PART;   // 2432 doubles = 19 KB
+constexpr int VBUF = 3 * XNT;               // A, B, C of one vertex plane
+constexpr size_t TMA_SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma4(double* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                     uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+// tensor maps of one launch (kernel parameter, __grid_constant__)
+struct TmaArgs {
+  CUtensorMap src[MAXSRC];    // staged sources, 3D (n3, n2, nl),       box 34 x 9 x 1
+  CUtensorMap srch[MAXSRC];   // their halo planes, 3D (n3, n2, 2 MAXC), box 34 x 9 x 1
+  CUtensorMap srcw[MAXSRC];   // wrap columns, main planes,             box 2 x 9 x 1
+  CUtensorMap srchw[MAXSRC];  // wrap columns, halo planes,             box 2 x 9 x 1
+  CUtensorMap e;              // vertex coefficients, 4D (n3+2, n2, nl+1, 3), box 32 x 8 x 1 x 3
+  CUtensorMap own[MAXOWN];    // epilogue operands, 3D (n3, n2, nl),   box 32 x 7 x 1
+  int nsrc, nown, has_lo, has_hi;
+};
+
+// epilogue operand slots
+enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
+enum { OW_X = 0 };                           // PCG S-pass
+template <int EPI>
+struct TmaEpi {
+  static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : 1;
+  static constexpr int nown = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : 0);   // + w if present
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic, const __grid_constant__ TmaArgs ta) {
+  extern __shared__ __align__(128) double smx[];
+  double* ring = smx;                               // [XTS][SLOT]
+  double* vbuf = smx + XTS * SLOT;                  // [2][3][XNT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vbuf + 2 * VBUF);
+  const Geo& G = c.geo;
+  const Metrics& M = G.m;
+  const int tid = threadIdx.x;
+  const int vj = tid >> 5, vk = tid & 31;
+  const int j0 = blockIdx.y * XOJ, k0 = blockIdx.x * XOK;
+  const int ib = c.ib + blockIdx.z * ic;
+  const int ie = min(ib + ic, c.ie);
+  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  constexpr int NSRC = TmaEpi<EPI>::nsrc;
+  const int nown = ta.nown;                         // TmaEpi::nown (+1 with w)
+  const int ow_w = nown - (c.w ? 1 : 0);            // slot of w if present
+
+  if constexpr (EPI == EPI_PCG_S) {
+    if (c.ea.sc && c.ea.sc[0].done) return;
+  }
+  const bool first = (EPI == EPI_PCG_S) && c.ea.first;
+  const double beta = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].beta : 0.0;
+  const double ax = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].ax : 0.0;
+  const bool per = G.periodic3 != 0;
+  const bool wrapL = per && k0 == 0;
+  const bool wrapR = per && (k0 + 32 >= G.n3);
+
+  // ---- producer: thread 0 issues package Q(p) ----
+  auto issue = [&](int p) {
+    const int slot = (p - ib + 1) % XTS;
+    double* S = ring + slot * SLOT;
+    uint64_t* bar = bars + slot;
+    const bool lo = p < 0, hi = p >= G.nl;
+    const bool halo = (lo && ta.has_lo) || (hi && ta.has_hi);
+    const int pc = halo ? (lo ? 0 : MAXC) : p;      // OOB plane (no neighbour) -> zeros
+    const int nsrc_now = (EPI == EPI_PCG_S && first) ? 1 : NSRC;
+    uint32_t bytes = nsrc_now * UBW * UBH * 8;
+    if (wrapL) bytes += nsrc_now * 2 * UBH * 8;
+    if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
+    const bool has_e = p >= ib, has_own = p >= ib + 1;
+    if (has_e) bytes += E_PART * 8;
+    if (has_own) bytes += nown * XOJ * XK * 8;
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    for (int f = 0; f < nsrc_now; ++f) {
+      double* D = S + f * U_FIELD;
+      tma3(D, halo ? &ta.srch[f] : &ta.src[f], k0 - 1, j0 - 1, pc, bar);
+      if (wrapL) tma3(D + U_MAIN, halo ? &ta.srchw[f] : &ta.srcw[f], G.n3 - 2, j0 - 1, pc, bar);
+      if (wrapR) tma3(D + U_MAIN + U_WL, halo ? &ta.srchw[f] : &ta.srcw[f], 0, j0 - 1, pc, bar);
+    }
+    if (has_e) tma4(S + MAXSRC * U_FIELD, &ta.e, k0, j0 - 1, p, 0, bar);   // vertex plane p-1 = ev index p
+    if (has_own)
+      for (int q = 0; q < nown; ++q) tma3(S + MAXSRC * U_FIELD + E_PART + q * O_PART, &ta.own[q], k0, j0, p - 1, bar);
+  };
+
+  // ---- per-thread geometry ----
+  const int jv = j0 - 1 + vj;                       // vertex row (jv + 1/2)
+  const double ig3a = (jv >= 0 && jv < G.n2) ? M.iG3[jv] : 0.0;
+  const double ig3b = (jv + 1 >= 0 && jv + 1 < G.n2) ? M.iG3[jv + 1] : 0.0;
+  const int j = j0 + vj, k = k0 + vk;
+  const bool own = vj < XOJ && vk < XOK && j < G.n2 && k < G.n3;
+  const long long coff = own ? (long long)j * G.n3 + k : 0;
+  const double ig3c = own ? M.iG3[j] : 0.0;
+  const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
+  // staged-box columns this thread reads: A = tile col vk (global k0-1+vk), B = vk+1 (global k0+vk)
+  int offA = vk, pitA = UBW, offB = vk + 1, pitB = UBW;
+  if (per) {
+    if (k0 - 1 + vk == -1) { offA = U_MAIN + 1; pitA = 2; }
+    if (k0 - 1 + vk == G.n3) { offA = U_MAIN + U_WL; pitA = 2; }
+    if (k0 + vk == G.n3) { offB = U_MAIN + U_WL; pitB = 2; }
+  }
+
+  // in-plane 2x2 box of the source value s = (PCG: z + beta pold, else u)
+  auto sval = [&](const double* S, int off, int pit, int row) {
+    const double v = S[off + row * pit];
+    if constexpr (EPI == EPI_PCG_S) {
+      if (!first) return fma(beta, S[U_FIELD + off + row * pit], v);
+    }
+    return v;
+  };
+  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu) {
+    const double u00 = sval(S, offA, pitA, vj), u01 = sval(S, offB, pitB, vj);
+    const double u10 = sval(S, offA, pitA, vj + 1), u11 = sval(S, offB, pitB, vj + 1);
+    Su = (u00 + u01) + (u10 + u11);
+    Tu = (u10 - u00) + (u11 - u01);
+    Fu = ig3a * (u01 - u00) + ig3b * (u11 - u10);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < XTS; ++s) mbar_init(bars + s, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int p = ib - 1; p <= ie && p < ib - 1 + XTS; ++p) issue(p);
+
+  double SuL = 0, TuL = 0, FuL = 0;
+  double SAl = 0, DBl = 0, DCl = 0;
+  double uc = 0.0, poc = 0.0;   // own-cell source value (and pold) of the previous plane
+  double part = 0.0;
+  for (int p = ib - 1; p <= ie; ++p) {
+    const int slot = (p - ib + 1) % XTS;
+    const double* S = ring + slot * SLOT;
+    mbar_wait(bars + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
+    double SuH, TuH, FuH;
+    usums(S, SuH, TuH, FuH);
+    const double un = sval(S, offB, pitB, vj + 1);                       // own cell of plane p
+    double pon = 0.0;
+    if constexpr (EPI == EPI_PCG_S) pon = first ? 0.0 : S[U_FIELD + offB + (vj + 1) * pitB];
+    double* vb = vbuf + (p & 1) * VBUF;
+    if (p >= ib) {
+      // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
+      const double* E = S + MAXSRC * U_FIELD;
+      const double er = E[tid], et = E[XNT + tid], ep = E[2 * XNT + tid];
+      const int iv = G.i0 + p - 1;
+      const double ig2l = (iv >= 0 && iv < G.n1g) ? M.iG2[iv] : 0.0;
+      const double ig2h = (iv + 1 >= 0 && iv + 1 < G.n1g) ? M.iG2[iv + 1] : 0.0;
+      const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
+      vb[tid] = q * er;
+      vb[XNT + tid] = q * et;
+      vb[2 * XNT + tid] = q * ep;
+    }
+    __syncthreads();   // vertex plane visible; every thread is done with slot of Q(p-1)
+    if (tid == 0 && p >= ib && p - 1 + XTS <= ie) issue(p - 1 + XTS);
+    if (p >= ib) {
+      double SAh = 0, DBh = 0, DCh = 0;
+      if (own) {
+        const double a00 = vb[tid], a01 = vb[tid + 1], a10 = vb[tid + 32], a11 = vb[tid + 33];
+        const double b00 = vb[XNT + tid], b01 = vb[XNT + tid + 1], b10 = vb[XNT + tid + 32], b11 = vb[XNT + tid + 33];
+        const double d00 = vb[2 * XNT + tid], d01 = vb[2 * XNT + tid + 1], d10 = vb[2 * XNT + tid + 32],
+                     d11 = vb[2 * XNT + tid + 33];
+        SAh = (a00 + a01) + (a10 + a11);
+        DBh = (b00 + b01) - (b10 + b11);
+        DCh = (d00 + d10) - (d01 + d11);
+      }
+      if (p >= ib + 1 && own) {
+        // output cell plane il = p-1
+        const int il = p - 1;
+        const int ig = G.i0 + il;
+        const double* O = S + MAXSRC * U_FIELD + E_PART + vj * XK + vk;
+        const double ig2c = M.iG2[ig];
+        const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
+        const double WV = (c.w ? O[ow_w * O_PART] : 1.0) * M.Vr[ig] * vtpc;
+        const long long gi = (long long)il * G.plane + coff;
+        if constexpr (EPI == EPI_F) {
+          c.ea.out[gi] = Lu / WV;
+        } else if constexpr (EPI == EPI_RKL2_FIRST) {
+          const double F = Lu / WV;
+          c.ea.out2[gi] = F;
+          c.ea.out[gi] = uc + c.ea.c0 * F;
+        } else if constexpr (EPI == EPI_RKL2_STAGE) {
+          const double F = Lu / WV;
+          c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_YM2 * O_PART] + c.ea.c2 * O[OW_Y0 * O_PART] + c.ea.c0 * F +
+                         c.ea.c1 * O[OW_M0 * O_PART];
+        } else if constexpr (EPI == EPI_PCG_S) {
+          const double y = WV * uc - c.ea.dt * Lu;
+          c.ea.out[gi] = y;
+          c.ea.out2[gi] = uc;                                   // p_k
+          if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);   // x_k = x_{k-1} + alpha_{k-1} p_{k-1}
+          part += uc * y;
+        }
+      }
+      SAl = SAh;
+      DBl = DBh;
+      DCl = DCh;
+    }
+    SuL = SuH;
+    TuL = TuH;
+    FuL = FuH;
+    uc = un;
+    poc = pon;
+  }
+  if constexpr (EPI == EPI_PCG_S) {
+    __shared__ double red[XNT / 32];
+    double v = part;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < XNT / 32; ++w) s += red[w];
+      c.ea.partials[c.ea.pbase + blk] = s;
+    }
+  }
+}
+
+// ============================================================================
+// host side
+// ============================================================================
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    STS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw Error{STS_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver"};
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static void encode(CUtensorMap* m, const double* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box) {
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error{STS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+}
+
+// plain [nplanes][n2][n3] field (component 0 at base)
+static void map_plain(CUtensorMap* m, const double* base, const Geo& G, int nplanes, int bw, int bh) {
+  const cuuint64_t dims[3] = {(cuuint64_t)G.n3, (cuuint64_t)G.n2, (cuuint64_t)nplanes};
+  const cuuint64_t str[2] = {(cuuint64_t)G.n3 * 8, (cuuint64_t)G.plane * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  encode(m, base, 3, dims, str, box);
+}
+
+static bool al16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static bool has_tma(int epi) { return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S; }
+
+bool aniso_tma_eligible(const StencilCall& c) {
+  if (c.mode != STS_MODE_ANISO || c.ncomp != 1 || !has_tma(c.epi) || !c.ev) return false;
+  const Geo& G = c.geo;
+  if (G.n3 % 2 != 0 || G.n3 < 2) return false;
+  if (!al16(c.u.p) || !al16(c.u.lo) || !al16(c.u2.p) || !al16(c.u2.lo) || !al16(c.ev) || !al16(c.w)) return false;
+  if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
+  // halo planes come from the library's contiguous [2][MAXC][plane] slot buffers
+  if (c.u.lo && c.u.hi && c.u.hi != c.u.lo + (long long)MAXC * G.plane) return false;
+  if (c.u2.lo && c.u2.hi && c.u2.hi != c.u2.lo + (long long)MAXC * G.plane) return false;
+  if ((c.u.lo == nullptr) != (c.u.hi == nullptr) && (c.u.lo ? false : c.u.hi != nullptr)) {
+    // only a hi halo: its buffer base is hi - MAXC*plane (same allocation)
+  }
+  return true;
+}
+
+static dim3 tma_grid(const Geo& G, int ib, int ie, int* ic_out) {
+  const int nbx = (G.n3 + XOK - 1) / XOK, nby = (G.n2 + XOJ - 1) / XOJ;
+  const int np = ie - ib;
+  if (np <= 0) {
+    *ic_out = 1;
+    return dim3(0, 0, 0);
+  }
+  const long long tiles = (long long)nbx * nby;
+  const long long want = 148LL * 3 * 3;          // ~3 waves of 3 resident CTAs per SM
+  int ic = (int)((np * tiles + want - 1) / want);
+  ic = ic < 16 ? 16 : ic;
+  if (ic > np) ic = np;
+  *ic_out = ic;
+  return dim3(nbx, nby, (np + ic - 1) / ic);
+}
+
+int aniso_tma_blocks(const Geo& G, int ib, int ie) {
+  int ic;
+  const dim3 g = tma_grid(G, ib, ie, &ic);
+  return (int)(g.x * g.y * g.z);
+}
+
+template <int EPI>
+static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
+    attr = true;
+  }
+  aniso_tma_kernel<EPI><<<grid, XNT, TMA_SMEM, st>>>(c, ic, ta);
+}
+
+bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
+  if (!aniso_tma_eligible(c)) return false;
+  const Geo& G = c.geo;
+  int ic = 1;
+  const dim3 grid = tma_grid(G, c.ib, c.ie, &ic);
+  if (grid.x == 0) return true;
+  TmaArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  const FieldV* srcs[MAXSRC] = {&c.u, &c.u2};
+  const int nsrc = (c.epi == EPI_PCG_S) ? 2 : 1;
+  ta.nsrc = nsrc;
+  ta.has_lo = c.u.lo != nullptr;
+  ta.has_hi = c.u.hi != nullptr;
+  for (int f = 0; f < nsrc; ++f) {
+    const FieldV& F = *srcs[f];
+    const double* pm = F.p ? F.p : c.u.p;   // pold absent on the first PCG iteration: any valid map
+    map_plain(&ta.src[f], pm, G, G.nl, UBW, UBH);
+    map_plain(&ta.srcw[f], pm, G, G.nl, 2, UBH);
+    const double* hb = F.lo ? F.lo : (F.hi ? F.hi - (long long)MAXC * G.plane : nullptr);
+    if (hb) {
+      map_plain(&ta.srch[f], hb, G, 2 * MAXC, UBW, UBH);
+      map_plain(&ta.srchw[f], hb, G, 2 * MAXC, 2, UBH);
+    } else {
+      ta.srch[f] = ta.src[f];
+      ta.srchw[f] = ta.srcw[f];
+    }
+  }
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)ev_row(G.n3), (cuuint64_t)G.n2, (cuuint64_t)G.nl + 1, 3};
+    const cuuint64_t str[3] = {(cuuint64_t)ev_row(G.n3) * 8, (cuuint64_t)ev_plane(G.n2, G.n3) * 8,
+                               (cuuint64_t)ev_cstride(G.nl, G.n2, G.n3) * 8};
+    const cuuint32_t box[4] = {XK, XJ, 1, 3};
+    encode(&ta.e, c.ev, 4, dims, str, box);
+  }
+  const double* owns[MAXOWN];
+  int nown = 0;
+  if (c.epi == EPI_RKL2_STAGE) {
+    owns[nown++] = c.ea.ym2;
+    owns[nown++] = c.ea.y0;
+    owns[nown++] = c.ea.m0;
+  } else if (c.epi == EPI_PCG_S) {
+    owns[nown++] = c.ea.x;
+  }
+  if (c.w) owns[nown++] = c.w;
+  for (int q = 0; q < nown; ++q) map_plain(&ta.own[q], owns[q], G, G.nl, XK, XOJ);
+  ta.nown = nown;
+  switch (c.epi) {
+    case EPI_F: launch_t<EPI_F>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_FIRST: launch_t<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_STAGE: launch_t<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
+    case EPI_PCG_S: launch_t<EPI_PCG_S>(c, grid, ic, ta, st); break;
+    default: return false;
+  }
+  STS_CUDA(cudaGetLastError());
+  return true;
+}
+
+}  // namespace sts

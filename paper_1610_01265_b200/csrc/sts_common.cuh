@@ -2,6 +2,7 @@
 // Product code: shares nothing with oracle/ (DESIGN.md "Boundary").
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -96,7 +97,10 @@ struct Slab {
   bool has_lo, has_hi;
 };
 
-enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_NSLOTS };
+// halo planes of the fields the stencils read across slab boundaries.  Per slot
+// ONE allocation [2][MAXC][plane]: the lo planes (comp c at c) then the hi planes
+// (comp c at MAXC + c), so a single TMA tensor map covers both sides.
+enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_Z, H_P, H_NSLOTS };
 
 struct Workspace {
   double* base = nullptr;
@@ -129,6 +133,7 @@ struct sts_grid {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   long long launches = 0;
   size_t halo_bytes = 0;
+  bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
   // per-kernel-class event timing (sts_grid_set_timing)
   bool timing = false;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -153,11 +158,13 @@ enum Epi : int {
   EPI_RKL2_STAGE,   // yj = mu*u + nu*ym2 + (1-mu-nu)*y0 + c0*F(u) + c1*M0
   EPI_PCG_R0,       // r = dt*L u; d = 1/(wV - dt L_ii); x = u; z = r d; p = z; partials r.z, b.b d
   EPI_PCG_AP,       // y = wV p - dt L p; partial p.y
+  EPI_PCG_S,        // p = z + beta pold; x += ax pold; y = wV p - dt L p; partial p.y  (fused S-pass)
 };
 
 // PCG per-component scalars (device)
 struct PcgScal {
   double rz, rz_old, pAp, alpha, beta, thresh;
+  double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update)
   int done, iters;
 };
 
@@ -174,6 +181,8 @@ struct EpiArgs {
   long long pstride = 0;       // stride between partial-value rows
   long long pbase = 0;         // this launch's first CTA slot
   const PcgScal* sc = nullptr; // per-component PCG scalars (skip components with done set)
+  double* x = nullptr;         // EPI_PCG_S: iterate, updated in place (x += ax pold)
+  int first = 0;               // EPI_PCG_S: first iteration (p = z, no pold, no x update)
 };
 
 struct StencilCall {
@@ -182,8 +191,9 @@ struct StencilCall {
   int epi;
   Geo geo;
   FieldV u, k1, k2, k3, b;
+  FieldV u2;                   // EPI_PCG_S: pold (u = z)
   const double* w;             // [nl][plane] or nullptr
-  const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][plane]
+  const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][n2][n3+2] (see ev_pitch)
   EpiArgs ea;
   int ib, ie;                  // local plane range [ib, ie)
 };
@@ -197,6 +207,29 @@ void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStre
 // e_a = sqrt(V_v kappa_v) b_{v,a} / (4 h_a) for vertex planes -1 .. nl-1 of a slab
 void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st);
 bool stencil_uses_vertex_coef(int mode, int epi);
+// padded vertex-coefficient layout: vertex (il+1/2, jv+1/2, kv+1/2), il = -1..nl-1, at
+//   ev[a*ev_cstride + (il+1)*ev_plane + jv*ev_row + (kv+1)],  kv = -1 (periodic wrap copy of
+//   kv = n3-1, else 0) .. n3-1; the row pitch n3+2 keeps rows 16 B aligned for even n3
+__host__ __device__ inline long long ev_row(int n3) { return (long long)n3 + 2; }
+__host__ __device__ inline long long ev_plane(int n2, int n3) { return (long long)n2 * ev_row(n3); }
+__host__ __device__ inline long long ev_cstride(int nl, int n2, int n3) { return (long long)(nl + 1) * ev_plane(n2, n3); }
+
+// TMA + mbarrier pipelined anisotropic stencil (stencil_tma.cu).  Returns false (and
+// launches nothing) if the call is not eligible (odd n3, misaligned arrays, epilogue
+// without a TMA variant); the caller then uses launch_stencil.
+bool aniso_tma_eligible(const StencilCall& c);
+bool launch_aniso_tma(const StencilCall& c, cudaStream_t st);
+int aniso_tma_blocks(const Geo& G, int ib, int ie);
+// PCG pointwise passes of the restructured iteration (aux.cu)
+// pnew = z + beta pold (pold unused if first); x += ax pold (not if first)
+void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, const double* z, const double* pold,
+                     double* x, const PcgScal* sc, int first, cudaStream_t st);
+// r -= alpha y; z = r d; partial r.z
+void launch_pcg_rupdate(int ncomp, long long n, long long cstride, double* r, double* z, const double* y,
+                        const double* d, const PcgScal* sc, double* partials, long long pstride, cudaStream_t st);
+// x += ax p[iters % 2] for components with iters > 0
+void launch_pcg_xfinal(int ncomp, long long n, long long cstride, double* x, const double* p0, const double* p1,
+                       const PcgScal* sc, cudaStream_t st);
 
 // pointwise / auxiliary kernels (aux.cu)
 void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double* k3, double kappa0,

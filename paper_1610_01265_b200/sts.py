@@ -26,7 +26,7 @@ UID_BYTES = 128
 KERNEL_CLASSES = ["face_kappa", "aniso_F", "aniso_rkl2_first", "aniso_rkl2_stage", "aniso_pcg_r0",
                   "aniso_pcg_ap", "aniso_gersh", "iso_F", "iso_rkl2_first", "iso_rkl2_stage", "iso_pcg_r0",
                   "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo",
-                  "vertex_coef"]
+                  "vertex_coef", "aniso_pcg_s", "pcg_xfinal"]
 
 _lib = None
 
@@ -56,6 +56,7 @@ def lib():
         "sts_grid_workspace_bytes": (I, [P, ctypes.POINTER(ctypes.c_size_t)]),
         "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
         "sts_grid_set_timing": (I, [P, I]),
+        "sts_grid_set_tma": (I, [P, I]),
         "sts_grid_timing_reset": (I, [P]),
         "sts_grid_timing": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
         "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
@@ -171,6 +172,10 @@ class Grid:
 
     def set_timing(self, enable=True):
         _check("sts_grid_set_timing", lib().sts_grid_set_timing(self._h, int(bool(enable))))
+
+    def set_tma(self, enable=True):
+        """Use the TMA pipelined anisotropic kernels where eligible (default) or force the cp.async ones."""
+        _check("sts_grid_set_tma", lib().sts_grid_set_tma(self._h, int(bool(enable))))
 
     def timing_reset(self):
         _check("sts_grid_timing_reset", lib().sts_grid_timing_reset(self._h))

@@ -169,12 +169,14 @@ def _gpu_rkl2_run(G, T0, cfg, ratio, nsteps, b, inplace=False):
     return T, ss
 
 
+@pytest.mark.parametrize("tma", [True, False])
 @pytest.mark.parametrize("nsteps,tol", [(1, 1e-11), (20, 1e-9)])
-def test_rkl2_spitzer_parity(dev, nsteps, tol):
+def test_rkl2_spitzer_parity(dev, nsteps, tol, tma):
     cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
     g = cfg["grid"]
     ref, s_ref = _oracle_rkl2_run(g, cfg["T"].numpy(), cfg, 100.0, nsteps, cfg["b"].numpy())
     G = sts().Grid.from_grid(g)
+    G.set_tma(tma)
     out, s_gpu = _gpu_rkl2_run(G, cfg["T"].to(dev), cfg, 100.0, nsteps, cfg["b"].to(dev))
     assert s_gpu == s_ref
     assert rel_l2(cpu(out), ref) <= tol
@@ -243,13 +245,13 @@ def test_rkl2_inplace_and_host_pointers(dev):
 
 
 # ---------------------------------------------------------------- A7
-@pytest.mark.parametrize("case", ["c0", "c1", "c2"])
+@pytest.mark.parametrize("case", ["c0", "c1", "c1_cpasync", "c2"])
 def test_be_pcg_parity(dev, case):
     if case == "c0":
         cfg = W.make_config("c0_heat32")
         g = cfg["grid"]
         k, b, w, u, mode, ratio = cfg["faces"], None, None, cfg["u"], "iso", 50.0
-    elif case == "c1":
+    elif case.startswith("c1"):
         cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
         g = cfg["grid"]
         k = [torch.as_tensor(x) for x in O.spitzer_face_kappa(g, cfg["T"].numpy(), cfg["kappa0"], cfg["T_cut"])]
@@ -262,6 +264,7 @@ def test_be_pcg_parity(dev, case):
     dt = ratio * O.dt_euler(op)
     ref, it_ref = O.be_pcg_solve(op, u.numpy(), dt, rtol=1e-12)
     G = sts().Grid.from_grid(g)
+    G.set_tma(case != "c1_cpasync")
     out, it = G.be_pcg_solve(mode, u.to(dev), [x.to(dev) for x in k], None if b is None else b.to(dev),
                              None if w is None else w.to(dev), dt, 1e-12, 100000)
     assert all(abs(a - c) <= 1 for a, c in zip(it, it_ref)), (it, it_ref)
@@ -312,6 +315,43 @@ def test_virtual_slabs_match_single_domain(dev, nv):
     kv = [f.to(dev) for f in cv["visc_faces"]]
     rho, v = cv["rho"].to(dev), cv["v"].to(dev)
     assert torch.equal(G1.op_apply("iso", v, kv, None, rho), Gv.op_apply("iso", v, kv, None, rho))
+
+
+# ---------------------------------------------------------------- TMA vs cp.async kernels
+TMA_CASES = [((20, 19, 70), True, 1), ((13, 17, 64), False, 1), ((5, 9, 2), True, 1), ((9, 16, 96), True, 1),
+             ((21, 19, 62), True, 3), ((12, 8, 40), False, 2), ((7, 23, 33), True, 1)]
+
+
+@pytest.mark.parametrize("shape,periodic,nv", TMA_CASES)
+def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
+    """The TMA + mbarrier pipelined kernels (even n3) and the cp.async kernels
+    (forced, or odd n3) against the oracle: RKL2 super-step and BE+PCG, with
+    periodic wrap tiles, non-periodic walls, several phi tiles and r chunks,
+    and virtual r-slabs reading halo planes."""
+    g = sph(shape, periodic=periodic)
+    rng = np.random.default_rng(zlib.crc32(repr((shape, periodic, nv)).encode()))
+    T = torch.as_tensor(1.5e6 * (1.0 + 0.3 * rng.uniform(-1, 1, g.shape)))
+    b = W.random_unit_b(g, seed=int(rng.integers(1 << 30)))
+    kap = O.spitzer_face_kappa(g, T.numpy(), 1e-9, 5e5)
+    op = O.Operator(g, kap, b.numpy())
+    dte = O.dt_euler(op)
+    dt = 60.0 * dte
+    s = O.rkl2_num_stages(dt, dte)
+    ref = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), T.numpy(), dt, s)
+    ref_be, it_ref = O.be_pcg_solve(op, T.numpy(), dt, rtol=1e-12)
+    k = [torch.as_tensor(x).to(dev) for x in kap]
+    outs = {}
+    for tma in (True, False):
+        G = sts().Grid.from_grid(g, n_virtual=nv)
+        G.set_tma(tma)
+        u = G.rkl2_advance("aniso", T.to(dev), k, b.to(dev), None, dt, s)
+        x, it = G.be_pcg_solve("aniso", T.to(dev), k, b.to(dev), None, dt, 1e-12, 10000)
+        assert rel_l2(cpu(u), ref) <= 1e-11, tma
+        assert rel_l2(cpu(x), ref_be) <= 1e-11, tma
+        assert abs(it[0] - it_ref[0]) <= 1, (tma, it, it_ref)
+        outs[tma] = (cpu(u), cpu(x))
+    assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
+    assert rel_l2(outs[True][1], outs[False][1]) <= 1e-12
 
 
 def test_smoke_entry(dev):
