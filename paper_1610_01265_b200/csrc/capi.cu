@@ -343,6 +343,107 @@ static void launch_pass(sts_grid* g, const StencilCall& c, cudaStream_t st) {
 }
 
 static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
+
+// CTAs one pass over local planes [c.ib, c.ie) launches (sizes the partial-sum rows)
+static int pass_blocks(const sts_grid* g, const StencilCall& c) {
+  if (g->tma && aniso_tma_eligible(c)) return aniso_tma_blocks(c.geo, c.ib, c.ie);
+  return stencil_blocks(c.mode, c.epi, c.geo, c.ib, c.ie);
+}
+
+static cudaStream_t comm_stream(sts_grid* g) {
+  if (!g->comm_stream) {
+    int lo = 0, hi = 0;
+    STS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    STS_CUDA(cudaStreamCreateWithPriority(&g->comm_stream, cudaStreamNonBlocking, hi));
+  }
+  if (!g->ev_a) STS_CUDA(cudaEventCreateWithFlags(&g->ev_a, cudaEventDisableTiming));
+  if (!g->ev_b) STS_CUDA(cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming));
+  return g->comm_stream;
+}
+
+struct Xch {
+  int slot;
+  const double* arr;
+  int ncomp;
+};
+
+// plane ranges of one sweep, in launch order: every slab's interior planes (which
+// read no halo) first, then the boundary planes next to a neighbour slab
+struct Range {
+  size_t si;
+  int ib, ie;
+  bool boundary;
+};
+static std::vector<Range> sweep_ranges(const sts_grid* g, bool overlap) {
+  std::vector<Range> v;
+  for (size_t si = 0; si < g->slabs.size(); ++si) {
+    const Slab& s = g->slabs[si];
+    if (!overlap) {
+      v.push_back({si, 0, s.nl, false});
+      continue;
+    }
+    const int lo = s.has_lo ? 1 : 0, hi = s.has_hi ? s.nl - 1 : s.nl;
+    if (hi > lo) v.push_back({si, lo, hi, false});
+  }
+  if (overlap)
+    for (size_t si = 0; si < g->slabs.size(); ++si) {
+      const Slab& s = g->slabs[si];
+      const int lo = s.has_lo ? 1 : 0;
+      if (s.has_lo) v.push_back({si, 0, std::min(1, s.nl), true});
+      if (s.has_hi && s.nl - 1 >= lo) v.push_back({si, s.nl - 1, s.nl, true});
+    }
+  return v;
+}
+
+// One stencil pass over every slab whose source fields `xs` need halo planes
+// (DESIGN.md §6): the halo exchange runs on the high-priority communication
+// stream (NCCL send/recv between ranks, device copies between virtual slabs)
+// while the interior planes are computed on `st`; the boundary planes follow once
+// the halos have landed.  `make(si)` returns the slab's StencilCall; returns the
+// number of CTAs launched (per-CTA partial sums are written from pbase 0 on).
+template <class Make>
+static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Make make) {
+  const bool overlap = needs_halos(g) && xs.size() > 0;
+  cudaStream_t cst = nullptr;
+  if (overlap) {
+    cst = comm_stream(g);
+    STS_CUDA(cudaEventRecord(g->ev_a, st));
+    STS_CUDA(cudaStreamWaitEvent(cst, g->ev_a, 0));
+    for (const Xch& x : xs) exchange(g, x.slot, x.arr, x.ncomp, cst);
+    STS_CUDA(cudaEventRecord(g->ev_b, cst));
+  }
+  int pb = 0;
+  bool waited = false;
+  for (const Range& r : sweep_ranges(g, overlap)) {
+    if (r.boundary && !waited) {
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
+      waited = true;
+    }
+    StencilCall c = make(r.si);
+    c.ib = r.ib;
+    c.ie = r.ie;
+    c.ea.pbase = pb;
+    pb += pass_blocks(g, c);
+    launch_pass(g, c, st);
+  }
+  if (overlap && !waited) STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
+  return pb;
+}
+
+// CTAs of a sweep (same ranges and kernel choice as sweep())
+template <class Make>
+static int sweep_blocks(sts_grid* g, bool has_x, Make make) {
+  int pb = 0;
+  for (const Range& r : sweep_ranges(g, needs_halos(g) && has_x)) {
+    StencilCall c = make(r.si);
+    c.ib = r.ib;
+    c.ie = r.ie;
+    pb += pass_blocks(g, c);
+  }
+  return pb;
+}
+
+
 static const double* off(const double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 
 // RKL2 coefficients, PAPER.md:134-138 (gamma~ per DESIGN R6)
@@ -685,14 +786,13 @@ int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out,
     if (sg.any_host) sg.begin(base + evn);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
     const auto ev = build_vertex_coefs(g, mode, base, k1, k2, k3, b, st);
-    exchange(g, H_U, u, ncomp, st);
-    for (size_t si = 0; si < g->slabs.size(); ++si) {
+    sweep(g, {{H_U, u, ncomp}}, st, [&](size_t si) {
       const Slab& s = g->slabs[si];
       StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
       c.ev = ev[si];
       c.ea.out = off(out, s);
-      launch_pass(g, c, st);
-    }
+      return c;
+    });
     sg.end({out});
   });
 }
@@ -780,16 +880,15 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
     const auto ev = build_vertex_coefs(g, mode, base + 3 * NFr, k1, k2, k3, b, st);
     // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
-    exchange(g, H_U, u0, ncomp, st);
-    for (size_t si = 0; si < g->slabs.size(); ++si) {
+    sweep(g, {{H_U, u0, ncomp}}, st, [&](size_t si) {
       const Slab& sl = g->slabs[si];
       StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
       c.ev = ev[si];
       c.ea.out = off(A, sl);
       c.ea.out2 = off(M0, sl);
       c.ea.c0 = co.mut[1] * dt;
-      launch_pass(g, c, st);
-    }
+      return c;
+    });
     // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
     const double* prev = u0;
     double* cur = A;
@@ -798,8 +897,7 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
       if (j == s) dst = u1;
       else if (prev == u0) dst = B;                       // never overwrite Y0
       else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
-      exchange(g, H_U, cur, ncomp, st);
-      for (size_t si = 0; si < g->slabs.size(); ++si) {
+      sweep(g, {{H_U, cur, ncomp}}, st, [&](size_t si) {
         const Slab& sl = g->slabs[si];
         StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
         c.ev = ev[si];
@@ -812,8 +910,8 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
         c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
         c.ea.c0 = co.mut[j] * dt;
         c.ea.c1 = co.gt[j] * dt;
-        launch_pass(g, c, st);
-      }
+        return c;
+      });
       prev = cur;
       cur = dst;
     }
@@ -874,19 +972,60 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.ea.x = off(x, g->slabs[0]);
       fused = aniso_tma_eligible(c);
     }
-    // reduction storage (per-CTA partials of every pass)
-    int sb_r0 = 0, sb_s = 0;
-    for (auto& sl : g->slabs) {
-      const Geo G = slab_geo(g, sl);
-      sb_r0 += stencil_blocks(mode, EPI_PCG_R0, G, 0, sl.nl);
-      sb_s += fused ? aniso_tma_blocks(G, 0, sl.nl) : stencil_blocks(mode, EPI_PCG_AP, G, 0, sl.nl);
-    }
-    const long long pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
+    // the passes (make(si) -> StencilCall of slab si; sweep() sets the plane range and pbase)
+    double* partials = nullptr;
+    long long pstride = 0;
+    PcgScal* sc = nullptr;
+    int k_cur = 1;   // iteration whose S-pass is being built
+    auto make_r0 = [&](size_t si) {
+      const Slab& sl = g->slabs[si];
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
+      c.ea.out = off(r, sl);
+      c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
+      c.ea.out3 = off(z, sl);
+      c.ea.out4 = off(d, sl);
+      c.ea.dt = dt;
+      c.ea.partials = partials;
+      c.ea.pstride = pstride;
+      return c;
+    };
+    auto make_s = [&](size_t si) {   // fused S-pass (TMA)
+      const Slab& sl = g->slabs[si];
+      const int first = (k_cur == 1);
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
+      c.u = view(g, sl, H_Z, z);
+      c.u2 = first ? FieldV{} : view(g, sl, H_P, pb[(k_cur - 1) & 1]);
+      c.ev = ev[si];
+      c.ea.out = off(y, sl);
+      c.ea.out2 = off(pb[k_cur & 1], sl);
+      c.ea.x = off(x, sl);
+      c.ea.first = first;
+      c.ea.dt = dt;
+      c.ea.partials = partials;
+      c.ea.pstride = pstride;
+      c.ea.sc = sc;
+      return c;
+    };
+    auto make_ap = [&](size_t si) {  // A p of the unfused S-pass
+      const Slab& sl = g->slabs[si];
+      double* pnew = pb[k_cur & 1];
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, pnew, k1, k2, k3, bb, w);
+      c.ev = ev[si];
+      c.ea.out = off(y, sl);
+      c.ea.dt = dt;
+      c.ea.partials = partials;
+      c.ea.pstride = pstride;
+      c.ea.sc = sc;
+      return c;
+    };
+    const int sb_r0 = sweep_blocks(g, true, make_r0);
+    const int sb_s = fused ? sweep_blocks(g, true, make_s) : sweep_blocks(g, true, make_ap);
+    pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
     const size_t red_doubles = (size_t)2 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
     ensure_red(g, red_doubles * sizeof(double));
-    double* partials = g->d_red;
+    partials = g->d_red;
     double* sums = partials + 2 * ncomp * pstride;
-    PcgScal* sc = reinterpret_cast<PcgScal*>(sums + 16);
+    sc = reinterpret_cast<PcgScal*>(sums + 16);
 
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
@@ -901,24 +1040,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     };
 
     // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
-    exchange(g, H_U, un, ncomp, st);
-    {
-      int pb0 = 0;
-      for (auto& sl : g->slabs) {
-        StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
-        c.ea.out = off(r, sl);
-        c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-        c.ea.out3 = off(z, sl);
-        c.ea.out4 = off(d, sl);
-        c.ea.dt = dt;
-        c.ea.partials = partials;
-        c.ea.pstride = pstride;
-        c.ea.pbase = pb0;
-        pb0 += stencil_blocks(mode, EPI_PCG_R0, c.geo, 0, sl.nl);
-        launch_pass(g, c, st);
-      }
-      reduce(sb_r0, 2, PH_R0);
-    }
+    reduce(sweep(g, {{H_U, un, ncomp}}, st, make_r0), 2, PH_R0);
     // iteration k (Fig. 1 with the x update deferred one iteration):
     //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
     //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
@@ -935,52 +1057,21 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       const int nb = std::min(batch, kmax - launched);
       for (int it = 0; it < nb; ++it) {
         const int k = launched + it + 1;
-        const int first = (k == 1);
+        k_cur = k;
         double* pold = pb[(k - 1) & 1];
         double* pnew = pb[k & 1];
-        int pbs = 0;
+        int nbs;
         if (fused) {
-          exchange(g, H_Z, z, ncomp, st);
-          if (!first) exchange(g, H_P, pold, ncomp, st);
-          for (size_t si = 0; si < g->slabs.size(); ++si) {
-            const Slab& sl = g->slabs[si];
-            StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
-            c.u = view(g, sl, H_Z, z);
-            c.u2 = first ? FieldV{} : view(g, sl, H_P, pold);
-            c.ev = ev[si];
-            c.ea.out = off(y, sl);
-            c.ea.out2 = off(pnew, sl);
-            c.ea.x = off(x, sl);
-            c.ea.first = first;
-            c.ea.dt = dt;
-            c.ea.partials = partials;
-            c.ea.pstride = pstride;
-            c.ea.pbase = pbs;
-            c.ea.sc = sc;
-            pbs += aniso_tma_blocks(c.geo, 0, sl.nl);
-            launch_pass(g, c, st);
-          }
+          if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, st, make_s);
+          else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, st, make_s);
         } else {
           {
             Timed t(g, STS_K_PCG_PUPDATE, st);
-            launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, first, st);
+            launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, k == 1, st);
           }
-          exchange(g, H_U, pnew, ncomp, st);
-          for (size_t si = 0; si < g->slabs.size(); ++si) {
-            const Slab& sl = g->slabs[si];
-            StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, pnew, k1, k2, k3, bb, w);
-            c.ev = ev[si];
-            c.ea.out = off(y, sl);
-            c.ea.dt = dt;
-            c.ea.partials = partials;
-            c.ea.pstride = pstride;
-            c.ea.pbase = pbs;
-            c.ea.sc = sc;
-            pbs += stencil_blocks(mode, EPI_PCG_AP, c.geo, 0, sl.nl);
-            launch_pass(g, c, st);
-          }
+          nbs = sweep(g, {{H_U, pnew, ncomp}}, st, make_ap);
         }
-        reduce(sb_s, 1, PH_AP);
+        reduce(nbs, 1, PH_AP);
         {
           Timed t(g, STS_K_PCG_UPDATE, st);
           launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride, st);

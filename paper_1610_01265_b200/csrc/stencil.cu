@@ -365,11 +365,12 @@ __global__ void __launch_bounds__(256) vertex_coef_kernel(Geo G, FieldV b, Field
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nv; e += (long long)gridDim.x * blockDim.x) {
     const int il = (int)(e / pp) - 1;
     const long long rem = e - (long long)(il + 1) * pp;
-    const int jv = (int)(rem / row);
-    int kv = (int)(rem - (long long)jv * row) - 1;
+    const int jv = (int)(rem / row) - 1;
+    int kv = (int)(rem - (long long)(jv + 1) * row) - 1;
     if (kv == -1 && G.periodic3) kv = G.n3 - 1;
     const int iv = G.i0 + il;
-    bool ok = kv >= 0 && kv < G.n3 && iv >= 0 && iv + 1 < G.n1g && jv + 1 < G.n2 && (G.periodic3 || kv + 1 < G.n3);
+    bool ok = kv >= 0 && kv < G.n3 && iv >= 0 && iv + 1 < G.n1g && jv >= 0 && jv + 1 < G.n2 &&
+              (G.periodic3 || kv + 1 < G.n3);
     double er = 0.0, et = 0.0, ep = 0.0;
     if (ok) {
       const int kv1 = (kv + 1 < G.n3) ? kv + 1 : 0;
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
   if (G.periodic3) kv = wrapk(kv, G.n3);
   else vok = vok && kv >= 0 && kv + 1 < G.n3;
   const double ig3a = vok ? M.iG3[jv] : 0.0, ig3b = vok ? M.iG3[jv + 1] : 0.0;
-  const long long eoff = vok ? (long long)jv * ev_row(G.n3) + kv + 1 : 0;
+  const long long eoff = vok ? (long long)(jv + 1) * ev_row(G.n3) + kv + 1 : 0;
   const long long epp = ev_plane(G.n2, G.n3);
   const long long es = (long long)(G.nl + 1) * epp;
   const int j = j0 + vj, k = k0 + vk;

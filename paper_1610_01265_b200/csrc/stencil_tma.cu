@@ -12,15 +12,24 @@
 // fast path: 27-29 % of DRAM peak, long-scoreboard bound).
 //
 // CTA = 8 warps x 32 lanes = 8 x 32 vertex columns -> 7 x 31 output cells.
-// Boxes per package Q(p) (cell plane p, global coordinates, OOB -> zeros):
-//   staged source f   : 34 cols x 9 rows  from (k0-1, j0-1)  of plane p
-//                       (p = -1 / nl: the library's halo planes of the neighbour slab)
-//   wrap columns      : 2 x 9 from (n3-2, j0-1) and (0, j0-1) (periodic phi, edge tiles only)
-//   vertex coeffs e   : 32 x 8 x 3 comps, vertex plane p-1 (padded e layout: no wrap)
-//   epilogue operands : 32 x 7 from (k0, j0), cell plane p-1
+// Boxes per package Q(p) (cell plane p, global coordinates, OOB -> zeros).  The
+// innermost (phi) box origin must be 16 B aligned -- an odd FP64 column origin
+// raises an illegal-instruction fault on sm_100a (measured, tools/probe) -- so
+// every box starts at the even column at or below the first column it needs and
+// the reader adds the shift back:
+//   staged source f   : 36 cols x 9 rows from (even(k0-1), j0-1) of plane p
+//                       (p = -1 / nl: the library's halo planes of the neighbour slab,
+//                        else OOB zeros; the vertices there carry e = 0 anyway)
+//   wrap columns      : 2 x 9 from (n3-2, j0-1) and (0, j0-1) (periodic phi, edge tiles)
+//   vertex coeffs e   : 34 x 8 per component from (even(k0), j0), vertex plane p-1
+//                       (padded e layout: zero row / wrap column built in)
+//   epilogue operands : 32 x 7 from (even(k0), j0), cell plane p-1
 // Epilogues: RKL2 first stage / stage recurrence (Fig. 2) and the fused
 // PCG S-pass  p = z + beta pold, x += ax pold, y = A p, partial p.y  (Fig. 1).
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "sts_common.cuh"
 
@@ -32,16 +41,18 @@ constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= warps / lan
 constexpr int XOJ = XJ - 1, XOK = XK - 1;   // output rows / cols
 constexpr int XNT = XJ * XK;
 constexpr int XTS = 3;                      // ring slots (packages in flight = XTS - 1)
-constexpr int UBW = 34, UBH = 9;            // staged-source box (cols x rows)
+constexpr int UBW = 36, UBH = 9;            // staged-source box (cols x rows)
+constexpr int EBW = 34;                     // vertex-coefficient box cols
 constexpr int MAXSRC = 2;                   // staged sources (PCG S-pass: z, pold)
 constexpr int MAXOWN = 4;                   // epilogue operand boxes
 // slot layout (doubles); every part starts on a 128 B boundary
-constexpr int U_MAIN = 320;                 // 9 x 34 = 306 -> 320
+constexpr int U_MAIN = 336;                 // 9 x 36 = 324 -> 336
 constexpr int U_WL = 32, U_WR = 32;         // 9 x 2 = 18 -> 32
 constexpr int U_FIELD = U_MAIN + U_WL + U_WR;
-constexpr int E_PART = 3 * XJ * XK;         // 768
+constexpr int E_COMP = XJ * EBW;            // 8 x 34 = 272 (2176 B)
+constexpr int E_PART = 3 * E_COMP;
 constexpr int O_PART = XOJ * XK;            // 7 x 32 = 224
-constexpr int SLOT = MAXSRC * U_FIELD + E_PART + MAXOWN * O_PART;   // 2432 doubles = 19 KB
+constexpr int SLOT = MAXSRC * U_FIELD + E_PART + MAXOWN * O_PART;   // 2512 doubles = 19.6 KB
 constexpr int VBUF = 3 * XNT;               // A, B, C of one vertex plane
 constexpr size_t TMA_SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 64;
 
@@ -86,13 +97,16 @@ __device__ __forceinline__ void tma4(double* dst, const CUtensorMap* map, int c0
 
 // tensor maps of one launch (kernel parameter, __grid_constant__)
 struct TmaArgs {
-  CUtensorMap src[MAXSRC];    // staged sources, 3D (n3, n2, nl),       box 34 x 9 x 1
-  CUtensorMap srch[MAXSRC];   // their halo planes, 3D (n3, n2, 2 MAXC), box 34 x 9 x 1
+  CUtensorMap src[MAXSRC];    // staged sources, 3D (n3, n2, nl),       box 36 x 9 x 1
+  CUtensorMap srch[MAXSRC];   // their halo planes, 3D (n3, n2, 2 MAXC), box 36 x 9 x 1
   CUtensorMap srcw[MAXSRC];   // wrap columns, main planes,             box 2 x 9 x 1
   CUtensorMap srchw[MAXSRC];  // wrap columns, halo planes,             box 2 x 9 x 1
-  CUtensorMap e;              // vertex coefficients, 4D (n3+2, n2, nl+1, 3), box 32 x 8 x 1 x 3
+  CUtensorMap e;              // vertex coefficients, 3D (n3+2, n2+1, 3 (nl+1)), box 34 x 8 x 1
+                              // (a 4D map with the component as 4th dim faults on sm_100a)
   CUtensorMap own[MAXOWN];    // epilogue operands, 3D (n3, n2, nl),   box 32 x 7 x 1
   int nsrc, nown, has_lo, has_hi;
+  int dbg;   // bisection switches (STS_TMA_DBG): 1 no src, 2 no wrap, 4 no e, 8 no own, 16 return early,
+             // 32 return after mbarrier init, 64 no waits
 };
 
 // epilogue operand slots
@@ -125,12 +139,15 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
   if constexpr (EPI == EPI_PCG_S) {
     if (c.ea.sc && c.ea.sc[0].done) return;
   }
+  if (ta.dbg & 16) return;
   const bool first = (EPI == EPI_PCG_S) && c.ea.first;
   const double beta = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].beta : 0.0;
   const double ax = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].ax : 0.0;
   const bool per = G.periodic3 != 0;
   const bool wrapL = per && k0 == 0;
   const bool wrapR = per && (k0 + 32 >= G.n3);
+  const int ou = (k0 - 1) & ~1;                     // even box origins (floor, also for -1 -> -2)
+  const int oe = k0 & ~1, se = k0 - oe;             // e / epilogue boxes and their column shift
 
   // ---- producer: thread 0 issues package Q(p) ----
   auto issue = [&](int p) {
@@ -139,25 +156,28 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
     uint64_t* bar = bars + slot;
     const bool lo = p < 0, hi = p >= G.nl;
     const bool halo = (lo && ta.has_lo) || (hi && ta.has_hi);
-    const int pc = halo ? (lo ? 0 : MAXC) : p;      // OOB plane (no neighbour) -> zeros
+    const int pc = halo ? (lo ? 0 : MAXC) : p;      // no neighbour: OOB plane -> zeros
     const int nsrc_now = (EPI == EPI_PCG_S && first) ? 1 : NSRC;
-    uint32_t bytes = nsrc_now * UBW * UBH * 8;
-    if (wrapL) bytes += nsrc_now * 2 * UBH * 8;
-    if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
-    const bool has_e = p >= ib, has_own = p >= ib + 1;
+    const bool dsrc = !(ta.dbg & 1), dwrap = !(ta.dbg & 2);
+    uint32_t bytes = dsrc ? nsrc_now * UBW * UBH * 8 : 0;
+    if (wrapL && dwrap) bytes += nsrc_now * 2 * UBH * 8;
+    if (wrapR && dwrap) bytes += nsrc_now * 2 * UBH * 8;
+    const bool has_e = p >= ib && !(ta.dbg & 4), has_own = p >= ib + 1 && !(ta.dbg & 8);
     if (has_e) bytes += E_PART * 8;
     if (has_own) bytes += nown * XOJ * XK * 8;
     fence_proxy_async();
     mbar_expect_tx(bar, bytes);
     for (int f = 0; f < nsrc_now; ++f) {
       double* D = S + f * U_FIELD;
-      tma3(D, halo ? &ta.srch[f] : &ta.src[f], k0 - 1, j0 - 1, pc, bar);
+      if (dsrc) tma3(D, halo ? &ta.srch[f] : &ta.src[f], ou, j0 - 1, pc, bar);
+      if (!dwrap) continue;
       if (wrapL) tma3(D + U_MAIN, halo ? &ta.srchw[f] : &ta.srcw[f], G.n3 - 2, j0 - 1, pc, bar);
       if (wrapR) tma3(D + U_MAIN + U_WL, halo ? &ta.srchw[f] : &ta.srcw[f], 0, j0 - 1, pc, bar);
     }
-    if (has_e) tma4(S + MAXSRC * U_FIELD, &ta.e, k0, j0 - 1, p, 0, bar);   // vertex plane p-1 = ev index p
+    if (has_e)   // vertex plane p-1 = ev plane index p (row jv+1), one 3D box per component
+      for (int a = 0; a < 3; ++a) tma3(S + MAXSRC * U_FIELD + a * E_COMP, &ta.e, oe, j0, a * (G.nl + 1) + p, bar);
     if (has_own)
-      for (int q = 0; q < nown; ++q) tma3(S + MAXSRC * U_FIELD + E_PART + q * O_PART, &ta.own[q], k0, j0, p - 1, bar);
+      for (int q = 0; q < nown; ++q) tma3(S + MAXSRC * U_FIELD + E_PART + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
   };
 
   // ---- per-thread geometry ----
@@ -169,25 +189,27 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
   const long long coff = own ? (long long)j * G.n3 + k : 0;
   const double ig3c = own ? M.iG3[j] : 0.0;
   const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
-  // staged-box columns this thread reads: A = tile col vk (global k0-1+vk), B = vk+1 (global k0+vk)
-  int offA = vk, pitA = UBW, offB = vk + 1, pitB = UBW;
-  if (per) {
-    if (k0 - 1 + vk == -1) { offA = U_MAIN + 1; pitA = 2; }
-    if (k0 - 1 + vk == G.n3) { offA = U_MAIN + U_WL; pitA = 2; }
-    if (k0 + vk == G.n3) { offB = U_MAIN + U_WL; pitB = 2; }
-  }
+  // offset (within a staged field block) of the cell at tile row r (global j0-1+r)
+  // and tile col t (global k0-1+t)
+  auto uoff = [&](int r, int t) {
+    const int gk = k0 - 1 + t;                        // global phi index
+    if (per && gk == -1) return U_MAIN + r * 2 + 1;   // periodic wrap: cell n3-1
+    if (per && gk == G.n3) return U_MAIN + U_WL + r * 2;   // periodic wrap: cell 0
+    return r * UBW + (gk - ou);                       // (non-periodic col -1 / n3: OOB zeros)
+  };
+  const int o00 = uoff(vj, vk), o01 = uoff(vj, vk + 1), o10 = uoff(vj + 1, vk), o11 = uoff(vj + 1, vk + 1);
 
   // in-plane 2x2 box of the source value s = (PCG: z + beta pold, else u)
-  auto sval = [&](const double* S, int off, int pit, int row) {
-    const double v = S[off + row * pit];
+  auto sval = [&](const double* S, int off) {
+    const double v = S[off];
     if constexpr (EPI == EPI_PCG_S) {
-      if (!first) return fma(beta, S[U_FIELD + off + row * pit], v);
+      if (!first) return fma(beta, S[U_FIELD + off], v);
     }
     return v;
   };
   auto usums = [&](const double* S, double& Su, double& Tu, double& Fu) {
-    const double u00 = sval(S, offA, pitA, vj), u01 = sval(S, offB, pitB, vj);
-    const double u10 = sval(S, offA, pitA, vj + 1), u11 = sval(S, offB, pitB, vj + 1);
+    const double u00 = sval(S, o00), u01 = sval(S, o01);
+    const double u10 = sval(S, o10), u11 = sval(S, o11);
     Su = (u00 + u01) + (u10 + u11);
     Tu = (u10 - u00) + (u11 - u01);
     Fu = ig3a * (u01 - u00) + ig3b * (u11 - u10);
@@ -198,6 +220,7 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
     mbar_fence_init();
   }
   __syncthreads();
+  if (ta.dbg & 32) return;
   if (tid == 0)
     for (int p = ib - 1; p <= ie && p < ib - 1 + XTS; ++p) issue(p);
 
@@ -208,17 +231,18 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
   for (int p = ib - 1; p <= ie; ++p) {
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * SLOT;
-    mbar_wait(bars + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
+    if (!(ta.dbg & 64)) mbar_wait(bars + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
     double SuH, TuH, FuH;
     usums(S, SuH, TuH, FuH);
-    const double un = sval(S, offB, pitB, vj + 1);                       // own cell of plane p
+    const double un = sval(S, o11);                                       // own cell of plane p
     double pon = 0.0;
-    if constexpr (EPI == EPI_PCG_S) pon = first ? 0.0 : S[U_FIELD + offB + (vj + 1) * pitB];
+    if constexpr (EPI == EPI_PCG_S) pon = first ? 0.0 : S[U_FIELD + o11];
     double* vb = vbuf + (p & 1) * VBUF;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
       const double* E = S + MAXSRC * U_FIELD;
-      const double er = E[tid], et = E[XNT + tid], ep = E[2 * XNT + tid];
+      const int ei = vj * EBW + vk + se;
+      const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const int iv = G.i0 + p - 1;
       const double ig2l = (iv >= 0 && iv < G.n1g) ? M.iG2[iv] : 0.0;
       const double ig2h = (iv + 1 >= 0 && iv + 1 < G.n1g) ? M.iG2[iv + 1] : 0.0;
@@ -244,7 +268,7 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
         // output cell plane il = p-1
         const int il = p - 1;
         const int ig = G.i0 + il;
-        const double* O = S + MAXSRC * U_FIELD + E_PART + vj * XK + vk;
+        const double* O = S + MAXSRC * U_FIELD + E_PART + vj * XK + vk + se;
         const double ig2c = M.iG2[ig];
         const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
         const double WV = (c.w ? O[ow_w * O_PART] : 1.0) * M.Vr[ig] * vtpc;
@@ -339,10 +363,7 @@ bool aniso_tma_eligible(const StencilCall& c) {
   // halo planes come from the library's contiguous [2][MAXC][plane] slot buffers
   if (c.u.lo && c.u.hi && c.u.hi != c.u.lo + (long long)MAXC * G.plane) return false;
   if (c.u2.lo && c.u2.hi && c.u2.hi != c.u2.lo + (long long)MAXC * G.plane) return false;
-  if ((c.u.lo == nullptr) != (c.u.hi == nullptr) && (c.u.lo ? false : c.u.hi != nullptr)) {
-    // only a hi halo: its buffer base is hi - MAXC*plane (same allocation)
-  }
-  return true;
+  return true;   // a slab with only a hi halo maps its slot buffer from hi - MAXC*plane
 }
 
 static dim3 tma_grid(const Geo& G, int ib, int ie, int* ic_out) {
@@ -405,11 +426,10 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     }
   }
   {
-    const cuuint64_t dims[4] = {(cuuint64_t)ev_row(G.n3), (cuuint64_t)G.n2, (cuuint64_t)G.nl + 1, 3};
-    const cuuint64_t str[3] = {(cuuint64_t)ev_row(G.n3) * 8, (cuuint64_t)ev_plane(G.n2, G.n3) * 8,
-                               (cuuint64_t)ev_cstride(G.nl, G.n2, G.n3) * 8};
-    const cuuint32_t box[4] = {XK, XJ, 1, 3};
-    encode(&ta.e, c.ev, 4, dims, str, box);
+    const cuuint64_t dims[3] = {(cuuint64_t)ev_row(G.n3), (cuuint64_t)G.n2 + 1, 3 * ((cuuint64_t)G.nl + 1)};
+    const cuuint64_t str[2] = {(cuuint64_t)ev_row(G.n3) * 8, (cuuint64_t)ev_plane(G.n2, G.n3) * 8};
+    const cuuint32_t box[3] = {EBW, XJ, 1};
+    encode(&ta.e, c.ev, 3, dims, str, box);
   }
   const double* owns[MAXOWN];
   int nown = 0;
@@ -423,6 +443,14 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
   if (c.w) owns[nown++] = c.w;
   for (int q = 0; q < nown; ++q) map_plain(&ta.own[q], owns[q], G, G.nl, XK, XOJ);
   ta.nown = nown;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("STS_TMA_DBG");
+      dbg = e ? atoi(e) : 0;
+    }
+    ta.dbg = dbg;
+  }
   switch (c.epi) {
     case EPI_F: launch_t<EPI_F>(c, grid, ic, ta, st); break;
     case EPI_RKL2_FIRST: launch_t<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;

@@ -207,11 +207,14 @@ void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStre
 // e_a = sqrt(V_v kappa_v) b_{v,a} / (4 h_a) for vertex planes -1 .. nl-1 of a slab
 void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st);
 bool stencil_uses_vertex_coef(int mode, int epi);
-// padded vertex-coefficient layout: vertex (il+1/2, jv+1/2, kv+1/2), il = -1..nl-1, at
-//   ev[a*ev_cstride + (il+1)*ev_plane + jv*ev_row + (kv+1)],  kv = -1 (periodic wrap copy of
-//   kv = n3-1, else 0) .. n3-1; the row pitch n3+2 keeps rows 16 B aligned for even n3
+// padded vertex-coefficient layout: vertex (il+1/2, jv+1/2, kv+1/2), il = -1..nl-1,
+// jv = -1..n2-1, kv = -1..n3-1, at
+//   ev[a*ev_cstride + (il+1)*ev_plane + (jv+1)*ev_row + (kv+1)]
+// (row jv = -1 is zeros, column kv = -1 is the periodic wrap copy of kv = n3-1, else
+// zeros): every TMA box starts at a non-negative coordinate; the row pitch n3+2 keeps
+// rows 16 B aligned for even n3
 __host__ __device__ inline long long ev_row(int n3) { return (long long)n3 + 2; }
-__host__ __device__ inline long long ev_plane(int n2, int n3) { return (long long)n2 * ev_row(n3); }
+__host__ __device__ inline long long ev_plane(int n2, int n3) { return (long long)(n2 + 1) * ev_row(n3); }
 __host__ __device__ inline long long ev_cstride(int nl, int n2, int n3) { return (long long)(nl + 1) * ev_plane(n2, n3); }
 
 // TMA + mbarrier pipelined anisotropic stencil (stencil_tma.cu).  Returns false (and

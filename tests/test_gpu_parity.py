@@ -339,6 +339,11 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
     s = O.rkl2_num_stages(dt, dte)
     ref = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), T.numpy(), dt, s)
     ref_be, it_ref = O.be_pcg_solve(op, T.numpy(), dt, rtol=1e-12)
+    # PCG stops on a residual, so its iterate is unique only to ~cond(A) * rtol: the GPU
+    # iterate must be as close to the oracle's as the oracle's is to the exact solve
+    import scipy.sparse.linalg as spl
+    exact = spl.spsolve(O.be_system(op, dt).tocsc(), op.WV * T.numpy().ravel()).reshape(g.shape)
+    tol_be = max(1e-11, rel_l2(ref_be, exact))
     k = [torch.as_tensor(x).to(dev) for x in kap]
     outs = {}
     for tma in (True, False):
@@ -347,7 +352,7 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
         u = G.rkl2_advance("aniso", T.to(dev), k, b.to(dev), None, dt, s)
         x, it = G.be_pcg_solve("aniso", T.to(dev), k, b.to(dev), None, dt, 1e-12, 10000)
         assert rel_l2(cpu(u), ref) <= 1e-11, tma
-        assert rel_l2(cpu(x), ref_be) <= 1e-11, tma
+        assert rel_l2(cpu(x), ref_be) <= tol_be, tma
         assert abs(it[0] - it_ref[0]) <= 1, (tma, it, it_ref)
         outs[tma] = (cpu(u), cpu(x))
     assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
