@@ -76,6 +76,8 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         "iso_rkl2_stage": 32 * c + 32 + 8 * c,
         "iso_pcg_r0": 8 * c + 32 + 24 * c + 8,
         "iso_pcg_ap": 16 * c + 32,
+        # fused S-pass: z, pold, x in (+ k1, k2, k3, w); p, y, x out (first: z in; p, y out)
+        "iso_pcg_s": (24 * c + 32) if first else (48 * c + 32),
         "iso_gersh": 32,
         # U-pass: r, y, d in; r, z out
         "pcg_update": 32 * c + 8,
@@ -86,14 +88,14 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
     return table[kind]
 
 
-def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True):
+def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False):
     """Total algorithmic bytes per class for one step on `ncells` local cells."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
         _cond_bytes(add, s_c, it_c, fused_c)
     if s_v:
-        _visc_bytes(add, s_v, it_v)
+        _visc_bytes(add, s_v, it_v, fused_v)
     return B
 
 
@@ -115,15 +117,18 @@ def _cond_bytes(add, s_c, it_c, fused):
         add("pcg_xfinal", bytes_per_cell("pcg_xfinal", 1))
 
 
-def _visc_bytes(add, s_v, it_v):
+def _visc_bytes(add, s_v, it_v, fused=False):
     add("iso_gersh", bytes_per_cell("iso_gersh"))
     add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
     add("iso_rkl2_stage", (s_v - 1) * bytes_per_cell("iso_rkl2_stage", 3))
     add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0", 3))
     for k in range(1, max(it_v) + 1):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
-        add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act, first=k == 1))
-        add("iso_pcg_ap", bytes_per_cell("iso_pcg_ap", active=act))
+        if fused:
+            add("iso_pcg_s", bytes_per_cell("iso_pcg_s", active=act, first=k == 1))
+        else:
+            add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act, first=k == 1))
+            add("iso_pcg_ap", bytes_per_cell("iso_pcg_ap", active=act))
         add("pcg_update", bytes_per_cell("pcg_update", active=act))
     n_fin = sum(1 for i in it_v if i > 0)
     if n_fin:
@@ -406,9 +411,10 @@ def main():
     peak, peak_kind = peaks()
     Bytes = {}
     fused_c = timing.get("aniso_pcg_s", (0, 0.0))[0] > 0
+    fused_v = timing.get("iso_pcg_s", (0, 0.0))[0] > 0
     for i in infos:
         for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
-                                      fused_c).items():
+                                      fused_c, fused_v).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
     kernels = {}
     for k, (n, kms) in timing.items():
@@ -432,7 +438,7 @@ def main():
     launches_dom = infos[0]
     n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
              "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
-             "iso_pcg_ap": max(launches_dom["it_visc"])}.get(dom)
+             "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"])}.get(dom)
     bpl = (Bytes[dom] / len(infos) / n_eff) if n_eff else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,

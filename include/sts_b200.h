@@ -134,7 +134,8 @@ int sts_grid_kernel_launches(const sts_grid* g, long long* count);
 #define STS_K_VERTEX_COEF 17
 #define STS_K_ANISO_PCG_S 18     /* fused PCG S-pass (p update + x update + A p), TMA path   */
 #define STS_K_PCG_XFINAL 19      /* final deferred x += alpha p after convergence            */
-#define STS_K_NCLASSES 20
+#define STS_K_ISO_PCG_S 20       /* fused PCG S-pass of the isotropic operator, TMA path      */
+#define STS_K_NCLASSES 21
 int sts_grid_set_timing(sts_grid* g, int enable);
 
 /*

@@ -335,9 +335,10 @@ static std::vector<const double*> build_vertex_coefs(sts_grid* g, int mode, doub
 
 // one stencil pass: the TMA pipelined kernel where eligible, else the cp.async kernels
 static void launch_pass(sts_grid* g, const StencilCall& c, cudaStream_t st) {
-  const int kind = (c.epi == EPI_PCG_S) ? STS_K_ANISO_PCG_S : stencil_kind(c.mode, c.epi);
+  const int kind = (c.epi == EPI_PCG_S) ? (c.mode == STS_MODE_ANISO ? STS_K_ANISO_PCG_S : STS_K_ISO_PCG_S)
+                                        : stencil_kind(c.mode, c.epi);
   Timed t(g, kind, st);
-  if (g->tma && launch_aniso_tma(c, st)) return;
+  if (g->tma && (launch_aniso_tma(c, st) || launch_iso_tma(c, st))) return;
   if (c.epi == EPI_PCG_S) throw Error{STS_ERR_STATE, "fused PCG S-pass launched without a TMA-eligible call"};
   launch_stencil(c, st);
 }
@@ -347,6 +348,7 @@ static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 // CTAs one pass over local planes [c.ib, c.ie) launches (sizes the partial-sum rows)
 static int pass_blocks(const sts_grid* g, const StencilCall& c) {
   if (g->tma && aniso_tma_eligible(c)) return aniso_tma_blocks(c.geo, c.ib, c.ie);
+  if (g->tma && iso_tma_eligible(c)) return iso_tma_blocks(c.geo, c.ib, c.ie);
   return stencil_blocks(c.mode, c.epi, c.geo, c.ib, c.ie);
 }
 
@@ -963,14 +965,14 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     const auto ev = build_vertex_coefs(g, mode, evbase, k1, k2, k3, b, st);
     // the S-pass (p update + x update + A p) is ONE fused TMA kernel where eligible
     bool fused = false;
-    if (g->tma && mode == STS_MODE_ANISO && ncomp == 1) {
-      StencilCall c = make_call(g, g->slabs[0], mode, 1, EPI_PCG_S, z, k1, k2, k3, bb, w);
+    if (g->tma) {
+      StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
       c.u2 = view(g, g->slabs[0], H_P, pb[0]);
       c.ev = ev[0];
       c.ea.out = off(y, g->slabs[0]);
       c.ea.out2 = off(pb[1], g->slabs[0]);
       c.ea.x = off(x, g->slabs[0]);
-      fused = aniso_tma_eligible(c);
+      fused = aniso_tma_eligible(c) || iso_tma_eligible(c);
     }
     // the passes (make(si) -> StencilCall of slab si; sweep() sets the plane range and pbase)
     double* partials = nullptr;

@@ -28,13 +28,6 @@ __device__ __forceinline__ int wrapk(int k, int n3) {
   return r < 0 ? r + n3 : r;
 }
 
-// pointer to local plane il (-1..nl) of component c of a field (nullptr if absent)
-__device__ __forceinline__ const double* plane_ptr(const FieldV& f, const Geo& G, int il, int c) {
-  if (il < 0) return f.lo ? f.lo + (long long)c * G.plane : nullptr;
-  if (il >= G.nl) return f.hi ? f.hi + (long long)c * G.plane : nullptr;
-  return f.p + (long long)c * G.cstride + (long long)il * G.plane;
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

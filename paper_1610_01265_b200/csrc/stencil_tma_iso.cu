@@ -1,0 +1,395 @@
+// TMA + mbarrier pipelined isotropic 7-point stencil pass, ncomp <= 3 (sm_100a).
+//
+// Operator (R2, PAPER.md:181 boxed viscosity term (1/rho) div(nu rho grad v)
+// component-wise, PAPER.md:329 constant-coefficient heat test):
+//   (L u)_i = sum_faces K_f (u_nb - u_i),   K_f = kappa_f A_f / h_f,   F = L u / (w V)
+// with exactly the arithmetic of iso_fast_kernel (stencil.cu).
+//
+// Warp-specialised: 8 consumer warps own an 8 x 32 (theta x phi) tile of cell
+// columns and march along r; one producer warp streams one "package" per r-plane
+// into a 3-slot shared-memory ring with cp.async.bulk.tensor (TMA):
+//   per component of each staged source field: 36 x 10 box from (k0-2, j0-1)
+//        (+ 2-column periodic-wrap boxes on the edge tiles),
+//   theta-face diffusivity k2: 32 x 9 from (k0, j0-1); phi-face k3: 34 x 8 from
+//   (k0-2, j0) (+ wrap), r-face k1 and w: 32 x 8, epilogue operands: 32 x 8 each.
+// Every box origin column is even (16 B aligned, see tma.cuh).  A full mbarrier per
+// slot signals "landed", an empty mbarrier (one arrival per consumer warp) signals
+// "free"; there is no CTA-wide barrier in the march.  The r-neighbours of the own
+// column (planes il +- 1, possibly the neighbour slab's halo plane) come from
+// registers, prefetched two planes ahead with plain loads.
+// Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2), and the
+// fused PCG S-pass p = z + beta pold, x += ax pold, y = A p, p.y (Fig. 1).
+#include "sts_common.cuh"
+#include "tma.cuh"
+
+namespace sts {
+
+using namespace tma;
+
+namespace {
+
+constexpr int IJ = 8, IK = 32;            // tile rows x cols = consumer warps x lanes
+constexpr int INT = IJ * IK;              // consumer threads
+constexpr int ITHREADS = INT + 32;        // + producer warp
+constexpr int IXTS = 3;                   // ring slots
+constexpr int SBW = 36, SBH = 10;         // staged source box
+constexpr int S_MAIN = 368;               // 360 -> 368 doubles (128 B multiple)
+constexpr int S_W = 32;                   // 2 x 10 wrap box -> 32
+constexpr int K2W = 32, K2H = 9, K2SZ = 288;
+constexpr int K3W = 34, K3H = 8, K3SZ = 272;
+constexpr int K3WR = 16;                  // 2 x 8 wrap box
+constexpr int OWN = 256;                  // 32 x 8 own box
+
+template <int EPI, int NC>
+struct IsoLay {
+  static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : 1;                               // z, pold
+  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 * NC : (EPI == EPI_PCG_S ? NC : 0);
+  static constexpr int SRC = 0;                                    // [f][c] main boxes
+  static constexpr int SRCW = SRC + nsrcf * NC * S_MAIN;           // [f][c][side] wrap boxes
+  static constexpr int K2 = SRCW + nsrcf * NC * 2 * S_W;
+  static constexpr int K3 = K2 + K2SZ;
+  static constexpr int K3R = K3 + K3SZ;
+  static constexpr int K1 = K3R + K3WR;
+  static constexpr int WB = K1 + OWN;
+  static constexpr int EP = WB + OWN;
+  static constexpr int SLOT = EP + nepi * OWN;
+  static constexpr size_t SMEM = (size_t)IXTS * SLOT * sizeof(double) + 2 * IXTS * sizeof(uint64_t) + 128;
+};
+
+}  // namespace
+
+struct IsoTmaArgs {
+  CUtensorMap src[2];     // staged sources (u | z, pold), 3D (n3, n2, NC nl), box 36 x 10
+  CUtensorMap srcw[2];    // their wrap columns, box 2 x 10
+  CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x9, 34x8, 2x8, 32x8, 32x8
+  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 8
+  int has_w;
+};
+
+template <int EPI, int NC>
+__global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int ic,
+                                                              const __grid_constant__ IsoTmaArgs ta) {
+  using Lay = IsoLay<EPI, NC>;
+  extern __shared__ __align__(128) double smi[];
+  double* ring = smi;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smi + IXTS * Lay::SLOT);
+  uint64_t* empty = full + IXTS;
+  const Geo& G = c.geo;
+  const Metrics& M = G.m;
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.y * IJ, k0 = blockIdx.x * IK;
+  const int ib = c.ib + blockIdx.z * ic;
+  const int ie = min(ib + ic, c.ie);
+  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  const bool per = G.periodic3 != 0;
+  const bool wrapL = per && k0 == 0;
+  const bool wrapR = per && (k0 + IK >= G.n3);
+  const bool first = (EPI == EPI_PCG_S) && c.ea.first;
+
+  bool skip[NC];
+  bool all = true;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    skip[q] = (EPI == EPI_PCG_S) && c.ea.sc && c.ea.sc[q].done;
+    all = all && skip[q];
+  }
+  if (EPI == EPI_PCG_S && all) return;
+  double beta[NC], axv[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    beta[q] = (EPI == EPI_PCG_S && !first) ? c.ea.sc[q].beta : 0.0;
+    axv[q] = (EPI == EPI_PCG_S && !first) ? c.ea.sc[q].ax : 0.0;
+  }
+
+  if (tid == 0) {
+    for (int s = 0; s < IXTS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, IJ);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // ======================= producer warp =======================
+  if (tid >= INT) {
+    if (tid != INT) return;
+    const int nsrcf_now = (EPI == EPI_PCG_S && first) ? 1 : Lay::nsrcf;
+    const int cpl = (int)(G.cstride / G.plane);   // planes per component of the (whole local) array
+    uint32_t bytes = nsrcf_now * NC * SBW * SBH * 8 + (K2SZ + K3W * K3H + OWN) * 8;
+    if (wrapL) bytes += nsrcf_now * NC * 2 * SBH * 8 + 2 * K3H * 8;
+    if (wrapR) bytes += nsrcf_now * NC * 2 * SBH * 8;
+    if (ta.has_w) bytes += OWN * 8;
+    bytes += Lay::nepi * OWN * 8;
+    for (int p = ib; p < ie; ++p) {
+      const int slot = (p - ib) % IXTS, n = (p - ib) / IXTS;
+      if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
+      double* S = ring + slot * Lay::SLOT;
+      uint64_t* bar = full + slot;
+      fence_proxy_async();
+      mbar_expect_tx(bar, bytes);
+      for (int f = 0; f < nsrcf_now; ++f)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          const int pl = q * cpl + p;
+          tma3(S + Lay::SRC + (f * NC + q) * S_MAIN, &ta.src[f], k0 - 2, j0 - 1, pl, bar);
+          if (wrapL) tma3(S + Lay::SRCW + ((f * NC + q) * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
+          if (wrapR) tma3(S + Lay::SRCW + ((f * NC + q) * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
+        }
+      tma3(S + Lay::K2, &ta.k2, k0, j0 - 1, p, bar);
+      tma3(S + Lay::K3, &ta.k3, k0 - 2, j0, p, bar);
+      if (wrapL) tma3(S + Lay::K3R, &ta.k3w, G.n3 - 2, j0, p, bar);
+      tma3(S + Lay::K1, &ta.k1, k0, j0, p, bar);
+      if (ta.has_w) tma3(S + Lay::WB, &ta.w, k0, j0, p, bar);
+#pragma unroll
+      for (int q = 0; q < Lay::nepi; ++q) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const int tj = tid >> 5, tk = tid & 31;
+  const int j = j0 + tj, k = k0 + tk;
+  const bool own = (j < G.n2) && (k < G.n3);
+  const long long coff = own ? (long long)j * G.n3 + k : 0;
+  const bool jm = j >= 1, jp = j + 1 < G.n2;
+  const bool kself = per && G.n3 == 1;
+  const bool km = !kself && (per || k >= 1), kp = !kself && (per || k + 1 < G.n3);
+  const int kmw = per ? (k >= 1 ? k - 1 : G.n3 - 1) : k - 1;
+  double f1tp = 0, f2p = 0, f2m = 0, f3p = 0, f3m = 0, vtp = 0;
+  if (own) {
+    f1tp = M.F1t[j] * M.F1p[k];
+    f2p = jp ? M.F2t[j] * M.F2p[k] : 0.0;
+    f2m = jm ? M.F2t[j - 1] * M.F2p[k] : 0.0;
+    f3p = kp ? M.F3t[j] * M.F3p[k] : 0.0;
+    f3m = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
+    vtp = M.Vt[j] * M.Vp[k];
+  }
+  // slot offsets of the own cell and its in-plane neighbours (source boxes: row tj+1, col tk+2);
+  // periodic phi wrap: cell n3-1 / cell 0 come from the 2-column wrap boxes
+  const int oc = (tj + 1) * SBW + tk + 2;
+  const bool kmw_box = per && k - 1 == -1, kpw_box = per && k + 1 == G.n3;
+  // source value of component q at main-box offset o, or from a wrap box (side 0: col n3-1, 1: col 0)
+  auto sv = [&](const double* S, int q, int o, bool wbox, int side) {
+    const int ff = wbox ? Lay::SRCW + (q * 2 + side) * S_W : Lay::SRC + q * S_MAIN;
+    const int oo = wbox ? (tj + 1) * 2 + (side == 0 ? 1 : 0) : o;
+    const double z = S[ff + oo];
+    if constexpr (EPI == EPI_PCG_S) {
+      if (!first) {
+        const int fp = wbox ? Lay::SRCW + ((NC + q) * 2 + side) * S_W : Lay::SRC + (NC + q) * S_MAIN;
+        return fma(beta[q], S[fp + oo], z);
+      }
+    }
+    return z;
+  };
+  // own-column value of plane il (il in [-1, nl]) through global memory (halo planes included)
+  auto col = [&](int il, int q) -> double {
+    if (!own) return 0.0;
+    const int ig = G.i0 + il;
+    if (ig < 0 || ig >= G.n1g) return 0.0;
+    const double* pz = plane_ptr(c.u, G, il, q);
+    if (!pz) return 0.0;
+    double v = __ldg(pz + coff);
+    if constexpr (EPI == EPI_PCG_S) {
+      if (!first) v = fma(beta[q], __ldg(plane_ptr(c.u2, G, il, q) + coff), v);
+    }
+    return v;
+  };
+
+  double udn[NC], uup[NC], unx[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    udn[q] = col(ib - 1, q);
+    uup[q] = col(ib + 1, q);
+    unx[q] = 0.0;
+  }
+  const int ig0 = G.i0 + ib;
+  double kdn = 0.0;
+  if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
+  double part[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) part[q] = 0.0;
+
+  for (int il = ib; il < ie; ++il) {
+    const int slot = (il - ib) % IXTS;
+    const double* S = ring + slot * Lay::SLOT;
+    // prefetch the own column two planes ahead (consumed next step)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) unx[q] = (il + 2 <= ie) ? col(il + 2, q) : 0.0;
+    mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
+    const int ig = G.i0 + il;
+    const bool ip = ig + 1 < G.n1g;
+    double Kup = 0.0;
+    if (own) {
+      const int o8 = tj * IK + tk;
+      const double f23r = M.F2r[ig], f3r = M.F3r[ig];
+      Kup = ip ? S[Lay::K1 + o8] * M.F1r[ig] * f1tp : 0.0;
+      const double Kjp = jp ? S[Lay::K2 + (tj + 1) * K2W + tk] * f23r * f2p : 0.0;
+      const double Kjm = jm ? S[Lay::K2 + tj * K2W + tk] * f23r * f2m : 0.0;
+      const double Kkp = kp ? S[Lay::K3 + tj * K3W + tk + 2] * f3r * f3p : 0.0;
+      const double k3m = kmw_box ? S[Lay::K3R + tj * 2 + 1] : S[Lay::K3 + tj * K3W + tk + 1];
+      const double Kkm = km ? k3m * f3r * f3m : 0.0;
+      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * M.Vr[ig] * vtp;
+      const long long gi = (long long)il * G.plane + coff;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        const double u0 = sv(S, q, oc, false, 0);
+        const double ujm = sv(S, q, oc - SBW, false, 0), ujp = sv(S, q, oc + SBW, false, 0);
+        const double ukm = sv(S, q, oc - 1, kmw_box, 0), ukp = sv(S, q, oc + 1, kpw_box, 1);
+        const double Lu = kdn * (udn[q] - u0) + Kup * (uup[q] - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
+                          Kkm * (ukm - u0) + Kkp * (ukp - u0);
+        const long long go = gi + (long long)q * G.cstride;
+        if (!skip[q]) {
+          if constexpr (EPI == EPI_F) {
+            c.ea.out[go] = Lu / WV;
+          } else if constexpr (EPI == EPI_RKL2_FIRST) {
+            const double F = Lu / WV;
+            c.ea.out2[go] = F;
+            c.ea.out[go] = u0 + c.ea.c0 * F;
+          } else if constexpr (EPI == EPI_RKL2_STAGE) {
+            const double F = Lu / WV;
+            c.ea.out[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c2 * S[Lay::EP + (NC + q) * OWN + o8] +
+                           c.ea.c0 * F + c.ea.c1 * S[Lay::EP + (2 * NC + q) * OWN + o8];
+          } else if constexpr (EPI == EPI_PCG_S) {
+            const double y = WV * u0 - c.ea.dt * Lu;
+            c.ea.out[go] = y;
+            c.ea.out2[go] = u0;                                   // p_k
+            if (!first) {
+              const double po = S[Lay::SRC + (NC + q) * S_MAIN + oc];
+              c.ea.x[go] = fma(axv[q], po, S[Lay::EP + q * OWN + o8]);
+            }
+            part[q] += u0 * y;
+          }
+        }
+        udn[q] = u0;
+      }
+    }
+    __syncwarp();
+    if (tk == 0) mbar_arrive(empty + slot);       // this warp is done with the slot
+    kdn = Kup;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      uup[q] = unx[q];
+    }
+  }
+  if constexpr (EPI == EPI_PCG_S) {
+    __shared__ double red[NC][IJ];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double v = part[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tk == 0) red[q][tj] = v;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory");   // consumer warps only
+    if (tid < NC) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < IJ; ++w) s += red[tid][w];
+      c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
+    }
+  }
+}
+
+// ============================================================================
+// host side
+// ============================================================================
+static bool iso_has_tma(int epi) {
+  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S;
+}
+
+bool iso_tma_eligible(const StencilCall& c) {
+  if (c.mode != STS_MODE_ISO || c.ncomp < 1 || c.ncomp > 3 || !iso_has_tma(c.epi)) return false;
+  const Geo& G = c.geo;
+  if (G.n3 % 2 != 0) return false;
+  if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
+  if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
+  return true;
+}
+
+static dim3 iso_grid(const Geo& G, int ib, int ie, int* ic_out) {
+  const int nbx = (G.n3 + IK - 1) / IK, nby = (G.n2 + IJ - 1) / IJ;
+  const int np = ie - ib;
+  if (np <= 0) {
+    *ic_out = 1;
+    return dim3(0, 0, 0);
+  }
+  const long long tiles = (long long)nbx * nby;
+  const long long want = 148LL * 2 * 8;          // >= ~8 waves of 2 resident CTAs per SM
+  int ic = (int)((np * tiles + want - 1) / want);
+  ic = ic < 32 ? 32 : ic;
+  if (ic > 128) ic = 128;
+  if (ic > np) ic = np;
+  *ic_out = ic;
+  return dim3(nbx, nby, (np + ic - 1) / ic);
+}
+
+int iso_tma_blocks(const Geo& G, int ib, int ie) {
+  int ic;
+  const dim3 g = iso_grid(G, ib, ie, &ic);
+  return (int)(g.x * g.y * g.z);
+}
+
+template <int EPI, int NC>
+static void launch_iso_t(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)IsoLay<EPI, NC>::SMEM));
+    attr = true;
+  }
+  iso_tma_kernel<EPI, NC><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+}
+
+template <int EPI>
+static void launch_iso_nc(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+  switch (c.ncomp) {
+    case 1: launch_iso_t<EPI, 1>(c, grid, ic, ta, st); break;
+    case 2: launch_iso_t<EPI, 2>(c, grid, ic, ta, st); break;
+    case 3: launch_iso_t<EPI, 3>(c, grid, ic, ta, st); break;
+    default: throw Error{STS_ERR_ARG, "ncomp must be 1..3"};
+  }
+}
+
+bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
+  if (!iso_tma_eligible(c)) return false;
+  const Geo& G = c.geo;
+  int ic = 1;
+  const dim3 grid = iso_grid(G, c.ib, c.ie, &ic);
+  if (grid.x == 0) return true;
+  const int NC = c.ncomp;
+  // component q of a [ncomp][nl_local][plane] array starts cpl planes after q-1; a virtual
+  // slab's base is offset into component 0, so the map spans (NC-1) cpl + nl planes from it
+  const int cpl = (int)(G.cstride / G.plane);
+  const int npl = (NC - 1) * cpl + G.nl;
+  IsoTmaArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  const double* srcs[2] = {c.u.p, c.u2.p ? c.u2.p : c.u.p};
+  for (int f = 0; f < 2; ++f) {
+    map_plain(&ta.src[f], srcs[f], G, npl, SBW, SBH);
+    map_plain(&ta.srcw[f], srcs[f], G, npl, 2, SBH);
+  }
+  map_plain(&ta.k2, c.k2.p, G, G.nl, K2W, K2H);
+  map_plain(&ta.k3, c.k3.p, G, G.nl, K3W, K3H);
+  map_plain(&ta.k3w, c.k3.p, G, G.nl, 2, K3H);
+  map_plain(&ta.k1, c.k1.p, G, G.nl, IK, IJ);
+  map_plain(&ta.w, c.w ? c.w : c.k1.p, G, G.nl, IK, IJ);
+  ta.has_w = c.w != nullptr;
+  if (c.epi == EPI_RKL2_STAGE) {
+    map_plain(&ta.epi[0], c.ea.ym2, G, npl, IK, IJ);
+    map_plain(&ta.epi[1], c.ea.y0, G, npl, IK, IJ);
+    map_plain(&ta.epi[2], c.ea.m0, G, npl, IK, IJ);
+  } else if (c.epi == EPI_PCG_S) {
+    map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
+  }
+  switch (c.epi) {
+    case EPI_F: launch_iso_nc<EPI_F>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_FIRST: launch_iso_nc<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_STAGE: launch_iso_nc<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
+    case EPI_PCG_S: launch_iso_nc<EPI_PCG_S>(c, grid, ic, ta, st); break;
+    default: return false;
+  }
+  STS_CUDA(cudaGetLastError());
+  return true;
+}
+
+}  // namespace sts

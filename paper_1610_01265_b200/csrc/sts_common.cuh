@@ -145,6 +145,13 @@ struct sts_grid {
 
 namespace sts {
 
+// pointer to local plane il (-1..nl) of component c of a field (nullptr if absent)
+__device__ __forceinline__ const double* plane_ptr(const FieldV& f, const Geo& G, int il, int c) {
+  if (il < 0) return f.lo ? f.lo + (long long)c * G.plane : nullptr;
+  if (il >= G.nl) return f.hi ? f.hi + (long long)c * G.plane : nullptr;
+  return f.p + (long long)c * G.cstride + (long long)il * G.plane;
+}
+
 Geo slab_geo(const sts_grid* g, const Slab& s);
 double* ws_get(sts_grid* g, size_t bytes);  // scratch of at least `bytes`, reused across calls
 
@@ -223,6 +230,10 @@ __host__ __device__ inline long long ev_cstride(int nl, int n2, int n3) { return
 bool aniso_tma_eligible(const StencilCall& c);
 bool launch_aniso_tma(const StencilCall& c, cudaStream_t st);
 int aniso_tma_blocks(const Geo& G, int ib, int ie);
+// the isotropic (ncomp <= 3) counterpart (stencil_tma_iso.cu)
+bool iso_tma_eligible(const StencilCall& c);
+bool launch_iso_tma(const StencilCall& c, cudaStream_t st);
+int iso_tma_blocks(const Geo& G, int ib, int ie);
 // PCG pointwise passes of the restructured iteration (aux.cu)
 // pnew = z + beta pold (pold unused if first); x += ax pold (not if first)
 void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, const double* z, const double* pold,

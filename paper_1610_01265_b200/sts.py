@@ -26,7 +26,7 @@ UID_BYTES = 128
 KERNEL_CLASSES = ["face_kappa", "aniso_F", "aniso_rkl2_first", "aniso_rkl2_stage", "aniso_pcg_r0",
                   "aniso_pcg_ap", "aniso_gersh", "iso_F", "iso_rkl2_first", "iso_rkl2_stage", "iso_pcg_r0",
                   "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo",
-                  "vertex_coef", "aniso_pcg_s", "pcg_xfinal"]
+                  "vertex_coef", "aniso_pcg_s", "pcg_xfinal", "iso_pcg_s"]
 
 _lib = None
 

@@ -359,6 +359,50 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
     assert rel_l2(outs[True][1], outs[False][1]) <= 1e-12
 
 
+ISO_CASES = [((20, 19, 70), True, 1, 3), ((13, 17, 64), False, 1, 3), ((5, 9, 2), True, 1, 2), ((9, 16, 96), True, 1, 1),
+             ((21, 19, 62), True, 3, 3), ((12, 8, 40), False, 2, 2), ((7, 23, 33), True, 1, 3)]
+
+
+@pytest.mark.parametrize("shape,periodic,nv,nc", ISO_CASES)
+def test_iso_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv, nc):
+    """Isotropic weighted (viscosity-type) operator, 1-3 components: warp-specialised
+    TMA kernels (even n3) vs cp.async kernels vs the oracle, RKL2 and BE+PCG."""
+    g = sph(shape, periodic=periodic)
+    rng = np.random.default_rng(zlib.crc32(repr(("iso", shape, periodic, nv, nc)).encode()))
+    k = [rng.uniform(0.5, 2.0, g.shape) for _ in range(3)]
+    w = rng.uniform(0.5, 2.0, g.shape)
+    v = rng.normal(size=(nc,) + g.shape)
+    op = O.Operator(g, k, None, w)
+    dte = O.dt_euler(op)
+    dt = 200.0 * dte
+    s = O.rkl2_num_stages(dt, dte)
+    ref = O.rkl2_advance(op.apply, v, dt, s)
+    ref_be, it_ref = O.be_pcg_solve(op, v, dt, rtol=1e-12)
+    import scipy.sparse.linalg as spl
+    A = O.be_system(op, dt).tocsc()
+    exact = np.stack([spl.spsolve(A, op.WV * x.ravel()).reshape(g.shape) for x in v])
+    tol_be = max(1e-11, rel_l2(ref_be, exact))
+    kd = [torch.as_tensor(x).to(dev) for x in k]
+    wd = torch.as_tensor(w).to(dev)
+    vd = torch.as_tensor(v).to(dev)
+    if nc == 1:
+        vd = vd[0].contiguous()
+    outs = {}
+    for tma in (True, False):
+        G = sts().Grid.from_grid(g, n_virtual=nv)
+        G.set_tma(tma)
+        F = G.op_apply("iso", vd, kd, None, wd)
+        assert rel_l2(cpu(F).reshape(v.shape), op.apply(v)) <= 1e-12, tma
+        u = G.rkl2_advance("iso", vd, kd, None, wd, dt, s)
+        x, it = G.be_pcg_solve("iso", vd, kd, None, wd, dt, 1e-12, 10000)
+        assert rel_l2(cpu(u).reshape(v.shape), ref) <= 1e-11, tma
+        assert rel_l2(cpu(x).reshape(v.shape), ref_be) <= tol_be, tma
+        assert all(abs(a - b) <= 1 for a, b in zip(it, it_ref)), (tma, it, it_ref)
+        outs[tma] = (cpu(u), cpu(x))
+    assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
+    assert rel_l2(outs[True][1], outs[False][1]) <= 1e-12
+
+
 def test_smoke_entry(dev):
     import __graft_entry__ as e
     e.smoke()
