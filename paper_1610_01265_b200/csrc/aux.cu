@@ -200,7 +200,37 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
   double acc[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) acc[q] = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+  // U unrolled elements per thread and trip, every load of a trip issued before any use
+  constexpr int U = 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; e + (U - 1) * stride < n; e += U * stride) {
+    double de[U], rr[NC][U], yy[NC][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) de[u] = __ldcs(d + e + u * stride);
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long o = e + u * stride + q * cs;
+        rr[q][u] = act[q] ? __ldcs(r + o) : 0.0;
+        yy[q][u] = act[q] ? __ldcs(y + o) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      if (!act[q]) continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long o = e + u * stride + q * cs;
+        const double rn = rr[q][u] - alpha[q] * yy[q][u];
+        const double zn = rn * de[u];
+        __stcs(r + o, rn);
+        __stcs(z + o, zn);
+        acc[q] += rn * zn;
+      }
+    }
+  }
+  for (; e < n; e += stride) {
     const double de = d[e];
 #pragma unroll
     for (int q = 0; q < NC; ++q) {

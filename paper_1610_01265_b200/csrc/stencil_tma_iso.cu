@@ -181,26 +181,31 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     }
     return z;
   };
-  // own-column value of plane il (il in [-1, nl]) through global memory (halo planes included)
-  auto col = [&](int il, int q) -> double {
+  // own-column raw values of plane il (il in [-1, nl]) through global memory (halo planes
+  // included): source (u | z) and, for the PCG S-pass, pold.  Combined (p = z + beta pold)
+  // only when used, so a prefetch two planes ahead does not stall on its own load.
+  auto colraw = [&](const FieldV& f, int il, int q) -> double {
     if (!own) return 0.0;
     const int ig = G.i0 + il;
     if (ig < 0 || ig >= G.n1g) return 0.0;
-    const double* pz = plane_ptr(c.u, G, il, q);
-    if (!pz) return 0.0;
-    double v = __ldg(pz + coff);
-    if constexpr (EPI == EPI_PCG_S) {
-      if (!first) v = fma(beta[q], __ldg(plane_ptr(c.u2, G, il, q) + coff), v);
+    const double* pz = plane_ptr(f, G, il, q);
+    return pz ? __ldg(pz + coff) : 0.0;
+  };
+  constexpr bool kP = (EPI == EPI_PCG_S);
+  auto comb = [&](double z, double po, int q) {
+    if constexpr (kP) {
+      if (!first) return fma(beta[q], po, z);
     }
-    return v;
+    return z;
   };
 
-  double udn[NC], uup[NC], unx[NC];
+  double udn[NC], uupz[NC], uupp[NC], unz[NC], unp[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    udn[q] = col(ib - 1, q);
-    uup[q] = col(ib + 1, q);
-    unx[q] = 0.0;
+    udn[q] = comb(colraw(c.u, ib - 1, q), (kP && !first) ? colraw(c.u2, ib - 1, q) : 0.0, q);
+    uupz[q] = colraw(c.u, ib + 1, q);
+    uupp[q] = (kP && !first) ? colraw(c.u2, ib + 1, q) : 0.0;
+    unz[q] = unp[q] = 0.0;
   }
   const int ig0 = G.i0 + ib;
   double kdn = 0.0;
@@ -214,7 +219,10 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     const double* S = ring + slot * Lay::SLOT;
     // prefetch the own column two planes ahead (consumed next step)
 #pragma unroll
-    for (int q = 0; q < NC; ++q) unx[q] = (il + 2 <= ie) ? col(il + 2, q) : 0.0;
+    for (int q = 0; q < NC; ++q) {
+      unz[q] = (il + 2 <= ie) ? colraw(c.u, il + 2, q) : 0.0;
+      unp[q] = (kP && !first && il + 2 <= ie) ? colraw(c.u2, il + 2, q) : 0.0;
+    }
     mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
     const int ig = G.i0 + il;
     const bool ip = ig + 1 < G.n1g;
@@ -235,7 +243,8 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
         const double u0 = sv(S, q, oc, false, 0);
         const double ujm = sv(S, q, oc - SBW, false, 0), ujp = sv(S, q, oc + SBW, false, 0);
         const double ukm = sv(S, q, oc - 1, kmw_box, 0), ukp = sv(S, q, oc + 1, kpw_box, 1);
-        const double Lu = kdn * (udn[q] - u0) + Kup * (uup[q] - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
+        const double uup = comb(uupz[q], uupp[q], q);
+        const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
         const long long go = gi + (long long)q * G.cstride;
         if (!skip[q]) {
@@ -268,7 +277,8 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     kdn = Kup;
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
-      uup[q] = unx[q];
+      uupz[q] = unz[q];
+      uupp[q] = unp[q];
     }
   }
   if constexpr (EPI == EPI_PCG_S) {
