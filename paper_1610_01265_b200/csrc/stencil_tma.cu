@@ -40,24 +40,23 @@ using namespace tma;
 
 namespace {
 
-constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= warps / lanes)
+constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= consumer warps / lanes)
 constexpr int XOJ = XJ - 1, XOK = XK - 1;   // output rows / cols
-constexpr int XNT = XJ * XK;
-constexpr int XTS = 3;                      // ring slots (packages in flight = XTS - 1)
+constexpr int XNT = XJ * XK;                // consumer threads
+constexpr int XTHREADS = XNT + 32;          // + producer warp
+constexpr int XTS = 4;                      // ring slots (packages in flight = XTS - 1)
 constexpr int UBW = 36, UBH = 9;            // staged-source box (cols x rows)
 constexpr int EBW = 34;                     // vertex-coefficient box cols
 constexpr int MAXSRC = 2;                   // staged sources (PCG S-pass: z, pold)
 constexpr int MAXOWN = 4;                   // epilogue operand boxes
-// slot layout (doubles); every part starts on a 128 B boundary
+// slot parts (doubles); every part starts on a 128 B boundary
 constexpr int U_MAIN = 336;                 // 9 x 36 = 324 -> 336
 constexpr int U_WL = 32, U_WR = 32;         // 9 x 2 = 18 -> 32
 constexpr int U_FIELD = U_MAIN + U_WL + U_WR;
 constexpr int E_COMP = XJ * EBW;            // 8 x 34 = 272 (2176 B)
 constexpr int E_PART = 3 * E_COMP;
 constexpr int O_PART = XOJ * XK;            // 7 x 32 = 224
-constexpr int SLOT = MAXSRC * U_FIELD + E_PART + MAXOWN * O_PART;   // 2512 doubles = 19.6 KB
 constexpr int VBUF = 3 * XNT;               // A, B, C of one vertex plane
-constexpr size_t TMA_SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 64;
 
 }  // namespace
 
@@ -70,83 +69,99 @@ struct TmaArgs {
   CUtensorMap e;              // vertex coefficients, 3D (n3+2, n2+1, 3 (nl+1)), box 34 x 8 x 1
                               // (a 4D map with the component as 4th dim faults on sm_100a)
   CUtensorMap own[MAXOWN];    // epilogue operands, 3D (n3, n2, nl),   box 32 x 7 x 1
-  int nsrc, nown, has_lo, has_hi;
-  int dbg;   // bisection switches (STS_TMA_DBG): 1 no src, 2 no wrap, 4 no e, 8 no own, 16 return early,
-             // 32 return after mbarrier init, 64 no waits
+  int has_lo, has_hi;
 };
 
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
 enum { OW_X = 0 };                           // PCG S-pass
-template <int EPI>
-struct TmaEpi {
+// slot layout of one (epilogue, has-w) variant
+template <int EPI, bool W>
+struct TmaLay {
   static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : 1;
-  static constexpr int nown = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : 0);   // + w if present
+  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : 0);
+  static constexpr int nown = nepi + (W ? 1 : 0);             // w is the last own box
+  static constexpr int E = nsrc * U_FIELD;
+  static constexpr int O = E + E_PART;
+  static constexpr int SLOT = O + nown * O_PART;
+  static constexpr size_t SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 2 * XTS * sizeof(uint64_t) + 128;
 };
 
-template <int EPI>
-__global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic, const __grid_constant__ TmaArgs ta) {
+template <int EPI, bool W>
+__global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, int ic,
+                                                                const __grid_constant__ TmaArgs ta) {
+  using Lay = TmaLay<EPI, W>;
   extern __shared__ __align__(128) double smx[];
   double* ring = smx;                               // [XTS][SLOT]
-  double* vbuf = smx + XTS * SLOT;                  // [2][3][XNT]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vbuf + 2 * VBUF);
+  double* vbuf = smx + XTS * Lay::SLOT;             // [2][3][XNT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(vbuf + 2 * VBUF);
+  uint64_t* empty = full + XTS;
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
-  const int vj = tid >> 5, vk = tid & 31;
   const int j0 = blockIdx.y * XOJ, k0 = blockIdx.x * XOK;
   const int ib = c.ib + blockIdx.z * ic;
   const int ie = min(ib + ic, c.ie);
   const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
-  constexpr int NSRC = TmaEpi<EPI>::nsrc;
-  const int nown = ta.nown;                         // TmaEpi::nown (+1 with w)
-  const int ow_w = nown - (c.w ? 1 : 0);            // slot of w if present
 
   if constexpr (EPI == EPI_PCG_S) {
     if (c.ea.sc && c.ea.sc[0].done) return;
   }
-  if (ta.dbg & 16) return;
   const bool first = (EPI == EPI_PCG_S) && c.ea.first;
-  const double beta = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].beta : 0.0;
-  const double ax = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].ax : 0.0;
   const bool per = G.periodic3 != 0;
   const bool wrapL = per && k0 == 0;
   const bool wrapR = per && (k0 + 32 >= G.n3);
   const int ou = (k0 - 1) & ~1;                     // even box origins (floor, also for -1 -> -2)
   const int oe = k0 & ~1, se = k0 - oe;             // e / epilogue boxes and their column shift
 
-  // ---- producer: thread 0 issues package Q(p) ----
-  auto issue = [&](int p) {
-    const int slot = (p - ib + 1) % XTS;
-    double* S = ring + slot * SLOT;
-    uint64_t* bar = bars + slot;
-    const bool lo = p < 0, hi = p >= G.nl;
-    const bool halo = (lo && ta.has_lo) || (hi && ta.has_hi);
-    const int pc = halo ? (lo ? 0 : MAXC) : p;      // no neighbour: OOB plane -> zeros
-    const int nsrc_now = (EPI == EPI_PCG_S && first) ? 1 : NSRC;
-    const bool dsrc = !(ta.dbg & 1), dwrap = !(ta.dbg & 2);
-    uint32_t bytes = dsrc ? nsrc_now * UBW * UBH * 8 : 0;
-    if (wrapL && dwrap) bytes += nsrc_now * 2 * UBH * 8;
-    if (wrapR && dwrap) bytes += nsrc_now * 2 * UBH * 8;
-    const bool has_e = p >= ib && !(ta.dbg & 4), has_own = p >= ib + 1 && !(ta.dbg & 8);
-    if (has_e) bytes += E_PART * 8;
-    if (has_own) bytes += nown * XOJ * XK * 8;
-    fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    for (int f = 0; f < nsrc_now; ++f) {
-      double* D = S + f * U_FIELD;
-      if (dsrc) tma3(D, halo ? &ta.srch[f] : &ta.src[f], ou, j0 - 1, pc, bar);
-      if (!dwrap) continue;
-      if (wrapL) tma3(D + U_MAIN, halo ? &ta.srchw[f] : &ta.srcw[f], G.n3 - 2, j0 - 1, pc, bar);
-      if (wrapR) tma3(D + U_MAIN + U_WL, halo ? &ta.srchw[f] : &ta.srcw[f], 0, j0 - 1, pc, bar);
+  if (tid == 0) {
+    for (int s = 0; s < XTS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, XJ);
     }
-    if (has_e)   // vertex plane p-1 = ev plane index p (row jv+1), one 3D box per component
-      for (int a = 0; a < 3; ++a) tma3(S + MAXSRC * U_FIELD + a * E_COMP, &ta.e, oe, j0, a * (G.nl + 1) + p, bar);
-    if (has_own)
-      for (int q = 0; q < nown; ++q) tma3(S + MAXSRC * U_FIELD + E_PART + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
-  };
+    mbar_fence_init();
+  }
+  __syncthreads();
 
-  // ---- per-thread geometry ----
+  // ======================= producer warp: package Q(p), p = ib-1 .. ie =======================
+  if (tid >= XNT) {
+    if (tid != XNT) return;
+    const int nsrc_now = (EPI == EPI_PCG_S && first) ? 1 : Lay::nsrc;
+    for (int p = ib - 1; p <= ie; ++p) {
+      const int slot = (p - ib + 1) % XTS, n = (p - ib + 1) / XTS;
+      if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
+      double* S = ring + slot * Lay::SLOT;
+      uint64_t* bar = full + slot;
+      const bool lo = p < 0, hi = p >= G.nl;
+      const bool halo = (lo && ta.has_lo) || (hi && ta.has_hi);
+      const int pc = halo ? (lo ? 0 : MAXC) : p;    // no neighbour: OOB plane -> zeros
+      const bool has_e = p >= ib, has_own = p >= ib + 1;
+      uint32_t bytes = nsrc_now * UBW * UBH * 8;
+      if (wrapL) bytes += nsrc_now * 2 * UBH * 8;
+      if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
+      if (has_e) bytes += E_PART * 8;
+      if (has_own) bytes += Lay::nown * XOJ * XK * 8;
+      fence_proxy_async();
+      mbar_expect_tx(bar, bytes);
+      for (int f = 0; f < nsrc_now; ++f) {
+        double* D = S + f * U_FIELD;
+        tma3(D, halo ? &ta.srch[f] : &ta.src[f], ou, j0 - 1, pc, bar);
+        if (wrapL) tma3(D + U_MAIN, halo ? &ta.srchw[f] : &ta.srcw[f], G.n3 - 2, j0 - 1, pc, bar);
+        if (wrapR) tma3(D + U_MAIN + U_WL, halo ? &ta.srchw[f] : &ta.srcw[f], 0, j0 - 1, pc, bar);
+      }
+      if (has_e)   // vertex plane p-1 = ev plane index p (row jv+1), one 3D box per component
+        for (int a = 0; a < 3; ++a) tma3(S + Lay::E + a * E_COMP, &ta.e, oe, j0, a * (G.nl + 1) + p, bar);
+      if (has_own)
+#pragma unroll
+        for (int q = 0; q < Lay::nown; ++q) tma3(S + Lay::O + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const int vj = tid >> 5, vk = tid & 31;
+  const double beta = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].beta : 0.0;
+  const double ax = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].ax : 0.0;
   const int jv = j0 - 1 + vj;                       // vertex row (jv + 1/2)
   const double ig3a = (jv >= 0 && jv < G.n2) ? M.iG3[jv] : 0.0;
   const double ig3b = (jv + 1 >= 0 && jv + 1 < G.n2) ? M.iG3[jv + 1] : 0.0;
@@ -181,23 +196,14 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
     Fu = ig3a * (u01 - u00) + ig3b * (u11 - u10);
   };
 
-  if (tid == 0) {
-    for (int s = 0; s < XTS; ++s) mbar_init(bars + s, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (ta.dbg & 32) return;
-  if (tid == 0)
-    for (int p = ib - 1; p <= ie && p < ib - 1 + XTS; ++p) issue(p);
-
   double SuL = 0, TuL = 0, FuL = 0;
   double SAl = 0, DBl = 0, DCl = 0;
   double uc = 0.0, poc = 0.0;   // own-cell source value (and pold) of the previous plane
   double part = 0.0;
   for (int p = ib - 1; p <= ie; ++p) {
     const int slot = (p - ib + 1) % XTS;
-    const double* S = ring + slot * SLOT;
-    if (!(ta.dbg & 64)) mbar_wait(bars + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
+    const double* S = ring + slot * Lay::SLOT;
+    mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
     double SuH, TuH, FuH;
     usums(S, SuH, TuH, FuH);
     const double un = sval(S, o11);                                       // own cell of plane p
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
     double* vb = vbuf + (p & 1) * VBUF;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
-      const double* E = S + MAXSRC * U_FIELD;
+      const double* E = S + Lay::E;
       const int ei = vj * EBW + vk + se;
       const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const int iv = G.i0 + p - 1;
@@ -216,10 +222,8 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
       vb[tid] = q * er;
       vb[XNT + tid] = q * et;
       vb[2 * XNT + tid] = q * ep;
-    }
-    __syncthreads();   // vertex plane visible; every thread is done with slot of Q(p-1)
-    if (tid == 0 && p >= ib && p - 1 + XTS <= ie) issue(p - 1 + XTS);
-    if (p >= ib) {
+      // consumer warps only: the vertex plane is complete
+      asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
       double SAh = 0, DBh = 0, DCh = 0;
       if (own) {
         const double a00 = vb[tid], a01 = vb[tid + 1], a10 = vb[tid + 32], a11 = vb[tid + 33];
@@ -234,10 +238,10 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
         // output cell plane il = p-1
         const int il = p - 1;
         const int ig = G.i0 + il;
-        const double* O = S + MAXSRC * U_FIELD + E_PART + vj * XK + vk + se;
+        const double* O = S + Lay::O + vj * XK + vk + se;
         const double ig2c = M.iG2[ig];
         const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
-        const double WV = (c.w ? O[ow_w * O_PART] : 1.0) * M.Vr[ig] * vtpc;
+        const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * M.Vr[ig] * vtpc;
         const long long gi = (long long)il * G.plane + coff;
         if constexpr (EPI == EPI_F) {
           c.ea.out[gi] = Lu / WV;
@@ -261,6 +265,8 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
       DBl = DBh;
       DCl = DCh;
     }
+    __syncwarp();
+    if (vk == 0) mbar_arrive(empty + slot);   // this warp is done with the slot of Q(p)
     SuL = SuH;
     TuL = TuH;
     FuL = FuH;
@@ -272,8 +278,8 @@ __global__ void __launch_bounds__(XNT, 3) aniso_tma_kernel(StencilCall c, int ic
     double v = part;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) red[tid >> 5] = v;
-    __syncthreads();
+    if (vk == 0) red[vj] = v;
+    asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
     if (tid == 0) {
       double s = 0.0;
 #pragma unroll
@@ -322,14 +328,21 @@ int aniso_tma_blocks(const Geo& G, int ib, int ie) {
   return (int)(g.x * g.y * g.z);
 }
 
-template <int EPI>
+template <int EPI, bool W>
 static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM));
+    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TmaLay<EPI, W>::SMEM));
     attr = true;
   }
-  aniso_tma_kernel<EPI><<<grid, XNT, TMA_SMEM, st>>>(c, ic, ta);
+  aniso_tma_kernel<EPI, W><<<grid, XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
+}
+
+template <int EPI>
+static void launch_w(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
+  if (c.w) launch_t<EPI, true>(c, grid, ic, ta, st);
+  else launch_t<EPI, false>(c, grid, ic, ta, st);
 }
 
 bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
@@ -342,7 +355,6 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
   memset(&ta, 0, sizeof(ta));
   const FieldV* srcs[MAXSRC] = {&c.u, &c.u2};
   const int nsrc = (c.epi == EPI_PCG_S) ? 2 : 1;
-  ta.nsrc = nsrc;
   ta.has_lo = c.u.lo != nullptr;
   ta.has_hi = c.u.hi != nullptr;
   for (int f = 0; f < nsrc; ++f) {
@@ -376,20 +388,11 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
   }
   if (c.w) owns[nown++] = c.w;
   for (int q = 0; q < nown; ++q) map_plain(&ta.own[q], owns[q], G, G.nl, XK, XOJ);
-  ta.nown = nown;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("STS_TMA_DBG");
-      dbg = e ? atoi(e) : 0;
-    }
-    ta.dbg = dbg;
-  }
   switch (c.epi) {
-    case EPI_F: launch_t<EPI_F>(c, grid, ic, ta, st); break;
-    case EPI_RKL2_FIRST: launch_t<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
-    case EPI_RKL2_STAGE: launch_t<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
-    case EPI_PCG_S: launch_t<EPI_PCG_S>(c, grid, ic, ta, st); break;
+    case EPI_F: launch_w<EPI_F>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_FIRST: launch_w<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_STAGE: launch_w<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
+    case EPI_PCG_S: launch_w<EPI_PCG_S>(c, grid, ic, ta, st); break;
     default: return false;
   }
   STS_CUDA(cudaGetLastError());
