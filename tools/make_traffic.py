@@ -1,0 +1,56 @@
+"""DRAM traffic per cell of the hot kernels from `ncu --set full` captures.
+
+  python tools/make_traffic.py gpurun_out/prof_*.ncu-rep > profiles/ncu_traffic.json
+
+The captures come from tools/prof_kernels.sh (tools/profile_step.py: the c4 recipe
+at the c3 size 256 x 256 x 512, one launch per kernel).  bench.py multiplies the
+per-cell figure by its local cell count to fill roofline.traffic.
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+CELLS = 256 * 256 * 512
+# demangled kernel name -> bench.py kernel class
+CLASSES = [
+    (r"^void aniso_tma_kernel<2,", "aniso_rkl2_stage"),
+    (r"^void aniso_tma_kernel<5,", "aniso_pcg_s"),
+    (r"^void iso_tma_kernel<2,", "iso_rkl2_stage"),
+    (r"^void iso_tma_kernel<5,", "iso_pcg_s"),
+    (r"^void pcg_rupdate_kernel<3>", "pcg_update_c3"),
+    (r"^void pcg_rupdate_kernel<1>", "pcg_update"),
+]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def main(paths):
+    out = {"cells": CELLS, "source": "ncu --set full --clock-control none, tools/prof_kernels.sh",
+           "dram_bytes_per_cell": {}, "dram_pct": {}, "duration_us": {}}
+    for p in paths:
+        txt = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"],
+                             capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(txt)))
+        if len(rows) < 3:
+            continue
+        h, u = rows[0], rows[1]
+        for r in rows[2:]:
+            d = dict(zip(h, r))
+            name = d.get("Kernel Name", "")
+            cls = next((c for pat, c in CLASSES if re.search(pat, name)), None)
+            if cls is None:
+                continue
+            rd = float(d["dram__bytes_read.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_read.sum")]]
+            wr = float(d["dram__bytes_write.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_write.sum")]]
+            out["dram_bytes_per_cell"][cls] = round((rd + wr) / CELLS, 3)
+            out["dram_pct"][cls] = float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"].replace(",", ""))
+            dur = float(d["gpu__time_duration.sum"].replace(",", ""))
+            unit = u[h.index("gpu__time_duration.sum")]
+            out["duration_us"][cls] = dur * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1.0)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
