@@ -5,13 +5,13 @@
 //   (L u)_i = sum_faces K_f (u_nb - u_i),   K_f = kappa_f A_f / h_f,   F = L u / (w V)
 // with exactly the arithmetic of iso_fast_kernel (stencil.cu).
 //
-// Warp-specialised: 8 consumer warps own an 8 x 32 (theta x phi) tile of cell
+// Warp-specialised: 7 consumer warps own a 7 x 32 (theta x phi) tile of cell
 // columns and march along r; one producer warp streams one "package" per r-plane
 // into a 3-slot shared-memory ring with cp.async.bulk.tensor (TMA):
-//   per component of each staged source field: 36 x 10 box from (k0-2, j0-1)
+//   per component of each staged source field: 36 x 9 box from (k0-2, j0-1)
 //        (+ 2-column periodic-wrap boxes on the edge tiles),
-//   theta-face diffusivity k2: 32 x 9 from (k0, j0-1); phi-face k3: 34 x 8 from
-//   (k0-2, j0) (+ wrap), r-face k1 and w: 32 x 8, epilogue operands: 32 x 8 each.
+//   theta-face diffusivity k2: 32 x 8 from (k0, j0-1); phi-face k3: 34 x 7 from
+//   (k0-2, j0) (+ wrap), r-face k1 and w: 32 x 7, epilogue operands: 32 x 7 each.
 // Every box origin column is even (16 B aligned, see tma.cuh).  A full mbarrier per
 // slot signals "landed", an empty mbarrier (one arrival per consumer warp) signals
 // "free"; there is no CTA-wide barrier in the march.  The r-neighbours of the own
@@ -28,25 +28,32 @@ using namespace tma;
 
 namespace {
 
-constexpr int IJ = 8, IK = 32;            // tile rows x cols = consumer warps x lanes
+// 7 consumer warps + 1 producer = 8 warps per CTA, 2 CTAs per SM: 4 warps per SM
+// sub-partition, so the 64K-register file allows 128 registers per thread (with 8
+// consumer warps the per-sub-partition limit drops to 96 and the 3-component PCG
+// S-pass spills)
+constexpr int IJ = 7, IK = 32;            // tile rows x cols = consumer warps x lanes
 constexpr int INT = IJ * IK;              // consumer threads
 constexpr int ITHREADS = INT + 32;        // + producer warp
 constexpr int IXTS = 3;                   // ring slots
-constexpr int SBW = 36, SBH = 10;         // staged source box
-constexpr int S_MAIN = 368;               // 360 -> 368 doubles (128 B multiple)
-constexpr int S_W = 32;                   // 2 x 10 wrap box -> 32
-constexpr int K2W = 32, K2H = 9, K2SZ = 288;
-constexpr int K3W = 34, K3H = 8, K3SZ = 272;
-constexpr int K3WR = 16;                  // 2 x 8 wrap box
-constexpr int OWN = 256;                  // 32 x 8 own box
+constexpr int SBW = 36, SBH = IJ + 2;     // staged source box
+constexpr int rnd16(int n) { return (n + 15) / 16 * 16; }   // 128 B multiples of doubles
+constexpr int S_MAIN = rnd16(SBW * SBH);  // 324 -> 336
+constexpr int S_W = rnd16(2 * SBH);       // 2 x 9 wrap box -> 32
+constexpr int K2W = 32, K2H = IJ + 1, K2SZ = rnd16(K2W * K2H);
+constexpr int K3W = 34, K3H = IJ, K3SZ = rnd16(K3W * K3H);
+constexpr int K3WR = rnd16(2 * K3H);      // 2 x 7 wrap box
+constexpr int OWN = IK * IJ;              // 32 x 7 own box (224 = 14 x 16)
 
 template <int EPI, int NC>
 struct IsoLay {
   static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : 1;                               // z, pold
   static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 * NC : (EPI == EPI_PCG_S ? NC : 0);
-  static constexpr int SRC = 0;                                    // [f][c] main boxes
-  static constexpr int SRCW = SRC + nsrcf * NC * S_MAIN;           // [f][c][side] wrap boxes
-  static constexpr int K2 = SRCW + nsrcf * NC * 2 * S_W;
+  // one block per staged field: NC main boxes, then the NC x 2 wrap boxes, so a
+  // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
+  static constexpr int WRP = NC * S_MAIN;                          // wrap boxes within a field block
+  static constexpr int FS = NC * S_MAIN + NC * 2 * S_W;            // field block stride
+  static constexpr int K2 = nsrcf * FS;
   static constexpr int K3 = K2 + K2SZ;
   static constexpr int K3R = K3 + K3SZ;
   static constexpr int K1 = K3R + K3WR;
@@ -59,17 +66,20 @@ struct IsoLay {
 }  // namespace
 
 struct IsoTmaArgs {
-  CUtensorMap src[2];     // staged sources (u | z, pold), 3D (n3, n2, NC nl), box 36 x 10
-  CUtensorMap srcw[2];    // their wrap columns, box 2 x 10
-  CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x9, 34x8, 2x8, 32x8, 32x8
-  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 8
+  CUtensorMap src[2];     // staged sources (u | z, pold), 3D (n3, n2, NC nl), box 36 x 9
+  CUtensorMap srcw[2];    // their wrap columns, box 2 x 9
+  CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x8, 34x7, 2x7, 32x7, 32x7
+  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 7
   int has_w;
 };
 
-template <int EPI, int NC>
+// FST: first PCG iteration (p = z, no pold, no x update) -- a template flag so the
+// steady-state S-pass carries no per-cell branches on it
+template <int EPI, int NC, bool FST>
 __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int ic,
                                                               const __grid_constant__ IsoTmaArgs ta) {
   using Lay = IsoLay<EPI, NC>;
+  constexpr bool kP = (EPI == EPI_PCG_S) && !FST;   // source = z + beta pold
   extern __shared__ __align__(128) double smi[];
   double* ring = smi;
   uint64_t* full = reinterpret_cast<uint64_t*>(smi + IXTS * Lay::SLOT);
@@ -84,7 +94,6 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   const bool per = G.periodic3 != 0;
   const bool wrapL = per && k0 == 0;
   const bool wrapR = per && (k0 + IK >= G.n3);
-  const bool first = (EPI == EPI_PCG_S) && c.ea.first;
 
   bool skip[NC];
   bool all = true;
@@ -94,13 +103,13 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     all = all && skip[q];
   }
   if (EPI == EPI_PCG_S && all) return;
-  double beta[NC], axv[NC];
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
-    beta[q] = (EPI == EPI_PCG_S && !first) ? c.ea.sc[q].beta : 0.0;
-    axv[q] = (EPI == EPI_PCG_S && !first) ? c.ea.sc[q].ax : 0.0;
-  }
 
+  // PCG scalars of this iteration, broadcast from shared memory (keeps them out of registers)
+  __shared__ double sbeta[NC], sax[NC];
+  if (tid < NC) {
+    sbeta[tid] = kP ? c.ea.sc[tid].beta : 0.0;
+    sax[tid] = kP ? c.ea.sc[tid].ax : 0.0;
+  }
   if (tid == 0) {
     for (int s = 0; s < IXTS; ++s) {
       mbar_init(full + s, 1);
@@ -113,9 +122,9 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   // ======================= producer warp =======================
   if (tid >= INT) {
     if (tid != INT) return;
-    const int nsrcf_now = (EPI == EPI_PCG_S && first) ? 1 : Lay::nsrcf;
+    constexpr int nsrcf_now = (EPI == EPI_PCG_S && FST) ? 1 : Lay::nsrcf;
     const int cpl = (int)(G.cstride / G.plane);   // planes per component of the (whole local) array
-    uint32_t bytes = nsrcf_now * NC * SBW * SBH * 8 + (K2SZ + K3W * K3H + OWN) * 8;
+    uint32_t bytes = nsrcf_now * NC * SBW * SBH * 8 + (K2W * K2H + K3W * K3H + OWN) * 8;
     if (wrapL) bytes += nsrcf_now * NC * 2 * SBH * 8 + 2 * K3H * 8;
     if (wrapR) bytes += nsrcf_now * NC * 2 * SBH * 8;
     if (ta.has_w) bytes += OWN * 8;
@@ -127,13 +136,15 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       uint64_t* bar = full + slot;
       fence_proxy_async();
       mbar_expect_tx(bar, bytes);
+#pragma unroll
       for (int f = 0; f < nsrcf_now; ++f)
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
           const int pl = q * cpl + p;
-          tma3(S + Lay::SRC + (f * NC + q) * S_MAIN, &ta.src[f], k0 - 2, j0 - 1, pl, bar);
-          if (wrapL) tma3(S + Lay::SRCW + ((f * NC + q) * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
-          if (wrapR) tma3(S + Lay::SRCW + ((f * NC + q) * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
+          double* F = S + f * Lay::FS;
+          tma3(F + q * S_MAIN, &ta.src[f], k0 - 2, j0 - 1, pl, bar);
+          if (wrapL) tma3(F + Lay::WRP + (q * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
+          if (wrapR) tma3(F + Lay::WRP + (q * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
         }
       tma3(S + Lay::K2, &ta.k2, k0, j0 - 1, p, bar);
       tma3(S + Lay::K3, &ta.k3, k0 - 2, j0, p, bar);
@@ -141,7 +152,8 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       tma3(S + Lay::K1, &ta.k1, k0, j0, p, bar);
       if (ta.has_w) tma3(S + Lay::WB, &ta.w, k0, j0, p, bar);
 #pragma unroll
-      for (int q = 0; q < Lay::nepi; ++q) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+      for (int q = 0; q < Lay::nepi; ++q)
+        tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
     }
     return;
   }
@@ -164,108 +176,114 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     f3m = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
     vtp = M.Vt[j] * M.Vp[k];
   }
-  // slot offsets of the own cell and its in-plane neighbours (source boxes: row tj+1, col tk+2);
-  // periodic phi wrap: cell n3-1 / cell 0 come from the 2-column wrap boxes
+  // smem offsets (relative to the slot) of the own cell, its in-plane neighbours per
+  // component (periodic phi wrap: cell n3-1 / 0 from the 2-column wrap boxes)
   const int oc = (tj + 1) * SBW + tk + 2;
-  const bool kmw_box = per && k - 1 == -1, kpw_box = per && k + 1 == G.n3;
-  // source value of component q at main-box offset o, or from a wrap box (side 0: col n3-1, 1: col 0)
-  auto sv = [&](const double* S, int q, int o, bool wbox, int side) {
-    const int ff = wbox ? Lay::SRCW + (q * 2 + side) * S_W : Lay::SRC + q * S_MAIN;
-    const int oo = wbox ? (tj + 1) * 2 + (side == 0 ? 1 : 0) : o;
-    const double z = S[ff + oo];
-    if constexpr (EPI == EPI_PCG_S) {
-      if (!first) {
-        const int fp = wbox ? Lay::SRCW + ((NC + q) * 2 + side) * S_W : Lay::SRC + (NC + q) * S_MAIN;
-        return fma(beta[q], S[fp + oo], z);
-      }
-    }
-    return z;
+  const bool kmw_box = per && k == 0, kpw_box = per && k + 1 == G.n3;
+  int okm[NC], okp[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    okm[q] = kmw_box ? Lay::WRP + (q * 2 + 0) * S_W + (tj + 1) * 2 + 1 : q * S_MAIN + oc - 1;
+    okp[q] = kpw_box ? Lay::WRP + (q * 2 + 1) * S_W + (tj + 1) * 2 : q * S_MAIN + oc + 1;
+  }
+  const int o8 = tj * IK + tk;
+  const int ok2p = Lay::K2 + (tj + 1) * K2W + tk, ok2m = ok2p - K2W;
+  const int ok3p = Lay::K3 + tj * K3W + tk + 2;
+  const int ok3m = kmw_box ? Lay::K3R + tj * 2 + 1 : ok3p - 1;
+  auto sv = [&](const double* S, int o, int q) {
+    if constexpr (kP) return fma(sbeta[q], S[o + Lay::FS], S[o]);
+    return S[o];
   };
-  // own-column raw values of plane il (il in [-1, nl]) through global memory (halo planes
-  // included): source (u | z) and, for the PCG S-pass, pold.  Combined (p = z + beta pold)
-  // only when used, so a prefetch two planes ahead does not stall on its own load.
-  auto colraw = [&](const FieldV& f, int il, int q) -> double {
+  // own column through global memory (r neighbours, incl. the neighbour slab's halo plane)
+  const long long cs = G.cstride, pl = G.plane;
+  auto colv = [&](const FieldV& f, int il, int q) -> double {
     if (!own) return 0.0;
-    const int ig = G.i0 + il;
-    if (ig < 0 || ig >= G.n1g) return 0.0;
-    const double* pz = plane_ptr(f, G, il, q);
-    return pz ? __ldg(pz + coff) : 0.0;
+    const double* pz;
+    if (il >= 0 && il < G.nl) pz = f.p + q * cs + il * pl;
+    else if (il == G.nl && f.hi) pz = f.hi + q * pl;
+    else if (il == -1 && f.lo) pz = f.lo + q * pl;
+    else return 0.0;
+    return __ldg(pz + coff);
   };
-  constexpr bool kP = (EPI == EPI_PCG_S);
   auto comb = [&](double z, double po, int q) {
-    if constexpr (kP) {
-      if (!first) return fma(beta[q], po, z);
-    }
+    if constexpr (kP) return fma(sbeta[q], po, z);
     return z;
   };
 
-  double udn[NC], uupz[NC], uupp[NC], unz[NC], unp[NC];
+  double udn[NC], uupz[NC], uupp[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    udn[q] = comb(colraw(c.u, ib - 1, q), (kP && !first) ? colraw(c.u2, ib - 1, q) : 0.0, q);
-    uupz[q] = colraw(c.u, ib + 1, q);
-    uupp[q] = (kP && !first) ? colraw(c.u2, ib + 1, q) : 0.0;
-    unz[q] = unp[q] = 0.0;
+    udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(c.u2, ib - 1, q) : 0.0, q);
+    uupz[q] = colv(c.u, ib + 1, q);
+    uupp[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
   }
   const int ig0 = G.i0 + ib;
   double kdn = 0.0;
   if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
+  // per-plane metrics, register-prefetched one plane ahead (F2r == F3r by construction)
+  double f1r_n = M.F1r[ig0], f23r_n = M.F2r[ig0], vr_n = M.Vr[ig0];
   double part[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) part[q] = 0.0;
+  double* o1 = c.ea.out + coff;
+  double* o2 = (EPI == EPI_RKL2_FIRST || EPI == EPI_PCG_S) ? c.ea.out2 + coff : nullptr;
+  double* ox = (EPI == EPI_PCG_S) ? c.ea.x + coff : nullptr;
 
   for (int il = ib; il < ie; ++il) {
     const int slot = (il - ib) % IXTS;
     const double* S = ring + slot * Lay::SLOT;
-    // prefetch the own column two planes ahead (consumed next step)
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      unz[q] = (il + 2 <= ie) ? colraw(c.u, il + 2, q) : 0.0;
-      unp[q] = (kP && !first && il + 2 <= ie) ? colraw(c.u2, il + 2, q) : 0.0;
-    }
-    mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
     const int ig = G.i0 + il;
     const bool ip = ig + 1 < G.n1g;
+    const double f1r = f1r_n, f23r = f23r_n, vr = vr_n;
+    // prefetch: own column two planes ahead, metrics one plane ahead
+    double unz[NC], unp[NC];
+    const bool more = il + 2 <= ie;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      unz[q] = more ? colv(c.u, il + 2, q) : 0.0;
+      unp[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
+    }
+    if (il + 1 < ie) {
+      f1r_n = M.F1r[ig + 1];
+      f23r_n = M.F2r[ig + 1];
+      vr_n = M.Vr[ig + 1];
+    }
+    mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
     double Kup = 0.0;
     if (own) {
-      const int o8 = tj * IK + tk;
-      const double f23r = M.F2r[ig], f3r = M.F3r[ig];
-      Kup = ip ? S[Lay::K1 + o8] * M.F1r[ig] * f1tp : 0.0;
-      const double Kjp = jp ? S[Lay::K2 + (tj + 1) * K2W + tk] * f23r * f2p : 0.0;
-      const double Kjm = jm ? S[Lay::K2 + tj * K2W + tk] * f23r * f2m : 0.0;
-      const double Kkp = kp ? S[Lay::K3 + tj * K3W + tk + 2] * f3r * f3p : 0.0;
-      const double k3m = kmw_box ? S[Lay::K3R + tj * 2 + 1] : S[Lay::K3 + tj * K3W + tk + 1];
-      const double Kkm = km ? k3m * f3r * f3m : 0.0;
-      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * M.Vr[ig] * vtp;
-      const long long gi = (long long)il * G.plane + coff;
+      Kup = ip ? S[Lay::K1 + o8] * f1r * f1tp : 0.0;
+      const double Kjp = jp ? S[ok2p] * f23r * f2p : 0.0;
+      const double Kjm = jm ? S[ok2m] * f23r * f2m : 0.0;
+      const double Kkp = kp ? S[ok3p] * f23r * f3p : 0.0;
+      const double Kkm = km ? S[ok3m] * f23r * f3m : 0.0;
+      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * vtp;
+      const long long gi = (long long)il * pl;
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
-        const double u0 = sv(S, q, oc, false, 0);
-        const double ujm = sv(S, q, oc - SBW, false, 0), ujp = sv(S, q, oc + SBW, false, 0);
-        const double ukm = sv(S, q, oc - 1, kmw_box, 0), ukp = sv(S, q, oc + 1, kpw_box, 1);
+        const int oq = q * S_MAIN + oc;
+        const double u0 = sv(S, oq, q);
+        const double ujm = sv(S, oq - SBW, q), ujp = sv(S, oq + SBW, q);
+        const double ukm = sv(S, okm[q], q), ukp = sv(S, okp[q], q);
         const double uup = comb(uupz[q], uupp[q], q);
         const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
-        const long long go = gi + (long long)q * G.cstride;
+        const long long go = gi + q * cs;
         if (!skip[q]) {
           if constexpr (EPI == EPI_F) {
-            c.ea.out[go] = Lu / WV;
+            o1[go] = Lu / WV;
           } else if constexpr (EPI == EPI_RKL2_FIRST) {
             const double F = Lu / WV;
-            c.ea.out2[go] = F;
-            c.ea.out[go] = u0 + c.ea.c0 * F;
+            o2[go] = F;
+            o1[go] = u0 + c.ea.c0 * F;
           } else if constexpr (EPI == EPI_RKL2_STAGE) {
             const double F = Lu / WV;
-            c.ea.out[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c2 * S[Lay::EP + (NC + q) * OWN + o8] +
-                           c.ea.c0 * F + c.ea.c1 * S[Lay::EP + (2 * NC + q) * OWN + o8];
+            o1[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c2 * S[Lay::EP + (NC + q) * OWN + o8] +
+                     c.ea.c0 * F + c.ea.c1 * S[Lay::EP + (2 * NC + q) * OWN + o8];
           } else if constexpr (EPI == EPI_PCG_S) {
             const double y = WV * u0 - c.ea.dt * Lu;
-            c.ea.out[go] = y;
-            c.ea.out2[go] = u0;                                   // p_k
-            if (!first) {
-              const double po = S[Lay::SRC + (NC + q) * S_MAIN + oc];
-              c.ea.x[go] = fma(axv[q], po, S[Lay::EP + q * OWN + o8]);
-            }
+            o1[go] = y;
+            o2[go] = u0;                                          // p_k
+            if constexpr (kP) ox[go] = fma(sax[q], S[oq + Lay::FS], S[Lay::EP + q * OWN + o8]);
             part[q] += u0 * y;
           }
         }
@@ -339,15 +357,21 @@ int iso_tma_blocks(const Geo& G, int ib, int ie) {
   return (int)(g.x * g.y * g.z);
 }
 
-template <int EPI, int NC>
-static void launch_iso_t(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+template <int EPI, int NC, bool FST>
+static void launch_iso_f(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC, FST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)IsoLay<EPI, NC>::SMEM));
     attr = true;
   }
-  iso_tma_kernel<EPI, NC><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+  iso_tma_kernel<EPI, NC, FST><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+}
+
+template <int EPI, int NC>
+static void launch_iso_t(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+  if (EPI == EPI_PCG_S && c.ea.first) launch_iso_f<EPI, NC, true>(c, grid, ic, ta, st);
+  else launch_iso_f<EPI, NC, false>(c, grid, ic, ta, st);
 }
 
 template <int EPI>

@@ -1,0 +1,197 @@
+"""GPU parity at BASELINE.json's FULL sizes, in bench.py's launch configuration
+(one Grid over the whole grid, TMA kernels on, device-resident inputs).
+
+The oracle cannot hold a 268M-cell operator, so (task ③ / DESIGN.md §0):
+  * RKL2 and F(u): sampled outputs.  After s stages a cell depends only on the
+    cells within s of it (27-point stencil, radius 1 per stage), so the oracle
+    runs the same super-step (same dt, same s) on the index box of half-width
+    s + 2 around each sampled cell -- with the TRUE domain walls where the box
+    touches them and periodic wrap in phi -- and its centre value must match.
+  * BE + PCG (a global solve): the GPU iterate must satisfy the ORACLE's linear
+    system -- residual rows r_i = b_i - (A x)_i evaluated by the oracle on sampled
+    blocks, in the preconditioned norm of the stopping test (DESIGN R8).
+Samples include the r_min wall, the theta poles, the periodic phi seam, the steep
+transition-region ramp and the interior.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+from oracle import core as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import __graft_entry__ as e
+    e.build()
+    return torch.device("cuda", 0)
+
+
+def _gather(t, idx):
+    """t[..., I, J, K] for the index arrays of W.subgrid (on the device), to numpy."""
+    I, J, K = (torch.as_tensor(a, device=t.device) for a in idx)
+    x = t.index_select(-3, I).index_select(-2, J).index_select(-1, K)
+    return x.cpu().numpy()
+
+
+SAMPLES = [(0, 0, 0), (2, 255, 1023), (6, 511, 512), (300, 130, 77), (511, 300, 1000)]
+
+
+@pytest.fixture(scope="module")
+def c4(dev):
+    from paper_1610_01265_b200 import sts
+    cfg = W.make_config("c4_scale512", device=dev)
+    G = sts.Grid.from_grid(cfg["grid"])
+    return cfg, G
+
+
+def test_c4_conduction_rkl2_sampled(dev, c4):
+    from paper_1610_01265_b200 import sts
+    cfg, G = c4
+    g = cfg["grid"]
+    T, b = cfg["T"], cfg["b"]
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G.dt_euler("aniso", k, b)
+    dt = 300.0 * dte
+    s = sts.rkl2_num_stages(dt, dte)
+    assert s == O.rkl2_num_stages(dt, dte)
+    out = G.rkl2_advance("aniso", T, k, b, None, dt, s)
+    F = G.op_apply("aniso", T, k, b)
+    torch.cuda.synchronize()
+    for c in SAMPLES:
+        sub, idx, loc = W.subgrid(g, c, s + 2)
+        Ts, bs = _gather(T, idx), _gather(b, idx)
+        kap = O.spitzer_face_kappa(sub, Ts, cfg["kappa0"], cfg["T_cut"])
+        op = O.Operator(sub, kap, bs)
+        # Gershgorin bound holds at every row of the box (dt_exp is the global minimum)
+        rows = np.asarray(abs(op.M).sum(axis=1)).ravel()
+        assert rows.max() <= (2.0 / dte) * (1 + 1e-12)
+        ref = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), Ts, dt, s)[loc]
+        got = float(out[c].item())
+        assert abs(got - ref) <= 1e-11 * abs(ref), (c, got, ref)
+        fref = op.apply(Ts)[loc]
+        scale = np.abs(op.apply(Ts)).max()
+        assert abs(float(F[c].item()) - fref) <= 1e-12 * scale, (c, float(F[c].item()), fref)
+
+
+def test_c4_viscosity_rkl2_sampled(dev, c4):
+    from paper_1610_01265_b200 import sts
+    cfg, G = c4
+    g = cfg["grid"]
+    kv, rho, v = cfg["visc_faces"], cfg["rho"], cfg["v"]
+    dte = G.dt_euler("iso", kv, None, rho)
+    dt = 300.0 * dte
+    s = sts.rkl2_num_stages(dt, dte)
+    out = G.rkl2_advance("iso", v, kv, None, rho, dt, s)
+    torch.cuda.synchronize()
+    for c in SAMPLES[:3]:
+        sub, idx, loc = W.subgrid(g, c, s + 2)
+        ks = [_gather(x, idx) for x in kv]
+        # faces leaving the box carry no flux in the oracle; they lie outside the
+        # domain of dependence of the centre cell
+        op = O.Operator(sub, ks, None, _gather(rho, idx))
+        ref = O.rkl2_advance(op.apply, _gather(v, idx), dt, s)
+        for q in range(3):
+            got = float(out[(q,) + tuple(c)].item())
+            r = ref[(q,) + tuple(loc)]
+            assert abs(got - r) <= 1e-11 * max(abs(r), np.abs(ref[q]).max() * 1e-3), (c, q, got, r)
+
+
+def _residual_check(G, mode, u, x, k, b, w, dt, idx_list, g, rtol, kap_fn):
+    """Sampled rows of the oracle's BE system at the GPU iterate x: the mean of the
+    preconditioned residual energy r_i^2 / A_ii must respect the stopping test
+    sum r^2/A_ii <= rtol^2 sum b^2/A_ii (DESIGN R8), within a sampling factor."""
+    num = den = 0.0
+    n = 0
+    for c in idx_list:
+        sub, idx, loc = W.subgrid(g, c, 4)
+        op = O.Operator(sub, *kap_fn(sub, idx))
+        A = O.be_system(op, dt).tocsr()
+        us = _gather(u, idx)
+        xs = _gather(x, idx)
+        comps = us.shape[0] if us.ndim == 4 else 1
+        us = us.reshape(comps, -1)
+        xs = xs.reshape(comps, -1)
+        # rows whose stencil lies inside the box (interior of the box, or a true wall)
+        shape = sub.shape
+        ii, jj, kk = np.meshgrid(*[np.arange(m) for m in shape], indexing="ij")
+        inner = np.ones(shape, dtype=bool)
+        for d, (a, L) in enumerate(zip((ii, jj, kk), shape)):
+            I = idx[d]
+            lo_wall = I[0] == 0
+            hi_wall = I[-1] == g.shape[d] - 1
+            if d == 2 and g.periodic3 and not sub.periodic3:
+                lo_wall = hi_wall = False
+            if d == 2 and sub.periodic3:
+                continue
+            if not lo_wall:
+                inner &= a >= 1
+            if not hi_wall:
+                inner &= a <= L - 2
+        rows = np.flatnonzero(inner.ravel())
+        D = A.diagonal()
+        for q in range(comps):
+            bq = op.WV * us[q]
+            r = bq - A @ xs[q]
+            num += float(np.sum(r[rows] ** 2 / D[rows]))
+            den += float(np.sum(bq[rows] ** 2 / D[rows]))
+            n += rows.size
+    assert n > 0
+    assert num <= 100.0 * rtol ** 2 * den, (num, den)
+
+
+def test_c4_pcg_residual_sampled(dev, c4):
+    cfg, G = c4
+    g = cfg["grid"]
+    T, b = cfg["T"], cfg["b"]
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G.dt_euler("aniso", k, b)
+    dt = 300.0 * dte
+    x, it = G.be_pcg_solve("aniso", T, k, b, None, dt, 1e-12, 50000)
+    assert 0 < it[0] < 50000
+    _residual_check(G, "aniso", T, x, k, b, None, dt, SAMPLES, g, 1e-12,
+                    lambda sub, idx: (O.spitzer_face_kappa(sub, _gather(T, idx), cfg["kappa0"], cfg["T_cut"]),
+                                      _gather(b, idx)))
+    kv, rho, v = cfg["visc_faces"], cfg["rho"], cfg["v"]
+    dtev = 300.0 * G.dt_euler("iso", kv, None, rho)
+    xv, itv = G.be_pcg_solve("iso", v, kv, None, rho, dtev, 1e-12, 50000)
+    assert all(0 < i < 50000 for i in itv)
+    _residual_check(G, "iso", v, xv, kv, None, rho, dtev, SAMPLES[:3], g, 1e-12,
+                    lambda sub, idx: ([_gather(f, idx) for f in kv], None, _gather(rho, idx)))
+
+
+def test_c3_dt_sweep_stages_and_iterations(dev):
+    """BASELINE configs[3]: 256 x 256 x 512, dt/dt_exp in {10, 100, 1000}: stage
+    counts follow Eq. (5) exactly, PCG iteration counts grow with dt, and the
+    sampled RKL2 result matches the oracle at the smallest ratio."""
+    from paper_1610_01265_b200 import sts
+    cfg = W.make_config("c3_spitzer256", device=dev)
+    g = cfg["grid"]
+    G = sts.Grid.from_grid(g)
+    T, b = cfg["T"], cfg["b"]
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G.dt_euler("aniso", k, b)
+    rec = {}
+    for ratio in (10.0, 100.0, 1000.0):
+        dt = ratio * dte
+        s = sts.rkl2_num_stages(dt, dte)
+        assert s == O.rkl2_num_stages(dt, dte)
+        _, it = G.be_pcg_solve("aniso", T, k, b, None, dt, 1e-12, 50000)
+        rec[ratio] = (s, it[0])
+        if ratio == 10.0:
+            out = G.rkl2_advance("aniso", T, k, b, None, dt, s)
+            for c in [(0, 0, 0), (3, 128, 511), (200, 60, 300)]:
+                sub, idx, loc = W.subgrid(g, c, s + 2)
+                Ts = _gather(T, idx)
+                op = O.Operator(sub, O.spitzer_face_kappa(sub, Ts, cfg["kappa0"], cfg["T_cut"]), _gather(b, idx))
+                ref = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), Ts, dt, s)[loc]
+                assert abs(float(out[c].item()) - ref) <= 1e-11 * abs(ref)
+    s_list = [rec[r][0] for r in (10.0, 100.0, 1000.0)]
+    it_list = [rec[r][1] for r in (10.0, 100.0, 1000.0)]
+    assert s_list == sorted(s_list) and it_list == sorted(it_list), rec
+    print("c3 sweep (ratio: stages, PCG iterations):", rec)
