@@ -195,3 +195,52 @@ def test_c3_dt_sweep_stages_and_iterations(dev):
     it_list = [rec[r][1] for r in (10.0, 100.0, 1000.0)]
     assert s_list == sorted(s_list) and it_list == sorted(it_list), rec
     print("c3 sweep (ratio: stages, PCG iterations):", rec)
+
+
+@pytest.mark.parametrize("name", ["c1_spitzer64", "c2_visc64"])
+def test_c1_c2_full_elementwise(dev, name):
+    """BASELINE configs[1] / [2] at their full 64 x 64 x 128 size, element by element
+    against the oracle: one RKL2 super-step (1e-11) and one BE + Jacobi-PCG step
+    (iterations +-1; the GPU iterate meets the oracle system's own stopping test --
+    a sparse direct solve for the exact answer is far too slow at this size)."""
+    from paper_1610_01265_b200 import sts
+    cfg = W.make_config(name)
+    g = cfg["grid"]
+    G = sts.Grid.from_grid(g)
+    if name == "c1_spitzer64":
+        ratio, mode = 100.0, "aniso"
+        T = cfg["T"]
+        kap = O.spitzer_face_kappa(g, T.numpy(), cfg["kappa0"], cfg["T_cut"])
+        op = O.Operator(g, kap, cfg["b"].numpy())
+        u, k, b, w = T, [torch.as_tensor(x) for x in kap], cfg["b"], None
+        kd = G.face_kappa_spitzer(T.to(dev), cfg["kappa0"], cfg["T_cut"])
+        for a, e in zip(kd, kap):
+            np.testing.assert_allclose(a.cpu().numpy(), e, rtol=1e-13, atol=0)
+    else:
+        ratio, mode = 500.0, "iso"
+        op = O.Operator(g, [f.numpy() for f in cfg["visc_faces"]], None, cfg["rho"].numpy())
+        u, k, b, w = cfg["v"], cfg["visc_faces"], None, cfg["rho"]
+    dte = O.dt_euler(op)
+    dt = ratio * dte
+    s = O.rkl2_num_stages(dt, dte)
+    dv = lambda x: None if x is None else x.to(dev)  # noqa: E731
+    kd = [x.to(dev) for x in k]
+    assert abs(G.dt_euler(mode, kd, dv(b), dv(w)) - dte) <= 1e-12 * dte
+    ref = O.rkl2_advance(lambda x: op.apply(x), u.numpy(), dt, s)
+    out = G.rkl2_advance(mode, u.to(dev), kd, dv(b), dv(w), dt, s)
+    d = out.cpu().numpy() - ref
+    assert np.linalg.norm(d) <= 1e-11 * np.linalg.norm(ref)
+    ref_be, it_ref = O.be_pcg_solve(op, u.numpy(), dt, rtol=1e-12)
+    x, it = G.be_pcg_solve(mode, u.to(dev), kd, dv(b), dv(w), dt, 1e-12, 100000)
+    assert all(abs(a - c) <= 1 for a, c in zip(it, it_ref)), (it, it_ref)
+    A = O.be_system(op, dt).tocsr()
+    D = A.diagonal()
+    uu = u.numpy().reshape(-1, g.ncells)
+    xx = x.cpu().numpy().reshape(uu.shape)
+    for q in range(uu.shape[0]):
+        bq = op.WV * uu[q]
+        r = bq - A @ xx[q]
+        # DESIGN R8 stopping test r.P^-1 r <= rtol^2 b.P^-1 b, with slack for the rounding
+        # of the recurrence residual vs the true residual
+        assert float(r @ (r / D)) <= (4e-12) ** 2 * float(bq @ (bq / D))
+    assert np.linalg.norm(xx - ref_be.reshape(uu.shape)) <= 1e-9 * np.linalg.norm(ref_be)
