@@ -83,7 +83,8 @@ struct TmaLay {
   static constexpr int nown = nepi + (W ? 1 : 0);             // w is the last own box
   static constexpr int E = nsrc * U_FIELD;
   static constexpr int O = E + E_PART;
-  static constexpr int SLOT = O + nown * O_PART;
+  static constexpr int MT = O + nown * O_PART;       // per-plane metrics written by the producer
+  static constexpr int SLOT = MT + 16;
   static constexpr size_t SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 2 * XTS * sizeof(uint64_t) + 128;
 };
 
@@ -141,6 +142,14 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
       if (has_e) bytes += E_PART * 8;
       if (has_own) bytes += Lay::nown * XOJ * XK * 8;
+      // per-plane metrics (plain stores: the mbarrier arrive below releases them to the
+      // consumers' acquiring wait): iG2 of cell planes p-1 and p, Vr of plane p-1
+      {
+        const int i = G.i0 + p;
+        S[Lay::MT + 0] = (i - 1 >= 0 && i - 1 < G.n1g) ? M.iG2[i - 1] : 0.0;
+        S[Lay::MT + 1] = (i >= 0 && i < G.n1g) ? M.iG2[i] : 0.0;
+        S[Lay::MT + 2] = (i - 1 >= 0 && i - 1 < G.n1g) ? M.Vr[i - 1] : 0.0;
+      }
       fence_proxy_async();
       mbar_expect_tx(bar, bytes);
       for (int f = 0; f < nsrc_now; ++f) {
@@ -215,9 +224,7 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       const double* E = S + Lay::E;
       const int ei = vj * EBW + vk + se;
       const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
-      const int iv = G.i0 + p - 1;
-      const double ig2l = (iv >= 0 && iv < G.n1g) ? M.iG2[iv] : 0.0;
-      const double ig2h = (iv + 1 >= 0 && iv + 1 < G.n1g) ? M.iG2[iv + 1] : 0.0;
+      const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
       const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
       vb[tid] = q * er;
       vb[XNT + tid] = q * et;
@@ -237,11 +244,10 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       if (p >= ib + 1 && own) {
         // output cell plane il = p-1
         const int il = p - 1;
-        const int ig = G.i0 + il;
         const double* O = S + Lay::O + vj * XK + vk + se;
-        const double ig2c = M.iG2[ig];
+        const double ig2c = S[Lay::MT + 0];                   // iG2 of plane p-1
         const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
-        const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * M.Vr[ig] * vtpc;
+        const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * S[Lay::MT + 2] * vtpc;
         const long long gi = (long long)il * G.plane + coff;
         if constexpr (EPI == EPI_F) {
           c.ea.out[gi] = Lu / WV;

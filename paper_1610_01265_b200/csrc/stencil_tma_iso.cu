@@ -210,18 +210,28 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     return z;
   };
 
-  double udn[NC], uupz[NC], uupp[NC];
+  // Register double buffering, unrolled by two (no register moves of in-flight loads,
+  // which would make every prefetch wait at the end of its own iteration):
+  //   Pre.z/p: own column of plane il+1 (r up-neighbour), loaded one step earlier;
+  //   Pre.f1r/f23r/vr: metrics of plane il (F2r == F3r by construction).
+  struct Pre {
+    double z[NC], p[NC];
+    double f1r, f23r, vr;
+  };
+  const int ig0 = G.i0 + ib;
+  Pre A, B;
+  double udn[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(c.u2, ib - 1, q) : 0.0, q);
-    uupz[q] = colv(c.u, ib + 1, q);
-    uupp[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
+    A.z[q] = colv(c.u, ib + 1, q);
+    A.p[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
   }
-  const int ig0 = G.i0 + ib;
+  A.f1r = M.F1r[ig0];
+  A.f23r = M.F2r[ig0];
+  A.vr = M.Vr[ig0];
   double kdn = 0.0;
   if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
-  // per-plane metrics, register-prefetched one plane ahead (F2r == F3r by construction)
-  double f1r_n = M.F1r[ig0], f23r_n = M.F2r[ig0], vr_n = M.Vr[ig0];
   double part[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) part[q] = 0.0;
@@ -229,34 +239,32 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   double* o2 = (EPI == EPI_RKL2_FIRST || EPI == EPI_PCG_S) ? c.ea.out2 + coff : nullptr;
   double* ox = (EPI == EPI_PCG_S) ? c.ea.x + coff : nullptr;
 
-  for (int il = ib; il < ie; ++il) {
+  auto body = [&](int il, const Pre& C, Pre& N) {
     const int slot = (il - ib) % IXTS;
     const double* S = ring + slot * Lay::SLOT;
     const int ig = G.i0 + il;
     const bool ip = ig + 1 < G.n1g;
-    const double f1r = f1r_n, f23r = f23r_n, vr = vr_n;
-    // prefetch: own column two planes ahead, metrics one plane ahead
-    double unz[NC], unp[NC];
+    // prefetch into the other buffer: own column two planes ahead, metrics one ahead
     const bool more = il + 2 <= ie;
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
-      unz[q] = more ? colv(c.u, il + 2, q) : 0.0;
-      unp[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
+      N.z[q] = more ? colv(c.u, il + 2, q) : 0.0;
+      N.p[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
     }
     if (il + 1 < ie) {
-      f1r_n = M.F1r[ig + 1];
-      f23r_n = M.F2r[ig + 1];
-      vr_n = M.Vr[ig + 1];
+      N.f1r = M.F1r[ig + 1];
+      N.f23r = M.F2r[ig + 1];
+      N.vr = M.Vr[ig + 1];
     }
     mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
     double Kup = 0.0;
     if (own) {
-      Kup = ip ? S[Lay::K1 + o8] * f1r * f1tp : 0.0;
-      const double Kjp = jp ? S[ok2p] * f23r * f2p : 0.0;
-      const double Kjm = jm ? S[ok2m] * f23r * f2m : 0.0;
-      const double Kkp = kp ? S[ok3p] * f23r * f3p : 0.0;
-      const double Kkm = km ? S[ok3m] * f23r * f3m : 0.0;
-      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * vtp;
+      Kup = ip ? S[Lay::K1 + o8] * C.f1r * f1tp : 0.0;
+      const double Kjp = jp ? S[ok2p] * C.f23r * f2p : 0.0;
+      const double Kjm = jm ? S[ok2m] * C.f23r * f2m : 0.0;
+      const double Kkp = kp ? S[ok3p] * C.f23r * f3p : 0.0;
+      const double Kkm = km ? S[ok3m] * C.f23r * f3m : 0.0;
+      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * C.vr * vtp;
       const long long gi = (long long)il * pl;
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
         const double u0 = sv(S, oq, q);
         const double ujm = sv(S, oq - SBW, q), ujp = sv(S, oq + SBW, q);
         const double ukm = sv(S, okm[q], q), ukp = sv(S, okp[q], q);
-        const double uup = comb(uupz[q], uupp[q], q);
+        const double uup = comb(C.z[q], C.p[q], q);
         const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
         const long long go = gi + q * cs;
@@ -293,12 +301,13 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     __syncwarp();
     if (tk == 0) mbar_arrive(empty + slot);       // this warp is done with the slot
     kdn = Kup;
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      uupz[q] = unz[q];
-      uupp[q] = unp[q];
-    }
+  };
+  int il = ib;
+  for (; il + 1 < ie; il += 2) {
+    body(il, A, B);
+    body(il + 1, B, A);
   }
+  if (il < ie) body(il, A, B);
   if constexpr (EPI == EPI_PCG_S) {
     __shared__ double red[NC][IJ];
 #pragma unroll
