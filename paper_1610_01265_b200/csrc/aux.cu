@@ -258,6 +258,83 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
   }
 }
 
+// 16-byte vectorised variant (n, cs even, arrays 16 B aligned): element pairs, two
+// pairs per thread and trip with every load of the trip issued before any use
+template <int NC>
+__global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long long cs2, double2* __restrict__ r,
+                                                             double2* __restrict__ z, const double2* __restrict__ y,
+                                                             const double2* __restrict__ d,
+                                                             const PcgScal* __restrict__ sc,
+                                                             double* __restrict__ partials, long long pstride) {
+  double alpha[NC];
+  bool act[NC];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    act[q] = !sc[q].done;
+    alpha[q] = sc[q].alpha;
+    any = any || act[q];
+  }
+  if (!any) return;
+  double acc[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+  constexpr int U = 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  auto one = [&](double2 de, double2 rr, double2 yy, long long o, int q) {
+    double2 rn, zn;
+    rn.x = rr.x - alpha[q] * yy.x;
+    rn.y = rr.y - alpha[q] * yy.y;
+    zn.x = rn.x * de.x;
+    zn.y = rn.y * de.y;
+    __stcs(r + o, rn);
+    __stcs(z + o, zn);
+    acc[q] += rn.x * zn.x;
+    acc[q] += rn.y * zn.y;
+  };
+  for (; m + (U - 1) * stride < n2; m += U * stride) {
+    double2 de[U], rr[NC][U], yy[NC][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) de[u] = __ldcs(d + m + u * stride);
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long o = m + u * stride + q * cs2;
+        if (act[q]) {
+          rr[q][u] = __ldcs(r + o);
+          yy[q][u] = __ldcs(y + o);
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      if (!act[q]) continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) one(de[u], rr[q][u], yy[q][u], m + u * stride + q * cs2, q);
+    }
+  }
+  for (; m < n2; m += stride) {
+    const double2 de = d[m];
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (act[q]) one(de, r[m + q * cs2], y[m + q * cs2], m + q * cs2, q);
+  }
+  __shared__ double red[NC][8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum_d(acc[q]);
+    if (lane == 0) red[q][wid] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < NC) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
+    partials[threadIdx.x * pstride + blockIdx.x] = s;
+  }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long cs, double* __restrict__ x,
                                                          const double* __restrict__ p0, const double* __restrict__ p1,
@@ -300,7 +377,16 @@ void launch_pcg_pnew(int ncomp, long long n, long long cs, double* pnew, const d
 
 void launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* z, const double* y, const double* d,
                         const PcgScal* sc, double* partials, long long pstride, cudaStream_t st) {
-  STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride);
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (n % 2 == 0 && cs % 2 == 0 && a16(r) && a16(z) && a16(y) && a16(d)) {
+    double2* r2 = reinterpret_cast<double2*>(r);
+    double2* z2 = reinterpret_cast<double2*>(z);
+    const double2* y2 = reinterpret_cast<const double2*>(y);
+    const double2* d2 = reinterpret_cast<const double2*>(d);
+    STS_NC_SWITCH(ncomp, pcg_rupdate_v2_kernel, n / 2, cs / 2, r2, z2, y2, d2, sc, partials, pstride);
+  } else {
+    STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride);
+  }
   STS_CUDA(cudaGetLastError());
 }
 
