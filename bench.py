@@ -408,6 +408,8 @@ def main():
     ap.add_argument("--config", default="c4_scale512", choices=list(RATIO))
     ap.add_argument("--impl", default="sts", choices=["sts", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--timing-steps", type=int, default=2,
+                    help="instrumented steps (after the timed region) for the per-kernel breakdown")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shape", default=None, help="override n1,n2,n3 (debug)")
     args = ap.parse_args()
@@ -448,8 +450,6 @@ def main():
     # ---------------- warm-up + timed region (device-resident inputs)
     for _ in range(max(args.warmup, 0)):
         info = step()
-    G.set_timing(True)
-    G.timing_reset()
     launches0 = G.kernel_launches
     sampler = ClockSampler(lrank)
     sampler.start()
@@ -465,17 +465,29 @@ def main():
     ms_local = e0.elapsed_time(e1)
     ms = allreduce_max(ms_local, dev, ws)
     launches = G.kernel_launches - launches0
-    timing = G.timing()
-    G.set_timing(False)
     units = sum(i["units"] for i in infos)
     value = ncells_total * units / (ms * 1e-3) / 1e9
+
+    # ---------------- per-kernel-class device time: separate instrumented steps (CUDA
+    # events around every launch on its stream), OUTSIDE the timed region above
+    G.set_timing(True)
+    G.timing_reset()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    pinfos = [step() for _ in range(max(1, min(args.steps, args.timing_steps)))]
+    p1.record(stream)
+    torch.cuda.synchronize()
+    timing = G.timing()
+    G.set_timing(False)
+    ms_prof = p0.elapsed_time(p1)
 
     # ---------------- roofline of the dominant kernel (rank 0's device timing)
     peak, peak_kind = peaks()
     Bytes = {}
     fused_c = timing.get("aniso_pcg_s", (0, 0.0))[0] > 0
     fused_v = timing.get("iso_pcg_s", (0, 0.0))[0] > 0
-    for i in infos:
+    for i in pinfos:
         for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
                                       fused_c, fused_v).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
@@ -483,7 +495,7 @@ def main():
     for k, (n, kms) in timing.items():
         if n == 0:
             continue
-        ent = {"launches": n, "ms": round(kms, 3), "share": round(kms / ms_local, 4)}
+        ent = {"launches": n, "ms": round(kms, 3), "share": round(kms / ms_prof, 4)}
         if k in Bytes and kms > 0:
             ent["achieved_gbs"] = round(Bytes[k] / (kms * 1e-3) / 1e9, 1)
             ent["frac"] = round(ent["achieved_gbs"] / peak, 4)
@@ -498,11 +510,11 @@ def main():
     except Exception:
         pass
     eff = [k for k in kernels if "achieved_gbs" in kernels[k]]
-    launches_dom = infos[0]
+    launches_dom = pinfos[0]
     n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
              "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
              "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"])}.get(dom)
-    bpl = (Bytes[dom] / len(infos) / n_eff) if n_eff else None
+    bpl = (Bytes[dom] / len(pinfos) / n_eff) if n_eff else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
