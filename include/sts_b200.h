@@ -212,6 +212,24 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
                  const double* b, const double* w, double dt, int s, void* stream);
 
 /*
+ * A8 — RKL2 with an explicit-Euler prefix and RKL2 sub-cycling, the high-mode
+ * remedies PAPER.md:341 (Sec. 6) reports ("sub-cycling explicit Euler steps for ~1/4
+ * of the time-step and completing the remainder of the step with RKL2", "sub-cycling
+ * the RKL2 method within each large time-step"):
+ *   n_euler explicit Euler steps  u <- u + dte F(u),  dte = euler_frac dt / n_euler,
+ *   then n_sub RKL2 super-steps of dtr = (1 - euler_frac) dt / n_sub, each with
+ *   s = rkl2_num_stages(dtr, dt_exp, 0) stages (Fig. 2).
+ *  Requirements: 0 <= euler_frac < 1; n_euler > 0 exactly when euler_frac > 0;
+ *  dte <= dt_exp (explicit stability); n_sub >= 1.
+ *  stages_out: host int[2] = {n_euler, s} (may be NULL).  u1 may alias u0.
+ *  euler_frac = 0, n_sub = 1 is exactly rkl2_advance with s = rkl2_num_stages(dt, dt_exp).
+ */
+int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
+                        const double* k1, const double* k2, const double* k3,
+                        const double* b, const double* w, double dt, double dt_exp,
+                        double euler_frac, int n_euler, int n_sub, int* stages_out, void* stream);
+
+/*
  * A7 — one backward-Euler step (Eqs. 2-4) solved by
  * point-Jacobi PCG (Fig. 1, PC1 of :468-470; DESIGN R7, R8):
  *   (wV - dt L) x = wV un,  x0 = un,  z = r / diag(A),

@@ -20,6 +20,7 @@ of /root/reference/PAPER.md, DESIGN.md "R<n>" is a listed reading):
   rkl2_num_stages()     s = ceil((sqrt(9+16 dt/dt_exp)-1)/2), s>=2     PAPER.md:142 Eq. (5), DESIGN R5
   rkl2_coeffs()         b_j, mu_j, nu_j, mu~_j, gamma~_j               PAPER.md:134-138, DESIGN R6
   rkl2_advance()        Fig. 2 recursion                               PAPER.md:117-125 (Fig. 2)
+  rkl2_hybrid_advance() Euler prefix + RKL2 sub-cycling               PAPER.md:341 (Sec. 6)
   be_system()           A = wV - dt L (symmetric form of Eq. 4)        PAPER.md:45-60 Eqs. (2)-(4), DESIGN R7
   pcg()                 Fig. 1 PCG, point-Jacobi PC1                   PAPER.md:70-92 (Fig. 1), :468-470 (App. A), DESIGN R8
   be_pcg_solve()        BE step via pcg() per component
@@ -379,6 +380,25 @@ def rkl2_advance(apply_M, u0, dt, s):
               + c["mut"][j] * dt * apply_M(ym1) + c["gt"][j] * dt * M0)
         ym2, ym1 = ym1, yj
     return ym1
+
+
+def rkl2_hybrid_advance(apply_M, u0, dt, dt_exp, euler_frac, n_euler, n_sub):
+    """PAPER.md:341 (Sec. 6): "sub-cycling explicit Euler steps for ~1/4 of the
+    time-step and completing the remainder of the step with RKL2", and "sub-cycling
+    the RKL2 method within each large time-step":
+      n_euler explicit Euler steps u <- u + dte M u, dte = euler_frac dt / n_euler,
+      then n_sub RKL2 super-steps of dtr = (1 - euler_frac) dt / n_sub, each with
+      s = rkl2_num_stages(dtr, dt_exp) (Eq. 5)."""
+    u = np.array(u0, dtype=np.float64)
+    if n_euler:
+        dte = euler_frac * dt / n_euler
+        for _ in range(n_euler):
+            u = u + dte * apply_M(u)
+    dtr = (1.0 - euler_frac) * dt / n_sub
+    s = rkl2_num_stages(dtr, dt_exp)
+    for _ in range(n_sub):
+        u = rkl2_advance(apply_M, u, dtr, s)
+    return u, s
 
 
 # --------------------------------------------------------------------------

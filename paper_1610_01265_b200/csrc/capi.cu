@@ -548,6 +548,50 @@ static const double* d_x1f(const sts_grid* g) {
 }
 static const double* d_x1c(const sts_grid* g) { return d_x1f(g) + g->n1g + 1; }
 
+// One RKL2 super-step (Fig. 2) Y0 = u0 -> u1 with frozen vertex
+// coefficients `ev`; M0, A, B are NF-sized scratch fields (A, B rotate the stages).
+static void rkl2_core(sts_grid* g, int mode, int ncomp, const double* u0, double* u1, const double* k1,
+                      const double* k2, const double* k3, const double* bb, const double* w, double dt, int s,
+                      const std::vector<const double*>& ev, double* M0, double* A, double* B, cudaStream_t st) {
+  const Rkl2Coef co = rkl2_coefs(s);
+  // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
+  sweep(g, {{H_U, u0, ncomp}}, st, [&](size_t si) {
+    const Slab& sl = g->slabs[si];
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
+    c.ev = ev[si];
+    c.ea.out = off(A, sl);
+    c.ea.out2 = off(M0, sl);
+    c.ea.c0 = co.mut[1] * dt;
+    return c;
+  });
+  // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
+  const double* prev = u0;
+  double* cur = A;
+  for (int j = 2; j <= s; ++j) {
+    double* dst;
+    if (j == s) dst = u1;
+    else if (prev == u0) dst = B;                       // never overwrite Y0
+    else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
+    sweep(g, {{H_U, cur, ncomp}}, st, [&](size_t si) {
+      const Slab& sl = g->slabs[si];
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
+      c.ev = ev[si];
+      c.ea.out = off(dst, sl);
+      c.ea.ym2 = off(prev, sl);
+      c.ea.y0 = off(u0, sl);
+      c.ea.m0 = off(M0, sl);
+      c.ea.mu = co.mu[j];
+      c.ea.nu = co.nu[j];
+      c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
+      c.ea.c0 = co.mut[j] * dt;
+      c.ea.c1 = co.gt[j] * dt;
+      return c;
+    });
+    prev = cur;
+    cur = dst;
+  }
+}
+
 }  // namespace sts
 
 using namespace sts;
@@ -874,48 +918,77 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
     const size_t NFr = rnd(NF);
     double* base = ws_get(g, (rnd(sg.total) + 3 * NFr + evn) * sizeof(double));
     if (sg.any_host) sg.begin(base + 3 * NFr + evn);
-    double* M0 = base;
-    double* A = base + NFr;
-    double* B = base + 2 * NFr;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
-    const Rkl2Coef co = rkl2_coefs(s);
     exchange_coeffs(g, mode, k1, k2, k3, b, st);
     const auto ev = build_vertex_coefs(g, mode, base + 3 * NFr, k1, k2, k3, b, st);
-    // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
-    sweep(g, {{H_U, u0, ncomp}}, st, [&](size_t si) {
-      const Slab& sl = g->slabs[si];
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
-      c.ev = ev[si];
-      c.ea.out = off(A, sl);
-      c.ea.out2 = off(M0, sl);
-      c.ea.c0 = co.mut[1] * dt;
-      return c;
-    });
-    // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
-    const double* prev = u0;
-    double* cur = A;
-    for (int j = 2; j <= s; ++j) {
-      double* dst;
-      if (j == s) dst = u1;
-      else if (prev == u0) dst = B;                       // never overwrite Y0
-      else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
+    rkl2_core(g, mode, ncomp, u0, u1, k1, k2, k3, bb, w, dt, s, ev, base, base + NFr, base + 2 * NFr, st);
+    sg.end({u1});
+  });
+}
+
+int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, double* u1, const double* k1,
+                        const double* k2, const double* k3, const double* b, const double* w, double dt,
+                        double dt_exp, double euler_frac, int n_euler, int n_sub, int* stages_out, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g && u0 && u1 && k1 && k2 && k3, "NULL argument");
+    check_mode(mode, ncomp, b);
+    STS_REQUIRE(std::isfinite(dt) && dt >= 0.0 && std::isfinite(dt_exp) && dt_exp > 0.0, "bad dt / dt_exp");
+    STS_REQUIRE(euler_frac >= 0.0 && euler_frac < 1.0, "euler_frac must be in [0, 1)");
+    STS_REQUIRE(n_sub >= 1 && n_euler >= 0, "n_sub >= 1, n_euler >= 0");
+    STS_REQUIRE((n_euler == 0) == (euler_frac == 0.0), "n_euler > 0 exactly when euler_frac > 0");
+    const double dte = n_euler ? euler_frac * dt / n_euler : 0.0;
+    STS_REQUIRE(dte <= dt_exp * (1.0 + 1e-12), "explicit Euler sub-step exceeds dt_exp");
+    const double dtr = (1.0 - euler_frac) * dt / n_sub;
+    const int s = rkl2_num_stages(dtr, dt_exp, 0);
+    STS_REQUIRE(s >= 2, "stage count");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    const size_t NF = N * ncomp;
+    Stage sg{g, st};
+    sg.input(u0, NF);
+    sg.input(k1, N);
+    sg.input(k2, N);
+    sg.input(k3, N);
+    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
+    sg.input(w, N);
+    sg.output(u1, NF);
+    const size_t evn = vertex_coef_doubles(g, mode);
+    const size_t NFr = rnd(NF);
+    // scratch: M0, A, B (RKL2 stages), E0, E1 (sub-step ping-pong), vertex coefficients
+    double* base = ws_get(g, (rnd(sg.total) + 5 * NFr + evn) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 5 * NFr + evn);
+    double* E[2] = {base + 3 * NFr, base + 4 * NFr};
+    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
+    exchange_coeffs(g, mode, k1, k2, k3, b, st);
+    const auto ev = build_vertex_coefs(g, mode, base + 5 * NFr, k1, k2, k3, b, st);
+    // explicit Euler prefix: u <- u + dte F(u), n_euler times
+    const double* cur = u0;
+    int e = 0;
+    for (int i = 0; i < n_euler; ++i) {
+      double* dst = E[e];
+      e ^= 1;
       sweep(g, {{H_U, cur, ncomp}}, st, [&](size_t si) {
         const Slab& sl = g->slabs[si];
-        StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
+        StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, cur, k1, k2, k3, bb, w);
         c.ev = ev[si];
         c.ea.out = off(dst, sl);
-        c.ea.ym2 = off(prev, sl);
-        c.ea.y0 = off(u0, sl);
-        c.ea.m0 = off(M0, sl);
-        c.ea.mu = co.mu[j];
-        c.ea.nu = co.nu[j];
-        c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
-        c.ea.c0 = co.mut[j] * dt;
-        c.ea.c1 = co.gt[j] * dt;
+        c.ea.out2 = off(base, sl);   // F(u) (unused scratch)
+        c.ea.c0 = dte;
         return c;
       });
-      prev = cur;
       cur = dst;
+    }
+    // the remainder as n_sub RKL2 super-steps (RKL2 sub-cycling)
+    for (int m = 1; m <= n_sub; ++m) {
+      double* dst = (m == n_sub) ? u1 : E[e];
+      if (m < n_sub) e ^= 1;
+      rkl2_core(g, mode, ncomp, cur, dst, k1, k2, k3, bb, w, dtr, s, ev, base, base + NFr, base + 2 * NFr, st);
+      cur = dst;
+    }
+    if (stages_out) {
+      stages_out[0] = n_euler;
+      stages_out[1] = s;
     }
     sg.end({u1});
   });

@@ -66,6 +66,7 @@ def lib():
         "sts_dt_euler": (I, [P, I, P, P, P, P, P, ctypes.POINTER(D), P]),
         "rkl2_num_stages": (I, [D, D, I]),
         "rkl2_advance": (I, [P, I, I, P, P, P, P, P, P, P, D, I, P]),
+        "rkl2_advance_hybrid": (I, [P, I, I, P, P, P, P, P, P, P, D, D, D, I, I, ctypes.POINTER(I), P]),
         "be_pcg_solve": (I, [P, I, I, P, P, P, P, P, P, P, D, D, I, ctypes.POINTER(I), P]),
     }
     for name, (res, args) in sig.items():
@@ -230,6 +231,21 @@ class Grid:
             self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
             float(dt), int(s), _stream(stream)))
         return out
+
+    def rkl2_advance_hybrid(self, mode, u0, k, b=None, w=None, dt=0.0, dt_exp=1.0, euler_frac=0.25,
+                            n_euler=None, n_sub=1, out=None, stream=None):
+        """PAPER.md:341 remedies: explicit-Euler prefix over euler_frac*dt (default sub-step
+        dt_exp/2, which annihilates the highest mode) + n_sub RKL2 sub-cycles.
+        Returns (u1, (n_euler, s))."""
+        if n_euler is None:
+            n_euler = 0 if euler_frac == 0 else int(math.ceil(euler_frac * dt / (0.5 * dt_exp) - 1e-12))
+        ncomp = 1 if u0.dim() == 3 else u0.shape[0]
+        out = self._alloc(ncomp, u0) if out is None else out
+        st = (ctypes.c_int * 2)()
+        _check("rkl2_advance_hybrid", lib().rkl2_advance_hybrid(
+            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            float(dt), float(dt_exp), float(euler_frac), int(n_euler), int(n_sub), st, _stream(stream)))
+        return out, (st[0], st[1])
 
     def be_pcg_solve(self, mode, un, k, b=None, w=None, dt=0.0, rtol=1e-12, kmax=100000, out=None,
                      stream=None, allow_not_converged=False):

@@ -406,3 +406,33 @@ def test_iso_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv, nc):
 def test_smoke_entry(dev):
     import __graft_entry__ as e
     e.smoke()
+
+
+# ---------------------------------------------------------------- A8 (PAPER.md:341 remedies)
+@pytest.mark.parametrize("frac,n_sub,tma", [(0.25, 1, True), (0.25, 2, False), (0.0, 3, True), (0.5, 1, True)])
+def test_rkl2_hybrid_parity(dev, frac, n_sub, tma):
+    cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
+    g = cfg["grid"]
+    kap = O.spitzer_face_kappa(g, cfg["T"].numpy(), cfg["kappa0"], cfg["T_cut"])
+    op = O.Operator(g, kap, cfg["b"].numpy())
+    dte = O.dt_euler(op)
+    dt = 100.0 * dte
+    n_euler = 0 if frac == 0 else int(math.ceil(frac * dt / (0.5 * dte) - 1e-12))
+    ref, s_ref = O.rkl2_hybrid_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), cfg["T"].numpy(), dt, dte,
+                                       frac, n_euler, n_sub)
+    G = sts().Grid.from_grid(g)
+    G.set_tma(tma)
+    out, (ne, s) = G.rkl2_advance_hybrid("aniso", cfg["T"].to(dev), [torch.as_tensor(x).to(dev) for x in kap],
+                                         cfg["b"].to(dev), None, dt, dte, frac, None, n_sub)
+    assert ne == n_euler and s == s_ref
+    assert rel_l2(cpu(out), ref) <= 1e-11
+    # viscosity (3 components, weighted) through the same entry point
+    cv = W.make_config("c2_visc64", shape=(12, 9, 40))
+    opv = O.Operator(cv["grid"], [f.numpy() for f in cv["visc_faces"]], None, cv["rho"].numpy())
+    dtev = O.dt_euler(opv)
+    ne_v = 0 if frac == 0 else int(math.ceil(frac * 50 * dtev / (0.5 * dtev) - 1e-12))
+    refv, _ = O.rkl2_hybrid_advance(opv.apply, cv["v"].numpy(), 50 * dtev, dtev, frac, ne_v, n_sub)
+    Gv = sts().Grid.from_grid(cv["grid"])
+    outv, _ = Gv.rkl2_advance_hybrid("iso", cv["v"].to(dev), [f.to(dev) for f in cv["visc_faces"]], None,
+                                     cv["rho"].to(dev), 50 * dtev, dtev, frac, None, n_sub)
+    assert rel_l2(cpu(outv), refv) <= 1e-11

@@ -148,3 +148,59 @@ def test_second_order_in_time():
         errs.append(np.linalg.norm(u - np.exp(lam * T)))
     order = math.log2(errs[1] / errs[2])
     assert 1.7 < order < 2.6, errs
+
+
+# ---------------------------------------------------------------- PAPER.md:341 remedies
+def _hybrid_G(z_over_dtexp, ratio, euler_frac, n_euler, n_sub):
+    """Amplification of the oracle's hybrid on the scalar ODE u' = lam u, with
+    lam = z_over_dtexp / dt_exp (dt_exp = 1)."""
+    lam = np.asarray(z_over_dtexp, dtype=np.float64)
+    u, s = O.rkl2_hybrid_advance(lambda u: lam * u, np.ones_like(lam), ratio, 1.0, euler_frac, n_euler, n_sub)
+    return u, s
+
+
+@pytest.mark.parametrize("ratio,frac,n_euler,n_sub", [(500.0, 0.25, 250, 1), (50.0, 0.25, 25, 2), (300.0, 0.0, 0, 10),
+                                                       (100.0, 0.5, 100, 3)])
+def test_hybrid_closed_form(ratio, frac, n_euler, n_sub):
+    """The hybrid applied to u' = lam u is (1 + dte lam)^n_euler R_s(dtr lam)^n_sub with
+    R_s the Legendre closed form -- written from the definition, not the oracle."""
+    z = -np.linspace(0.0, 2.0, 41)                           # lam dt_exp over the stable range
+    got, s = _hybrid_G(z, ratio, frac, n_euler, n_sub)
+    dte = frac * ratio / n_euler if n_euler else 0.0
+    dtr = (1 - frac) * ratio / n_sub
+    smin = next(t for t in range(2, 100000) if (t * t + t - 2) / 4.0 >= dtr * (1 - 1e-15))
+    assert s == smin
+    want = (1.0 + dte * z) ** n_euler * _legendre_R(s, dtr * z) ** n_sub
+    np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-13)
+
+
+def test_hybrid_reduces_to_rkl2():
+    z = -np.linspace(0.0, 2.0, 17)
+    got, s = _hybrid_G(z, 123.0, 0.0, 0, 1)
+    assert s == O.rkl2_num_stages(123.0, 1.0)
+    np.testing.assert_allclose(got, _scalar_G(s, 123.0 * z), rtol=1e-13, atol=1e-15)
+
+
+def test_paper_euler_prefix_damps_high_modes_more_than_be():
+    """explicit Euler over ~1/4 of the step 'damps high modes more than
+    even a full step with BE' (Fig. 8 ratio 500, dte = dt_exp/2): over the upper half
+    of the discrete spectrum the hybrid's amplification is below BE's 1/(1 - dt lam)."""
+    ratio = GOLD["rkl2_high_mode_damping"]["ratio"]
+    z = -np.linspace(1.0, 2.0, 101)                          # lam dt_exp, upper half
+    got, _ = _hybrid_G(z, ratio, 0.25, int(0.25 * ratio / 0.5), 1)
+    be = 1.0 / (1.0 - ratio * z)
+    assert np.all(np.abs(got) <= np.abs(be))
+    # ... while plain RKL2 at that ratio leaves ~0.5 there (PAPER.md:339)
+    s = O.rkl2_num_stages(ratio, 1.0)
+    assert np.abs(_scalar_G(s, ratio * z[-1])) > 0.3
+
+
+def test_paper_rkl2_subcycling_approaches_be():
+    """sub-cycling RKL2 (~10 sub-cycles) gives a solution close to BE:
+    the high-mode amplification moves from ~0.5 (one super-step) to near BE's."""
+    ratio = 500.0
+    z = -np.linspace(1.5, 2.0, 51)
+    one = np.abs(_scalar_G(O.rkl2_num_stages(ratio, 1.0), ratio * z))
+    sub, _ = _hybrid_G(z, ratio, 0.0, 0, 10)
+    be = np.abs(1.0 / (1.0 - ratio * z))
+    assert np.max(np.abs(np.abs(sub) - be)) < 0.25 * np.min(np.abs(one - be))
