@@ -1,6 +1,7 @@
 // Pointwise kernels of the path: lagged Spitzer face diffusivity (A3) and the
 // PCG vector updates / deterministic dot-product reductions (A7).
 #include "sts_common.cuh"
+#include "pcg.cuh"
 
 namespace sts {
 
@@ -71,78 +72,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// x += alpha p ; r -= alpha y ; z = r d ; partial r.z   (z is not stored: p-update recomputes it)
-template <int NC>
-__global__ void __launch_bounds__(256) pcg_update_kernel(long long n, long long cs, double* __restrict__ x,
-                                                         double* __restrict__ r, const double* __restrict__ p,
-                                                         const double* __restrict__ y, const double* __restrict__ d,
-                                                         const PcgScal* __restrict__ sc, double* __restrict__ partials,
-                                                         long long pstride) {
-  double alpha[NC];
-  bool act[NC];
-  bool any = false;
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
-    act[q] = !sc[q].done;
-    alpha[q] = sc[q].alpha;
-    any = any || act[q];
-  }
-  if (!any) return;
-  double acc[NC];
-#pragma unroll
-  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const double de = d[e];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      if (!act[q]) continue;
-      const long long o = e + q * cs;
-      x[o] += alpha[q] * p[o];
-      const double rn = r[o] - alpha[q] * y[o];
-      r[o] = rn;
-      acc[q] += rn * (rn * de);
-    }
-  }
-  __shared__ double red[NC][8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
-    const double s = warp_sum_d(acc[q]);
-    if (lane == 0) red[q][wid] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x < NC) {
-    double s = 0.0;
-    for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
-    partials[threadIdx.x * pstride + blockIdx.x] = s;
-  }
-}
-
-template <int NC>
-__global__ void __launch_bounds__(256) pcg_pupdate_kernel(long long n, long long cs, double* __restrict__ p,
-                                                          const double* __restrict__ r, const double* __restrict__ d,
-                                                          const PcgScal* __restrict__ sc) {
-  double beta[NC];
-  bool act[NC];
-  bool any = false;
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
-    act[q] = !sc[q].done;
-    beta[q] = sc[q].beta;
-    any = any || act[q];
-  }
-  if (!any) return;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const double de = d[e];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      if (!act[q]) continue;
-      const long long o = e + q * cs;
-      p[o] = r[o] * de + beta[q] * p[o];
-    }
-  }
-}
-
 // ---- restructured iteration (DESIGN.md §5 "PCG passes"): the x update of Fig. 1
 // is deferred to the next p pass, so one iteration is
 //   S-pass (stencil): p_k = z_k + beta p_{k-1};  x += alpha_{k-1} p_{k-1};  y = A p_k;  p_k.y
@@ -186,7 +115,8 @@ template <int NC>
 __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long cs, double* __restrict__ r,
                                                           double* __restrict__ z, const double* __restrict__ y,
                                                           const double* __restrict__ d, const PcgScal* __restrict__ sc,
-                                                          double* __restrict__ partials, long long pstride) {
+                                                          double* __restrict__ partials, long long pstride,
+                                                          FinRed fin) {
   double alpha[NC];
   bool act[NC];
   bool any = false;
@@ -256,6 +186,12 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
     for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
     partials[threadIdx.x * pstride + blockIdx.x] = s;
   }
+  if (fin.ticket) {
+    __shared__ double fred[32];
+    __shared__ unsigned flag;
+    fused_final_reduce(fin, partials, pstride, gridDim.x, threadIdx.x, blockDim.x, fred, &flag,
+                       [] { __syncthreads(); });
+  }
 }
 
 // 16-byte vectorised variant (n, cs even, arrays 16 B aligned): element pairs, two
@@ -265,7 +201,8 @@ __global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long 
                                                              double2* __restrict__ z, const double2* __restrict__ y,
                                                              const double2* __restrict__ d,
                                                              const PcgScal* __restrict__ sc,
-                                                             double* __restrict__ partials, long long pstride) {
+                                                             double* __restrict__ partials, long long pstride,
+                                                             FinRed fin) {
   double alpha[NC];
   bool act[NC];
   bool any = false;
@@ -333,6 +270,12 @@ __global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long 
     for (int w = 0; w < 8; ++w) s += red[threadIdx.x][w];
     partials[threadIdx.x * pstride + blockIdx.x] = s;
   }
+  if (fin.ticket) {
+    __shared__ double fred[32];
+    __shared__ unsigned flag;
+    fused_final_reduce(fin, partials, pstride, gridDim.x, threadIdx.x, blockDim.x, fred, &flag,
+                       [] { __syncthreads(); });
+  }
 }
 
 template <int NC>
@@ -376,16 +319,16 @@ void launch_pcg_pnew(int ncomp, long long n, long long cs, double* pnew, const d
 }
 
 void launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* z, const double* y, const double* d,
-                        const PcgScal* sc, double* partials, long long pstride, cudaStream_t st) {
+                        const PcgScal* sc, double* partials, long long pstride, const FinRed& fin, cudaStream_t st) {
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (n % 2 == 0 && cs % 2 == 0 && a16(r) && a16(z) && a16(y) && a16(d)) {
     double2* r2 = reinterpret_cast<double2*>(r);
     double2* z2 = reinterpret_cast<double2*>(z);
     const double2* y2 = reinterpret_cast<const double2*>(y);
     const double2* d2 = reinterpret_cast<const double2*>(d);
-    STS_NC_SWITCH(ncomp, pcg_rupdate_v2_kernel, n / 2, cs / 2, r2, z2, y2, d2, sc, partials, pstride);
+    STS_NC_SWITCH(ncomp, pcg_rupdate_v2_kernel, n / 2, cs / 2, r2, z2, y2, d2, sc, partials, pstride, fin);
   } else {
-    STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride);
+    STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride, fin);
   }
   STS_CUDA(cudaGetLastError());
 }
@@ -394,54 +337,6 @@ void launch_pcg_xfinal(int ncomp, long long n, long long cs, double* x, const do
                        const PcgScal* sc, cudaStream_t st) {
   STS_NC_SWITCH(ncomp, pcg_xfinal_kernel, n, cs, x, p0, p1, sc);
   STS_CUDA(cudaGetLastError());
-}
-
-void launch_pcg_update(int ncomp, long long n, long long cs, double* x, double* r, const double* p,
-                       const double* y, const double* d, const PcgScal* sc, double* partials,
-                       long long pstride, cudaStream_t st) {
-  switch (ncomp) {
-    case 1: pcg_update_kernel<1><<<PW_BLOCKS, 256, 0, st>>>(n, cs, x, r, p, y, d, sc, partials, pstride); break;
-    case 2: pcg_update_kernel<2><<<PW_BLOCKS, 256, 0, st>>>(n, cs, x, r, p, y, d, sc, partials, pstride); break;
-    case 3: pcg_update_kernel<3><<<PW_BLOCKS, 256, 0, st>>>(n, cs, x, r, p, y, d, sc, partials, pstride); break;
-    default: throw Error{STS_ERR_ARG, "ncomp"};
-  }
-  STS_CUDA(cudaGetLastError());
-}
-
-void launch_pcg_pupdate(int ncomp, long long n, long long cs, double* p, const double* r, const double* d,
-                        const PcgScal* sc, cudaStream_t st) {
-  switch (ncomp) {
-    case 1: pcg_pupdate_kernel<1><<<PW_BLOCKS, 256, 0, st>>>(n, cs, p, r, d, sc); break;
-    case 2: pcg_pupdate_kernel<2><<<PW_BLOCKS, 256, 0, st>>>(n, cs, p, r, d, sc); break;
-    case 3: pcg_pupdate_kernel<3><<<PW_BLOCKS, 256, 0, st>>>(n, cs, p, r, d, sc); break;
-    default: throw Error{STS_ERR_ARG, "ncomp"};
-  }
-  STS_CUDA(cudaGetLastError());
-}
-
-// scalar recurrences of Fig. 1 (one thread per component)
-__device__ void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal* sc, double rtol2) {
-  PcgScal& s = sc[c];
-  if (phase == PH_R0) {
-    s.rz = sums[c * nq + 0];
-    s.thresh = rtol2 * sums[c * nq + 1];
-    s.iters = 0;
-    s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
-    s.beta = 0.0;
-    s.ax = 0.0;
-  } else if (phase == PH_AP) {
-    if (s.done) return;
-    s.pAp = sums[c * nq];
-    s.alpha = s.rz / s.pAp;                // alpha_k = r_r / (p_k . y_k)
-  } else if (phase == PH_RZ) {
-    if (s.done) return;
-    s.rz_old = s.rz;
-    s.rz = sums[c * nq];                   // r_r = r_{k+1} . z_{k+1}
-    s.iters += 1;
-    s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k, applied by the next p pass / final pass
-    if (s.rz <= s.thresh) s.done = 1;      // check r_r for convergence
-    else s.beta = s.rz / s.rz_old;         // beta_k = r_r / r_old
-  }
 }
 
 // one CTA: fixed-order sums of the per-CTA partials (deterministic), then the phase

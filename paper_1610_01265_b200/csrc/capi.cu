@@ -404,7 +404,8 @@ static std::vector<Range> sweep_ranges(const sts_grid* g, bool overlap) {
 // the halos have landed.  `make(si)` returns the slab's StencilCall; returns the
 // number of CTAs launched (per-CTA partial sums are written from pbase 0 on).
 template <class Make>
-static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Make make) {
+static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Make make,
+                 const FinRed* fin = nullptr) {
   const bool overlap = needs_halos(g) && xs.size() > 0;
   cudaStream_t cst = nullptr;
   if (overlap) {
@@ -414,22 +415,31 @@ static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Ma
     for (const Xch& x : xs) exchange(g, x.slot, x.arr, x.ncomp, cst);
     STS_CUDA(cudaEventRecord(g->ev_b, cst));
   }
-  int pb = 0;
-  bool waited = false;
-  for (const Range& r : sweep_ranges(g, overlap)) {
-    if (r.boundary && !waited) {
-      STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
-      waited = true;
-    }
+  const std::vector<Range> ranges = sweep_ranges(g, overlap);
+  std::vector<StencilCall> calls;
+  int total = 0;
+  for (const Range& r : ranges) {
     StencilCall c = make(r.si);
     c.ib = r.ib;
     c.ie = r.ie;
-    c.ea.pbase = pb;
-    pb += pass_blocks(g, c);
-    launch_pass(g, c, st);
+    c.ea.pbase = total;
+    total += pass_blocks(g, c);
+    calls.push_back(c);
+  }
+  bool waited = false;
+  for (size_t i = 0; i < calls.size(); ++i) {
+    if (ranges[i].boundary && !waited) {
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
+      waited = true;
+    }
+    if (fin && i + 1 == calls.size()) {   // the last launch finishes the pass's reduction
+      calls[i].ea.fin = *fin;
+      calls[i].ea.fin.ntot = total;
+    }
+    launch_pass(g, calls[i], st);
   }
   if (overlap && !waited) STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
-  return pb;
+  return total;
 }
 
 // CTAs of a sweep (same ranges and kernel choice as sweep())
@@ -661,6 +671,7 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const doub
       }
       STS_CUDA(cudaMallocHost(&g->h_pinned, 4096));
       STS_CUDA(cudaMalloc(&g->d_ticket, 64 * sizeof(unsigned int)));
+      STS_CUDA(cudaMemset(g->d_ticket, 0, 64 * sizeof(unsigned int)));
     } catch (...) {
       sts_grid_destroy(g);
       throw;
@@ -1102,6 +1113,19 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     double* sums = partials + 2 * ncomp * pstride;
     sc = reinterpret_cast<PcgScal*>(sums + 16);
 
+    // fused final reductions (single process): the last CTA of the S-pass / U-pass sums
+    // the partials and runs the scalar phase, saving two launches per iteration
+    FinRed fin_s;
+    fin_s.ticket = g->d_ticket;
+    fin_s.sums = sums;
+    fin_s.sc = sc;
+    fin_s.ncomp = ncomp;
+    fin_s.nq = 1;
+    fin_s.phase = PH_AP;
+    fin_s.rtol2 = rtol2;
+    FinRed fin_u = fin_s;
+    fin_u.phase = PH_RZ;
+    fin_u.ntot = PW_BLOCKS;
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
       if (g->comm) {
@@ -1137,8 +1161,9 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
         double* pnew = pb[k & 1];
         int nbs;
         if (fused) {
-          if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, st, make_s);
-          else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, st, make_s);
+          const FinRed* fs = g->comm ? nullptr : &fin_s;
+          if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, st, make_s, fs);
+          else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, st, make_s, fs);
         } else {
           {
             Timed t(g, STS_K_PCG_PUPDATE, st);
@@ -1146,12 +1171,13 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
           }
           nbs = sweep(g, {{H_U, pnew, ncomp}}, st, make_ap);
         }
-        reduce(nbs, 1, PH_AP);
+        if (!(fused && !g->comm)) reduce(nbs, 1, PH_AP);   // else finished by the S-pass's last CTA
         {
           Timed t(g, STS_K_PCG_UPDATE, st);
-          launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride, st);
+          launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
+                             g->comm ? FinRed{} : fin_u, st);
         }
-        reduce(PW_BLOCKS, 1, PH_RZ);
+        if (g->comm) reduce(PW_BLOCKS, 1, PH_RZ);
       }
       launched += nb;
       batch = std::min(batch * 2, 64);

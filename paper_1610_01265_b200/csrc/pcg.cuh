@@ -1,0 +1,73 @@
+// PCG scalar recurrences and the fused ("last CTA") final reduction, shared by the
+// pointwise and the stencil kernels.  Device code only; product path.
+#pragma once
+
+#include "sts_common.cuh"
+
+namespace sts {
+
+// scalar recurrences of Fig. 1 (one thread per component)
+__device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal* sc, double rtol2) {
+  PcgScal& s = sc[c];
+  if (phase == PH_R0) {
+    s.rz = sums[c * nq + 0];
+    s.thresh = rtol2 * sums[c * nq + 1];
+    s.iters = 0;
+    s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
+    s.beta = 0.0;
+    s.ax = 0.0;
+  } else if (phase == PH_AP) {
+    if (s.done) return;
+    s.pAp = sums[c * nq];
+    s.alpha = s.rz / s.pAp;                // alpha_k = r_r / (p_k . y_k)
+  } else if (phase == PH_RZ) {
+    if (s.done) return;
+    s.rz_old = s.rz;
+    s.rz = sums[c * nq];                   // r_r = r_{k+1} . z_{k+1}
+    s.iters += 1;
+    s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k, applied by the next p pass / final pass
+    if (s.rz <= s.thresh) s.done = 1;      // check r_r for convergence
+    else s.beta = s.rz / s.rz_old;         // beta_k = r_r / r_old
+  }
+}
+
+
+// Fused final reduction of a PCG pass (single process: no all-reduce between the
+// partial sums and the scalar update).  Every CTA of the LAST launch of the pass
+// takes a ticket after its partials are visible; the CTA drawing the last ticket
+// sums all `ntot` partial slots of every row in a fixed order (deterministic,
+// independent of which CTA is last), runs the scalar phase and re-arms the ticket.
+// The earlier launches of the pass (interior / boundary planes, virtual slabs) ran
+// before this one on the same stream, so their partials are complete.
+//   nthr threads participate; sync() is the barrier among them.
+template <class Sync>
+__device__ inline void fused_final_reduce(const FinRed& f, const double* partials, long long pstride,
+                                          unsigned long long nblk, int tid, int nthr, double* red /*[32]*/,
+                                          unsigned* s_flag, Sync sync) {
+  __threadfence();
+  sync();
+  if (tid == 0) *s_flag = (atomicAdd(f.ticket, 1u) == (unsigned)(nblk - 1)) ? 1u : 0u;
+  sync();
+  if (*s_flag == 0u) return;
+  __threadfence();
+  const int lane = tid & 31, wid = tid >> 5, nw = (nthr + 31) >> 5;
+  for (int row = 0; row < f.ncomp * f.nq; ++row) {
+    const double* src = partials + row * pstride;
+    double a = 0.0;
+    for (long long b = tid; b < f.ntot; b += nthr) a += __ldcg(src + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) red[wid] = a;
+    sync();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < nw; ++w) v += red[w];
+      f.sums[row] = v;
+    }
+    sync();
+  }
+  if (tid < f.ncomp) pcg_phase(f.sums, tid, f.nq, f.phase, f.sc, f.rtol2);
+  if (tid == 0) *f.ticket = 0u;
+}
+
+}  // namespace sts

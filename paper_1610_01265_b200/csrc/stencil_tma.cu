@@ -33,6 +33,7 @@
 
 #include "sts_common.cuh"
 #include "tma.cuh"
+#include "pcg.cuh"
 
 namespace sts {
 
@@ -292,6 +293,13 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       for (int w = 0; w < XNT / 32; ++w) s += red[w];
       c.ea.partials[c.ea.pbase + blk] = s;
     }
+    if (c.ea.fin.ticket) {
+      __shared__ double fred[32];
+      __shared__ unsigned flag;
+      fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
+                         (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, XNT, fred, &flag,
+                         [] { asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory"); });
+    }
   }
 }
 
@@ -320,10 +328,7 @@ static dim3 tma_grid(const Geo& G, int ib, int ie, int* ic_out) {
     return dim3(0, 0, 0);
   }
   const long long tiles = (long long)nbx * nby;
-  const long long want = 148LL * 3 * 3;          // ~3 waves of 3 resident CTAs per SM
-  int ic = (int)((np * tiles + want - 1) / want);
-  ic = ic < 16 ? 16 : ic;
-  if (ic > np) ic = np;
+  const int ic = choose_chunk(tiles, np, 148LL * 3, 2.0, 6);
   *ic_out = ic;
   return dim3(nbx, nby, (np + ic - 1) / ic);
 }

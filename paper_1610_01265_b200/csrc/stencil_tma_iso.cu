@@ -21,6 +21,7 @@
 // fused PCG S-pass p = z + beta pold, x += ax pold, y = A p, p.y (Fig. 1).
 #include "sts_common.cuh"
 #include "tma.cuh"
+#include "pcg.cuh"
 
 namespace sts {
 
@@ -324,6 +325,13 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       for (int w = 0; w < IJ; ++w) s += red[tid][w];
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
+    if (c.ea.fin.ticket) {
+      __shared__ double fred[32];
+      __shared__ unsigned flag;
+      fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
+                         (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, INT, fred, &flag,
+                         [] { asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory"); });
+    }
   }
 }
 
@@ -351,11 +359,8 @@ static dim3 iso_grid(const Geo& G, int ib, int ie, int* ic_out) {
     return dim3(0, 0, 0);
   }
   const long long tiles = (long long)nbx * nby;
-  const long long want = 148LL * 2 * 8;          // >= ~8 waves of 2 resident CTAs per SM
-  int ic = (int)((np * tiles + want - 1) / want);
-  ic = ic < 32 ? 32 : ic;
-  if (ic > 128) ic = 128;
-  if (ic > np) ic = np;
+  // (long marches leave a ragged last wave: cap the chunk at 128 planes)
+  const int ic = choose_chunk(tiles, np, 148LL * 2, 0.5, 4, 128);
   *ic_out = ic;
   return dim3(nbx, nby, (np + ic - 1) / ic);
 }

@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstddef>
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -175,6 +176,16 @@ struct PcgScal {
   int done, iters;
 };
 
+// fused final reduction of a PCG pass (pcg.cuh: fused_final_reduce)
+struct FinRed {
+  unsigned int* ticket = nullptr;   // zeroed counter; null: no fused reduction in this launch
+  double* sums = nullptr;
+  PcgScal* sc = nullptr;
+  int ncomp = 1, nq = 1, phase = 0;
+  long long ntot = 0;               // partial slots per row summed by the last CTA
+  double rtol2 = 0.0;
+};
+
 struct EpiArgs {
   double* out = nullptr;       // primary output   [ncomp][nl][plane]
   double* out2 = nullptr;      // secondary output (M0 / x / ...)
@@ -190,6 +201,7 @@ struct EpiArgs {
   const PcgScal* sc = nullptr; // per-component PCG scalars (skip components with done set)
   double* x = nullptr;         // EPI_PCG_S: iterate, updated in place (x += ax pold)
   int first = 0;               // EPI_PCG_S: first iteration (p = z, no pold, no x update)
+  FinRed fin;                  // fused final reduction (last launch of a single-process pass)
 };
 
 struct StencilCall {
@@ -230,6 +242,26 @@ __host__ __device__ inline long long ev_cstride(int nl, int n2, int n3) { return
 bool aniso_tma_eligible(const StencilCall& c);
 bool launch_aniso_tma(const StencilCall& c, cudaStream_t st);
 int aniso_tma_blocks(const Geo& G, int ib, int ie);
+// r-chunk length of a 2.5-D march: minimises (waves of `slots` resident CTAs) x
+// (planes a CTA streams = ic + extra), i.e. wave quantisation against the planes
+// each extra chunk re-reads (extra = 2 for the vertex scheme, ~0.5 for 7-point)
+inline int choose_chunk(long long tiles, int np, long long slots, double extra, int icmin, int icmax = 1 << 30) {
+  const int hi = std::max(1, std::min(np, icmax));
+  int best = hi;
+  double bc = 1e300;
+  for (int ic = std::max(1, std::min(icmin, hi)); ic <= hi; ++ic) {
+    const long long nch = (np + ic - 1) / ic;
+    if (ic != hi && (long long)(np + nch - 1) / nch != ic) continue;   // only distinct chunkings
+    const long long ctas = tiles * nch;
+    const double cost = (double)((ctas + slots - 1) / slots) * (ic + extra);
+    if (cost < bc * (1 - 1e-9)) {
+      bc = cost;
+      best = ic;
+    }
+  }
+  return best;
+}
+
 // the isotropic (ncomp <= 3) counterpart (stencil_tma_iso.cu)
 bool iso_tma_eligible(const StencilCall& c);
 bool launch_iso_tma(const StencilCall& c, cudaStream_t st);
@@ -238,9 +270,10 @@ int iso_tma_blocks(const Geo& G, int ib, int ie);
 // pnew = z + beta pold (pold unused if first); x += ax pold (not if first)
 void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, const double* z, const double* pold,
                      double* x, const PcgScal* sc, int first, cudaStream_t st);
-// r -= alpha y; z = r d; partial r.z
+// r -= alpha y; z = r d; partial r.z  (fin.ticket set: the last CTA also finishes the reduction)
 void launch_pcg_rupdate(int ncomp, long long n, long long cstride, double* r, double* z, const double* y,
-                        const double* d, const PcgScal* sc, double* partials, long long pstride, cudaStream_t st);
+                        const double* d, const PcgScal* sc, double* partials, long long pstride,
+                        const FinRed& fin, cudaStream_t st);
 // x += ax p[iters % 2] for components with iters > 0
 void launch_pcg_xfinal(int ncomp, long long n, long long cstride, double* x, const double* p0, const double* p1,
                        const PcgScal* sc, cudaStream_t st);
@@ -257,12 +290,5 @@ void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, i
                        double* sums, int phase, PcgScal* sc, double rtol2, cudaStream_t st);
 void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal* sc, double rtol2,
                        cudaStream_t st);
-// x += a p; r -= a y; z = r d; partial r.z      (all local cells, per component)
-void launch_pcg_update(int ncomp, long long n, long long cstride, double* x, double* r, const double* p,
-                       const double* y, const double* d, const PcgScal* sc, double* partials,
-                       long long pstride, cudaStream_t st);
-// p = r d + beta p
-void launch_pcg_pupdate(int ncomp, long long n, long long cstride, double* p, const double* r,
-                        const double* d, const PcgScal* sc, cudaStream_t st);
 
 }  // namespace sts
