@@ -145,6 +145,13 @@ int sts_grid_set_timing(sts_grid* g, int enable);
  * cp.async kernels everywhere.  Results agree to rounding either way.
  */
 int sts_grid_set_tma(sts_grid* g, int enable);
+
+/*
+ * enable != 0 (the default): single-process PCG solves replay one captured CUDA
+ * graph per pair of iterations (k, k+1 >= 2); 0 launches every kernel directly.
+ * Graphs are never used while per-launch timing is on or with an NCCL communicator.
+ */
+int sts_grid_set_graphs(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
 

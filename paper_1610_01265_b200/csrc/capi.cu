@@ -363,6 +363,13 @@ static cudaStream_t comm_stream(sts_grid* g) {
   return g->comm_stream;
 }
 
+// the library's own non-blocking stream for CUDA-graph capture / replay
+static cudaStream_t graph_stream(sts_grid* g) {
+  if (!g->graph_stream) STS_CUDA(cudaStreamCreateWithFlags(&g->graph_stream, cudaStreamNonBlocking));
+  if (!g->ev_c) STS_CUDA(cudaEventCreateWithFlags(&g->ev_c, cudaEventDisableTiming));
+  return g->graph_stream;
+}
+
 struct Xch {
   int slot;
   const double* arr;
@@ -693,6 +700,8 @@ int sts_grid_destroy(sts_grid* g) {
     if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
     if (g->ev_a) cudaEventDestroy(g->ev_a);
     if (g->ev_b) cudaEventDestroy(g->ev_b);
+    if (g->ev_c) cudaEventDestroy(g->ev_c);
+    if (g->graph_stream) cudaStreamDestroy(g->graph_stream);
     for (auto& r : g->pending) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -726,6 +735,13 @@ int sts_grid_set_timing(sts_grid* g, int enable) {
   return guard([&] {
     STS_REQUIRE(g, "NULL grid");
     g->timing = enable != 0;
+  });
+}
+
+int sts_grid_set_graphs(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->graphs = enable != 0;
   });
 }
 
@@ -1144,43 +1160,110 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
     //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
     auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
+    // one PCG iteration k on stream `is`
+    auto iteration = [&](int k, cudaStream_t is) {
+      k_cur = k;
+      double* pold = pb[(k - 1) & 1];
+      double* pnew = pb[k & 1];
+      int nbs;
+      if (fused) {
+        // (the last CTA finishes the reduction when the pass has few CTAs; large passes
+        // keep the 1024-thread reduction kernel, which sums ~1e4 partials faster)
+        const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_s;
+        if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, is, make_s, fs);
+        else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, is, make_s, fs);
+      } else {
+        {
+          Timed t(g, STS_K_PCG_PUPDATE, is);
+          launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, k == 1, is);
+        }
+        nbs = sweep(g, {{H_U, pnew, ncomp}}, is, make_ap);
+      }
+      if (!(fused && !g->comm && sb_s <= 4096)) {           // else finished by the S-pass's last CTA
+        Timed t(g, STS_K_PCG_REDUCE, is);
+        launch_pcg_reduce(partials, pstride, nbs, ncomp, 1, sums, g->comm ? PH_NONE : PH_AP, sc, rtol2, is);
+        if (g->comm) {
+          STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
+          launch_pcg_scalar(sums, ncomp, 1, PH_AP, sc, rtol2, is);
+          g->launches += 1;
+        }
+      }
+      {
+        Timed t(g, STS_K_PCG_UPDATE, is);
+        launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
+                           g->comm ? FinRed{} : fin_u, is);
+      }
+      if (g->comm) {
+        Timed t(g, STS_K_PCG_REDUCE, is);
+        launch_pcg_reduce(partials, pstride, PW_BLOCKS, ncomp, 1, sums, PH_NONE, sc, rtol2, is);
+        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
+        launch_pcg_scalar(sums, ncomp, 1, PH_RZ, sc, rtol2, is);
+        g->launches += 1;
+      }
+    };
+    // Iterations k >= 2 come in identical pairs (k even, k odd: the p buffers swap back),
+    // so a single process replays one captured CUDA graph per pair: no host launch work
+    // and minimal launch gaps per iteration.  Instrumented runs (per-launch events) and
+    // NCCL runs launch directly.  The graph runs on the library's own non-blocking
+    // stream (capture is not allowed on the legacy default stream), forked from and
+    // joined back to the caller's stream.
+    const bool use_graph = g->graphs && !g->timing && g->comm == nullptr;
+    cudaStream_t is = st;
+    cudaGraphExec_t pair_exec = nullptr;
+    long long pair_launches = 0;
+    if (use_graph) {
+      is = graph_stream(g);
+      STS_CUDA(cudaEventRecord(g->ev_c, st));
+      STS_CUDA(cudaStreamWaitEvent(is, g->ev_c, 0));
+    }
     int launched = 0;
     int batch = 4;
     bool all_done = false;
-    while (true) {
-      STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, st));
-      STS_CUDA(cudaStreamSynchronize(st));
-      all_done = true;
-      for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
-      if (all_done || launched >= kmax) break;
-      const int nb = std::min(batch, kmax - launched);
-      for (int it = 0; it < nb; ++it) {
-        const int k = launched + it + 1;
-        k_cur = k;
-        double* pold = pb[(k - 1) & 1];
-        double* pnew = pb[k & 1];
-        int nbs;
-        if (fused) {
-          const FinRed* fs = g->comm ? nullptr : &fin_s;
-          if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, st, make_s, fs);
-          else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, st, make_s, fs);
-        } else {
-          {
-            Timed t(g, STS_K_PCG_PUPDATE, st);
-            launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, k == 1, st);
+    try {
+      while (true) {
+        STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, is));
+        STS_CUDA(cudaStreamSynchronize(is));
+        all_done = true;
+        for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
+        if (all_done || launched >= kmax) break;
+        const int nb = std::min(batch, kmax - launched);
+        int it = 0;
+        while (it < nb) {
+          const int k = launched + it + 1;
+          // (the first pair, k = 2, 3, runs directly: every kernel variant it uses has then
+          // had its one-time attribute setup outside the capture)
+          if (use_graph && k >= 4 && (k % 2) == 0 && it + 2 <= nb) {
+            if (!pair_exec) {
+              const long long l0 = g->launches;
+              cudaGraph_t graph;
+              STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
+              iteration(k, is);
+              iteration(k + 1, is);
+              STS_CUDA(cudaStreamEndCapture(is, &graph));
+              STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
+              STS_CUDA(cudaGraphDestroy(graph));
+              pair_launches = g->launches - l0;
+              g->launches = l0;
+            }
+            STS_CUDA(cudaGraphLaunch(pair_exec, is));
+            g->launches += pair_launches;
+            it += 2;
+          } else {
+            iteration(k, is);
+            it += 1;
           }
-          nbs = sweep(g, {{H_U, pnew, ncomp}}, st, make_ap);
         }
-        if (!(fused && !g->comm)) reduce(nbs, 1, PH_AP);   // else finished by the S-pass's last CTA
-        {
-          Timed t(g, STS_K_PCG_UPDATE, st);
-          launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
-                             g->comm ? FinRed{} : fin_u, st);
-        }
-        if (g->comm) reduce(PW_BLOCKS, 1, PH_RZ);
+        launched += nb;
+        batch = std::min(batch * 2, 64);
       }
-      launched += nb;
-      batch = std::min(batch * 2, 64);
+    } catch (...) {
+      if (pair_exec) cudaGraphExecDestroy(pair_exec);
+      throw;
+    }
+    if (pair_exec) STS_CUDA(cudaGraphExecDestroy(pair_exec));
+    if (use_graph) {
+      STS_CUDA(cudaEventRecord(g->ev_c, is));
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_c, 0));
     }
     {
       Timed t(g, STS_K_PCG_XFINAL, st);

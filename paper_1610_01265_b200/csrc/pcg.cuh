@@ -53,8 +53,17 @@ __device__ inline void fused_final_reduce(const FinRed& f, const double* partial
   const int lane = tid & 31, wid = tid >> 5, nw = (nthr + 31) >> 5;
   for (int row = 0; row < f.ncomp * f.nq; ++row) {
     const double* src = partials + row * pstride;
-    double a = 0.0;
-    for (long long b = tid; b < f.ntot; b += nthr) a += __ldcg(src + b);
+    // four independent accumulators per thread (loads in flight), combined in a fixed order
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    long long b = tid;
+    for (; b + 3LL * nthr < f.ntot; b += 4LL * nthr) {
+      a0 += __ldcg(src + b);
+      a1 += __ldcg(src + b + nthr);
+      a2 += __ldcg(src + b + 2LL * nthr);
+      a3 += __ldcg(src + b + 3LL * nthr);
+    }
+    for (; b < f.ntot; b += nthr) a0 += __ldcg(src + b);
+    double a = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) red[wid] = a;

@@ -135,6 +135,9 @@ struct sts_grid {
   long long launches = 0;
   size_t halo_bytes = 0;
   bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
+  bool graphs = true;                   // CUDA-graph replay of PCG iteration pairs (sts_grid_set_graphs)
+  cudaStream_t graph_stream = nullptr;  // non-blocking stream for capture / replay
+  cudaEvent_t ev_c = nullptr;
   // per-kernel-class event timing (sts_grid_set_timing)
   bool timing = false;
   struct Rec { int kind; cudaEvent_t a, b; };

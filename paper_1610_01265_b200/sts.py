@@ -57,6 +57,7 @@ def lib():
         "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
         "sts_grid_set_timing": (I, [P, I]),
         "sts_grid_set_tma": (I, [P, I]),
+        "sts_grid_set_graphs": (I, [P, I]),
         "sts_grid_timing_reset": (I, [P]),
         "sts_grid_timing": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
         "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
@@ -177,6 +178,10 @@ class Grid:
     def set_tma(self, enable=True):
         """Use the TMA pipelined anisotropic kernels where eligible (default) or force the cp.async ones."""
         _check("sts_grid_set_tma", lib().sts_grid_set_tma(self._h, int(bool(enable))))
+
+    def set_graphs(self, enable=True):
+        """Replay PCG iteration pairs as CUDA graphs (default) or launch every kernel directly."""
+        _check("sts_grid_set_graphs", lib().sts_grid_set_graphs(self._h, int(bool(enable))))
 
     def timing_reset(self):
         _check("sts_grid_timing_reset", lib().sts_grid_timing_reset(self._h))

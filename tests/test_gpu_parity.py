@@ -245,7 +245,7 @@ def test_rkl2_inplace_and_host_pointers(dev):
 
 
 # ---------------------------------------------------------------- A7
-@pytest.mark.parametrize("case", ["c0", "c1", "c1_cpasync", "c2"])
+@pytest.mark.parametrize("case", ["c0", "c1", "c1_cpasync", "c1_nograph", "c2", "c2_nograph"])
 def test_be_pcg_parity(dev, case):
     if case == "c0":
         cfg = W.make_config("c0_heat32")
@@ -265,6 +265,7 @@ def test_be_pcg_parity(dev, case):
     ref, it_ref = O.be_pcg_solve(op, u.numpy(), dt, rtol=1e-12)
     G = sts().Grid.from_grid(g)
     G.set_tma(case != "c1_cpasync")
+    G.set_graphs(not case.endswith("nograph"))
     out, it = G.be_pcg_solve(mode, u.to(dev), [x.to(dev) for x in k], None if b is None else b.to(dev),
                              None if w is None else w.to(dev), dt, 1e-12, 100000)
     assert all(abs(a - c) <= 1 for a, c in zip(it, it_ref)), (it, it_ref)
@@ -401,6 +402,32 @@ def test_iso_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv, nc):
         outs[tma] = (cpu(u), cpu(x))
     assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
     assert rel_l2(outs[True][1], outs[False][1]) <= 2 * tol_be   # both within tol_be of the oracle
+
+
+@pytest.mark.parametrize("nv", [1, 3])
+@pytest.mark.parametrize("mode", ["aniso", "iso"])
+def test_pcg_graph_replay_is_bitwise_identical(dev, nv, mode):
+    """CUDA-graph replay of iteration pairs (incl. the virtual-slab fork/join of the
+    halo exchange inside the graph) runs exactly the kernels of direct launches."""
+    cfg = W.make_config("c1_spitzer64" if mode == "aniso" else "c2_visc64", shape=(21, 19, 70))
+    g = cfg["grid"]
+    outs = []
+    for graphs in (True, False):
+        G = sts().Grid.from_grid(g, n_virtual=nv)
+        G.set_graphs(graphs)
+        if mode == "aniso":
+            T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+            k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+            dte = G.dt_euler("aniso", k, b)
+            x, it = G.be_pcg_solve("aniso", T, k, b, None, 100 * dte, 1e-12, 10000)
+        else:
+            kv = [f.to(dev) for f in cfg["visc_faces"]]
+            rho, v = cfg["rho"].to(dev), cfg["v"].to(dev)
+            dte = G.dt_euler("iso", kv, None, rho)
+            x, it = G.be_pcg_solve("iso", v, kv, None, rho, 500 * dte, 1e-12, 10000)
+        outs.append((x.clone(), it))
+    assert outs[0][1] == outs[1][1]
+    assert torch.equal(outs[0][0], outs[1][0])
 
 
 def test_smoke_entry(dev):
