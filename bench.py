@@ -207,7 +207,7 @@ class Step:
         self.T_rk, self.T_be = alloc(*shape), alloc(*shape)
         self.v_rk, self.v_be = alloc(3, *shape), alloc(3, *shape)
 
-    def cond(self):
+    def cond(self, after_rkl2=None):
         from paper_1610_01265_b200 import sts
         G, I = self.G, self.inp
         if "T" not in I:
@@ -219,10 +219,12 @@ class Step:
         dt = self.ratio * dte
         s_c = sts.rkl2_num_stages(dt, dte)
         G.rkl2_advance("aniso", T, self.k, b, None, dt, s_c, out=self.T_rk)
+        if after_rkl2:
+            after_rkl2()
         _, (it_c,) = G.be_pcg_solve("aniso", T, self.k, b, None, dt, RTOL, KMAX, out=self.T_be)
         return s_c, it_c
 
-    def visc(self):
+    def visc(self, after_rkl2=None):
         from paper_1610_01265_b200 import sts
         G, I = self.G, self.inp
         if "v" not in I:
@@ -233,6 +235,8 @@ class Step:
         dtv = self.ratio * dtev
         s_v = sts.rkl2_num_stages(dtv, dtev)
         G.rkl2_advance("iso", v, kv, None, rho, dtv, s_v, out=self.v_rk)
+        if after_rkl2:
+            after_rkl2()
         _, it_v = G.be_pcg_solve("iso", v, kv, None, rho, dtv, RTOL, KMAX, out=self.v_be)
         return s_v, it_v
 
@@ -271,6 +275,13 @@ class E2EStep:
             sum(nb(x) for x in host_inp.get("visc_faces", ()))
         self.d2h = sum(nb(t) for t in self.out_host.values())
 
+    def _d2h(self, names, cs):
+        ev = cs.record_event()
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(ev)
+            for n in names:
+                self.out_host[n].copy_(getattr(self.step, n), non_blocking=True)
+
     def __call__(self):
         H, D, st = self.host, self.dinp, self.step
         cs = torch.cuda.current_stream()
@@ -285,19 +296,12 @@ class E2EStep:
                 d.copy_(h, non_blocking=True)
             ev_visc = self.copy.record_event()
         cs.wait_event(ev_cond)
-        s_c, it_c = st.cond()
-        done_cond = cs.record_event()
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(done_cond)
-            self.out_host["T_rk"].copy_(st.T_rk, non_blocking=True)
-            self.out_host["T_be"].copy_(st.T_be, non_blocking=True)
+        # every result travels back as soon as it exists, behind the next computation
+        s_c, it_c = st.cond(after_rkl2=lambda: self._d2h(("T_rk",), cs))
+        self._d2h(("T_be",), cs)
         cs.wait_event(ev_visc)
-        s_v, it_v = st.visc()
-        done_visc = cs.record_event()
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(done_visc)
-            self.out_host["v_rk"].copy_(st.v_rk, non_blocking=True)
-            self.out_host["v_be"].copy_(st.v_be, non_blocking=True)
+        s_v, it_v = st.visc(after_rkl2=lambda: self._d2h(("v_rk",), cs))
+        self._d2h(("v_be",), cs)
         cs.wait_stream(self.copy)
         return {"s_cond": s_c, "it_cond": it_c, "s_visc": s_v, "it_visc": it_v,
                 "units": s_c + it_c + s_v + max(it_v)}

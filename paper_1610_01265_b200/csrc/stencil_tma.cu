@@ -89,7 +89,8 @@ struct TmaLay {
   static constexpr size_t SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 2 * XTS * sizeof(uint64_t) + 128;
 };
 
-template <int EPI, bool W>
+// FR: this launch finishes the pass's dot-product reduction in its last CTA
+template <int EPI, bool W, bool FR>
 __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, int ic,
                                                                 const __grid_constant__ TmaArgs ta) {
   using Lay = TmaLay<EPI, W>;
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       for (int w = 0; w < XNT / 32; ++w) s += red[w];
       c.ea.partials[c.ea.pbase + blk] = s;
     }
-    if (c.ea.fin.ticket) {
+    if constexpr (FR) {
       __shared__ double fred[32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
@@ -339,21 +340,28 @@ int aniso_tma_blocks(const Geo& G, int ib, int ie) {
   return (int)(g.x * g.y * g.z);
 }
 
-template <int EPI, bool W>
+template <int EPI, bool W, bool FR>
 static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI, W, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)TmaLay<EPI, W>::SMEM));
     attr = true;
   }
-  aniso_tma_kernel<EPI, W><<<grid, XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
+  aniso_tma_kernel<EPI, W, FR><<<grid, XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
 }
 
 template <int EPI>
 static void launch_w(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
-  if (c.w) launch_t<EPI, true>(c, grid, ic, ta, st);
-  else launch_t<EPI, false>(c, grid, ic, ta, st);
+  constexpr bool kS = (EPI == EPI_PCG_S);
+  const bool fr = kS && c.ea.fin.ticket;
+  if (c.w) {
+    if (fr) launch_t<EPI, true, kS>(c, grid, ic, ta, st);
+    else launch_t<EPI, true, false>(c, grid, ic, ta, st);
+  } else {
+    if (fr) launch_t<EPI, false, kS>(c, grid, ic, ta, st);
+    else launch_t<EPI, false, false>(c, grid, ic, ta, st);
+  }
 }
 
 bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {

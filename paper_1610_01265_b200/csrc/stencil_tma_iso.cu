@@ -76,7 +76,9 @@ struct IsoTmaArgs {
 
 // FST: first PCG iteration (p = z, no pold, no x update) -- a template flag so the
 // steady-state S-pass carries no per-cell branches on it
-template <int EPI, int NC, bool FST>
+// FR: this launch finishes the pass's dot-product reduction in its last CTA (a
+// separate instantiation, so the large-grid variant carries none of that code)
+template <int EPI, int NC, bool FST, bool FR>
 __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int ic,
                                                               const __grid_constant__ IsoTmaArgs ta) {
   using Lay = IsoLay<EPI, NC>;
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       for (int w = 0; w < IJ; ++w) s += red[tid][w];
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
-    if (c.ea.fin.ticket) {
+    if constexpr (FR) {
       __shared__ double fred[32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
@@ -371,15 +373,21 @@ int iso_tma_blocks(const Geo& G, int ib, int ie) {
   return (int)(g.x * g.y * g.z);
 }
 
-template <int EPI, int NC, bool FST>
-static void launch_iso_f(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+template <int EPI, int NC, bool FST, bool FR>
+static void launch_iso_g(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC, FST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC, FST, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)IsoLay<EPI, NC>::SMEM));
     attr = true;
   }
-  iso_tma_kernel<EPI, NC, FST><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+  iso_tma_kernel<EPI, NC, FST, FR><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+}
+
+template <int EPI, int NC, bool FST>
+static void launch_iso_f(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
+  if (EPI == EPI_PCG_S && c.ea.fin.ticket) launch_iso_g<EPI, NC, FST, (EPI == EPI_PCG_S)>(c, grid, ic, ta, st);
+  else launch_iso_g<EPI, NC, FST, false>(c, grid, ic, ta, st);
 }
 
 template <int EPI, int NC>
