@@ -191,20 +191,36 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   };
   const int o00 = uoff(vj, vk), o01 = uoff(vj, vk + 1), o10 = uoff(vj + 1, vk), o11 = uoff(vj + 1, vk + 1);
 
-  // in-plane 2x2 box of the source value s = (PCG: z + beta pold, else u)
-  auto sval = [&](const double* S, int off) {
-    const double v = S[off];
-    if constexpr (EPI == EPI_PCG_S) {
-      if (!first) return fma(beta, S[U_FIELD + off], v);
+  // in-plane 2x2 box of the source value s (PCG: z + beta pold, else u): each lane
+  // loads its column (rows vj, vj+1) and takes column vk+1 from lane vk+1 by shuffle
+  // (lane 31 loads it), halving the shared-memory loads of the march
+  constexpr bool kP = (EPI == EPI_PCG_S);
+  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu, double& un, double& pon) {
+    double z00 = S[o00], z10 = S[o10];
+    double q00 = 0.0, q10 = 0.0;
+    if (kP && !first) {
+      q00 = S[U_FIELD + o00];
+      q10 = S[U_FIELD + o10];
+      z00 = fma(beta, q00, z00);
+      z10 = fma(beta, q10, z10);
     }
-    return v;
-  };
-  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu) {
-    const double u00 = sval(S, o00), u01 = sval(S, o01);
-    const double u10 = sval(S, o10), u11 = sval(S, o11);
-    Su = (u00 + u01) + (u10 + u11);
-    Tu = (u10 - u00) + (u11 - u01);
-    Fu = ig3a * (u01 - u00) + ig3b * (u11 - u10);
+    double z01 = __shfl_down_sync(0xffffffffu, z00, 1), z11 = __shfl_down_sync(0xffffffffu, z10, 1);
+    double q11 = 0.0;
+    if (kP && !first) q11 = __shfl_down_sync(0xffffffffu, q10, 1);
+    if (vk == XK - 1) {
+      z01 = S[o01];
+      z11 = S[o11];
+      if (kP && !first) {
+        q11 = S[U_FIELD + o11];
+        z01 = fma(beta, S[U_FIELD + o01], z01);
+        z11 = fma(beta, q11, z11);
+      }
+    }
+    Su = (z00 + z01) + (z10 + z11);
+    Tu = (z10 - z00) + (z11 - z01);
+    Fu = ig3a * (z01 - z00) + ig3b * (z11 - z10);
+    un = z11;     // own cell of this plane
+    pon = q11;    // its pold (PCG)
   };
 
   double SuL = 0, TuL = 0, FuL = 0;
@@ -215,11 +231,8 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
     mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
-    double SuH, TuH, FuH;
-    usums(S, SuH, TuH, FuH);
-    const double un = sval(S, o11);                                       // own cell of plane p
-    double pon = 0.0;
-    if constexpr (EPI == EPI_PCG_S) pon = first ? 0.0 : S[U_FIELD + o11];
+    double SuH, TuH, FuH, un, pon;
+    usums(S, SuH, TuH, FuH, un, pon);
     double* vb = vbuf + (p & 1) * VBUF;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
@@ -228,20 +241,22 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
       const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
-      vb[tid] = q * er;
-      vb[XNT + tid] = q * et;
-      vb[2 * XNT + tid] = q * ep;
+      // vertex values A, B, C = q e; the horizontal pair sums/differences by shuffle,
+      // the vertical pair through shared memory (the next vertex row is the next warp)
+      const double A = q * er, B = q * et, C = q * ep;
+      const double hA = A + __shfl_down_sync(0xffffffffu, A, 1);
+      const double hB = B + __shfl_down_sync(0xffffffffu, B, 1);
+      const double dC = C - __shfl_down_sync(0xffffffffu, C, 1);
+      vb[tid] = hA;
+      vb[XNT + tid] = hB;
+      vb[2 * XNT + tid] = dC;
       // consumer warps only: the vertex plane is complete
       asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
       double SAh = 0, DBh = 0, DCh = 0;
       if (own) {
-        const double a00 = vb[tid], a01 = vb[tid + 1], a10 = vb[tid + 32], a11 = vb[tid + 33];
-        const double b00 = vb[XNT + tid], b01 = vb[XNT + tid + 1], b10 = vb[XNT + tid + 32], b11 = vb[XNT + tid + 33];
-        const double d00 = vb[2 * XNT + tid], d01 = vb[2 * XNT + tid + 1], d10 = vb[2 * XNT + tid + 32],
-                     d11 = vb[2 * XNT + tid + 33];
-        SAh = (a00 + a01) + (a10 + a11);
-        DBh = (b00 + b01) - (b10 + b11);
-        DCh = (d00 + d10) - (d01 + d11);
+        SAh = hA + vb[tid + 32];
+        DBh = hB - vb[XNT + tid + 32];
+        DCh = dC + vb[2 * XNT + tid + 32];
       }
       if (p >= ib + 1 && own) {
         // output cell plane il = p-1
