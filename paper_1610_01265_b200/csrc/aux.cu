@@ -3,6 +3,8 @@
 #include "sts_common.cuh"
 #include "pcg.cuh"
 
+#include <algorithm>
+
 namespace sts {
 
 // ----------------------------------------------------------------------------
@@ -318,19 +320,51 @@ void launch_pcg_pnew(int ncomp, long long n, long long cs, double* pnew, const d
   STS_CUDA(cudaGetLastError());
 }
 
-void launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* z, const double* y, const double* d,
-                        const PcgScal* sc, double* partials, long long pstride, const FinRed& fin, cudaStream_t st) {
+// grid of the U-pass: exactly the resident capacity (blocks per SM x 148, at most
+// PW_BLOCKS), so the grid-stride loop has no partial last wave
+template <class K>
+static int resident_grid(K kernel) {
+  static int cached = 0;
+  if (!cached) {
+    int per_sm = 0;
+    STS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+    int dev = 0, sms = 148;
+    STS_CUDA(cudaGetDevice(&dev));
+    STS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    cached = std::max(1, std::min(PW_BLOCKS, per_sm * sms));
+  }
+  return cached;
+}
+
+template <int NC>
+static int rupdate_nc(long long n, long long cs, double* r, double* z, const double* y, const double* d,
+                      const PcgScal* sc, double* partials, long long pstride, FinRed fin, cudaStream_t st) {
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (n % 2 == 0 && cs % 2 == 0 && a16(r) && a16(z) && a16(y) && a16(d)) {
-    double2* r2 = reinterpret_cast<double2*>(r);
-    double2* z2 = reinterpret_cast<double2*>(z);
-    const double2* y2 = reinterpret_cast<const double2*>(y);
-    const double2* d2 = reinterpret_cast<const double2*>(d);
-    STS_NC_SWITCH(ncomp, pcg_rupdate_v2_kernel, n / 2, cs / 2, r2, z2, y2, d2, sc, partials, pstride, fin);
-  } else {
-    STS_NC_SWITCH(ncomp, pcg_rupdate_kernel, n, cs, r, z, y, d, sc, partials, pstride, fin);
+    const int nb = resident_grid(pcg_rupdate_v2_kernel<NC>);
+    fin.ntot = nb;
+    pcg_rupdate_v2_kernel<NC><<<nb, 256, 0, st>>>(n / 2, cs / 2, reinterpret_cast<double2*>(r),
+                                                  reinterpret_cast<double2*>(z), reinterpret_cast<const double2*>(y),
+                                                  reinterpret_cast<const double2*>(d), sc, partials, pstride, fin);
+    return nb;
+  }
+  const int nb = resident_grid(pcg_rupdate_kernel<NC>);
+  fin.ntot = nb;
+  pcg_rupdate_kernel<NC><<<nb, 256, 0, st>>>(n, cs, r, z, y, d, sc, partials, pstride, fin);
+  return nb;
+}
+
+int launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* z, const double* y, const double* d,
+                       const PcgScal* sc, double* partials, long long pstride, const FinRed& fin, cudaStream_t st) {
+  int nb = 0;
+  switch (ncomp) {
+    case 1: nb = rupdate_nc<1>(n, cs, r, z, y, d, sc, partials, pstride, fin, st); break;
+    case 2: nb = rupdate_nc<2>(n, cs, r, z, y, d, sc, partials, pstride, fin, st); break;
+    case 3: nb = rupdate_nc<3>(n, cs, r, z, y, d, sc, partials, pstride, fin, st); break;
+    default: throw Error{STS_ERR_ARG, "ncomp"};
   }
   STS_CUDA(cudaGetLastError());
+  return nb;
 }
 
 void launch_pcg_xfinal(int ncomp, long long n, long long cs, double* x, const double* p0, const double* p1,

@@ -1141,7 +1141,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     fin_s.rtol2 = rtol2;
     FinRed fin_u = fin_s;
     fin_u.phase = PH_RZ;
-    fin_u.ntot = PW_BLOCKS;
+    fin_u.ntot = PW_BLOCKS;   // set to the launched grid by launch_pcg_rupdate
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
       if (g->comm) {
@@ -1188,14 +1188,15 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
           g->launches += 1;
         }
       }
+      int nbu;
       {
         Timed t(g, STS_K_PCG_UPDATE, is);
-        launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
-                           g->comm ? FinRed{} : fin_u, is);
+        nbu = launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
+                                 g->comm ? FinRed{} : fin_u, is);
       }
       if (g->comm) {
         Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, PW_BLOCKS, ncomp, 1, sums, PH_NONE, sc, rtol2, is);
+        launch_pcg_reduce(partials, pstride, nbu, ncomp, 1, sums, PH_NONE, sc, rtol2, is);
         STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
         launch_pcg_scalar(sums, ncomp, 1, PH_RZ, sc, rtol2, is);
         g->launches += 1;

@@ -273,8 +273,9 @@ int iso_tma_blocks(const Geo& G, int ib, int ie);
 // pnew = z + beta pold (pold unused if first); x += ax pold (not if first)
 void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, const double* z, const double* pold,
                      double* x, const PcgScal* sc, int first, cudaStream_t st);
-// r -= alpha y; z = r d; partial r.z  (fin.ticket set: the last CTA also finishes the reduction)
-void launch_pcg_rupdate(int ncomp, long long n, long long cstride, double* r, double* z, const double* y,
+// r -= alpha y; z = r d; partial r.z  (fin.ticket set: the last CTA also finishes the reduction);
+// returns the number of CTAs (partial slots per row) launched
+int launch_pcg_rupdate(int ncomp, long long n, long long cstride, double* r, double* z, const double* y,
                         const double* d, const PcgScal* sc, double* partials, long long pstride,
                         const FinRed& fin, cudaStream_t st);
 // x += ax p[iters % 2] for components with iters > 0
