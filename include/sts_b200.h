@@ -108,6 +108,17 @@ int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes);
 int sts_grid_kernel_launches(const sts_grid* g, long long* count);
 
 /*
+ * Communication profile (Sec. 2.4 and the boxed terms of Figs. 1-2):
+ * `local` counts neighbour (halo) exchange events -- one per operator application
+ * that reads across slab boundaries -- and `global` counts all-rank reductions
+ * (PCG dot products; the convergence test rides on the r.z reduction).  Counted
+ * for distributed (NCCL) and virtual-slab grids alike, never for a single slab.
+ * RKL2: local = s per super-step, global = 0.  BE+PCG: local = iterations + 1,
+ * global = 2 iterations + 1.
+ */
+int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_);
+
+/*
  * Per-kernel-class device timing (instrumentation used by bench.py for the
  * roofline): when enabled, every launch is bracketed by cudaEventRecord on the
  * stream it is launched on.  sts_grid_timing synchronises the recorded events

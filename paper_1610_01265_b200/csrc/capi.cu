@@ -416,6 +416,7 @@ static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Ma
   const bool overlap = needs_halos(g) && xs.size() > 0;
   cudaStream_t cst = nullptr;
   if (overlap) {
+    g->comm_local += 1;
     cst = comm_stream(g);
     STS_CUDA(cudaEventRecord(g->ev_a, st));
     STS_CUDA(cudaStreamWaitEvent(cst, g->ev_a, 0));
@@ -728,6 +729,14 @@ int sts_grid_kernel_launches(const sts_grid* g, long long* count) {
   return guard([&] {
     STS_REQUIRE(g && count, "NULL argument");
     *count = g->launches;
+  });
+}
+
+int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_) {
+  return guard([&] {
+    STS_REQUIRE(g && local && global_, "NULL argument");
+    *local = g->comm_local;
+    *global_ = g->comm_global;
   });
 }
 
@@ -1156,6 +1165,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
 
     // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
     reduce(sweep(g, {{H_U, un, ncomp}}, st, make_r0), 2, PH_R0);
+    if (needs_halos(g)) g->comm_global += 1;
     // iteration k (Fig. 1 with the x update deferred one iteration):
     //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
     //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
@@ -1163,6 +1173,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     // one PCG iteration k on stream `is`
     auto iteration = [&](int k, cudaStream_t is) {
       k_cur = k;
+      if (needs_halos(g)) g->comm_global += 2;   // p.y (alpha) and r.z (beta + convergence)
       double* pold = pb[(k - 1) & 1];
       double* pnew = pb[k & 1];
       int nbs;
@@ -1211,7 +1222,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     const bool use_graph = g->graphs && !g->timing && g->comm == nullptr;
     cudaStream_t is = st;
     cudaGraphExec_t pair_exec = nullptr;
-    long long pair_launches = 0;
+    long long pair_launches = 0, pair_local = 0, pair_global = 0;
     if (use_graph) {
       is = graph_stream(g);
       STS_CUDA(cudaEventRecord(g->ev_c, st));
@@ -1235,7 +1246,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
           // had its one-time attribute setup outside the capture)
           if (use_graph && k >= 4 && (k % 2) == 0 && it + 2 <= nb) {
             if (!pair_exec) {
-              const long long l0 = g->launches;
+              const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
               cudaGraph_t graph;
               STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
               iteration(k, is);
@@ -1244,10 +1255,16 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
               STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
               STS_CUDA(cudaGraphDestroy(graph));
               pair_launches = g->launches - l0;
+              pair_local = g->comm_local - cl0;
+              pair_global = g->comm_global - cg0;
               g->launches = l0;
+              g->comm_local = cl0;
+              g->comm_global = cg0;
             }
             STS_CUDA(cudaGraphLaunch(pair_exec, is));
             g->launches += pair_launches;
+            g->comm_local += pair_local;
+            g->comm_global += pair_global;
             it += 2;
           } else {
             iteration(k, is);

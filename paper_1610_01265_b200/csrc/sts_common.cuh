@@ -133,6 +133,7 @@ struct sts_grid {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   long long launches = 0;
+  long long comm_local = 0, comm_global = 0;   // sts_grid_comm_counts
   size_t halo_bytes = 0;
   bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
   bool graphs = true;                   // CUDA-graph replay of PCG iteration pairs (sts_grid_set_graphs)

@@ -55,6 +55,7 @@ def lib():
         "sts_grid_destroy": (I, [P]),
         "sts_grid_workspace_bytes": (I, [P, ctypes.POINTER(ctypes.c_size_t)]),
         "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
+        "sts_grid_comm_counts": (I, [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
         "sts_grid_set_timing": (I, [P, I]),
         "sts_grid_set_tma": (I, [P, I]),
         "sts_grid_set_graphs": (I, [P, I]),
@@ -165,6 +166,13 @@ class Grid:
         v = ctypes.c_longlong()
         _check("sts_grid_kernel_launches", lib().sts_grid_kernel_launches(self._h, ctypes.byref(v)))
         return v.value
+
+    @property
+    def comm_counts(self):
+        """(local halo-exchange events, global reductions) so far (Sec. 2.4)."""
+        a, b = ctypes.c_longlong(), ctypes.c_longlong()
+        _check("sts_grid_comm_counts", lib().sts_grid_comm_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     @property
     def workspace_bytes(self):

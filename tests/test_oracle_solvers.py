@@ -227,3 +227,98 @@ def test_vector_field_componentwise():
     for c in range(3):
         t0 = np.sum(op.WV * v[c].ravel())
         assert abs(np.sum(op.WV * x[c].ravel()) - t0) < 1e-10 * np.sum(op.WV * np.abs(v[c].ravel()))
+
+
+# ---------------------------------------------------------------- Sec. 3 / Sec. 6 properties
+def _heat_op(shape=(15, 15, 15)):
+    g = W.uniform_cartesian(*shape)
+    return g, O.Operator(g, [np.ones(g.shape)] * 3)
+
+
+@pytest.mark.parametrize("ratio", [5.0, 50.0, 500.0])
+def test_rkl2_stable_and_nonnegative_on_config0_data(ratio):
+    """PAPER.md:339 'strongly A-stable ... positive preserving', on BASELINE configs[0]
+    data (Gaussian bump + noise): 20 super-steps keep the max-norm non-increasing and
+    the solution non-negative (DESIGN R13: not for arbitrary data, see next test)."""
+    cfg = W.make_config("c0_heat32", shape=(16, 16, 16))
+    g = cfg["grid"]
+    op = O.Operator(g, [f.numpy() for f in cfg["faces"]])
+    dte = O.dt_euler(op)
+    s = O.rkl2_num_stages(ratio * dte, dte)
+    u = cfg["u"].numpy().copy()
+    prev = np.abs(u).max()
+    for _ in range(20):
+        u = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), u, ratio * dte, s)
+        m = np.abs(u).max()
+        assert m <= prev * (1 + 1e-13)
+        assert u.min() >= -1e-12 * m
+        prev = m
+
+
+def test_rkl2_positivity_is_not_unconditional():
+    """DESIGN R13: a single-cell delta goes negative after one RKL2 super-step once
+    s > 2 (min ~ -2 % of the peak at 5 dt_Euler), while BE stays non-negative -- the
+    'positive preserving' remark of PAPER.md:339 holds for smooth data only."""
+    g, op = _heat_op()
+    u0 = np.zeros(g.shape)
+    u0[7, 7, 7] = 1.0
+    dte = O.dt_euler(op)
+    for ratio in (5.0, 50.0, 500.0):
+        s = O.rkl2_num_stages(ratio * dte, dte)
+        u = O.rkl2_advance(lambda x: (op.M @ x.ravel()).reshape(x.shape), u0, ratio * dte, s)
+        ub, _ = O.be_pcg_solve(op, u0, ratio * dte, rtol=1e-13)
+        assert u.min() < -1e-3
+        assert ub.min() >= -1e-12
+        assert abs(u.sum() - 1.0) < 1e-12 and abs(ub.sum() - 1.0) < 1e-9   # both conserve
+
+
+def test_be_first_order_in_time():
+    """BE (Eq. 4) is first order: on u' = lam u the error at fixed T halves with dt."""
+    lam = -np.logspace(-1, 1, 20)
+    T = 0.5
+    errs = []
+    for n in (16, 32, 64):
+        dt = T / n
+        u = np.ones_like(lam)
+        for _ in range(n):
+            u = u / (1.0 - dt * lam)
+        errs.append(np.linalg.norm(u - np.exp(lam * T)))
+    order = math.log2(errs[1] / errs[2])
+    assert 0.8 < order < 1.2, errs
+
+
+def test_fig3_speedup_model():
+    """PAPER.md:149 (Fig. 3): RKL2 vs explicit Euler speedup = ratio / s, one sub-step
+    costing one Euler step; s from Eq. (5) makes the curve jagged: between jumps of s
+    it grows strictly with the ratio."""
+    sp = lambda r: r / O.rkl2_num_stages(r, 1.0)  # noqa: E731
+    assert sp(1.0) == 0.5 and sp(100.0) == 5.0 and abs(sp(500.0) - 500.0 / 45.0) < 1e-12
+    rs = np.linspace(1.0, 300.0, 3000)
+    ss = [O.rkl2_num_stages(r, 1.0) for r in rs]
+    for a in range(len(rs) - 1):
+        if ss[a] == ss[a + 1]:
+            assert sp(rs[a + 1]) > sp(rs[a])
+        else:
+            assert ss[a + 1] == ss[a] + 1
+
+
+def test_rkl2_and_be_agree_on_lagged_conduction():
+    """PAPER.md Sec. 6 validation (Fig. 10): with lagged Spitzer diffusivity both
+    methods advance the same nonlinear problem -- 5 steps at 20 dt_Euler differ by a
+    few per cent at most."""
+    cfg = W.make_config("c1_spitzer64", shape=(12, 10, 40))
+    g = cfg["grid"]
+    b = cfg["b"].numpy()
+    Tr = cfg["T"].numpy().copy()
+    Tb = Tr.copy()
+    dt = None
+    for _ in range(5):
+        opr = O.Operator(g, O.spitzer_face_kappa(g, Tr, cfg["kappa0"], cfg["T_cut"]), b)
+        opb = O.Operator(g, O.spitzer_face_kappa(g, Tb, cfg["kappa0"], cfg["T_cut"]), b)
+        if dt is None:
+            dt = 20.0 * O.dt_euler(opr)
+        s = O.rkl2_num_stages(dt, O.dt_euler(opr))
+        Tr = O.rkl2_advance(lambda x: (opr.M @ x.ravel()).reshape(x.shape), Tr, dt, s)
+        Tb, _ = O.be_pcg_solve(opb, Tb, dt, rtol=1e-12)
+    d = np.linalg.norm(Tr - Tb) / np.linalg.norm(Tb)
+    assert d < 0.05
