@@ -74,10 +74,13 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         "aniso_gersh": 48,
         "iso_rkl2_first": 8 * c + 32 + 16 * c,
         "iso_rkl2_stage": 32 * c + 32 + 8 * c,
-        "iso_pcg_r0": 8 * c + 32 + 24 * c + 8,
+        "iso_pcg_r0": 8 * c + 32 + 16 * c + 8,     # fused path: r, x, d (no z)
         "iso_pcg_ap": 16 * c + 32,
-        # fused S-pass: z, pold, x in (+ k1, k2, k3, w); p, y, x out (first: z in; p, y out)
-        "iso_pcg_s": (24 * c + 32) if first else (48 * c + 32),
+        # fused S-pass: r, pold, x (+ d, k1, k2, k3, w) in; p, y, x out (first: r, d in; p, y out);
+        # z = r d is formed in the pass, never stored
+        "iso_pcg_s": (24 * c + 40) if first else (48 * c + 40),
+        # U-pass of the isotropic fused path: r, y, d in; r out (no z)
+        "pcg_update_noz": 24 * c + 8,
         "iso_gersh": 32,
         # U-pass: r, y, d in; r, z out
         "pcg_update": 32 * c + 8,
@@ -126,10 +129,11 @@ def _visc_bytes(add, s_v, it_v, fused=False):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
         if fused:
             add("iso_pcg_s", bytes_per_cell("iso_pcg_s", active=act, first=k == 1))
+            add("pcg_update", bytes_per_cell("pcg_update_noz", active=act))
         else:
             add("pcg_pupdate", bytes_per_cell("pcg_pupdate", active=act, first=k == 1))
             add("iso_pcg_ap", bytes_per_cell("iso_pcg_ap", active=act))
-        add("pcg_update", bytes_per_cell("pcg_update", active=act))
+            add("pcg_update", bytes_per_cell("pcg_update", active=act))
     n_fin = sum(1 for i in it_v if i > 0)
     if n_fin:
         add("pcg_xfinal", bytes_per_cell("pcg_xfinal", active=n_fin))

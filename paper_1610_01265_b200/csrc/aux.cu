@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
         const double rn = rr[q][u] - alpha[q] * yy[q][u];
         const double zn = rn * de[u];
         __stcs(r + o, rn);
-        __stcs(z + o, zn);
+        if (z) __stcs(z + o, zn);
         acc[q] += rn * zn;
       }
     }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
       const double rn = r[o] - alpha[q] * y[o];
       const double zn = rn * de;
       r[o] = rn;
-      z[o] = zn;
+      if (z) z[o] = zn;
       acc[q] += rn * zn;
     }
   }
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long 
     zn.x = rn.x * de.x;
     zn.y = rn.y * de.y;
     __stcs(r + o, rn);
-    __stcs(z + o, zn);
+    if (z) __stcs(z + o, zn);
     acc[q] += rn.x * zn.x;
     acc[q] += rn.y * zn.y;
   };

@@ -1081,8 +1081,12 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.ea.out = off(y, g->slabs[0]);
       c.ea.out2 = off(pb[1], g->slabs[0]);
       c.ea.x = off(x, g->slabs[0]);
+      c.u3 = view(g, g->slabs[0], H_D, d);
       fused = aniso_tma_eligible(c) || iso_tma_eligible(c);
     }
+    // isotropic fused S-pass: z = r d is formed inside the stencil pass from the staged
+    // r and d, so neither the initial residual pass nor the U-pass stores z
+    const bool zd = fused && mode == STS_MODE_ISO;
     // the passes (make(si) -> StencilCall of slab si; sweep() sets the plane range and pbase)
     double* partials = nullptr;
     long long pstride = 0;
@@ -1093,7 +1097,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
       c.ea.out = off(r, sl);
       c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-      c.ea.out3 = off(z, sl);
+      c.ea.out3 = zd ? nullptr : off(z, sl);
       c.ea.out4 = off(d, sl);
       c.ea.dt = dt;
       c.ea.partials = partials;
@@ -1103,9 +1107,10 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     auto make_s = [&](size_t si) {   // fused S-pass (TMA)
       const Slab& sl = g->slabs[si];
       const int first = (k_cur == 1);
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
-      c.u = view(g, sl, H_Z, z);
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, zd ? r : z, k1, k2, k3, bb, w);
+      c.u = view(g, sl, H_Z, zd ? r : z);
       c.u2 = first ? FieldV{} : view(g, sl, H_P, pb[(k_cur - 1) & 1]);
+      if (zd) c.u3 = view(g, sl, H_D, d);
       c.ev = ev[si];
       c.ea.out = off(y, sl);
       c.ea.out2 = off(pb[k_cur & 1], sl);
@@ -1166,6 +1171,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
     reduce(sweep(g, {{H_U, un, ncomp}}, st, make_r0), 2, PH_R0);
     if (needs_halos(g)) g->comm_global += 1;
+    if (zd) exchange(g, H_D, d, 1, st);   // d is fixed for the whole solve: its halo once
     // iteration k (Fig. 1 with the x update deferred one iteration):
     //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
     //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
@@ -1181,8 +1187,9 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
         // (the last CTA finishes the reduction when the pass has few CTAs; large passes
         // keep the 1024-thread reduction kernel, which sums ~1e4 partials faster)
         const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_s;
-        if (k == 1) nbs = sweep(g, {{H_Z, z, ncomp}}, is, make_s, fs);
-        else nbs = sweep(g, {{H_Z, z, ncomp}, {H_P, pold, ncomp}}, is, make_s, fs);
+        const double* zr = zd ? r : z;
+        if (k == 1) nbs = sweep(g, {{H_Z, zr, ncomp}}, is, make_s, fs);
+        else nbs = sweep(g, {{H_Z, zr, ncomp}, {H_P, pold, ncomp}}, is, make_s, fs);
       } else {
         {
           Timed t(g, STS_K_PCG_PUPDATE, is);
@@ -1202,7 +1209,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       int nbu;
       {
         Timed t(g, STS_K_PCG_UPDATE, is);
-        nbu = launch_pcg_rupdate(ncomp, (long long)N, cs, r, z, y, d, sc, partials, pstride,
+        nbu = launch_pcg_rupdate(ncomp, (long long)N, cs, r, zd ? nullptr : z, y, d, sc, partials, pstride,
                                  g->comm ? FinRed{} : fin_u, is);
       }
       if (g->comm) {

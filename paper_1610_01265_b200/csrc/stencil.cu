@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(NT, 3) aniso_kernel(StencilCall c, int ic, uns
       const double bb = WV * uc;
       c.ea.out[gi] = r;
       if (c.ea.out2) c.ea.out2[gi] = uc;
-      c.ea.out3[gi] = z;
+      if (c.ea.out3) c.ea.out3[gi] = z;
       c.ea.out4[gi] = d;
       part0 += r * z;
       part1 += bb * bb * d;
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(NT, 4) iso_kernel(StencilCall c, int ic, unsig
           const double bb = WV * uc[q];
           c.ea.out[go] = r;
           if (c.ea.out2) c.ea.out2[go] = uc[q];
-          c.ea.out3[go] = z;
+          if (c.ea.out3) c.ea.out3[go] = z;
           if (q == 0) c.ea.out4[gi] = d;
           part0[q] += r * z;
           part1[q] += bb * bb * d;

@@ -54,13 +54,18 @@ struct IsoLay {
   // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
   static constexpr int WRP = NC * S_MAIN;                          // wrap boxes within a field block
   static constexpr int FS = NC * S_MAIN + NC * 2 * S_W;            // field block stride
-  static constexpr int K2 = nsrcf * FS;
+  // PCG S-pass: the Jacobi inverse diagonal d (one component, main + 2 wrap boxes), so
+  // z = r d is formed on the fly and the U-pass never stores z
+  static constexpr int nd = (EPI == EPI_PCG_S) ? 1 : 0;
+  static constexpr int DB = nsrcf * FS;
+  static constexpr int K2 = DB + nd * (S_MAIN + 2 * S_W);
   static constexpr int K3 = K2 + K2SZ;
   static constexpr int K3R = K3 + K3SZ;
   static constexpr int K1 = K3R + K3WR;
   static constexpr int WB = K1 + OWN;
   static constexpr int EP = WB + OWN;
-  static constexpr int SLOT = EP + nepi * OWN;
+  static constexpr int MT = EP + nepi * OWN;      // per-plane metrics written by the producer
+  static constexpr int SLOT = MT + 16;
   static constexpr size_t SMEM = (size_t)IXTS * SLOT * sizeof(double) + 2 * IXTS * sizeof(uint64_t) + 128;
 };
 
@@ -71,6 +76,7 @@ struct IsoTmaArgs {
   CUtensorMap srcw[2];    // their wrap columns, box 2 x 9
   CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x8, 34x7, 2x7, 32x7, 32x7
   CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 7
+  CUtensorMap dm, dmw;    // PCG S-pass: d, box 36 x 9 / its wrap columns 2 x 9
   int has_w;
 };
 
@@ -132,11 +138,22 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     if (wrapR) bytes += nsrcf_now * NC * 2 * SBH * 8;
     if (ta.has_w) bytes += OWN * 8;
     bytes += Lay::nepi * OWN * 8;
+    if (Lay::nd) {
+      bytes += SBW * SBH * 8;
+      if (wrapL) bytes += 2 * SBH * 8;
+      if (wrapR) bytes += 2 * SBH * 8;
+    }
     for (int p = ib; p < ie; ++p) {
       const int slot = (p - ib) % IXTS, n = (p - ib) / IXTS;
       if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
       double* S = ring + slot * Lay::SLOT;
       uint64_t* bar = full + slot;
+      {  // per-plane metrics (plain stores, released by the arrive below); F2r == F3r
+        const int ig = G.i0 + p;
+        S[Lay::MT + 0] = M.F1r[ig];
+        S[Lay::MT + 1] = M.F2r[ig];
+        S[Lay::MT + 2] = M.Vr[ig];
+      }
       fence_proxy_async();
       mbar_expect_tx(bar, bytes);
 #pragma unroll
@@ -149,6 +166,11 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
           if (wrapL) tma3(F + Lay::WRP + (q * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
           if (wrapR) tma3(F + Lay::WRP + (q * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
         }
+      if (Lay::nd) {
+        tma3(S + Lay::DB, &ta.dm, k0 - 2, j0 - 1, p, bar);
+        if (wrapL) tma3(S + Lay::DB + S_MAIN, &ta.dmw, G.n3 - 2, j0 - 1, p, bar);
+        if (wrapR) tma3(S + Lay::DB + S_MAIN + S_W, &ta.dmw, 0, j0 - 1, p, bar);
+      }
       tma3(S + Lay::K2, &ta.k2, k0, j0 - 1, p, bar);
       tma3(S + Lay::K3, &ta.k3, k0 - 2, j0, p, bar);
       if (wrapL) tma3(S + Lay::K3R, &ta.k3w, G.n3 - 2, j0, p, bar);
@@ -183,18 +205,26 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   // component (periodic phi wrap: cell n3-1 / 0 from the 2-column wrap boxes)
   const int oc = (tj + 1) * SBW + tk + 2;
   const bool kmw_box = per && k == 0, kpw_box = per && k + 1 == G.n3;
-  int okm[NC], okp[NC];
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
-    okm[q] = kmw_box ? Lay::WRP + (q * 2 + 0) * S_W + (tj + 1) * 2 + 1 : q * S_MAIN + oc - 1;
-    okp[q] = kpw_box ? Lay::WRP + (q * 2 + 1) * S_W + (tj + 1) * 2 : q * S_MAIN + oc + 1;
-  }
+  // component q of the k-1 / k+1 neighbour: base + q * stride (main box or wrap box)
+  const int okm0 = kmw_box ? Lay::WRP + 0 * S_W + (tj + 1) * 2 + 1 : oc - 1;
+  const int okp0 = kpw_box ? Lay::WRP + 1 * S_W + (tj + 1) * 2 : oc + 1;
+  const int okms = kmw_box ? 2 * S_W : S_MAIN, okps = kpw_box ? 2 * S_W : S_MAIN;
   const int o8 = tj * IK + tk;
   const int ok2p = Lay::K2 + (tj + 1) * K2W + tk, ok2m = ok2p - K2W;
   const int ok3p = Lay::K3 + tj * K3W + tk + 2;
   const int ok3m = kmw_box ? Lay::K3R + tj * 2 + 1 : ok3p - 1;
-  auto sv = [&](const double* S, int o, int q) {
-    if constexpr (kP) return fma(sbeta[q], S[o + Lay::FS], S[o]);
+  // d offsets of the same five positions (one component)
+  const int dc = Lay::DB + oc;
+  const int dkm = kmw_box ? Lay::DB + S_MAIN + 0 * S_W + (tj + 1) * 2 + 1 : dc - 1;
+  const int dkp = kpw_box ? Lay::DB + S_MAIN + 1 * S_W + (tj + 1) * 2 : dc + 1;
+  constexpr bool kS = (EPI == EPI_PCG_S);
+  // source value at (field-0 offset o, d offset od): PCG p = r d + beta pold (first: r d), else u
+  auto sv = [&](const double* S, int o, int od, int q) {
+    if constexpr (kS) {
+      const double z = S[o] * S[od];
+      if constexpr (kP) return fma(sbeta[q], S[o + Lay::FS], z);
+      return z;
+    }
     return S[o];
   };
   // own column through global memory (r neighbours, incl. the neighbour slab's halo plane)
@@ -208,31 +238,32 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     else return 0.0;
     return __ldg(pz + coff);
   };
-  auto comb = [&](double z, double po, int q) {
-    if constexpr (kP) return fma(sbeta[q], po, z);
+  auto comb = [&](double z, double po, double dd, int q) {
+    if constexpr (kS) {
+      if constexpr (kP) return fma(sbeta[q], po, z * dd);
+      return z * dd;
+    }
     return z;
   };
 
   // Register double buffering, unrolled by two (no register moves of in-flight loads,
   // which would make every prefetch wait at the end of its own iteration):
   //   Pre.z/p: own column of plane il+1 (r up-neighbour), loaded one step earlier;
-  //   Pre.f1r/f23r/vr: metrics of plane il (F2r == F3r by construction).
   struct Pre {
-    double z[NC], p[NC];
-    double f1r, f23r, vr;
+    double z[NC], p[NC], d;
   };
   const int ig0 = G.i0 + ib;
   Pre A, B;
   double udn[NC];
 #pragma unroll
+  const double ddn = kS ? colv(c.u3, ib - 1, 0) : 1.0;
+  A.d = kS ? colv(c.u3, ib + 1, 0) : 1.0;
+  B.d = 1.0;
   for (int q = 0; q < NC; ++q) {
-    udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(c.u2, ib - 1, q) : 0.0, q);
+    udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(c.u2, ib - 1, q) : 0.0, ddn, q);
     A.z[q] = colv(c.u, ib + 1, q);
     A.p[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
   }
-  A.f1r = M.F1r[ig0];
-  A.f23r = M.F2r[ig0];
-  A.vr = M.Vr[ig0];
   double kdn = 0.0;
   if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
   double part[NC];
@@ -254,28 +285,25 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       N.z[q] = more ? colv(c.u, il + 2, q) : 0.0;
       N.p[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
     }
-    if (il + 1 < ie) {
-      N.f1r = M.F1r[ig + 1];
-      N.f23r = M.F2r[ig + 1];
-      N.vr = M.Vr[ig + 1];
-    }
+    if constexpr (kS) N.d = more ? colv(c.u3, il + 2, 0) : 1.0;
     mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
     double Kup = 0.0;
     if (own) {
-      Kup = ip ? S[Lay::K1 + o8] * C.f1r * f1tp : 0.0;
-      const double Kjp = jp ? S[ok2p] * C.f23r * f2p : 0.0;
-      const double Kjm = jm ? S[ok2m] * C.f23r * f2m : 0.0;
-      const double Kkp = kp ? S[ok3p] * C.f23r * f3p : 0.0;
-      const double Kkm = km ? S[ok3m] * C.f23r * f3m : 0.0;
-      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * C.vr * vtp;
+      const double f1r = S[Lay::MT + 0], f23r = S[Lay::MT + 1], vr = S[Lay::MT + 2];
+      Kup = ip ? S[Lay::K1 + o8] * f1r * f1tp : 0.0;
+      const double Kjp = jp ? S[ok2p] * f23r * f2p : 0.0;
+      const double Kjm = jm ? S[ok2m] * f23r * f2m : 0.0;
+      const double Kkp = kp ? S[ok3p] * f23r * f3p : 0.0;
+      const double Kkm = km ? S[ok3m] * f23r * f3m : 0.0;
+      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * vtp;
       const long long gi = (long long)il * pl;
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
         const int oq = q * S_MAIN + oc;
-        const double u0 = sv(S, oq, q);
-        const double ujm = sv(S, oq - SBW, q), ujp = sv(S, oq + SBW, q);
-        const double ukm = sv(S, okm[q], q), ukp = sv(S, okp[q], q);
-        const double uup = comb(C.z[q], C.p[q], q);
+        const double u0 = sv(S, oq, dc, q);
+        const double ujm = sv(S, oq - SBW, dc - SBW, q), ujp = sv(S, oq + SBW, dc + SBW, q);
+        const double ukm = sv(S, okm0 + q * okms, dkm, q), ukp = sv(S, okp0 + q * okps, dkp, q);
+        const double uup = comb(C.z[q], C.p[q], C.d, q);
         const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
         const long long go = gi + q * cs;
@@ -350,6 +378,7 @@ bool iso_tma_eligible(const StencilCall& c) {
   if (G.n3 % 2 != 0) return false;
   if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
   if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
+  if (c.epi == EPI_PCG_S && (!c.u3.p || !al16(c.u3.p))) return false;
   return true;
 }
 
@@ -436,6 +465,8 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     map_plain(&ta.epi[2], c.ea.m0, G, npl, IK, IJ);
   } else if (c.epi == EPI_PCG_S) {
     map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
+    map_plain(&ta.dm, c.u3.p, G, G.nl, SBW, SBH);
+    map_plain(&ta.dmw, c.u3.p, G, G.nl, 2, SBH);
   }
   switch (c.epi) {
     case EPI_F: launch_iso_nc<EPI_F>(c, grid, ic, ta, st); break;

@@ -101,7 +101,7 @@ struct Slab {
 // halo planes of the fields the stencils read across slab boundaries.  Per slot
 // ONE allocation [2][MAXC][plane]: the lo planes (comp c at c) then the hi planes
 // (comp c at MAXC + c), so a single TMA tensor map covers both sides.
-enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_Z, H_P, H_NSLOTS };
+enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_Z, H_P, H_D, H_NSLOTS };
 
 struct Workspace {
   double* base = nullptr;
@@ -214,7 +214,8 @@ struct StencilCall {
   int epi;
   Geo geo;
   FieldV u, k1, k2, k3, b;
-  FieldV u2;                   // EPI_PCG_S: pold (u = z)
+  FieldV u2;                   // EPI_PCG_S: pold (u = z, or r for the isotropic S-pass)
+  FieldV u3;                   // isotropic EPI_PCG_S: the Jacobi inverse diagonal d (z = r d formed on the fly)
   const double* w;             // [nl][plane] or nullptr
   const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][n2][n3+2] (see ev_pitch)
   EpiArgs ea;
