@@ -4,7 +4,8 @@ set -x
 mkdir -p gpurun_out
 CMD="python tools/profile_step.py --config c3_spitzer256 --visc"
 $CMD > gpurun_out/plain_prof.log 2>&1 || exit 1
-for k in ${KERNELS:-"aniso_tma_kernel<.int.2>" "aniso_tma_kernel<.int.5>" "iso_fast_kernel<.int.4,..int.3>" "iso_fast_kernel<.int.2,..int.3>" "pcg_rupdate_kernel<.int.3>" "pcg_pnew_kernel<.int.3>"}; do
+KLIST=${KERNELS:-"aniso_tma_kernel<.int.2,..bool.0,..bool.0> aniso_tma_kernel<.int.5,..bool.0,..bool.0> iso_tma_kernel<.int.2,..int.3,..bool.0,..bool.0> iso_tma_kernel<.int.5,..int.3,..bool.0,..bool.0> pcg_rupdate_v2_kernel<.int.3> pcg_rupdate_v2_kernel<.int.1>"}
+for k in $KLIST; do
   tag=$(echo "$k" | tr -c 'a-zA-Z0-9_\n' '_')
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 2 -c 1 \
       -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_$tag.log 2>&1
