@@ -42,7 +42,7 @@ RATIO = {"c1_spitzer64": 100.0, "c2_visc64": 500.0, "c3_spitzer256": 100.0, "c4_
 RTOL = 1e-12
 KMAX = 50000
 # bounded CPU sample of the same workload for the oracle baseline (cells of the box)
-CPU_BOX = (16, 48, 96)
+CPU_BOX = (12, 40, 64)
 
 
 def peaks():
@@ -371,21 +371,41 @@ def oracle_step(cfg, ratio):
     return s_c + it_c[0] + s_v + max(it_v)
 
 
+def oracle_step_c(cfg, ratio):
+    """The same step with the plain-C oracle (oracle/c/sts_oracle.c, single thread)."""
+    from oracle import c_oracle as C
+    g = cfg["grid"]
+    T, b = cfg["T"].numpy(), cfg["b"].numpy()
+    kap = C.face_kappa(g, T, cfg["kappa0"], cfg["T_cut"])
+    dte = C.dt_euler(g, kap, b)
+    dt = ratio * dte
+    s_c = C.rkl2_num_stages(dt, dte)
+    C.rkl2_advance(g, T, kap, b, None, dt, s_c)
+    _, it_c = C.be_pcg_solve(g, T, kap, b, None, dt, RTOL)
+    kv, rho, v = [f.numpy() for f in cfg["visc_faces"]], cfg["rho"].numpy(), cfg["v"].numpy()
+    dtev = C.dt_euler(g, kv, None, rho)
+    s_v = C.rkl2_num_stages(ratio * dtev, dtev)
+    C.rkl2_advance(g, v, kv, None, rho, ratio * dtev, s_v)
+    _, it_v = C.be_pcg_solve(g, v, kv, None, rho, ratio * dtev, RTOL)
+    return s_c + it_c[0] + s_v + max(it_v)
+
+
 def time_oracle(name, ratio, steps=1, warmup=0):
+    """The plain-C oracle (BASELINE north_star) timed on one host core."""
     from threadpoolctl import threadpool_limits
     cfg = cpu_box_config(name)
     ncells = cfg["grid"].ncells
     with threadpool_limits(limits=1):
         torch.set_num_threads(1)
         for _ in range(warmup):
-            oracle_step(cfg, ratio)
+            oracle_step_c(cfg, ratio)
         t0 = time.perf_counter()
         units = 0
         for _ in range(steps):
-            units += oracle_step(cfg, ratio)
+            units += oracle_step_c(cfg, ratio)
         dt = time.perf_counter() - t0
     return {"value": ncells * units / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle (numpy/scipy, 1 thread) full step of {name}'s recipe on a "
+            "sample": f"oracle (plain C, gcc -O2, 1 thread) full step of {name}'s recipe on a "
                       f"{'x'.join(map(str, CPU_BOX))} block at r_min ({ncells} cells), dt = {ratio:g} dt_exp of "
                       f"the block, {steps} step(s): {units} cell-updates per cell in {dt:.1f} s"}, dt / steps
 
