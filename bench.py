@@ -67,7 +67,7 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         "aniso_F": 8 + 24 + 8,
         "aniso_rkl2_first": 8 + 24 + 16,
         "aniso_rkl2_stage": 8 + 24 + 24 + 8,
-        "aniso_pcg_r0": 8 + 48 + 32,
+        "aniso_pcg_r0": 8 + 24 + 32,          # TMA R0: u, e in; r, x, z, d out
         "aniso_pcg_ap": 8 + 24 + 8,
         # fused S-pass: z, pold, x, e in; p, y, x out (first iteration: z, e in; p, y out)
         "aniso_pcg_s": (8 + 24 + 16) if first else (24 + 24 + 24),

@@ -1095,6 +1095,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     auto make_r0 = [&](size_t si) {
       const Slab& sl = g->slabs[si];
       StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
+      c.ev = ev[si];
       c.ea.out = off(r, sl);
       c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
       c.ea.out3 = zd ? nullptr : off(z, sl);

@@ -226,7 +226,12 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   double SuL = 0, TuL = 0, FuL = 0;
   double SAl = 0, DBl = 0, DCl = 0;
   double uc = 0.0, poc = 0.0;   // own-cell source value (and pold) of the previous plane
-  double part = 0.0;
+  double part = 0.0, part2 = 0.0;
+  constexpr bool kR0 = (EPI == EPI_PCG_R0);
+  // R0: L_ii = -sum over the cell's 8 vertices of W^2, W = the cell's weight in q_v =
+  // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex);
+  // the 4 vertices of the plane below are summed one step earlier (ldlo)
+  double ldlo = 0.0;
   for (int p = ib - 1; p <= ie; ++p) {
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
@@ -241,6 +246,24 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
       const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
+      double ldhi = 0.0, ldnext = 0.0;
+      if constexpr (kR0) {
+        if (own) {
+          // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
+          // the own cell (j, k) sits at (st, sp) = (+,+) in vertex (vj,vk), (+,-) in (vj,vk+1),
+          // (-,+) in (vj+1,vk), (-,-) in (vj+1,vk+1)
+          const int e4[4] = {ei, ei + 1, ei + EBW, ei + EBW + 1};
+          const double st4[4] = {1.0, 1.0, -1.0, -1.0}, sp4[4] = {1.0, -1.0, 1.0, -1.0};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const double r_ = E[e4[t]], t_ = E[E_COMP + e4[t]], p_ = E[2 * E_COMP + e4[t]];
+            const double wl = -r_ + st4[t] * t_ * ig2l + sp4[t] * p_ * ig2l * ig3c;
+            const double wh = r_ + st4[t] * t_ * ig2h + sp4[t] * p_ * ig2h * ig3c;
+            ldhi += wl * wl;
+            ldnext += wh * wh;
+          }
+        }
+      }
       // vertex values A, B, C = q e; the horizontal pair sums/differences by shuffle,
       // the vertical pair through shared memory (the next vertex row is the next warp)
       const double A = q * er, B = q * et, C = q * ep;
@@ -276,6 +299,19 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
           const double F = Lu / WV;
           c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_YM2 * O_PART] + c.ea.c2 * O[OW_Y0 * O_PART] + c.ea.c0 * F +
                          c.ea.c1 * O[OW_M0 * O_PART];
+        } else if constexpr (kR0) {
+          // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
+          const double Ld = -(ldlo + ldhi);
+          const double r = c.ea.dt * Lu;
+          const double dinv = 1.0 / (WV - c.ea.dt * Ld);
+          const double z = r * dinv;
+          const double bb = WV * uc;
+          c.ea.out[gi] = r;
+          if (c.ea.out2) c.ea.out2[gi] = uc;
+          if (c.ea.out3) c.ea.out3[gi] = z;
+          c.ea.out4[gi] = dinv;
+          part += r * z;
+          part2 += bb * bb * dinv;
         } else if constexpr (EPI == EPI_PCG_S) {
           const double y = WV * uc - c.ea.dt * Lu;
           c.ea.out[gi] = y;
@@ -287,6 +323,7 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       SAl = SAh;
       DBl = DBh;
       DCl = DCh;
+      ldlo = ldnext;
     }
     __syncwarp();
     if (vk == 0) mbar_arrive(empty + slot);   // this warp is done with the slot of Q(p)
@@ -295,6 +332,26 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
     FuL = FuH;
     uc = un;
     poc = pon;
+  }
+  if constexpr (kR0) {
+    __shared__ double red2[2][XNT / 32];
+    double v = part, v2 = part2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+      v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    if (vk == 0) {
+      red2[0][vj] = v;
+      red2[1][vj] = v2;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
+    if (tid < 2) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < XNT / 32; ++w) s += red2[tid][w];
+      c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
+    }
   }
   if constexpr (EPI == EPI_PCG_S) {
     __shared__ double red[XNT / 32];
@@ -322,7 +379,9 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
 // ============================================================================
 // host side
 // ============================================================================
-static bool has_tma(int epi) { return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S; }
+static bool has_tma(int epi) {
+  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0;
+}
 
 bool aniso_tma_eligible(const StencilCall& c) {
   if (c.mode != STS_MODE_ANISO || c.ncomp != 1 || !has_tma(c.epi) || !c.ev) return false;
@@ -427,6 +486,7 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_RKL2_FIRST: launch_w<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
     case EPI_RKL2_STAGE: launch_w<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_w<EPI_PCG_S>(c, grid, ic, ta, st); break;
+    case EPI_PCG_R0: launch_w<EPI_PCG_R0>(c, grid, ic, ta, st); break;
     default: return false;
   }
   STS_CUDA(cudaGetLastError());

@@ -266,11 +266,14 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   }
   double kdn = 0.0;
   if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
-  double part[NC];
+  double part[NC], part2[NC];
 #pragma unroll
-  for (int q = 0; q < NC; ++q) part[q] = 0.0;
+  for (int q = 0; q < NC; ++q) part[q] = part2[q] = 0.0;
+  constexpr bool kR0 = (EPI == EPI_PCG_R0);
   double* o1 = c.ea.out + coff;
-  double* o2 = (EPI == EPI_RKL2_FIRST || EPI == EPI_PCG_S) ? c.ea.out2 + coff : nullptr;
+  double* o2 = ((EPI == EPI_RKL2_FIRST || EPI == EPI_PCG_S || kR0) && c.ea.out2) ? c.ea.out2 + coff : nullptr;
+  double* o3 = (kR0 && c.ea.out3) ? c.ea.out3 + coff : nullptr;
+  double* o4 = kR0 ? c.ea.out4 + coff : nullptr;
   double* ox = (EPI == EPI_PCG_S) ? c.ea.x + coff : nullptr;
 
   auto body = [&](int il, const Pre& C, Pre& N) {
@@ -297,6 +300,13 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       const double Kkm = km ? S[ok3m] * f23r * f3m : 0.0;
       const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * vtp;
       const long long gi = (long long)il * pl;
+      double dinv = 0.0;
+      if constexpr (kR0) {
+        // PC1: d = 1/A_ii, A = wV - dt L, L_ii = -(sum of the face coefficients)
+        const double Ldiag = -(kdn + Kup + Kjp + Kjm + Kkp + Kkm);
+        dinv = 1.0 / (WV - c.ea.dt * Ldiag);
+        o4[gi] = dinv;
+      }
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
         const int oq = q * S_MAIN + oc;
@@ -318,6 +328,16 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
             const double F = Lu / WV;
             o1[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c2 * S[Lay::EP + (NC + q) * OWN + o8] +
                      c.ea.c0 * F + c.ea.c1 * S[Lay::EP + (2 * NC + q) * OWN + o8];
+          } else if constexpr (kR0) {
+            // r0 = b - A x0 = dt L u (x0 = u^n); z0 = r0 d; partials r.z and b.P^-1 b
+            const double r = c.ea.dt * Lu;
+            const double z = r * dinv;
+            const double bb = WV * u0;
+            o1[go] = r;
+            if (o2) o2[go] = u0;
+            if (o3) o3[go] = z;
+            part[q] += r * z;
+            part2[q] += bb * bb * dinv;
           } else if constexpr (EPI == EPI_PCG_S) {
             const double y = WV * u0 - c.ea.dt * Lu;
             o1[go] = y;
@@ -339,6 +359,30 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     body(il + 1, B, A);
   }
   if (il < ie) body(il, A, B);
+  if constexpr (kR0) {
+    // partial rows 2c (r.z) and 2c+1 (b.P^-1 b), the layout of the R0 reduction
+    __shared__ double red2[2 * NC][IJ];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double v = part[q], v2 = part2[q];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      if (tk == 0) {
+        red2[2 * q][tj] = v;
+        red2[2 * q + 1][tj] = v2;
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory");
+    if (tid < 2 * NC) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < IJ; ++w) s += red2[tid][w];
+      c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
+    }
+  }
   if constexpr (EPI == EPI_PCG_S) {
     __shared__ double red[NC][IJ];
 #pragma unroll
@@ -369,7 +413,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
 // host side
 // ============================================================================
 static bool iso_has_tma(int epi) {
-  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S;
+  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0;
 }
 
 bool iso_tma_eligible(const StencilCall& c) {
@@ -379,6 +423,7 @@ bool iso_tma_eligible(const StencilCall& c) {
   if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
   if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
   if (c.epi == EPI_PCG_S && (!c.u3.p || !al16(c.u3.p))) return false;
+  if (c.epi == EPI_PCG_R0 && (!c.ea.out4 || c.ea.sc)) return false;
   return true;
 }
 
@@ -473,6 +518,7 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_RKL2_FIRST: launch_iso_nc<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
     case EPI_RKL2_STAGE: launch_iso_nc<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_iso_nc<EPI_PCG_S>(c, grid, ic, ta, st); break;
+    case EPI_PCG_R0: launch_iso_nc<EPI_PCG_R0>(c, grid, ic, ta, st); break;
     default: return false;
   }
   STS_CUDA(cudaGetLastError());
