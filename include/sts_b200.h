@@ -28,6 +28,9 @@
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Entry points
  *    that return host-visible values (dt, iteration counts) synchronise the
  *    stream; the others are asynchronous.
+ *  - A grid handle owns scratch, halo buffers and reduction counters: calls on one
+ *    handle must not run concurrently (from several host threads or on several
+ *    streams at once); use one handle per concurrent stream.
  *  - Return value: STS_OK (0) or a negative STS_ERR_* code;
  *    sts_last_error() returns a thread-local message for the last failure.
  *    Calls never abort the process.
