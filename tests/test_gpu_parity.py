@@ -493,3 +493,52 @@ def test_communication_profile_matches_paper(dev, graphs):
     G1 = sts().Grid.from_grid(g)                      # a single slab communicates nothing
     G1.rkl2_advance("aniso", T, k, b, None, 100 * dte, s)
     assert G1.comm_counts == (0, 0)
+
+
+def test_host_pointer_paths_match_device(dev):
+    """The C ABI accepts host arrays (the end-to-end path): every entry point stages
+    them and returns the same results as with device arrays."""
+    cfg = W.make_config("c1_spitzer64", shape=(9, 17, 40))
+    g = cfg["grid"]
+    G = sts().Grid.from_grid(g)
+    T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    kh = G.face_kappa_spitzer(cfg["T"].clone(), cfg["kappa0"], cfg["T_cut"])
+    assert all(torch.equal(a.cpu(), c) for a, c in zip(k, kh))
+    dte = G.dt_euler("aniso", k, b)
+    assert G.dt_euler("aniso", [x.cpu() for x in k], b.cpu()) == dte
+    F = G.op_apply("aniso", T, k, b)
+    assert torch.equal(G.op_apply("aniso", cfg["T"].clone(), [x.cpu() for x in k], b.cpu()), F.cpu())
+    x, it = G.be_pcg_solve("aniso", T, k, b, None, 50 * dte, 1e-12, 10000)
+    xh, ith = G.be_pcg_solve("aniso", cfg["T"].clone().pin_memory(), [x_.cpu() for x_ in k], b.cpu(), None,
+                             50 * dte, 1e-12, 10000)
+    assert ith == it and torch.equal(xh, x.cpu())
+    u, st = G.rkl2_advance_hybrid("aniso", T, k, b, None, 50 * dte, dte, 0.25)
+    uh, sth = G.rkl2_advance_hybrid("aniso", cfg["T"].clone(), [x_.cpu() for x_ in k], b.cpu(), None, 50 * dte,
+                                    dte, 0.25)
+    assert st == sth and torch.equal(uh, u.cpu())
+
+
+def test_argument_errors_on_a_live_grid(dev):
+    """Invalid calls return STS_ERR_* with a message and leave the handle usable."""
+    S = sts()
+    cfg = W.make_config("c1_spitzer64", shape=(6, 5, 8))
+    G = S.Grid.from_grid(cfg["grid"])
+    T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    with pytest.raises(S.StsError, match="s must be >= 2"):
+        G.rkl2_advance("aniso", T, k, b, None, 1.0, 1)
+    with pytest.raises(S.StsError, match="requires b"):
+        G.rkl2_advance("aniso", T, k, None, None, 1.0, 3)
+    with pytest.raises(S.StsError, match="ncomp"):
+        G.op_apply("aniso", torch.stack([T, T]), k, b)
+    with pytest.raises(S.StsError, match="kmax"):
+        G.be_pcg_solve("aniso", T, k, b, None, 1.0, 1e-12, 0)
+    with pytest.raises(S.StsError, match="alias"):
+        G.op_apply("aniso", T, k, b, out=T)
+    with pytest.raises(S.StsError, match="dt_exp"):
+        G.rkl2_advance_hybrid("aniso", T, k, b, None, 10.0, 1.0, 0.5, n_euler=1)
+    with pytest.raises(S.StsError, match="kmax reached"):
+        G.be_pcg_solve("aniso", T, k, b, None, 1.0, 1e-12, 1)
+    dte = G.dt_euler("aniso", k, b)                     # still usable
+    assert math.isfinite(dte) and dte > 0
