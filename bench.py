@@ -87,22 +87,27 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         # p pass of the unfused S-pass: z, pold, x in; p, x out (first: z in, p out)
         "pcg_pupdate": 16 * c if first else 40 * c,
         "pcg_xfinal": 24 * c,
+        # merged iteration (one pass): zold, wold, pold, x (+ e, d) in; z, p, w, x out
+        # (first: z0 (+ e, d) in; z, p, w out); R0 of the merged path also writes z0
+        "aniso_pcg_m": (8 + 24 + 8 + 24) if first else (32 + 24 + 8 + 32),
+        "iso_pcg_m": (32 * c + 40) if first else (64 * c + 40),
+        "iso_pcg_r0_m": 8 * c + 32 + 24 * c + 8,
     }
     return table[kind]
 
 
-def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False):
+def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False, merged_c=False, merged_v=False):
     """Total algorithmic bytes per class for one step on `ncells` local cells."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
-        _cond_bytes(add, s_c, it_c, fused_c)
+        _cond_bytes(add, s_c, it_c, fused_c, merged_c)
     if s_v:
-        _visc_bytes(add, s_v, it_v, fused_v)
+        _visc_bytes(add, s_v, it_v, fused_v, merged_v)
     return B
 
 
-def _cond_bytes(add, s_c, it_c, fused):
+def _cond_bytes(add, s_c, it_c, fused, merged=False):
     add("face_kappa", bytes_per_cell("face_kappa"))
     add("vertex_coef", 2 * bytes_per_cell("vertex_coef"))   # once per RKL2 advance and per PCG solve
     add("aniso_gersh", bytes_per_cell("aniso_gersh"))
@@ -110,6 +115,9 @@ def _cond_bytes(add, s_c, it_c, fused):
     add("aniso_rkl2_stage", (s_c - 1) * bytes_per_cell("aniso_rkl2_stage"))
     add("aniso_pcg_r0", bytes_per_cell("aniso_pcg_r0"))
     for k in range(1, it_c + 1):
+        if merged:
+            add("aniso_pcg_m", bytes_per_cell("aniso_pcg_m", first=k == 1))
+            continue
         if fused:
             add("aniso_pcg_s", bytes_per_cell("aniso_pcg_s", first=k == 1))
         else:
@@ -120,13 +128,16 @@ def _cond_bytes(add, s_c, it_c, fused):
         add("pcg_xfinal", bytes_per_cell("pcg_xfinal", 1))
 
 
-def _visc_bytes(add, s_v, it_v, fused=False):
+def _visc_bytes(add, s_v, it_v, fused=False, merged=False):
     add("iso_gersh", bytes_per_cell("iso_gersh"))
     add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
     add("iso_rkl2_stage", (s_v - 1) * bytes_per_cell("iso_rkl2_stage", 3))
-    add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0", 3))
+    add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0_m" if merged else "iso_pcg_r0", 3))
     for k in range(1, max(it_v) + 1):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
+        if merged:
+            add("iso_pcg_m", bytes_per_cell("iso_pcg_m", active=act, first=k == 1))
+            continue
         if fused:
             add("iso_pcg_s", bytes_per_cell("iso_pcg_s", active=act, first=k == 1))
             add("pcg_update", bytes_per_cell("pcg_update_noz", active=act))
@@ -515,9 +526,11 @@ def main():
     Bytes = {}
     fused_c = timing.get("aniso_pcg_s", (0, 0.0))[0] > 0
     fused_v = timing.get("iso_pcg_s", (0, 0.0))[0] > 0
+    merged_c = timing.get("aniso_pcg_m", (0, 0.0))[0] > 0
+    merged_v = timing.get("iso_pcg_m", (0, 0.0))[0] > 0
     for i in pinfos:
         for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
-                                      fused_c, fused_v).items():
+                                      fused_c, fused_v, merged_c, merged_v).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
     kernels = {}
     for k, (n, kms) in timing.items():
@@ -541,7 +554,8 @@ def main():
     launches_dom = pinfos[0]
     n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
              "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
-             "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"])}.get(dom)
+             "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"]),
+             "aniso_pcg_m": launches_dom["it_cond"], "iso_pcg_m": max(launches_dom["it_visc"])}.get(dom)
     bpl = (Bytes[dom] / len(pinfos) / n_eff) if n_eff else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,

@@ -149,7 +149,9 @@ int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_
 #define STS_K_ANISO_PCG_S 18     /* fused PCG S-pass (p update + x update + A p), TMA path   */
 #define STS_K_PCG_XFINAL 19      /* final deferred x += alpha p after convergence            */
 #define STS_K_ISO_PCG_S 20       /* fused PCG S-pass of the isotropic operator, TMA path      */
-#define STS_K_NCLASSES 21
+#define STS_K_ANISO_PCG_M 21     /* one-pass (merged) PCG iteration, anisotropic, TMA path    */
+#define STS_K_ISO_PCG_M 22       /* one-pass (merged) PCG iteration, isotropic, TMA path      */
+#define STS_K_NCLASSES 23
 int sts_grid_set_timing(sts_grid* g, int enable);
 
 /*
@@ -166,6 +168,18 @@ int sts_grid_set_tma(sts_grid* g, int enable);
  * Graphs are never used while per-launch timing is on or with an NCCL communicator.
  */
 int sts_grid_set_graphs(sts_grid* g, int enable);
+
+/*
+ * PCG iteration structure of be_pcg_solve (A-B measurement / testing).
+ * enable != 0 (the default): where the TMA kernels are eligible, ONE fused pass
+ * per iteration (DESIGN.md §5.3 "merged PCG"): it forms z_k = z_{k-1} -
+ * alpha_{k-1} d y_{k-1} and p_k = z_k + beta_k p_{k-1} on the fly, applies A,
+ * and reduces r_k.z_k, p_k.A p_k, z_k.A p_k and (d A p_k).A p_k together; the
+ * next r.z follows from the expansion of (r - alpha y).d(r - alpha y), so one
+ * global reduction per iteration replaces Fig. 1's two.  The
+ * iterates equal Fig. 1's in exact arithmetic.  0: the two-pass S / U iteration.
+ */
+int sts_grid_set_pcg_merged(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
 

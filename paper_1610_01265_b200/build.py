@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", f) for f in ("stencil.cu", "stencil_tma.cu", "stencil_tma_iso.cu", "aux.cu", "capi.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", h) for h in ("sts_common.cuh", "tma.cuh")] + \
+DEPS = SRC + [os.path.join(HERE, "csrc", h) for h in ("sts_common.cuh", "tma.cuh", "pcg.cuh")] + \
     [os.path.join(ROOT, "include", "sts_b200.h")]
 OUT = os.path.join(HERE, "libsts_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

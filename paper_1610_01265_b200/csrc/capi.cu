@@ -335,11 +335,14 @@ static std::vector<const double*> build_vertex_coefs(sts_grid* g, int mode, doub
 
 // one stencil pass: the TMA pipelined kernel where eligible, else the cp.async kernels
 static void launch_pass(sts_grid* g, const StencilCall& c, cudaStream_t st) {
-  const int kind = (c.epi == EPI_PCG_S) ? (c.mode == STS_MODE_ANISO ? STS_K_ANISO_PCG_S : STS_K_ISO_PCG_S)
-                                        : stencil_kind(c.mode, c.epi);
+  const bool aniso = c.mode == STS_MODE_ANISO;
+  const int kind = (c.epi == EPI_PCG_S)   ? (aniso ? STS_K_ANISO_PCG_S : STS_K_ISO_PCG_S)
+                   : (c.epi == EPI_PCG_M) ? (aniso ? STS_K_ANISO_PCG_M : STS_K_ISO_PCG_M)
+                                          : stencil_kind(c.mode, c.epi);
   Timed t(g, kind, st);
   if (g->tma && (launch_aniso_tma(c, st) || launch_iso_tma(c, st))) return;
-  if (c.epi == EPI_PCG_S) throw Error{STS_ERR_STATE, "fused PCG S-pass launched without a TMA-eligible call"};
+  if (c.epi == EPI_PCG_S || c.epi == EPI_PCG_M)
+    throw Error{STS_ERR_STATE, "fused PCG pass launched without a TMA-eligible call"};
   launch_stencil(c, st);
 }
 
@@ -348,7 +351,7 @@ static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 // CTAs one pass over local planes [c.ib, c.ie) launches (sizes the partial-sum rows)
 static int pass_blocks(const sts_grid* g, const StencilCall& c) {
   if (g->tma && aniso_tma_eligible(c)) return aniso_tma_blocks(c.geo, c.ib, c.ie);
-  if (g->tma && iso_tma_eligible(c)) return iso_tma_blocks(c.geo, c.ib, c.ie);
+  if (g->tma && iso_tma_eligible(c)) return iso_tma_blocks(c);
   return stencil_blocks(c.mode, c.epi, c.geo, c.ib, c.ie);
 }
 
@@ -754,6 +757,13 @@ int sts_grid_set_graphs(sts_grid* g, int enable) {
   });
 }
 
+int sts_grid_set_pcg_merged(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->pcg_merged = enable != 0;
+  });
+}
+
 int sts_grid_set_tma(sts_grid* g, int enable) {
   return guard([&] {
     STS_REQUIRE(g, "NULL grid");
@@ -1056,15 +1066,19 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     sg.output(un1, NF);
     const size_t evn = vertex_coef_doubles(g, mode);
     const size_t NFr = rnd(NF), Nr = rnd(N);
-    // scratch: r, z, y, p0, p1 [ncomp][nl][plane]; d [nl][plane]; vertex coefficients
-    double* base = ws_get(g, (5 * NFr + Nr + evn + rnd(sg.total)) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 5 * NFr + Nr + evn);
+    // scratch: six [ncomp][nl][plane] fields (two-pass: r, z, y, p0, p1; merged: z0, z1,
+    // w0, w1, p0, p1); d [nl][plane]; vertex coefficients
+    double* base = ws_get(g, (6 * NFr + Nr + evn + rnd(sg.total)) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 6 * NFr + Nr + evn);
     double* r = base;
     double* z = base + NFr;
     double* y = base + 2 * NFr;
     double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
-    double* d = base + 5 * NFr;
-    double* evbase = base + 5 * NFr + Nr;
+    double* d = base + 6 * NFr;
+    double* evbase = base + 6 * NFr + Nr;
+    // merged iteration buffers (ping-pong by iteration parity; the p pair is pb)
+    double* zb[2] = {base, base + NFr};
+    double* wb[2] = {base + 2 * NFr, base + 5 * NFr};
     double* x = un1;
     const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
     const double rtol2 = rtol * rtol;
@@ -1084,6 +1098,21 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.u3 = view(g, g->slabs[0], H_D, d);
       fused = aniso_tma_eligible(c) || iso_tma_eligible(c);
     }
+    // merged iteration (one pass + one reduction per iteration, sts_grid_set_pcg_merged)
+    bool merged = false;
+    if (g->tma && g->pcg_merged) {
+      StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_M, zb[0], k1, k2, k3, bb, w);
+      c.u2 = view(g, g->slabs[0], H_W, wb[0]);
+      c.u3 = view(g, g->slabs[0], H_P, pb[0]);
+      c.ev = ev[0];
+      c.ea.out = off(zb[1], g->slabs[0]);
+      c.ea.out2 = off(pb[1], g->slabs[0]);
+      c.ea.out3 = off(wb[1], g->slabs[0]);
+      c.ea.x = off(x, g->slabs[0]);
+      c.ea.dinv = off(d, g->slabs[0]);
+      merged = aniso_tma_eligible(c) || iso_tma_eligible(c);
+    }
+    if (merged) fused = false;
     // isotropic fused S-pass: z = r d is formed inside the stencil pass from the staged
     // r and d, so neither the initial residual pass nor the U-pass stores z
     const bool zd = fused && mode == STS_MODE_ISO;
@@ -1096,9 +1125,9 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       const Slab& sl = g->slabs[si];
       StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
       c.ev = ev[si];
-      c.ea.out = off(r, sl);
+      c.ea.out = merged ? off(wb[0], sl) : off(r, sl);   // (merged: r0 itself is not needed)
       c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-      c.ea.out3 = zd ? nullptr : off(z, sl);
+      c.ea.out3 = merged ? off(zb[0], sl) : (zd ? nullptr : off(z, sl));
       c.ea.out4 = off(d, sl);
       c.ea.dt = dt;
       c.ea.partials = partials;
@@ -1123,6 +1152,27 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.ea.sc = sc;
       return c;
     };
+    auto make_m = [&](size_t si) {   // merged iteration k_cur (TMA)
+      const Slab& sl = g->slabs[si];
+      const int first = (k_cur == 1);
+      const int a = (k_cur - 1) & 1, b2 = k_cur & 1;
+      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_M, zb[a], k1, k2, k3, bb, w);
+      c.u = view(g, sl, H_Z, zb[a]);
+      c.u2 = first ? FieldV{} : view(g, sl, H_W, wb[a]);
+      c.u3 = first ? FieldV{} : view(g, sl, H_P, pb[a]);
+      c.ev = ev[si];
+      c.ea.out = off(zb[b2], sl);
+      c.ea.out2 = off(pb[b2], sl);
+      c.ea.out3 = off(wb[b2], sl);
+      c.ea.x = off(x, sl);
+      c.ea.dinv = off(d, sl);
+      c.ea.first = first;
+      c.ea.dt = dt;
+      c.ea.partials = partials;
+      c.ea.pstride = pstride;
+      c.ea.sc = sc;
+      return c;
+    };
     auto make_ap = [&](size_t si) {  // A p of the unfused S-pass
       const Slab& sl = g->slabs[si];
       double* pnew = pb[k_cur & 1];
@@ -1136,12 +1186,14 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       return c;
     };
     const int sb_r0 = sweep_blocks(g, true, make_r0);
-    const int sb_s = fused ? sweep_blocks(g, true, make_s) : sweep_blocks(g, true, make_ap);
+    const int sb_s = merged ? sweep_blocks(g, true, make_m)
+                            : (fused ? sweep_blocks(g, true, make_s) : sweep_blocks(g, true, make_ap));
     pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
-    const size_t red_doubles = (size_t)2 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
+    // partial rows: ncomp x (2 for R0, 1 per two-pass phase, 4 for the merged pass)
+    const size_t red_doubles = (size_t)4 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
     ensure_red(g, red_doubles * sizeof(double));
     partials = g->d_red;
-    double* sums = partials + 2 * ncomp * pstride;
+    double* sums = partials + 4 * ncomp * pstride;
     sc = reinterpret_cast<PcgScal*>(sums + 16);
 
     // fused final reductions (single process): the last CTA of the S-pass / U-pass sums
@@ -1156,6 +1208,9 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     fin_s.rtol2 = rtol2;
     FinRed fin_u = fin_s;
     fin_u.phase = PH_RZ;
+    FinRed fin_m = fin_s;
+    fin_m.nq = 4;
+    fin_m.phase = PH_M;
     fin_u.ntot = PW_BLOCKS;   // set to the launched grid by launch_pcg_rupdate
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
@@ -1178,7 +1233,29 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
     auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
     // one PCG iteration k on stream `is`
+    // merged iteration k: ONE pass (z_k, p_k, y_k = A p_k, w_k = d y_k, x_k; partials
+    // r_k.z_k, p_k.y_k, z_k.y_k, w_k.y_k) and ONE reduction (alpha_k, r_{k+1}.z_{k+1},
+    // convergence, beta_{k+1}: pcg.cuh PH_M)
+    auto iteration_m = [&](int k, cudaStream_t is) {
+      k_cur = k;
+      if (needs_halos(g)) g->comm_global += 1;
+      const int a = (k - 1) & 1;
+      const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_m;
+      int nbs;
+      if (k == 1) nbs = sweep(g, {{H_Z, zb[0], ncomp}}, is, make_m, fs);
+      else nbs = sweep(g, {{H_Z, zb[a], ncomp}, {H_W, wb[a], ncomp}, {H_P, pb[a], ncomp}}, is, make_m, fs);
+      if (!fs) {
+        Timed t(g, STS_K_PCG_REDUCE, is);
+        launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is);
+        if (g->comm) {
+          STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * 4, ncclDouble, ncclSum, g->comm, is));
+          launch_pcg_scalar(sums, ncomp, 4, PH_M, sc, rtol2, is);
+          g->launches += 1;
+        }
+      }
+    };
     auto iteration = [&](int k, cudaStream_t is) {
+      if (merged) return iteration_m(k, is);
       k_cur = k;
       if (needs_halos(g)) g->comm_global += 2;   // p.y (alpha) and r.z (beta + convergence)
       double* pold = pb[(k - 1) & 1];

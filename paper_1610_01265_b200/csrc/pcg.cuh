@@ -28,6 +28,23 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k, applied by the next p pass / final pass
     if (s.rz <= s.thresh) s.done = 1;      // check r_r for convergence
     else s.beta = s.rz / s.rz_old;         // beta_k = r_r / r_old
+  } else if (phase == PH_M) {
+    // merged iteration k (one pass, one reduction): sums of the pass
+    // are r_k.z_k (= z_k^2 / d), p_k.y_k, z_k.y_k and (d y_k).y_k with y_k = A p_k.
+    // alpha_k as in Fig. 1; r_{k+1} = r_k - alpha_k y_k gives
+    //   r_{k+1}.z_{k+1} = r_k.z_k - 2 alpha_k z_k.y_k + alpha_k^2 (d y_k).y_k
+    // (exact in exact arithmetic; r_k.z_k is the pass's own sum, so rounding does
+    // not accumulate across iterations).  The pass forms z_{k+1} = z_k - alpha_k d y_k.
+    if (s.done) return;
+    const double rz = sums[c * nq + 0];
+    s.pAp = sums[c * nq + 1];
+    s.alpha = rz / s.pAp;
+    s.rz_old = rz;
+    s.rz = rz - 2.0 * s.alpha * sums[c * nq + 2] + s.alpha * s.alpha * sums[c * nq + 3];
+    s.iters += 1;
+    s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k (next pass / final pass)
+    if (s.rz <= s.thresh) s.done = 1;
+    else s.beta = s.rz / rz;               // beta_{k+1} = r_{k+1}.z_{k+1} / r_k.z_k
   }
 }
 

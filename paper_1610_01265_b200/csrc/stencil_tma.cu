@@ -45,10 +45,10 @@ constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= consumer wa
 constexpr int XOJ = XJ - 1, XOK = XK - 1;   // output rows / cols
 constexpr int XNT = XJ * XK;                // consumer threads
 constexpr int XTHREADS = XNT + 32;          // + producer warp
-constexpr int XTS = 4;                      // ring slots (packages in flight = XTS - 1)
+// ring slots (packages in flight = slots - 1): TmaLay::NS, 4 (3 for the merged PCG pass)
 constexpr int UBW = 36, UBH = 9;            // staged-source box (cols x rows)
 constexpr int EBW = 34;                     // vertex-coefficient box cols
-constexpr int MAXSRC = 2;                   // staged sources (PCG S-pass: z, pold)
+constexpr int MAXSRC = 3;                   // staged sources (PCG S-pass: z, pold; merged: zold, wold, pold)
 constexpr int MAXOWN = 4;                   // epilogue operand boxes
 // slot parts (doubles); every part starts on a 128 B boundary
 constexpr int U_MAIN = 336;                 // 9 x 36 = 324 -> 336
@@ -75,18 +75,19 @@ struct TmaArgs {
 
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
-enum { OW_X = 0 };                           // PCG S-pass
+enum { OW_X = 0, OW_D = 1 };                 // PCG S-pass (x) / merged pass (x, d)
 // slot layout of one (epilogue, has-w) variant
 template <int EPI, bool W>
 struct TmaLay {
-  static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : 1;
-  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : 0);
+  static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
+  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : (EPI == EPI_PCG_M ? 2 : 0));
   static constexpr int nown = nepi + (W ? 1 : 0);             // w is the last own box
   static constexpr int E = nsrc * U_FIELD;
   static constexpr int O = E + E_PART;
   static constexpr int MT = O + nown * O_PART;       // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  static constexpr size_t SMEM = (size_t)(XTS * SLOT + 2 * VBUF) * sizeof(double) + 2 * XTS * sizeof(uint64_t) + 128;
+  static constexpr int NS = (EPI == EPI_PCG_M) ? 3 : 4;   // (3 CTAs per SM for the larger merged slot)
+  static constexpr size_t SMEM = (size_t)(NS * SLOT + 2 * VBUF) * sizeof(double) + 2 * NS * sizeof(uint64_t) + 128;
 };
 
 // FR: this launch finishes the pass's dot-product reduction in its last CTA
@@ -94,6 +95,8 @@ template <int EPI, bool W, bool FR>
 __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, int ic,
                                                                 const __grid_constant__ TmaArgs ta) {
   using Lay = TmaLay<EPI, W>;
+  constexpr int XTS = Lay::NS;
+  constexpr bool kM = (EPI == EPI_PCG_M);
   extern __shared__ __align__(128) double smx[];
   double* ring = smx;                               // [XTS][SLOT]
   double* vbuf = smx + XTS * Lay::SLOT;             // [2][3][XNT]
@@ -107,16 +110,29 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   const int ie = min(ib + ic, c.ie);
   const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
 
-  if constexpr (EPI == EPI_PCG_S) {
+  if constexpr (EPI == EPI_PCG_S || kM) {
     if (c.ea.sc && c.ea.sc[0].done) return;
   }
-  const bool first = (EPI == EPI_PCG_S) && c.ea.first;
+  const bool first = (EPI == EPI_PCG_S || kM) && c.ea.first;
   const bool per = G.periodic3 != 0;
   const bool wrapL = per && k0 == 0;
   const bool wrapR = per && (k0 + 32 >= G.n3);
   const int ou = (k0 - 1) & ~1;                     // even box origins (floor, also for -1 -> -2)
   const int oe = k0 & ~1, se = k0 - oe;             // e / epilogue boxes and their column shift
 
+  // warp-uniform values in shared memory (broadcast loads instead of registers):
+  // 1/g3 of the vertex rows j0-1 .. j0+XJ-1 (row vj of a warp and the one above it)
+  // and the PCG scalars beta_k, alpha_{k-1}
+  __shared__ double sg3[XJ + 1], sbx[2];
+  if (tid <= XJ) {
+    const int r = j0 - 1 + tid;
+    sg3[tid] = (r >= 0 && r < G.n2) ? M.iG3[r] : 0.0;
+  }
+  if (tid == XJ + 1) {
+    const bool kPcg = (EPI == EPI_PCG_S || kM) && !first;
+    sbx[0] = kPcg ? c.ea.sc[0].beta : 0.0;
+    sbx[1] = kPcg ? c.ea.sc[0].ax : 0.0;
+  }
   if (tid == 0) {
     for (int s = 0; s < XTS; ++s) {
       mbar_init(full + s, 1);
@@ -129,7 +145,7 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   // ======================= producer warp: package Q(p), p = ib-1 .. ie =======================
   if (tid >= XNT) {
     if (tid != XNT) return;
-    const int nsrc_now = (EPI == EPI_PCG_S && first) ? 1 : Lay::nsrc;
+    const int nsrc_now = ((EPI == EPI_PCG_S || kM) && first) ? 1 : Lay::nsrc;
     for (int p = ib - 1; p <= ie; ++p) {
       const int slot = (p - ib + 1) % XTS, n = (p - ib + 1) / XTS;
       if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
@@ -171,15 +187,14 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
 
   // ======================= consumer warps =======================
   const int vj = tid >> 5, vk = tid & 31;
-  const double beta = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].beta : 0.0;
-  const double ax = (EPI == EPI_PCG_S && !first) ? c.ea.sc[0].ax : 0.0;
-  const int jv = j0 - 1 + vj;                       // vertex row (jv + 1/2)
-  const double ig3a = (jv >= 0 && jv < G.n2) ? M.iG3[jv] : 0.0;
-  const double ig3b = (jv + 1 >= 0 && jv + 1 < G.n2) ? M.iG3[jv + 1] : 0.0;
+#define beta sbx[0]
+#define ax sbx[1]
+#define ig3a sg3[vj]       /* vertex row jv = j0-1+vj */
+#define ig3b sg3[vj + 1]   /* and jv+1 (= the own cell row j) */
   const int j = j0 + vj, k = k0 + vk;
   const bool own = vj < XOJ && vk < XOK && j < G.n2 && k < G.n3;
   const long long coff = own ? (long long)j * G.n3 + k : 0;
-  const double ig3c = own ? M.iG3[j] : 0.0;
+#define ig3c sg3[vj + 1]   /* own cells only */
   const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
   // offset (within a staged field block) of the cell at tile row r (global j0-1+r)
   // and tile col t (global k0-1+t)
@@ -194,25 +209,34 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   // in-plane 2x2 box of the source value s (PCG: z + beta pold, else u): each lane
   // loads its column (rows vj, vj+1) and takes column vk+1 from lane vk+1 by shuffle
   // (lane 31 loads it), halving the shared-memory loads of the march
+  // merged PCG (kM): fields zold, wold, pold; z = zold - ax wold, source p = z + beta pold
   constexpr bool kP = (EPI == EPI_PCG_S);
-  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu, double& un, double& pon) {
-    double z00 = S[o00], z10 = S[o10];
+  constexpr int PF = kM ? 2 * U_FIELD : U_FIELD;    // pold field offset
+  auto zof = [&](const double* S, int o) {
+    if (kM && !first) return fma(-ax, S[U_FIELD + o], S[o]);
+    return S[o];
+  };
+  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu, double& un, double& pon, double& zn) {
+    double z00 = zof(S, o00), z10 = zof(S, o10);
+    double zk10 = z10;
     double q00 = 0.0, q10 = 0.0;
-    if (kP && !first) {
-      q00 = S[U_FIELD + o00];
-      q10 = S[U_FIELD + o10];
+    if ((kP || kM) && !first) {
+      q00 = S[PF + o00];
+      q10 = S[PF + o10];
       z00 = fma(beta, q00, z00);
       z10 = fma(beta, q10, z10);
     }
     double z01 = __shfl_down_sync(0xffffffffu, z00, 1), z11 = __shfl_down_sync(0xffffffffu, z10, 1);
-    double q11 = 0.0;
-    if (kP && !first) q11 = __shfl_down_sync(0xffffffffu, q10, 1);
+    double q11 = 0.0, zk11 = 0.0;
+    if ((kP || kM) && !first) q11 = __shfl_down_sync(0xffffffffu, q10, 1);
+    if (kM) zk11 = __shfl_down_sync(0xffffffffu, zk10, 1);
     if (vk == XK - 1) {
-      z01 = S[o01];
-      z11 = S[o11];
-      if (kP && !first) {
-        q11 = S[U_FIELD + o11];
-        z01 = fma(beta, S[U_FIELD + o01], z01);
+      z01 = zof(S, o01);
+      z11 = zof(S, o11);
+      zk11 = z11;
+      if ((kP || kM) && !first) {
+        q11 = S[PF + o11];
+        z01 = fma(beta, S[PF + o01], z01);
         z11 = fma(beta, q11, z11);
       }
     }
@@ -221,12 +245,13 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
     Fu = ig3a * (z01 - z00) + ig3b * (z11 - z10);
     un = z11;     // own cell of this plane
     pon = q11;    // its pold (PCG)
+    zn = zk11;    // its z (merged PCG)
   };
 
   double SuL = 0, TuL = 0, FuL = 0;
   double SAl = 0, DBl = 0, DCl = 0;
-  double uc = 0.0, poc = 0.0;   // own-cell source value (and pold) of the previous plane
-  double part = 0.0, part2 = 0.0;
+  double uc = 0.0, poc = 0.0, zc = 0.0;   // own-cell source value (pold, z) of the previous plane
+  double part = 0.0, part2 = 0.0, part3 = 0.0, part4 = 0.0;
   constexpr bool kR0 = (EPI == EPI_PCG_R0);
   // R0: L_ii = -sum over the cell's 8 vertices of W^2, W = the cell's weight in q_v =
   // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex);
@@ -236,8 +261,8 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
     mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
-    double SuH, TuH, FuH, un, pon;
-    usums(S, SuH, TuH, FuH, un, pon);
+    double SuH, TuH, FuH, un, pon, zn;
+    usums(S, SuH, TuH, FuH, un, pon, zn);
     double* vb = vbuf + (p & 1) * VBUF;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
@@ -318,6 +343,20 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
           c.ea.out2[gi] = uc;                                   // p_k
           if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);   // x_k = x_{k-1} + alpha_{k-1} p_{k-1}
           part += uc * y;
+        } else if constexpr (kM) {
+          // y_k = A p_k, w_k = d y_k; z_k, p_k, w_k to the other buffers, x in place;
+          // partials r_k.z_k = z_k^2 / d, p_k.y_k, z_k.y_k, w_k.y_k
+          const double y = WV * uc - c.ea.dt * Lu;
+          const double dd = O[OW_D * O_PART];
+          const double wk = dd * y;
+          c.ea.out[gi] = zc;
+          c.ea.out2[gi] = uc;
+          c.ea.out3[gi] = wk;
+          if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);
+          part += zc * zc / dd;
+          part2 += uc * y;
+          part3 += zc * y;
+          part4 += wk * y;
         }
       }
       SAl = SAh;
@@ -332,6 +371,7 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
     FuL = FuH;
     uc = un;
     poc = pon;
+    zc = zn;
   }
   if constexpr (kR0) {
     __shared__ double red2[2][XNT / 32];
@@ -353,18 +393,24 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
   }
-  if constexpr (EPI == EPI_PCG_S) {
-    __shared__ double red[XNT / 32];
-    double v = part;
+  if constexpr (EPI == EPI_PCG_S || kM) {
+    // partial rows: S-pass p.y; merged r.z, p.y, z.y, w.y
+    constexpr int NQ = kM ? 4 : 1;
+    __shared__ double red[NQ][XNT / 32];
+    double pv[4] = {part, part2, part3, part4};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (vk == 0) red[vj] = v;
+    for (int t = 0; t < NQ; ++t) {
+      double v = pv[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (vk == 0) red[t][vj] = v;
+    }
     asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
-    if (tid == 0) {
+    if (tid < NQ) {
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < XNT / 32; ++w) s += red[w];
-      c.ea.partials[c.ea.pbase + blk] = s;
+      for (int w = 0; w < XNT / 32; ++w) s += red[tid][w];
+      c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
     if constexpr (FR) {
       __shared__ double fred[32];
@@ -376,11 +422,18 @@ __global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, i
   }
 }
 
+#undef beta
+#undef ax
+#undef ig3a
+#undef ig3b
+#undef ig3c
+
 // ============================================================================
 // host side
 // ============================================================================
 static bool has_tma(int epi) {
-  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0;
+  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0 ||
+         epi == EPI_PCG_M;
 }
 
 bool aniso_tma_eligible(const StencilCall& c) {
@@ -392,6 +445,10 @@ bool aniso_tma_eligible(const StencilCall& c) {
   // halo planes come from the library's contiguous [2][MAXC][plane] slot buffers
   if (c.u.lo && c.u.hi && c.u.hi != c.u.lo + (long long)MAXC * G.plane) return false;
   if (c.u2.lo && c.u2.hi && c.u2.hi != c.u2.lo + (long long)MAXC * G.plane) return false;
+  if (c.epi == EPI_PCG_M) {
+    if (!al16(c.u3.p) || !al16(c.u3.lo) || !c.ea.dinv || !al16(c.ea.dinv) || !c.ea.x || !c.ea.out3) return false;
+    if (c.u3.lo && c.u3.hi && c.u3.hi != c.u3.lo + (long long)MAXC * G.plane) return false;
+  }
   return true;   // a slab with only a hi halo maps its slot buffer from hi - MAXC*plane
 }
 
@@ -427,7 +484,7 @@ static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta,
 
 template <int EPI>
 static void launch_w(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
-  constexpr bool kS = (EPI == EPI_PCG_S);
+  constexpr bool kS = (EPI == EPI_PCG_S || EPI == EPI_PCG_M);
   const bool fr = kS && c.ea.fin.ticket;
   if (c.w) {
     if (fr) launch_t<EPI, true, kS>(c, grid, ic, ta, st);
@@ -446,8 +503,8 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
   if (grid.x == 0) return true;
   TmaArgs ta;
   memset(&ta, 0, sizeof(ta));
-  const FieldV* srcs[MAXSRC] = {&c.u, &c.u2};
-  const int nsrc = (c.epi == EPI_PCG_S) ? 2 : 1;
+  const FieldV* srcs[MAXSRC] = {&c.u, &c.u2, &c.u3};
+  const int nsrc = (c.epi == EPI_PCG_S) ? 2 : (c.epi == EPI_PCG_M ? 3 : 1);
   ta.has_lo = c.u.lo != nullptr;
   ta.has_hi = c.u.hi != nullptr;
   for (int f = 0; f < nsrc; ++f) {
@@ -478,6 +535,9 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     owns[nown++] = c.ea.m0;
   } else if (c.epi == EPI_PCG_S) {
     owns[nown++] = c.ea.x;
+  } else if (c.epi == EPI_PCG_M) {
+    owns[nown++] = c.ea.x;
+    owns[nown++] = c.ea.dinv;
   }
   if (c.w) owns[nown++] = c.w;
   for (int q = 0; q < nown; ++q) map_plain(&ta.own[q], owns[q], G, G.nl, XK, XOJ);
@@ -487,6 +547,7 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_RKL2_STAGE: launch_w<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_w<EPI_PCG_S>(c, grid, ic, ta, st); break;
     case EPI_PCG_R0: launch_w<EPI_PCG_R0>(c, grid, ic, ta, st); break;
+    case EPI_PCG_M: launch_w<EPI_PCG_M>(c, grid, ic, ta, st); break;
     default: return false;
   }
   STS_CUDA(cudaGetLastError());

@@ -29,53 +29,82 @@ using namespace tma;
 
 namespace {
 
-// 7 consumer warps + 1 producer = 8 warps per CTA, 2 CTAs per SM: 4 warps per SM
-// sub-partition, so the 64K-register file allows 128 registers per thread (with 8
-// consumer warps the per-sub-partition limit drops to 96 and the 3-component PCG
-// S-pass spills)
-constexpr int IJ = 7, IK = 32;            // tile rows x cols = consumer warps x lanes
-constexpr int INT = IJ * IK;              // consumer threads
-constexpr int ITHREADS = INT + 32;        // + producer warp
-constexpr int IXTS = 3;                   // ring slots
-constexpr int SBW = 36, SBH = IJ + 2;     // staged source box
+constexpr int IK = 32;                    // tile cols = lanes
+constexpr int SBW = 36;                   // staged source box cols
 constexpr int rnd16(int n) { return (n + 15) / 16 * 16; }   // 128 B multiples of doubles
-constexpr int S_MAIN = rnd16(SBW * SBH);  // 324 -> 336
-constexpr int S_W = rnd16(2 * SBH);       // 2 x 9 wrap box -> 32
-constexpr int K2W = 32, K2H = IJ + 1, K2SZ = rnd16(K2W * K2H);
-constexpr int K3W = 34, K3H = IJ, K3SZ = rnd16(K3W * K3H);
-constexpr int K3WR = rnd16(2 * K3H);      // 2 x 7 wrap box
-constexpr int OWN = IK * IJ;              // 32 x 7 own box (224 = 14 x 16)
+constexpr int K2W = 32, K3W = 34;
+constexpr int SMEM_1CTA = 232448;         // max dynamic shared memory of one CTA (227 KB)
+
+// Tile geometry of IJ rows: IJ consumer warps own an IJ x 32 (theta x phi) tile
+// and one producer warp streams its packages.
+//  * IJ = 7, 2 CTAs per SM: 8 warps per CTA -> 4 warps per SM sub-partition, so the
+//    64K-register file allows 128 registers per thread (8 consumer warps would drop
+//    that to 96 and the 3-component PCG S-pass spills);
+//  * IJ = 11, 1 CTA per SM (the 3-component merged PCG pass, whose three staged
+//    fields make a 7-row slot too large for three ring slots at 2 CTAs per SM):
+//    12 warps -> 3 per sub-partition -> 168 registers (no spills), 3 slots of 63 KB.
+//    (14 rows would put 4 warps on a sub-partition again: 128 registers, spills.)
+template <int IJ_>
+struct IsoTile {
+  static constexpr int IJ = IJ_;
+  static constexpr int INT = IJ * IK;               // consumer threads
+  static constexpr int THREADS = INT + 32;          // + producer warp
+  static constexpr int SBH = IJ + 2;                // staged source box rows
+  static constexpr int S_MAIN = rnd16(SBW * SBH);   // 7 rows: 324 -> 336
+  static constexpr int S_W = rnd16(2 * SBH);        // 2 x SBH wrap box
+  static constexpr int K2H = IJ + 1, K2SZ = rnd16(K2W * K2H);
+  static constexpr int K3H = IJ, K3SZ = rnd16(K3W * K3H);
+  static constexpr int K3WR = rnd16(2 * K3H);       // 2 x IJ wrap box
+  static constexpr int OWN = IK * IJ;               // 32 x IJ own box
+};
+
+// rows of the tile of one (epilogue, ncomp) variant (host and device)
+__host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 11 : 7; }
 
 template <int EPI, int NC>
-struct IsoLay {
-  static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : 1;                               // z, pold
-  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 * NC : (EPI == EPI_PCG_S ? NC : 0);
+struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
+  using T = IsoTile<iso_rows(EPI, NC)>;
+  static constexpr int MINB = T::IJ > 7 ? 1 : 2;   // CTAs per SM (launch bounds)
+  // staged fields: u | PCG S-pass r, pold | merged PCG zold, wold, pold
+  static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
+  // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x, then d (one component)
+  static constexpr int nepi =
+      (EPI == EPI_RKL2_STAGE) ? 3 * NC : (EPI == EPI_PCG_S ? NC : (EPI == EPI_PCG_M ? NC + 1 : 0));
   // one block per staged field: NC main boxes, then the NC x 2 wrap boxes, so a
   // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
-  static constexpr int WRP = NC * S_MAIN;                          // wrap boxes within a field block
-  static constexpr int FS = NC * S_MAIN + NC * 2 * S_W;            // field block stride
+  static constexpr int WRP = NC * T::S_MAIN;                          // wrap boxes within a field block
+  static constexpr int FS = NC * T::S_MAIN + NC * 2 * T::S_W;         // field block stride
   // PCG S-pass: the Jacobi inverse diagonal d (one component, main + 2 wrap boxes), so
   // z = r d is formed on the fly and the U-pass never stores z
   static constexpr int nd = (EPI == EPI_PCG_S) ? 1 : 0;
   static constexpr int DB = nsrcf * FS;
-  static constexpr int K2 = DB + nd * (S_MAIN + 2 * S_W);
-  static constexpr int K3 = K2 + K2SZ;
-  static constexpr int K3R = K3 + K3SZ;
-  static constexpr int K1 = K3R + K3WR;
-  static constexpr int WB = K1 + OWN;
-  static constexpr int EP = WB + OWN;
-  static constexpr int MT = EP + nepi * OWN;      // per-plane metrics written by the producer
+  static constexpr int K2 = DB + nd * (T::S_MAIN + 2 * T::S_W);
+  static constexpr int K3 = K2 + T::K2SZ;
+  static constexpr int K3R = K3 + T::K3SZ;
+  static constexpr int K1 = K3R + T::K3WR;
+  static constexpr int WB = K1 + T::OWN;
+  static constexpr int EP = WB + T::OWN;
+  static constexpr int MT = EP + nepi * T::OWN;      // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  static constexpr size_t SMEM = (size_t)IXTS * SLOT * sizeof(double) + 2 * IXTS * sizeof(uint64_t) + 128;
+  // merged PCG at 2 CTAs per SM: the six per-column metric products live in shared
+  // memory (COL doubles per consumer thread, after the mbarriers) instead of 12 registers
+  static constexpr int COL = (EPI == EPI_PCG_M && MINB == 2) ? 6 : 0;
+  static constexpr int FIX = COL * T::INT * 8 + 128;
+  // ring slots: 3 where MINB CTAs per SM fit (2 CTAs: <= 113 KB each), else 2
+  static constexpr int NS = (MINB == 2) ? ((3 * (SLOT * 8 + 16) + FIX <= 113 * 1024) ? 3 : 2)
+                                        : ((4 * (SLOT * 8 + 16) + FIX <= SMEM_1CTA) ? 4 : 3);
+  static constexpr size_t SMEM =
+      (size_t)NS * SLOT * sizeof(double) + 2 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
+  static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
 };
 
 }  // namespace
 
 struct IsoTmaArgs {
-  CUtensorMap src[2];     // staged sources (u | z, pold), 3D (n3, n2, NC nl), box 36 x 9
-  CUtensorMap srcw[2];    // their wrap columns, box 2 x 9
+  CUtensorMap src[3];     // staged sources (u | r, pold | zold, wold, pold), 3D (n3, n2, NC nl), box 36 x 9
+  CUtensorMap srcw[3];    // their wrap columns, box 2 x 9
   CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x8, 34x7, 2x7, 32x7, 32x7
-  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 7
+  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 7 (merged PCG: x, d)
   CUtensorMap dm, dmw;    // PCG S-pass: d, box 36 x 9 / its wrap columns 2 x 9
   int has_w;
 };
@@ -85,14 +114,19 @@ struct IsoTmaArgs {
 // FR: this launch finishes the pass's dot-product reduction in its last CTA (a
 // separate instantiation, so the large-grid variant carries none of that code)
 template <int EPI, int NC, bool FST, bool FR>
-__global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int ic,
-                                                              const __grid_constant__ IsoTmaArgs ta) {
+__global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MINB)
+    iso_tma_kernel(StencilCall c, int ic, const __grid_constant__ IsoTmaArgs ta) {
   using Lay = IsoLay<EPI, NC>;
-  constexpr bool kP = (EPI == EPI_PCG_S) && !FST;   // source = z + beta pold
+  constexpr int IJ = Lay::IJ, INT = Lay::INT, SBH = Lay::SBH, S_MAIN = Lay::S_MAIN, S_W = Lay::S_W;
+  constexpr int K2H = Lay::K2H, K3H = Lay::K3H, OWN = Lay::OWN;
+  constexpr int NS = Lay::NS;
+  constexpr bool kS = (EPI == EPI_PCG_S);
+  constexpr bool kM = (EPI == EPI_PCG_M);
+  constexpr bool kP = (kS || kM) && !FST;   // source = z + beta pold (merged: z = zold - ax wold)
   extern __shared__ __align__(128) double smi[];
   double* ring = smi;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smi + IXTS * Lay::SLOT);
-  uint64_t* empty = full + IXTS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smi + NS * Lay::SLOT);
+  uint64_t* empty = full + NS;
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
@@ -108,10 +142,10 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   bool all = true;
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    skip[q] = (EPI == EPI_PCG_S) && c.ea.sc && c.ea.sc[q].done;
+    skip[q] = (kS || kM) && c.ea.sc && c.ea.sc[q].done;
     all = all && skip[q];
   }
-  if (EPI == EPI_PCG_S && all) return;
+  if ((kS || kM) && all) return;
 
   // PCG scalars of this iteration, broadcast from shared memory (keeps them out of registers)
   __shared__ double sbeta[NC], sax[NC];
@@ -120,7 +154,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     sax[tid] = kP ? c.ea.sc[tid].ax : 0.0;
   }
   if (tid == 0) {
-    for (int s = 0; s < IXTS; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, IJ);
     }
@@ -131,7 +165,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   // ======================= producer warp =======================
   if (tid >= INT) {
     if (tid != INT) return;
-    constexpr int nsrcf_now = (EPI == EPI_PCG_S && FST) ? 1 : Lay::nsrcf;
+    constexpr int nsrcf_now = ((kS || kM) && FST) ? 1 : Lay::nsrcf;
     const int cpl = (int)(G.cstride / G.plane);   // planes per component of the (whole local) array
     uint32_t bytes = nsrcf_now * NC * SBW * SBH * 8 + (K2W * K2H + K3W * K3H + OWN) * 8;
     if (wrapL) bytes += nsrcf_now * NC * 2 * SBH * 8 + 2 * K3H * 8;
@@ -144,7 +178,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
       if (wrapR) bytes += 2 * SBH * 8;
     }
     for (int p = ib; p < ie; ++p) {
-      const int slot = (p - ib) % IXTS, n = (p - ib) / IXTS;
+      const int slot = (p - ib) % NS, n = (p - ib) / NS;
       if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
       double* S = ring + slot * Lay::SLOT;
       uint64_t* bar = full + slot;
@@ -192,15 +226,25 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   const bool kself = per && G.n3 == 1;
   const bool km = !kself && (per || k >= 1), kp = !kself && (per || k + 1 < G.n3);
   const int kmw = per ? (k >= 1 ? k - 1 : G.n3 - 1) : k - 1;
-  double f1tp = 0, f2p = 0, f2m = 0, f3p = 0, f3m = 0, vtp = 0;
+  double cv[6] = {0, 0, 0, 0, 0, 0};   // f1tp, f2p, f2m, f3p, f3m, vtp
   if (own) {
-    f1tp = M.F1t[j] * M.F1p[k];
-    f2p = jp ? M.F2t[j] * M.F2p[k] : 0.0;
-    f2m = jm ? M.F2t[j - 1] * M.F2p[k] : 0.0;
-    f3p = kp ? M.F3t[j] * M.F3p[k] : 0.0;
-    f3m = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
-    vtp = M.Vt[j] * M.Vp[k];
+    cv[0] = M.F1t[j] * M.F1p[k];
+    cv[1] = jp ? M.F2t[j] * M.F2p[k] : 0.0;
+    cv[2] = jm ? M.F2t[j - 1] * M.F2p[k] : 0.0;
+    cv[3] = kp ? M.F3t[j] * M.F3p[k] : 0.0;
+    cv[4] = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
+    cv[5] = M.Vt[j] * M.Vp[k];
   }
+  double* const colc = reinterpret_cast<double*>(empty + NS);
+  if constexpr (Lay::COL > 0) {
+#pragma unroll
+    for (int t = 0; t < 6; ++t) colc[t * INT + tid] = cv[t];   // read back by this thread only
+  }
+  // column constant t: a register, or (merged PCG) this thread's shared-memory copy
+  auto CV = [&](int t) -> double {
+    if constexpr (Lay::COL > 0) return colc[t * INT + tid];
+    return cv[t];
+  };
   // smem offsets (relative to the slot) of the own cell, its in-plane neighbours per
   // component (periodic phi wrap: cell n3-1 / 0 from the 2-column wrap boxes)
   const int oc = (tj + 1) * SBW + tk + 2;
@@ -217,13 +261,21 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
   const int dc = Lay::DB + oc;
   const int dkm = kmw_box ? Lay::DB + S_MAIN + 0 * S_W + (tj + 1) * 2 + 1 : dc - 1;
   const int dkp = kpw_box ? Lay::DB + S_MAIN + 1 * S_W + (tj + 1) * 2 : dc + 1;
-  constexpr bool kS = (EPI == EPI_PCG_S);
-  // source value at (field-0 offset o, d offset od): PCG p = r d + beta pold (first: r d), else u
+  // merged PCG: z_k at a staged position (field 0 zold, field 1 wold)
+  auto zm = [&](const double* S, int o, int q) {
+    if constexpr (kP) return fma(-sax[q], S[o + Lay::FS], S[o]);
+    return S[o];
+  };
+  // source value at (field-0 offset o, d offset od): PCG S-pass p = r d + beta pold
+  // (first: r d); merged p = zm + beta pold (first: z0); else u
   auto sv = [&](const double* S, int o, int od, int q) {
     if constexpr (kS) {
       const double z = S[o] * S[od];
       if constexpr (kP) return fma(sbeta[q], S[o + Lay::FS], z);
       return z;
+    } else if constexpr (kM) {
+      if constexpr (kP) return fma(sbeta[q], S[o + 2 * Lay::FS], zm(S, o, q));
+      return S[o];
     }
     return S[o];
   };
@@ -238,46 +290,62 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     else return 0.0;
     return __ldg(pz + coff);
   };
+  // the source value from own-column loads: (z, pold, d) | merged (zold, wold, pold)
   auto comb = [&](double z, double po, double dd, int q) {
     if constexpr (kS) {
       if constexpr (kP) return fma(sbeta[q], po, z * dd);
       return z * dd;
+    } else if constexpr (kM) {
+      if constexpr (kP) return fma(sbeta[q], po, fma(-sax[q], dd, z));
+      return z;
     }
     return z;
   };
 
   // Register double buffering, unrolled by two (no register moves of in-flight loads,
   // which would make every prefetch wait at the end of its own iteration):
-  //   Pre.z/p: own column of plane il+1 (r up-neighbour), loaded one step earlier;
+  //   Pre.z/p(/w): own column of plane il+1 (r up-neighbour), loaded one step earlier;
   struct Pre {
-    double z[NC], p[NC], d;
+    double z[NC], p[NC], w[kM ? NC : 1], d;
   };
   const int ig0 = G.i0 + ib;
   Pre A, B;
   double udn[NC];
-#pragma unroll
+  // merged: own-column fields are u = zold, u2 = wold, u3 = pold
+  const FieldV& fP = kM ? c.u3 : c.u2;
   const double ddn = kS ? colv(c.u3, ib - 1, 0) : 1.0;
   A.d = kS ? colv(c.u3, ib + 1, 0) : 1.0;
   B.d = 1.0;
+#pragma unroll
   for (int q = 0; q < NC; ++q) {
-    udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(c.u2, ib - 1, q) : 0.0, ddn, q);
+    if constexpr (kM) {
+      udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(fP, ib - 1, q) : 0.0, kP ? colv(c.u2, ib - 1, q) : 0.0, q);
+      A.w[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
+    } else {
+      udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(fP, ib - 1, q) : 0.0, ddn, q);
+    }
     A.z[q] = colv(c.u, ib + 1, q);
-    A.p[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
+    A.p[q] = kP ? colv(fP, ib + 1, q) : 0.0;
   }
   double kdn = 0.0;
-  if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * f1tp;
-  double part[NC], part2[NC];
+  if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * cv[0];
+  constexpr int NQ = kM ? 4 : (EPI == EPI_PCG_R0 ? 2 : 1);   // partial sums per component
+  double part[NC][NQ];
 #pragma unroll
-  for (int q = 0; q < NC; ++q) part[q] = part2[q] = 0.0;
+  for (int q = 0; q < NC; ++q)
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) part[q][t] = 0.0;
   constexpr bool kR0 = (EPI == EPI_PCG_R0);
-  double* o1 = c.ea.out + coff;
-  double* o2 = ((EPI == EPI_RKL2_FIRST || EPI == EPI_PCG_S || kR0) && c.ea.out2) ? c.ea.out2 + coff : nullptr;
-  double* o3 = (kR0 && c.ea.out3) ? c.ea.out3 + coff : nullptr;
-  double* o4 = kR0 ? c.ea.out4 + coff : nullptr;
-  double* ox = (EPI == EPI_PCG_S) ? c.ea.x + coff : nullptr;
+  // outputs are addressed from the kernel parameters (constant bank) + the cell index,
+  // which keeps the pointers out of registers
+  double* const o1 = c.ea.out;
+  double* const o2 = c.ea.out2;
+  double* const o3 = c.ea.out3;
+  double* const o4 = c.ea.out4;
+  double* const ox = c.ea.x;
 
   auto body = [&](int il, const Pre& C, Pre& N) {
-    const int slot = (il - ib) % IXTS;
+    const int slot = (il - ib) % NS;
     const double* S = ring + slot * Lay::SLOT;
     const int ig = G.i0 + il;
     const bool ip = ig + 1 < G.n1g;
@@ -286,26 +354,31 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
       N.z[q] = more ? colv(c.u, il + 2, q) : 0.0;
-      N.p[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
+      N.p[q] = (kP && more) ? colv(fP, il + 2, q) : 0.0;
+      if constexpr (kM) N.w[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
     }
     if constexpr (kS) N.d = more ? colv(c.u3, il + 2, 0) : 1.0;
-    mbar_wait(full + slot, (uint32_t)(((il - ib) / IXTS) & 1));
+    mbar_wait(full + slot, (uint32_t)(((il - ib) / NS) & 1));
     double Kup = 0.0;
     if (own) {
       const double f1r = S[Lay::MT + 0], f23r = S[Lay::MT + 1], vr = S[Lay::MT + 2];
-      Kup = ip ? S[Lay::K1 + o8] * f1r * f1tp : 0.0;
-      const double Kjp = jp ? S[ok2p] * f23r * f2p : 0.0;
-      const double Kjm = jm ? S[ok2m] * f23r * f2m : 0.0;
-      const double Kkp = kp ? S[ok3p] * f23r * f3p : 0.0;
-      const double Kkm = km ? S[ok3m] * f23r * f3m : 0.0;
-      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * vtp;
-      const long long gi = (long long)il * pl;
-      double dinv = 0.0;
+      Kup = ip ? S[Lay::K1 + o8] * f1r * CV(0) : 0.0;
+      const double Kjp = jp ? S[ok2p] * f23r * CV(1) : 0.0;
+      const double Kjm = jm ? S[ok2m] * f23r * CV(2) : 0.0;
+      const double Kkp = kp ? S[ok3p] * f23r * CV(3) : 0.0;
+      const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
+      const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
+      const long long gi = (long long)il * pl + coff;
+      double dinv = 0.0, dcell = 0.0, idcell = 0.0;
       if constexpr (kR0) {
         // PC1: d = 1/A_ii, A = wV - dt L, L_ii = -(sum of the face coefficients)
         const double Ldiag = -(kdn + Kup + Kjp + Kjm + Kkp + Kkm);
         dinv = 1.0 / (WV - c.ea.dt * Ldiag);
         o4[gi] = dinv;
+      }
+      if constexpr (kM) {
+        dcell = S[Lay::EP + NC * OWN + o8];   // d of the own cell; r.z = z^2 / d
+        idcell = 1.0 / dcell;
       }
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
@@ -313,7 +386,7 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
         const double u0 = sv(S, oq, dc, q);
         const double ujm = sv(S, oq - SBW, dc - SBW, q), ujp = sv(S, oq + SBW, dc + SBW, q);
         const double ukm = sv(S, okm0 + q * okms, dkm, q), ukp = sv(S, okp0 + q * okps, dkp, q);
-        const double uup = comb(C.z[q], C.p[q], C.d, q);
+        const double uup = kM ? comb(C.z[q], C.p[q], C.w[kM ? q : 0], q) : comb(C.z[q], C.p[q], C.d, q);
         const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
         const long long go = gi + q * cs;
@@ -336,14 +409,27 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
             o1[go] = r;
             if (o2) o2[go] = u0;
             if (o3) o3[go] = z;
-            part[q] += r * z;
-            part2[q] += bb * bb * dinv;
-          } else if constexpr (EPI == EPI_PCG_S) {
+            part[q][0] += r * z;
+            part[q][1] += bb * bb * dinv;
+          } else if constexpr (kS) {
             const double y = WV * u0 - c.ea.dt * Lu;
             o1[go] = y;
             o2[go] = u0;                                          // p_k
             if constexpr (kP) ox[go] = fma(sax[q], S[oq + Lay::FS], S[Lay::EP + q * OWN + o8]);
-            part[q] += u0 * y;
+            part[q][0] += u0 * y;
+          } else if constexpr (kM) {
+            // y_k = A p_k, w_k = d y_k; z_k, p_k, w_k to the other buffers, x in place
+            const double zk = zm(S, oq, q);
+            const double y = WV * u0 - c.ea.dt * Lu;
+            const double wk = dcell * y;
+            o1[go] = zk;
+            o2[go] = u0;
+            o3[go] = wk;
+            if constexpr (kP) ox[go] = fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
+            part[q][0] += zk * zk * idcell;
+            part[q][1] += u0 * y;
+            part[q][2] += zk * y;
+            part[q][3] += wk * y;
           }
         }
         udn[q] = u0;
@@ -359,47 +445,26 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
     body(il + 1, B, A);
   }
   if (il < ie) body(il, A, B);
-  if constexpr (kR0) {
-    // partial rows 2c (r.z) and 2c+1 (b.P^-1 b), the layout of the R0 reduction
-    __shared__ double red2[2 * NC][IJ];
+  if constexpr (kR0 || kS || kM) {
+    // partial rows q*NQ + t (R0: r.z, b.P^-1 b; S: p.y; merged: r.z, p.y, z.y, w.y)
+    __shared__ double red[NC * NQ][IJ];
 #pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      double v = part[q], v2 = part2[q];
+    for (int q = 0; q < NC; ++q)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v += __shfl_xor_sync(0xffffffffu, v, o);
-        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      for (int t = 0; t < NQ; ++t) {
+        double v = part[q][t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (tk == 0) red[q * NQ + t][tj] = v;
       }
-      if (tk == 0) {
-        red2[2 * q][tj] = v;
-        red2[2 * q + 1][tj] = v2;
-      }
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory");
-    if (tid < 2 * NC) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < IJ; ++w) s += red2[tid][w];
-      c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
-    }
-  }
-  if constexpr (EPI == EPI_PCG_S) {
-    __shared__ double red[NC][IJ];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      double v = part[q];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (tk == 0) red[q][tj] = v;
-    }
     asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory");   // consumer warps only
-    if (tid < NC) {
+    if (tid < NC * NQ) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < IJ; ++w) s += red[tid][w];
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
-    if constexpr (FR) {
+    if constexpr (FR && (kS || kM)) {
       __shared__ double fred[32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
@@ -413,7 +478,8 @@ __global__ void __launch_bounds__(ITHREADS, 2) iso_tma_kernel(StencilCall c, int
 // host side
 // ============================================================================
 static bool iso_has_tma(int epi) {
-  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0;
+  return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0 ||
+         epi == EPI_PCG_M;
 }
 
 bool iso_tma_eligible(const StencilCall& c) {
@@ -423,12 +489,14 @@ bool iso_tma_eligible(const StencilCall& c) {
   if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
   if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
   if (c.epi == EPI_PCG_S && (!c.u3.p || !al16(c.u3.p))) return false;
+  if (c.epi == EPI_PCG_M && (!al16(c.u3.p) || !c.ea.dinv || !al16(c.ea.dinv) || !c.ea.x || !c.ea.out3)) return false;
   if (c.epi == EPI_PCG_R0 && (!c.ea.out4 || c.ea.sc)) return false;
   return true;
 }
 
-static dim3 iso_grid(const Geo& G, int ib, int ie, int* ic_out) {
-  const int nbx = (G.n3 + IK - 1) / IK, nby = (G.n2 + IJ - 1) / IJ;
+static dim3 iso_grid(const Geo& G, int ib, int ie, int rows, int* ic_out) {
+  const int nbx = (G.n3 + IK - 1) / IK, nby = (G.n2 + rows - 1) / rows;
+  const long long per_sm = rows > 7 ? 1 : 2;   // resident CTAs per SM (IsoLay::MINB)
   const int np = ie - ib;
   if (np <= 0) {
     *ic_out = 1;
@@ -436,14 +504,14 @@ static dim3 iso_grid(const Geo& G, int ib, int ie, int* ic_out) {
   }
   const long long tiles = (long long)nbx * nby;
   // (long marches leave a ragged last wave: cap the chunk at 128 planes)
-  const int ic = choose_chunk(tiles, np, 148LL * 2, 0.5, 4, 128);
+  const int ic = choose_chunk(tiles, np, 148LL * per_sm, 0.5, 4, 128);
   *ic_out = ic;
   return dim3(nbx, nby, (np + ic - 1) / ic);
 }
 
-int iso_tma_blocks(const Geo& G, int ib, int ie) {
+int iso_tma_blocks(const StencilCall& c) {
   int ic;
-  const dim3 g = iso_grid(G, ib, ie, &ic);
+  const dim3 g = iso_grid(c.geo, c.ib, c.ie, iso_rows(c.epi, c.ncomp), &ic);
   return (int)(g.x * g.y * g.z);
 }
 
@@ -455,18 +523,19 @@ static void launch_iso_g(const StencilCall& c, dim3 grid, int ic, const IsoTmaAr
                                   (int)IsoLay<EPI, NC>::SMEM));
     attr = true;
   }
-  iso_tma_kernel<EPI, NC, FST, FR><<<grid, ITHREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+  iso_tma_kernel<EPI, NC, FST, FR><<<grid, IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
 }
 
 template <int EPI, int NC, bool FST>
 static void launch_iso_f(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
-  if (EPI == EPI_PCG_S && c.ea.fin.ticket) launch_iso_g<EPI, NC, FST, (EPI == EPI_PCG_S)>(c, grid, ic, ta, st);
+  constexpr bool kPcg = (EPI == EPI_PCG_S || EPI == EPI_PCG_M);
+  if (kPcg && c.ea.fin.ticket) launch_iso_g<EPI, NC, FST, kPcg>(c, grid, ic, ta, st);
   else launch_iso_g<EPI, NC, FST, false>(c, grid, ic, ta, st);
 }
 
 template <int EPI, int NC>
 static void launch_iso_t(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
-  if (EPI == EPI_PCG_S && c.ea.first) launch_iso_f<EPI, NC, true>(c, grid, ic, ta, st);
+  if ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) && c.ea.first) launch_iso_f<EPI, NC, true>(c, grid, ic, ta, st);
   else launch_iso_f<EPI, NC, false>(c, grid, ic, ta, st);
 }
 
@@ -484,7 +553,8 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
   if (!iso_tma_eligible(c)) return false;
   const Geo& G = c.geo;
   int ic = 1;
-  const dim3 grid = iso_grid(G, c.ib, c.ie, &ic);
+  const int IJ = iso_rows(c.epi, c.ncomp), SBH = IJ + 2, K2H = IJ + 1, K3H = IJ;
+  const dim3 grid = iso_grid(G, c.ib, c.ie, IJ, &ic);
   if (grid.x == 0) return true;
   const int NC = c.ncomp;
   // component q of a [ncomp][nl_local][plane] array starts cpl planes after q-1; a virtual
@@ -493,8 +563,8 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
   const int npl = (NC - 1) * cpl + G.nl;
   IsoTmaArgs ta;
   memset(&ta, 0, sizeof(ta));
-  const double* srcs[2] = {c.u.p, c.u2.p ? c.u2.p : c.u.p};
-  for (int f = 0; f < 2; ++f) {
+  const double* srcs[3] = {c.u.p, c.u2.p ? c.u2.p : c.u.p, (c.epi == EPI_PCG_M && c.u3.p) ? c.u3.p : c.u.p};
+  for (int f = 0; f < 3; ++f) {
     map_plain(&ta.src[f], srcs[f], G, npl, SBW, SBH);
     map_plain(&ta.srcw[f], srcs[f], G, npl, 2, SBH);
   }
@@ -512,6 +582,9 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
     map_plain(&ta.dm, c.u3.p, G, G.nl, SBW, SBH);
     map_plain(&ta.dmw, c.u3.p, G, G.nl, 2, SBH);
+  } else if (c.epi == EPI_PCG_M) {
+    map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
+    map_plain(&ta.epi[1], c.ea.dinv, G, G.nl, IK, IJ);
   }
   switch (c.epi) {
     case EPI_F: launch_iso_nc<EPI_F>(c, grid, ic, ta, st); break;
@@ -519,6 +592,7 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_RKL2_STAGE: launch_iso_nc<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_iso_nc<EPI_PCG_S>(c, grid, ic, ta, st); break;
     case EPI_PCG_R0: launch_iso_nc<EPI_PCG_R0>(c, grid, ic, ta, st); break;
+    case EPI_PCG_M: launch_iso_nc<EPI_PCG_M>(c, grid, ic, ta, st); break;
     default: return false;
   }
   STS_CUDA(cudaGetLastError());

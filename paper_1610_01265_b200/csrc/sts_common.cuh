@@ -101,7 +101,7 @@ struct Slab {
 // halo planes of the fields the stencils read across slab boundaries.  Per slot
 // ONE allocation [2][MAXC][plane]: the lo planes (comp c at c) then the hi planes
 // (comp c at MAXC + c), so a single TMA tensor map covers both sides.
-enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_Z, H_P, H_D, H_NSLOTS };
+enum HaloSlot { H_U = 0, H_K1, H_K2, H_K3, H_B, H_AUX, H_Z, H_P, H_D, H_W, H_NSLOTS };
 
 struct Workspace {
   double* base = nullptr;
@@ -137,6 +137,7 @@ struct sts_grid {
   size_t halo_bytes = 0;
   bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
   bool graphs = true;                   // CUDA-graph replay of PCG iteration pairs (sts_grid_set_graphs)
+  bool pcg_merged = true;               // one-pass PCG iteration where eligible (sts_grid_set_pcg_merged)
   cudaStream_t graph_stream = nullptr;  // non-blocking stream for capture / replay
   cudaEvent_t ev_c = nullptr;
   // per-kernel-class event timing (sts_grid_set_timing)
@@ -171,12 +172,15 @@ enum Epi : int {
   EPI_PCG_R0,       // r = dt*L u; d = 1/(wV - dt L_ii); x = u; z = r d; p = z; partials r.z, b.b d
   EPI_PCG_AP,       // y = wV p - dt L p; partial p.y
   EPI_PCG_S,        // p = z + beta pold; x += ax pold; y = wV p - dt L p; partial p.y  (fused S-pass)
+  EPI_PCG_M,        // merged iteration: z = zold - ax wold; p = z + beta pold; x += ax pold;
+                    // y = wV p - dt L p; w = d y; partials z.z/d, p.y, z.y, w.y
 };
 
 // PCG per-component scalars (device)
 struct PcgScal {
   double rz, rz_old, pAp, alpha, beta, thresh;
-  double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update)
+  double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update;
+                    // the merged iteration also applies it to z)
   int done, iters;
 };
 
@@ -206,6 +210,7 @@ struct EpiArgs {
   double* x = nullptr;         // EPI_PCG_S: iterate, updated in place (x += ax pold)
   int first = 0;               // EPI_PCG_S: first iteration (p = z, no pold, no x update)
   FinRed fin;                  // fused final reduction (last launch of a single-process pass)
+  const double* dinv = nullptr;// EPI_PCG_M: the Jacobi inverse diagonal d (own cells)
 };
 
 struct StencilCall {
@@ -214,8 +219,9 @@ struct StencilCall {
   int epi;
   Geo geo;
   FieldV u, k1, k2, k3, b;
-  FieldV u2;                   // EPI_PCG_S: pold (u = z, or r for the isotropic S-pass)
-  FieldV u3;                   // isotropic EPI_PCG_S: the Jacobi inverse diagonal d (z = r d formed on the fly)
+  FieldV u2;                   // EPI_PCG_S: pold (u = z, or r for the isotropic S-pass); EPI_PCG_M: wold
+  FieldV u3;                   // isotropic EPI_PCG_S: the Jacobi inverse diagonal d (z = r d formed on the fly);
+                               // EPI_PCG_M: pold
   const double* w;             // [nl][plane] or nullptr
   const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][n2][n3+2] (see ev_pitch)
   EpiArgs ea;
@@ -270,7 +276,7 @@ inline int choose_chunk(long long tiles, int np, long long slots, double extra, 
 // the isotropic (ncomp <= 3) counterpart (stencil_tma_iso.cu)
 bool iso_tma_eligible(const StencilCall& c);
 bool launch_iso_tma(const StencilCall& c, cudaStream_t st);
-int iso_tma_blocks(const Geo& G, int ib, int ie);
+int iso_tma_blocks(const StencilCall& c);
 // PCG pointwise passes of the restructured iteration (aux.cu)
 // pnew = z + beta pold (pold unused if first); x += ax pold (not if first)
 void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, const double* z, const double* pold,
@@ -289,7 +295,7 @@ void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double*
                        double T_cut, double fc_r0, double fc_w, const double* x1f_d, const double* x1c_d,
                        cudaStream_t st);
 
-enum PcgPhase { PH_NONE = 0, PH_R0 = 1, PH_AP = 2, PH_RZ = 3 };
+enum PcgPhase { PH_NONE = 0, PH_R0 = 1, PH_AP = 2, PH_RZ = 3, PH_M = 4 };
 constexpr int PW_BLOCKS = 148 * 8;   // grid of the pointwise PCG kernels
 // sums[c*nq + q] = sum_b partials[(c*nq+q)*pstride + b], then the phase's scalar update
 void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, int ncomp, int nq,

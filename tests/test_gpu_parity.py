@@ -245,9 +245,12 @@ def test_rkl2_inplace_and_host_pointers(dev):
 
 
 # ---------------------------------------------------------------- A7
-@pytest.mark.parametrize("case", ["c0", "c1", "c1_cpasync", "c1_nograph", "c2", "c2_nograph"])
+@pytest.mark.parametrize("case", ["c0", "c0_twopass", "c1", "c1_cpasync", "c1_nograph", "c1_twopass", "c2",
+                                  "c2_nograph", "c2_twopass", "c2_twopass_nograph"])
 def test_be_pcg_parity(dev, case):
-    if case == "c0":
+    """BE + Jacobi-PCG vs the oracle (Fig. 1): merged one-pass iteration (default),
+    the two-pass S / U iteration, the cp.async kernels, with and without graphs."""
+    if case.startswith("c0"):
         cfg = W.make_config("c0_heat32")
         g = cfg["grid"]
         k, b, w, u, mode, ratio = cfg["faces"], None, None, cfg["u"], "iso", 50.0
@@ -266,6 +269,7 @@ def test_be_pcg_parity(dev, case):
     G = sts().Grid.from_grid(g)
     G.set_tma(case != "c1_cpasync")
     G.set_graphs(not case.endswith("nograph"))
+    G.set_pcg_merged("twopass" not in case)
     out, it = G.be_pcg_solve(mode, u.to(dev), [x.to(dev) for x in k], None if b is None else b.to(dev),
                              None if w is None else w.to(dev), dt, 1e-12, 100000)
     assert all(abs(a - c) <= 1 for a, c in zip(it, it_ref)), (it, it_ref)
@@ -347,17 +351,19 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
     tol_be = max(1e-11, rel_l2(ref_be, exact))
     k = [torch.as_tensor(x).to(dev) for x in kap]
     outs = {}
-    for tma in (True, False):
+    for tma, merged in ((True, True), (True, False), (False, False)):
         G = sts().Grid.from_grid(g, n_virtual=nv)
         G.set_tma(tma)
+        G.set_pcg_merged(merged)
         u = G.rkl2_advance("aniso", T.to(dev), k, b.to(dev), None, dt, s)
         x, it = G.be_pcg_solve("aniso", T.to(dev), k, b.to(dev), None, dt, 1e-12, 10000)
         assert rel_l2(cpu(u), ref) <= 1e-11, tma
-        assert rel_l2(cpu(x), ref_be) <= tol_be, tma
-        assert abs(it[0] - it_ref[0]) <= 1, (tma, it, it_ref)
-        outs[tma] = (cpu(u), cpu(x))
-    assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
-    assert rel_l2(outs[True][1], outs[False][1]) <= 2 * tol_be   # both within tol_be of the oracle
+        assert rel_l2(cpu(x), ref_be) <= tol_be, (tma, merged)
+        assert abs(it[0] - it_ref[0]) <= 1, (tma, merged, it, it_ref)
+        outs[(tma, merged)] = (cpu(u), cpu(x))
+    assert rel_l2(outs[(True, True)][0], outs[(False, False)][0]) <= 1e-13
+    for key in ((True, True), (True, False)):
+        assert rel_l2(outs[key][1], outs[(False, False)][1]) <= 2 * tol_be   # all within tol_be of the oracle
 
 
 ISO_CASES = [((20, 19, 70), True, 1, 3), ((13, 17, 64), False, 1, 3), ((5, 9, 2), True, 1, 2), ((9, 16, 96), True, 1, 1),
@@ -389,24 +395,27 @@ def test_iso_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv, nc):
     if nc == 1:
         vd = vd[0].contiguous()
     outs = {}
-    for tma in (True, False):
+    for tma, merged in ((True, True), (True, False), (False, False)):
         G = sts().Grid.from_grid(g, n_virtual=nv)
         G.set_tma(tma)
+        G.set_pcg_merged(merged)
         F = G.op_apply("iso", vd, kd, None, wd)
         assert rel_l2(cpu(F).reshape(v.shape), op.apply(v)) <= 1e-12, tma
         u = G.rkl2_advance("iso", vd, kd, None, wd, dt, s)
         x, it = G.be_pcg_solve("iso", vd, kd, None, wd, dt, 1e-12, 10000)
         assert rel_l2(cpu(u).reshape(v.shape), ref) <= 1e-11, tma
-        assert rel_l2(cpu(x).reshape(v.shape), ref_be) <= tol_be, tma
-        assert all(abs(a - b) <= 1 for a, b in zip(it, it_ref)), (tma, it, it_ref)
-        outs[tma] = (cpu(u), cpu(x))
-    assert rel_l2(outs[True][0], outs[False][0]) <= 1e-13
-    assert rel_l2(outs[True][1], outs[False][1]) <= 2 * tol_be   # both within tol_be of the oracle
+        assert rel_l2(cpu(x).reshape(v.shape), ref_be) <= tol_be, (tma, merged)
+        assert all(abs(a - b) <= 1 for a, b in zip(it, it_ref)), (tma, merged, it, it_ref)
+        outs[(tma, merged)] = (cpu(u), cpu(x))
+    assert rel_l2(outs[(True, True)][0], outs[(False, False)][0]) <= 1e-13
+    for key in ((True, True), (True, False)):
+        assert rel_l2(outs[key][1], outs[(False, False)][1]) <= 2 * tol_be   # all within tol_be of the oracle
 
 
+@pytest.mark.parametrize("merged", [True, False])
 @pytest.mark.parametrize("nv", [1, 3])
 @pytest.mark.parametrize("mode", ["aniso", "iso"])
-def test_pcg_graph_replay_is_bitwise_identical(dev, nv, mode):
+def test_pcg_graph_replay_is_bitwise_identical(dev, nv, mode, merged):
     """CUDA-graph replay of iteration pairs (incl. the virtual-slab fork/join of the
     halo exchange inside the graph) runs exactly the kernels of direct launches."""
     cfg = W.make_config("c1_spitzer64" if mode == "aniso" else "c2_visc64", shape=(21, 19, 70))
@@ -415,6 +424,7 @@ def test_pcg_graph_replay_is_bitwise_identical(dev, nv, mode):
     for graphs in (True, False):
         G = sts().Grid.from_grid(g, n_virtual=nv)
         G.set_graphs(graphs)
+        G.set_pcg_merged(merged)
         if mode == "aniso":
             T, b = cfg["T"].to(dev), cfg["b"].to(dev)
             k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
@@ -465,16 +475,19 @@ def test_rkl2_hybrid_parity(dev, frac, n_sub, tma):
     assert rel_l2(cpu(outv), refv) <= 1e-11
 
 
+@pytest.mark.parametrize("merged", [True, False])
 @pytest.mark.parametrize("graphs", [True, False])
-def test_communication_profile_matches_paper(dev, graphs):
+def test_communication_profile_matches_paper(dev, graphs, merged):
     """PAPER.md Sec. 2.4 / Figs. 1-2 boxed terms: an RKL2 super-step needs s neighbour
     exchanges and no global reduction; BE+PCG needs one exchange per matvec (+1 for the
-    initial residual) and global reductions every iteration -- counted on a
-    decomposed (virtual-slab) grid, graph replay included."""
+    initial residual) and global reductions every iteration -- two (Fig. 1) in the
+    two-pass iteration, one in the merged iteration -- counted on a decomposed
+    (virtual-slab) grid, graph replay included."""
     cfg = W.make_config("c1_spitzer64", shape=(21, 19, 70))
     g = cfg["grid"]
     G = sts().Grid.from_grid(g, n_virtual=3)
     G.set_graphs(graphs)
+    G.set_pcg_merged(merged)
     T, b = cfg["T"].to(dev), cfg["b"].to(dev)
     k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
     dte = G.dt_euler("aniso", k, b)
@@ -489,7 +502,7 @@ def test_communication_profile_matches_paper(dev, graphs):
     # passes (every kernel exits on the device-side done flag); those count as events
     n = (l2 - l1) - 1
     assert n >= it[0] and n - it[0] <= 64
-    assert g2 - g1 == 2 * n + 1
+    assert g2 - g1 == (1 if merged else 2) * n + 1
     G1 = sts().Grid.from_grid(g)                      # a single slab communicates nothing
     G1.rkl2_advance("aniso", T, k, b, None, 100 * dte, s)
     assert G1.comm_counts == (0, 0)

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", default="c3_spitzer256")
     ap.add_argument("--visc", action="store_true", help="add the c4 viscosity inputs")
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--twopass", action="store_true", help="two-pass S / U PCG iteration instead of merged")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     from paper_1610_01265_b200 import sts
@@ -22,6 +23,7 @@ def main():
     shape = W.CONFIGS[a.config][1]
     cfg = W.make_config(name, device=dev, shape=shape)
     G = sts.Grid.from_grid(cfg["grid"])
+    G.set_pcg_merged(not a.twopass)
     inp = {k: cfg[k] for k in ("T", "b", "rho", "visc_faces", "v", "kappa0", "T_cut") if k in cfg}
     step = bench.Step(G, inp, 300.0, dev)
     for _ in range(a.steps):
