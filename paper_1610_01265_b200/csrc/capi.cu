@@ -350,7 +350,7 @@ static double* off(double* p, const Slab& s) { return p ? p + s.off : nullptr; }
 
 // CTAs one pass over local planes [c.ib, c.ie) launches (sizes the partial-sum rows)
 static int pass_blocks(const sts_grid* g, const StencilCall& c) {
-  if (g->tma && aniso_tma_eligible(c)) return aniso_tma_blocks(c.geo, c.ib, c.ie);
+  if (g->tma && aniso_tma_eligible(c)) return aniso_tma_blocks(c);
   if (g->tma && iso_tma_eligible(c)) return iso_tma_blocks(c);
   return stencil_blocks(c.mode, c.epi, c.geo, c.ib, c.ie);
 }

@@ -73,6 +73,15 @@ struct TmaArgs {
   int has_lo, has_hi;
 };
 
+// resident CTAs per SM and ring slots of the merged PCG pass (compile-time knobs)
+#ifndef ANISO_M_MINB
+#define ANISO_M_MINB 3
+#endif
+#ifndef ANISO_M_NS
+#define ANISO_M_NS 3
+#endif
+constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : 3; }
+
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
 enum { OW_X = 0, OW_D = 1 };                 // PCG S-pass (x) / merged pass (x, d)
@@ -86,13 +95,14 @@ struct TmaLay {
   static constexpr int O = E + E_PART;
   static constexpr int MT = O + nown * O_PART;       // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  static constexpr int NS = (EPI == EPI_PCG_M) ? 3 : 4;   // (3 CTAs per SM for the larger merged slot)
+  static constexpr int NS = (EPI == EPI_PCG_M) ? ANISO_M_NS : 4;   // (the merged pass has a larger slot)
+  static constexpr int MINB = aniso_minb(EPI);
   static constexpr size_t SMEM = (size_t)(NS * SLOT + 2 * VBUF) * sizeof(double) + 2 * NS * sizeof(uint64_t) + 128;
 };
 
 // FR: this launch finishes the pass's dot-product reduction in its last CTA
 template <int EPI, bool W, bool FR>
-__global__ void __launch_bounds__(XTHREADS, 3) aniso_tma_kernel(StencilCall c, int ic,
+__global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kernel(StencilCall c, int ic,
                                                                 const __grid_constant__ TmaArgs ta) {
   using Lay = TmaLay<EPI, W>;
   constexpr int XTS = Lay::NS;
@@ -452,7 +462,7 @@ bool aniso_tma_eligible(const StencilCall& c) {
   return true;   // a slab with only a hi halo maps its slot buffer from hi - MAXC*plane
 }
 
-static dim3 tma_grid(const Geo& G, int ib, int ie, int* ic_out) {
+static dim3 tma_grid(const Geo& G, int ib, int ie, int minb, int* ic_out) {
   const int nbx = (G.n3 + XOK - 1) / XOK, nby = (G.n2 + XOJ - 1) / XOJ;
   const int np = ie - ib;
   if (np <= 0) {
@@ -460,14 +470,14 @@ static dim3 tma_grid(const Geo& G, int ib, int ie, int* ic_out) {
     return dim3(0, 0, 0);
   }
   const long long tiles = (long long)nbx * nby;
-  const int ic = choose_chunk(tiles, np, 148LL * 3, 2.0, 6);
+  const int ic = choose_chunk(tiles, np, 148LL * minb, 2.0, 6);
   *ic_out = ic;
   return dim3(nbx, nby, (np + ic - 1) / ic);
 }
 
-int aniso_tma_blocks(const Geo& G, int ib, int ie) {
+int aniso_tma_blocks(const StencilCall& c) {
   int ic;
-  const dim3 g = tma_grid(G, ib, ie, &ic);
+  const dim3 g = tma_grid(c.geo, c.ib, c.ie, aniso_minb(c.epi), &ic);
   return (int)(g.x * g.y * g.z);
 }
 
@@ -499,7 +509,7 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
   if (!aniso_tma_eligible(c)) return false;
   const Geo& G = c.geo;
   int ic = 1;
-  const dim3 grid = tma_grid(G, c.ib, c.ie, &ic);
+  const dim3 grid = tma_grid(G, c.ib, c.ie, aniso_minb(c.epi), &ic);
   if (grid.x == 0) return true;
   TmaArgs ta;
   memset(&ta, 0, sizeof(ta));

@@ -58,13 +58,17 @@ struct IsoTile {
   static constexpr int OWN = IK * IJ;               // 32 x IJ own box
 };
 
-// rows of the tile of one (epilogue, ncomp) variant (host and device)
-__host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 11 : 7; }
+// rows of the tile and resident CTAs per SM of one (epilogue, ncomp) variant (host and device)
+#ifndef ISO_M3_ROWS
+#define ISO_M3_ROWS 9
+#endif
+__host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? ISO_M3_ROWS : 7; }
+__host__ __device__ constexpr int iso_minb(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 1 : 2; }
 
 template <int EPI, int NC>
 struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   using T = IsoTile<iso_rows(EPI, NC)>;
-  static constexpr int MINB = T::IJ > 7 ? 1 : 2;   // CTAs per SM (launch bounds)
+  static constexpr int MINB = iso_minb(EPI, NC);   // CTAs per SM (launch bounds)
   // staged fields: u | PCG S-pass r, pold | merged PCG zold, wold, pold
   static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
   // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x, then d (one component)
@@ -91,8 +95,9 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int COL = (EPI == EPI_PCG_M && MINB == 2) ? 6 : 0;
   static constexpr int FIX = COL * T::INT * 8 + 128;
   // ring slots: 3 where MINB CTAs per SM fit (2 CTAs: <= 113 KB each), else 2
+  static constexpr int NS1 = (SMEM_1CTA - 2048 - FIX) / (SLOT * 8 + 16);   // one CTA per SM: all that fit
   static constexpr int NS = (MINB == 2) ? ((3 * (SLOT * 8 + 16) + FIX <= 113 * 1024) ? 3 : 2)
-                                        : ((4 * (SLOT * 8 + 16) + FIX <= SMEM_1CTA) ? 4 : 3);
+                                        : (NS1 > 6 ? 6 : NS1);
   static constexpr size_t SMEM =
       (size_t)NS * SLOT * sizeof(double) + 2 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
   static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
@@ -304,9 +309,10 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 
   // Register double buffering, unrolled by two (no register moves of in-flight loads,
   // which would make every prefetch wait at the end of its own iteration):
-  //   Pre.z/p(/w): own column of plane il+1 (r up-neighbour), loaded one step earlier;
+  //   Pre.z/p: own column of plane il+1 (r up-neighbour), loaded one step earlier
+  //   (not used by the merged PCG march, which takes it from the next slot);
   struct Pre {
-    double z[NC], p[NC], w[kM ? NC : 1], d;
+    double z[NC], p[NC], d;
   };
   const int ig0 = G.i0 + ib;
   Pre A, B;
@@ -319,13 +325,13 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     if constexpr (kM) {
+      // (the merged march takes the up neighbour from the next plane's slot, below)
       udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(fP, ib - 1, q) : 0.0, kP ? colv(c.u2, ib - 1, q) : 0.0, q);
-      A.w[q] = kP ? colv(c.u2, ib + 1, q) : 0.0;
     } else {
       udn[q] = comb(colv(c.u, ib - 1, q), kP ? colv(fP, ib - 1, q) : 0.0, ddn, q);
+      A.z[q] = colv(c.u, ib + 1, q);
+      A.p[q] = kP ? colv(fP, ib + 1, q) : 0.0;
     }
-    A.z[q] = colv(c.u, ib + 1, q);
-    A.p[q] = kP ? colv(fP, ib + 1, q) : 0.0;
   }
   double kdn = 0.0;
   if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * cv[0];
@@ -355,7 +361,6 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     for (int q = 0; q < NC; ++q) {
       N.z[q] = more ? colv(c.u, il + 2, q) : 0.0;
       N.p[q] = (kP && more) ? colv(fP, il + 2, q) : 0.0;
-      if constexpr (kM) N.w[q] = (kP && more) ? colv(c.u2, il + 2, q) : 0.0;
     }
     if constexpr (kS) N.d = more ? colv(c.u3, il + 2, 0) : 1.0;
     mbar_wait(full + slot, (uint32_t)(((il - ib) / NS) & 1));
@@ -369,16 +374,12 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
       const double WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
       const long long gi = (long long)il * pl + coff;
-      double dinv = 0.0, dcell = 0.0, idcell = 0.0;
+      double dinv = 0.0;
       if constexpr (kR0) {
         // PC1: d = 1/A_ii, A = wV - dt L, L_ii = -(sum of the face coefficients)
         const double Ldiag = -(kdn + Kup + Kjp + Kjm + Kkp + Kkm);
         dinv = 1.0 / (WV - c.ea.dt * Ldiag);
         o4[gi] = dinv;
-      }
-      if constexpr (kM) {
-        dcell = S[Lay::EP + NC * OWN + o8];   // d of the own cell; r.z = z^2 / d
-        idcell = 1.0 / dcell;
       }
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         const double u0 = sv(S, oq, dc, q);
         const double ujm = sv(S, oq - SBW, dc - SBW, q), ujp = sv(S, oq + SBW, dc + SBW, q);
         const double ukm = sv(S, okm0 + q * okms, dkm, q), ukp = sv(S, okp0 + q * okps, dkp, q);
-        const double uup = kM ? comb(C.z[q], C.p[q], C.w[kM ? q : 0], q) : comb(C.z[q], C.p[q], C.d, q);
+        const double uup = comb(C.z[q], C.p[q], C.d, q);
         const double Lu = kdn * (udn[q] - u0) + Kup * (uup - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) +
                           Kkm * (ukm - u0) + Kkp * (ukp - u0);
         const long long go = gi + q * cs;
@@ -417,19 +418,6 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
             o2[go] = u0;                                          // p_k
             if constexpr (kP) ox[go] = fma(sax[q], S[oq + Lay::FS], S[Lay::EP + q * OWN + o8]);
             part[q][0] += u0 * y;
-          } else if constexpr (kM) {
-            // y_k = A p_k, w_k = d y_k; z_k, p_k, w_k to the other buffers, x in place
-            const double zk = zm(S, oq, q);
-            const double y = WV * u0 - c.ea.dt * Lu;
-            const double wk = dcell * y;
-            o1[go] = zk;
-            o2[go] = u0;
-            o3[go] = wk;
-            if constexpr (kP) ox[go] = fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
-            part[q][0] += zk * zk * idcell;
-            part[q][1] += u0 * y;
-            part[q][2] += zk * y;
-            part[q][3] += wk * y;
           }
         }
         udn[q] = u0;
@@ -439,12 +427,109 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     if (tk == 0) mbar_arrive(empty + slot);       // this warp is done with the slot
     kdn = Kup;
   };
-  int il = ib;
-  for (; il + 1 < ie; il += 2) {
-    body(il, A, B);
-    body(il + 1, B, A);
+  if constexpr (kM) {
+    // Merged PCG march with a delayed up neighbour (no own-column loads in the loop):
+    // when plane il's slot lands, its p, z, x (and r.z) are final and stored, and its
+    // L p is complete except the r-up term; that term needs p at (il+1, own cell),
+    // which is the own cell of the NEXT slot, so y, w and the y-partials of plane il
+    // are finished one plane later.  The last plane's up neighbour comes from global
+    // memory (the neighbour slab's halo plane at a slab boundary).
+    // per-plane state carried to the next plane; two sets, unrolled by two (no moves)
+    struct St {
+      double L[NC], u[NC], z[NC];   // L p without the r-up term, p, z of the own cell
+      double WV, dc, K;              // wV, d of the own cell, r-up face coefficient
+    };
+    St SA, SB;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      SA.u[q] = udn[q];              // plane ib-1 (the down neighbour of plane ib)
+      SA.L[q] = SA.z[q] = 0.0;
+    }
+    SA.WV = SA.dc = 0.0;
+    SA.K = kdn;
+    auto finish = [&](int il, const St& P, const double* uup) {   // y-dependent outputs of plane il
+      const long long gi = (long long)il * pl + coff;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        if (skip[q]) continue;
+        const double Lu = P.L[q] + P.K * (uup[q] - P.u[q]);
+        const double y = P.WV * P.u[q] - c.ea.dt * Lu;
+        const double wk = P.dc * y;
+        o3[gi + q * cs] = wk;
+        part[q][1] += P.u[q] * y;
+        part[q][2] += P.z[q] * y;
+        part[q][3] += wk * y;
+      }
+    };
+    auto mbody = [&](int il, const St& P, St& C) {
+      const int slot = (il - ib) % NS;
+      const double* S = ring + slot * Lay::SLOT;
+      const int ig = G.i0 + il;
+      const bool ip = ig + 1 < G.n1g;
+      mbar_wait(full + slot, (uint32_t)(((il - ib) / NS) & 1));
+      C.K = 0.0;
+      if (own) {
+        const double f1r = S[Lay::MT + 0], f23r = S[Lay::MT + 1], vr = S[Lay::MT + 2];
+        C.K = ip ? S[Lay::K1 + o8] * f1r * CV(0) : 0.0;
+        const double Kjp = jp ? S[ok2p] * f23r * CV(1) : 0.0;
+        const double Kjm = jm ? S[ok2m] * f23r * CV(2) : 0.0;
+        const double Kkp = kp ? S[ok3p] * f23r * CV(3) : 0.0;
+        const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
+        C.WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
+        C.dc = S[Lay::EP + NC * OWN + o8];   // d of the own cell; r.z = z^2 / d
+        const double idcell = 1.0 / C.dc;
+        const long long gi = (long long)il * pl + coff;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          const int oq = q * S_MAIN + oc;
+          const double zk = zm(S, oq, q);
+          const double u0 = kP ? fma(sbeta[q], S[oq + 2 * Lay::FS], zk) : zk;
+          const double ujm = sv(S, oq - SBW, 0, q), ujp = sv(S, oq + SBW, 0, q);
+          const double ukm = sv(S, okm0 + q * okms, 0, q), ukp = sv(S, okp0 + q * okps, 0, q);
+          C.L[q] = P.K * (P.u[q] - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) + Kkm * (ukm - u0) + Kkp * (ukp - u0);
+          C.u[q] = u0;
+          C.z[q] = zk;
+          if (!skip[q]) {
+            const long long go = gi + q * cs;
+            o1[go] = zk;
+            o2[go] = u0;
+            if constexpr (kP) ox[go] = fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
+            part[q][0] += zk * zk * idcell;
+          }
+        }
+        if (il > ib) finish(il - 1, P, C.u);   // plane il-1's up neighbour is this plane's own cell
+      }
+      __syncwarp();
+      if (tk == 0) mbar_arrive(empty + slot);       // this warp is done with the slot
+    };
+    // the last plane: its up neighbour from global memory (the neighbour slab's halo plane)
+    auto tail = [&](const St& P) {
+      if (!own || ie <= ib) return;
+      double uup[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        uup[q] = comb(colv(c.u, ie, q), kP ? colv(fP, ie, q) : 0.0, kP ? colv(c.u2, ie, q) : 0.0, q);
+      finish(ie - 1, P, uup);
+    };
+    int il = ib;
+    for (; il + 1 < ie; il += 2) {
+      mbody(il, SA, SB);
+      mbody(il + 1, SB, SA);
+    }
+    if (il < ie) {
+      mbody(il, SA, SB);
+      tail(SB);
+    } else {
+      tail(SA);
+    }
+  } else {
+    int il = ib;
+    for (; il + 1 < ie; il += 2) {
+      body(il, A, B);
+      body(il + 1, B, A);
+    }
+    if (il < ie) body(il, A, B);
   }
-  if (il < ie) body(il, A, B);
   if constexpr (kR0 || kS || kM) {
     // partial rows q*NQ + t (R0: r.z, b.P^-1 b; S: p.y; merged: r.z, p.y, z.y, w.y)
     __shared__ double red[NC * NQ][IJ];
@@ -494,9 +579,9 @@ bool iso_tma_eligible(const StencilCall& c) {
   return true;
 }
 
-static dim3 iso_grid(const Geo& G, int ib, int ie, int rows, int* ic_out) {
+static dim3 iso_grid(const Geo& G, int ib, int ie, int rows, int minb, int* ic_out) {
   const int nbx = (G.n3 + IK - 1) / IK, nby = (G.n2 + rows - 1) / rows;
-  const long long per_sm = rows > 7 ? 1 : 2;   // resident CTAs per SM (IsoLay::MINB)
+  const long long per_sm = minb;   // resident CTAs per SM (IsoLay::MINB)
   const int np = ie - ib;
   if (np <= 0) {
     *ic_out = 1;
@@ -511,7 +596,7 @@ static dim3 iso_grid(const Geo& G, int ib, int ie, int rows, int* ic_out) {
 
 int iso_tma_blocks(const StencilCall& c) {
   int ic;
-  const dim3 g = iso_grid(c.geo, c.ib, c.ie, iso_rows(c.epi, c.ncomp), &ic);
+  const dim3 g = iso_grid(c.geo, c.ib, c.ie, iso_rows(c.epi, c.ncomp), iso_minb(c.epi, c.ncomp), &ic);
   return (int)(g.x * g.y * g.z);
 }
 
@@ -554,7 +639,7 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
   const Geo& G = c.geo;
   int ic = 1;
   const int IJ = iso_rows(c.epi, c.ncomp), SBH = IJ + 2, K2H = IJ + 1, K3H = IJ;
-  const dim3 grid = iso_grid(G, c.ib, c.ie, IJ, &ic);
+  const dim3 grid = iso_grid(G, c.ib, c.ie, IJ, iso_minb(c.epi, c.ncomp), &ic);
   if (grid.x == 0) return true;
   const int NC = c.ncomp;
   // component q of a [ncomp][nl_local][plane] array starts cpl planes after q-1; a virtual

@@ -252,7 +252,7 @@ __host__ __device__ inline long long ev_cstride(int nl, int n2, int n3) { return
 // without a TMA variant); the caller then uses launch_stencil.
 bool aniso_tma_eligible(const StencilCall& c);
 bool launch_aniso_tma(const StencilCall& c, cudaStream_t st);
-int aniso_tma_blocks(const Geo& G, int ib, int ie);
+int aniso_tma_blocks(const StencilCall& c);
 // r-chunk length of a 2.5-D march: minimises (waves of `slots` resident CTAs) x
 // (planes a CTA streams = ic + extra), i.e. wave quantisation against the planes
 // each extra chunk re-reads (extra = 2 for the vertex scheme, ~0.5 for 7-point)
