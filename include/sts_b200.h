@@ -273,7 +273,10 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
  *  the A p products each component used (may be NULL).  kmax >= 1.
  *  Returns STS_ERR_NOT_CONVERGED (un1 = last iterate) if a component hits kmax.
  *  Synchronises `stream` (the host polls the device-side convergence flags
- *  once per batch of iterations).
+ *  once per batch of iterations).  By default each iteration is one fused
+ *  stencil pass and one reduction (sts_grid_set_pcg_merged; the convergence
+ *  test uses r.z of the next iterate from the expansion of (r - alpha y).d(r -
+ *  alpha y), so the count can differ from Fig. 1's by one at a tie).
  */
 int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1,
                  const double* k1, const double* k2, const double* k3,

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           c.ea.out2[gi] = uc;
           c.ea.out3[gi] = wk;
           if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);
-          part += zc * zc / dd;
+          part += zc * zc * rcp_pos(dd);
           part2 += uc * y;
           part3 += zc * y;
           part4 += wk * y;

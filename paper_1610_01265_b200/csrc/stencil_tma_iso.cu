@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
         C.WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
         C.dc = S[Lay::EP + NC * OWN + o8];   // d of the own cell; r.z = z^2 / d
-        const double idcell = 1.0 / C.dc;
+        const double idcell = rcp_pos(C.dc);
         const long long gi = (long long)il * pl + coff;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {

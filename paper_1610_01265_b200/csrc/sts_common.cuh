@@ -158,6 +158,17 @@ __device__ __forceinline__ const double* plane_ptr(const FieldV& f, const Geo& G
   return f.p + (long long)c * G.cstride + (long long)il * G.plane;
 }
 
+// 1/x for positive normal x (the Jacobi d of a PCG solve): the hardware approximation
+// refined by two Newton steps (~1 ulp; no special-case branch, unlike 1.0 / x)
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 Geo slab_geo(const sts_grid* g, const Slab& s);
 double* ws_get(sts_grid* g, size_t bytes);  // scratch of at least `bytes`, reused across calls
 

@@ -358,7 +358,9 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
         u = G.rkl2_advance("aniso", T.to(dev), k, b.to(dev), None, dt, s)
         x, it = G.be_pcg_solve("aniso", T.to(dev), k, b.to(dev), None, dt, 1e-12, 10000)
         assert rel_l2(cpu(u), ref) <= 1e-11, tma
-        assert rel_l2(cpu(x), ref_be) <= tol_be, (tma, merged)
+        # DESIGN R12: both residual-stopped iterates lie within tol_be of the direct solve
+        assert rel_l2(cpu(x), exact) <= 2 * tol_be, (tma, merged)
+        assert rel_l2(cpu(x), ref_be) <= 2 * tol_be, (tma, merged)
         assert abs(it[0] - it_ref[0]) <= 1, (tma, merged, it, it_ref)
         outs[(tma, merged)] = (cpu(u), cpu(x))
     assert rel_l2(outs[(True, True)][0], outs[(False, False)][0]) <= 1e-13
@@ -404,7 +406,9 @@ def test_iso_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv, nc):
         u = G.rkl2_advance("iso", vd, kd, None, wd, dt, s)
         x, it = G.be_pcg_solve("iso", vd, kd, None, wd, dt, 1e-12, 10000)
         assert rel_l2(cpu(u).reshape(v.shape), ref) <= 1e-11, tma
-        assert rel_l2(cpu(x).reshape(v.shape), ref_be) <= tol_be, (tma, merged)
+        # DESIGN R12: both residual-stopped iterates lie within tol_be of the direct solve
+        assert rel_l2(cpu(x).reshape(v.shape), exact) <= 2 * tol_be, (tma, merged)
+        assert rel_l2(cpu(x).reshape(v.shape), ref_be) <= 2 * tol_be, (tma, merged)
         assert all(abs(a - b) <= 1 for a, b in zip(it, it_ref)), (tma, merged, it, it_ref)
         outs[(tma, merged)] = (cpu(u), cpu(x))
     assert rel_l2(outs[(True, True)][0], outs[(False, False)][0]) <= 1e-13
