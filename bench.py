@@ -90,7 +90,8 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         # merged iteration (one pass): zold, wold, pold, x (+ e, d) in; z, p, w, x out
         # (first: z0 (+ e, d) in; z, p, w out); R0 of the merged path also writes z0
         "aniso_pcg_m": (8 + 24 + 8 + 24) if first else (32 + 24 + 8 + 32),
-        "iso_pcg_m": (32 * c + 40) if first else (64 * c + 40),
+        # (the isotropic pass recomputes d from the staged face coefficients)
+        "iso_pcg_m": (32 * c + 32) if first else (64 * c + 32),
         "iso_pcg_r0_m": 8 * c + 32 + 24 * c + 8,
     }
     return table[kind]

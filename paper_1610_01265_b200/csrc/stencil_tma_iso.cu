@@ -71,9 +71,10 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int MINB = iso_minb(EPI, NC);   // CTAs per SM (launch bounds)
   // staged fields: u | PCG S-pass r, pold | merged PCG zold, wold, pold
   static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
-  // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x, then d (one component)
+  // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x (d is recomputed from
+  // the staged face coefficients: A_ii = wV - dt L_ii, d = 1 / A_ii as in the R0 pass)
   static constexpr int nepi =
-      (EPI == EPI_RKL2_STAGE) ? 3 * NC : (EPI == EPI_PCG_S ? NC : (EPI == EPI_PCG_M ? NC + 1 : 0));
+      (EPI == EPI_RKL2_STAGE) ? 3 * NC : ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) ? NC : 0);
   // one block per staged field: NC main boxes, then the NC x 2 wrap boxes, so a
   // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
   static constexpr int WRP = NC * T::S_MAIN;                          // wrap boxes within a field block
@@ -476,8 +477,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         const double Kkp = kp ? S[ok3p] * f23r * CV(3) : 0.0;
         const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
         C.WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
-        C.dc = S[Lay::EP + NC * OWN + o8];   // d of the own cell; r.z = z^2 / d
-        const double idcell = rcp_pos(C.dc);
+        // PC1 diagonal of the own cell, the R0 pass's arithmetic (bit-identical d):
+        // A_ii = wV - dt L_ii, L_ii = -(sum of the six face coefficients); r.z = z^2 A_ii
+        const double Aii = C.WV - c.ea.dt * -(P.K + C.K + Kjp + Kjm + Kkp + Kkm);
+        C.dc = 1.0 / Aii;
+        const double idcell = Aii;
         const long long gi = (long long)il * pl + coff;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
@@ -574,7 +578,7 @@ bool iso_tma_eligible(const StencilCall& c) {
   if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
   if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
   if (c.epi == EPI_PCG_S && (!c.u3.p || !al16(c.u3.p))) return false;
-  if (c.epi == EPI_PCG_M && (!al16(c.u3.p) || !c.ea.dinv || !al16(c.ea.dinv) || !c.ea.x || !c.ea.out3)) return false;
+  if (c.epi == EPI_PCG_M && (!al16(c.u3.p) || !c.ea.x || !c.ea.out3)) return false;
   if (c.epi == EPI_PCG_R0 && (!c.ea.out4 || c.ea.sc)) return false;
   return true;
 }
@@ -669,7 +673,6 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     map_plain(&ta.dmw, c.u3.p, G, G.nl, 2, SBH);
   } else if (c.epi == EPI_PCG_M) {
     map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
-    map_plain(&ta.epi[1], c.ea.dinv, G, G.nl, IK, IJ);
   }
   switch (c.epi) {
     case EPI_F: launch_iso_nc<EPI_F>(c, grid, ic, ta, st); break;
