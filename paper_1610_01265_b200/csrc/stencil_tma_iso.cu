@@ -48,7 +48,6 @@ template <int IJ_>
 struct IsoTile {
   static constexpr int IJ = IJ_;
   static constexpr int INT = IJ * IK;               // consumer threads
-  static constexpr int THREADS = INT + 32;          // + producer warp
   static constexpr int SBH = IJ + 2;                // staged source box rows
   static constexpr int S_MAIN = rnd16(SBW * SBH);   // 7 rows: 324 -> 336
   static constexpr int S_W = rnd16(2 * SBH);        // 2 x SBH wrap box
@@ -69,6 +68,12 @@ template <int EPI, int NC>
 struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   using T = IsoTile<iso_rows(EPI, NC)>;
   static constexpr int MINB = iso_minb(EPI, NC);   // CTAs per SM (launch bounds)
+  // merged PCG, one CTA per SM: a "former" warp turns each landed slot's zold, wold,
+  // pold into z_k = zold - alpha wold (field 0) and p_k = z_k + beta pold (field 1)
+  // once per staged position, instead of every consumer re-forming its 5-point
+  // neighbourhood; consumers wait on a per-slot "formed" mbarrier
+  static constexpr bool FORM = (EPI == EPI_PCG_M) && MINB == 1;
+  static constexpr int THREADS = T::INT + 32 + (FORM ? 32 : 0);
   // staged fields: u | PCG S-pass r, pold | merged PCG zold, wold, pold
   static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
   // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x (d is recomputed from
@@ -100,7 +105,7 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int NS = (MINB == 2) ? ((3 * (SLOT * 8 + 16) + FIX <= 113 * 1024) ? 3 : 2)
                                         : (NS1 > 6 ? 6 : NS1);
   static constexpr size_t SMEM =
-      (size_t)NS * SLOT * sizeof(double) + 2 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
+      (size_t)NS * SLOT * sizeof(double) + 3 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
   static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
 };
 
@@ -133,6 +138,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   double* ring = smi;
   uint64_t* full = reinterpret_cast<uint64_t*>(smi + NS * Lay::SLOT);
   uint64_t* empty = full + NS;
+  uint64_t* formed = empty + NS;     // (merged PCG with a former warp)
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
@@ -163,12 +169,39 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, IJ);
+      mbar_init(formed + s, 1);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
   // ======================= producer warp =======================
+  constexpr bool kF = Lay::FORM && kP;   // consumers read formed z_k / p_k
+  // ======================= former warp (merged PCG) =======================
+  if (Lay::FORM && tid >= INT + 32) {
+    const int lane = tid & 31;
+    for (int p = ib; p < ie; ++p) {
+      const int slot = (p - ib) % NS;
+      mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
+      if constexpr (kF) {
+        double* S = ring + slot * Lay::SLOT;
+        auto form = [&](int o, int q) {
+          const double z = fma(-sax[q], S[o + Lay::FS], S[o]);
+          S[o] = z;
+          S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
+        };
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          for (int o = lane; o < SBW * SBH; o += 32) form(q * S_MAIN + o, q);
+          if (wrapL || wrapR)
+            for (int o = lane; o < 2 * S_W; o += 32) form(Lay::WRP + q * 2 * S_W + o, q);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(formed + slot);   // release: the formed fields to the consumers
+    }
+    return;
+  }
   if (tid >= INT) {
     if (tid != INT) return;
     constexpr int nsrcf_now = ((kS || kM) && FST) ? 1 : Lay::nsrcf;
@@ -241,7 +274,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     cv[4] = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
     cv[5] = M.Vt[j] * M.Vp[k];
   }
-  double* const colc = reinterpret_cast<double*>(empty + NS);
+  double* const colc = reinterpret_cast<double*>(formed + NS);
   if constexpr (Lay::COL > 0) {
 #pragma unroll
     for (int t = 0; t < 6; ++t) colc[t * INT + tid] = cv[t];   // read back by this thread only
@@ -269,7 +302,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   const int dkp = kpw_box ? Lay::DB + S_MAIN + 1 * S_W + (tj + 1) * 2 : dc + 1;
   // merged PCG: z_k at a staged position (field 0 zold, field 1 wold)
   auto zm = [&](const double* S, int o, int q) {
-    if constexpr (kP) return fma(-sax[q], S[o + Lay::FS], S[o]);
+    if constexpr (kP && !kF) return fma(-sax[q], S[o + Lay::FS], S[o]);
     return S[o];
   };
   // source value at (field-0 offset o, d offset od): PCG S-pass p = r d + beta pold
@@ -280,6 +313,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       if constexpr (kP) return fma(sbeta[q], S[o + Lay::FS], z);
       return z;
     } else if constexpr (kM) {
+      if constexpr (kF) return S[o + Lay::FS];
       if constexpr (kP) return fma(sbeta[q], S[o + 2 * Lay::FS], zm(S, o, q));
       return S[o];
     }
@@ -467,7 +501,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       const double* S = ring + slot * Lay::SLOT;
       const int ig = G.i0 + il;
       const bool ip = ig + 1 < G.n1g;
-      mbar_wait(full + slot, (uint32_t)(((il - ib) / NS) & 1));
+      mbar_wait((Lay::FORM ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
       C.K = 0.0;
       if (own) {
         const double f1r = S[Lay::MT + 0], f23r = S[Lay::MT + 1], vr = S[Lay::MT + 2];
@@ -487,7 +521,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         for (int q = 0; q < NC; ++q) {
           const int oq = q * S_MAIN + oc;
           const double zk = zm(S, oq, q);
-          const double u0 = kP ? fma(sbeta[q], S[oq + 2 * Lay::FS], zk) : zk;
+          const double u0 = kF ? S[oq + Lay::FS] : (kP ? fma(sbeta[q], S[oq + 2 * Lay::FS], zk) : zk);
           const double ujm = sv(S, oq - SBW, 0, q), ujp = sv(S, oq + SBW, 0, q);
           const double ukm = sv(S, okm0 + q * okms, 0, q), ukp = sv(S, okp0 + q * okps, 0, q);
           C.L[q] = P.K * (P.u[q] - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) + Kkm * (ukm - u0) + Kkp * (ukp - u0);
