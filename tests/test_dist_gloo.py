@@ -163,6 +163,91 @@ def test_distributed_pcg_matches_single_domain(aniso):
 
 
 # ----------------------------------------------------------------------------
+def _dist_pcg_merged(rank, world, aniso):
+    """The library's default merged iteration on r-slabs: per iteration ONE halo
+    exchange of z, w, p (their boundary planes) and ONE all-reduce of the four
+    partial sums r.z, p.y, z.y, w.y per rank."""
+    import workloads as W
+    from oracle import core as O
+    shape = (12, 9, 14)
+    g = W.spherical_grid(*shape)
+    cfg = W.make_config("c1_spitzer64", shape=shape)
+    T = cfg["T"].numpy()
+    kap = O.spitzer_face_kappa(g, T, cfg["kappa0"], cfg["T_cut"])
+    op = O.Operator(g, kap, cfg["b"].numpy() if aniso else None)
+    dt = 50.0 * O.dt_euler(op)
+    A = O.be_system(op, dt).tocsr()
+    rhs = op.WV * T.ravel()
+    n1, n2, n3 = shape
+    plane = n2 * n3
+    i0, nl = W.split_planes(n1, world)[rank]
+    rows = slice(i0 * plane, (i0 + nl) * plane)
+    ext = np.arange((i0 - 1) * plane, (i0 + nl + 1) * plane)
+    valid = (ext >= 0) & (ext < n1 * plane)
+    A_ext = A[rows][:, ext[valid]]
+    d = 1.0 / A.diagonal()[rows]
+    n_allreduce = 0
+
+    def halo(v):
+        return _exchange(torch.as_tensor(v), nl, plane, rank, world).numpy()[valid]
+
+    def allreduce(vals):
+        nonlocal n_allreduce
+        n_allreduce += 1
+        t = torch.tensor(vals, dtype=torch.float64)
+        dist.all_reduce(t)
+        return t.tolist()
+
+    b = rhs[rows]
+    x = T.ravel()[rows].copy()
+    z = (b - A_ext @ halo(x)) * d
+    thresh = 1e-24 * allreduce([float(b @ (b * d))])[0]
+    rz0 = allreduce([float(np.sum(z * z / d))])[0]
+    k = 0
+    if rz0 > thresh:
+        w = p = None
+        alpha = beta = 0.0
+        while k < 10000:
+            k += 1
+            if k > 1:
+                # the pass forms z_k and p_k at every staged position (own + halo planes):
+                # exchanging z, w, p of the previous iteration is all it needs
+                zh, wh, ph = halo(z), halo(w), halo(p)
+                z = z - alpha * w
+                x = x + alpha * p
+                p = z + beta * p
+                pe = zh - alpha * wh
+                pe = pe + beta * ph
+            else:
+                p = z.copy()
+                pe = halo(p)
+            y = A_ext @ pe
+            w = d * y
+            rz, pAp, zy, wy = allreduce([float(np.sum(z * z / d)), float(p @ y), float(z @ y), float(w @ y)])
+            alpha = rz / pAp
+            rz_next = rz - 2.0 * alpha * zy + alpha * alpha * wy
+            if rz_next <= thresh:
+                x = x + alpha * p
+                break
+            beta = rz_next / rz
+    ref, it = O.be_pcg_solve(op, T, dt, rtol=1e-12)
+    assert abs(k - it[0]) <= 1, (k, it)
+    assert n_allreduce == k + 2          # one per iteration (+ the two of the initial residual)
+    xs = [None] * world
+    dist.all_gather_object(xs, x)
+    xg = np.concatenate(xs)
+    import scipy.sparse.linalg as spl
+    exact = spl.spsolve(A.tocsc(), rhs)
+    tol = max(1e-11, np.linalg.norm(ref.ravel() - exact) / np.linalg.norm(exact))
+    assert np.linalg.norm(xg - ref.ravel()) <= 2 * tol * np.linalg.norm(ref)   # DESIGN R12
+
+
+@pytest.mark.parametrize("aniso", [True, False])
+def test_distributed_merged_pcg_matches_single_domain(aniso):
+    _run(_dist_pcg_merged, 2, aniso)
+
+
+# ----------------------------------------------------------------------------
 def _bench_helpers(rank, world):
     import bench
     dev = torch.device("cpu")
