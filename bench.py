@@ -265,24 +265,35 @@ class Step:
 
 class E2EStep:
     """The same step end to end from pinned HOST memory, as a user with host arrays
-    runs it through the public API: every step uploads that step's inputs once
-    (on a copy stream: the viscosity inputs travel while conduction computes),
-    runs the library on the device copies, and reads every result back into
-    pinned host buffers (the conduction results while viscosity computes)."""
+    runs it through the public API: every step uploads that step's inputs once and
+    reads every result back into pinned host buffers; the library runs on the device
+    copies.  Copies overlap computation: H2D and D2H run on their own streams (PCIe
+    is full duplex), the viscosity inputs travel while conduction computes, each
+    result travels back as soon as it exists, and -- across consecutive steps -- the
+    NEXT step's conduction inputs travel (into the second of two input buffer sets)
+    while this step's viscosity computes.  Only the first step of a run uploads its
+    conduction inputs exposed and only the last one's final result download is
+    exposed; `start()` begins a run (no input of the run is ever uploaded before the
+    run's timed region), `__call__(prefetch)` runs one step."""
 
     IN_KEYS = ("T", "b", "rho", "v")
+    COND_KEYS = ("T", "b")
+    VISC_KEYS = ("rho", "v")
 
     def __init__(self, G, host_inp, ratio, dev):
         self.host = host_inp
-        dinp = dict(host_inp)
-        for key in self.IN_KEYS:
-            if key in host_inp:
-                dinp[key] = torch.empty_like(host_inp[key], device=dev)
-        if "visc_faces" in host_inp:
-            dinp["visc_faces"] = tuple(torch.empty_like(x, device=dev) for x in host_inp["visc_faces"])
-        self.step = Step(G, dinp, ratio, dev)
-        self.dinp = dinp
-        self.copy = torch.cuda.Stream(dev)
+        self.sets = []
+        for _ in range(2):
+            dinp = dict(host_inp)
+            for key in self.IN_KEYS:
+                if key in host_inp:
+                    dinp[key] = torch.empty_like(host_inp[key], device=dev)
+            if "visc_faces" in host_inp:
+                dinp["visc_faces"] = tuple(torch.empty_like(x, device=dev) for x in host_inp["visc_faces"])
+            self.sets.append(dinp)
+        self.step = Step(G, self.sets[0], ratio, dev)
+        self.h2d_s = torch.cuda.Stream(dev)
+        self.d2h_s = torch.cuda.Stream(dev)
         pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
         st = self.step
         self.out_host = {"T_rk": pin(st.T_rk), "T_be": pin(st.T_be), "v_rk": pin(st.v_rk), "v_be": pin(st.v_be)}
@@ -290,37 +301,70 @@ class E2EStep:
         self.h2d = sum(nb(host_inp[k]) for k in self.IN_KEYS if k in host_inp) + \
             sum(nb(x) for x in host_inp.get("visc_faces", ()))
         self.d2h = sum(nb(t) for t in self.out_host.values())
+        self.ev_d2h = {}          # output name -> event after its last download
+        self.ev_used = [None, None]   # input set -> event after its last use (viscosity done)
+        self.ev_cond_in = [None, None]
+        self.n = 0
+
+    def start(self):
+        self.n = 0
+        self.ev_cond_in = [None, None]
+
+    def _h2d(self, keys, faces, s, wait_ev):
+        H, D = self.host, self.sets[s]
+        with torch.cuda.stream(self.h2d_s):
+            if wait_ev is not None:
+                self.h2d_s.wait_event(wait_ev)
+            for key in keys:
+                if key in H:
+                    D[key].copy_(H[key], non_blocking=True)
+            if faces and "visc_faces" in H:
+                for d, h in zip(D["visc_faces"], H["visc_faces"]):
+                    d.copy_(h, non_blocking=True)
+            return self.h2d_s.record_event()
 
     def _d2h(self, names, cs):
         ev = cs.record_event()
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(ev)
+        with torch.cuda.stream(self.d2h_s):
+            self.d2h_s.wait_event(ev)
             for n in names:
                 self.out_host[n].copy_(getattr(self.step, n), non_blocking=True)
+                self.ev_d2h[n] = self.d2h_s.record_event()
 
-    def __call__(self):
-        H, D, st = self.host, self.dinp, self.step
+    def _wait_out(self, cs, names):
+        for n in names:
+            if n in self.ev_d2h:
+                cs.wait_event(self.ev_d2h[n])
+
+    def __call__(self, prefetch=True):
+        st = self.step
         cs = torch.cuda.current_stream()
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_stream(cs)
-            for key in ("T", "b"):
-                D[key].copy_(H[key], non_blocking=True)
-            ev_cond = self.copy.record_event()
-            for key in ("rho", "v"):
-                D[key].copy_(H[key], non_blocking=True)
-            for d, h in zip(D["visc_faces"], H["visc_faces"]):
-                d.copy_(h, non_blocking=True)
-            ev_visc = self.copy.record_event()
-        cs.wait_event(ev_cond)
-        # every result travels back as soon as it exists, behind the next computation
+        s = self.n % 2
+        st.inp = self.sets[s]
+        if self.ev_cond_in[s] is None:            # first step of the run: its own upload
+            self.ev_cond_in[s] = self._h2d(self.COND_KEYS, False, s, self.ev_used[s])
+        ev_visc_in = self._h2d(self.VISC_KEYS, True, s, self.ev_used[s])
+        cs.wait_event(self.ev_cond_in[s])
+        self._wait_out(cs, ("T_rk", "T_be"))       # (the previous step's downloads of these)
         s_c, it_c = st.cond(after_rkl2=lambda: self._d2h(("T_rk",), cs))
         self._d2h(("T_be",), cs)
-        cs.wait_event(ev_visc)
+        self.ev_cond_in[s] = None
+        if prefetch:                              # the next step's conduction inputs, other set
+            o = 1 - s
+            self.ev_cond_in[o] = self._h2d(self.COND_KEYS, False, o, self.ev_used[o])
+        cs.wait_event(ev_visc_in)
+        self._wait_out(cs, ("v_rk", "v_be"))
         s_v, it_v = st.visc(after_rkl2=lambda: self._d2h(("v_rk",), cs))
+        self.ev_used[s] = cs.record_event()
         self._d2h(("v_be",), cs)
-        cs.wait_stream(self.copy)
+        self.n += 1
         return {"s_cond": s_c, "it_cond": it_c, "s_visc": s_v, "it_visc": it_v,
                 "units": s_c + it_c + s_v + max(it_v)}
+
+    def finish(self, cs):
+        """Make `cs` wait for every outstanding download (the end of the timed region)."""
+        cs.wait_stream(self.d2h_s)
+        cs.wait_stream(self.h2d_s)
 
 
 def dist_info():
@@ -447,7 +491,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4_scale512", choices=list(RATIO))
     ap.add_argument("--impl", default="sts", choices=["sts", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3,
+                    help="end-to-end steps from pinned host memory (pipelined across steps)")
     ap.add_argument("--timing-steps", type=int, default=2,
                     help="instrumented steps (after the timed region) for the per-kernel breakdown")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -572,14 +617,20 @@ def main():
         for key in ("T", "b", "rho", "v"):
             host_inp[key] = inp[key].cpu().pin_memory()
         host_inp["visc_faces"] = tuple(x.cpu().pin_memory() for x in inp["visc_faces"])
+        inp.clear()            # (the device inputs of the device-timed leg: the e2e leg has its own)
+        torch.cuda.empty_cache()
         hstep = E2EStep(G, host_inp, ratio, dev)
-        hstep()  # warm-up
+        hstep.start()
+        hstep(prefetch=False)  # warm-up
+        hstep.finish(stream)
         barrier(ws, dev)
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        hinfos = [hstep() for _ in range(args.e2e_steps)]
+        hstep.start()
+        hinfos = [hstep(prefetch=i + 1 < args.e2e_steps) for i in range(args.e2e_steps)]
+        hstep.finish(stream)
         t1.record(stream)
         torch.cuda.synchronize()
         barrier(ws, dev)

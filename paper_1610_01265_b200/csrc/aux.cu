@@ -412,4 +412,16 @@ void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal
   STS_CUDA(cudaGetLastError());
 }
 
+// small device results to mapped pinned host memory by SM stores: the host reads
+// them after a stream sync without a DMA copy, which would queue behind large
+// transfers a caller runs on the copy engines (e.g. the previous result's download)
+__global__ void publish_kernel(const double* __restrict__ src, int n, double* dst) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void launch_publish(const double* src, int n, double* dst_mapped, cudaStream_t st) {
+  publish_kernel<<<1, 32, 0, st>>>(src, n, dst_mapped);
+  STS_CUDA(cudaGetLastError());
+}
+
 }  // namespace sts

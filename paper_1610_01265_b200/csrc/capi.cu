@@ -680,7 +680,8 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const doub
         sl.has_hi = sl.i0 + sl.nl < n1;
         g->slabs.push_back(sl);
       }
-      STS_CUDA(cudaMallocHost(&g->h_pinned, 4096));
+      STS_CUDA(cudaHostAlloc(&g->h_pinned, 4096, cudaHostAllocMapped));
+      STS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->d_pinned), g->h_pinned, 0));
       STS_CUDA(cudaMalloc(&g->d_ticket, 64 * sizeof(unsigned int)));
       STS_CUDA(cudaMemset(g->d_ticket, 0, 64 * sizeof(unsigned int)));
     } catch (...) {
@@ -914,7 +915,7 @@ int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, cons
       launch_gershgorin(c, dmax, st);
     }
     if (g->comm) STS_NCCL(ncclAllReduce(g->d_red, g->d_red, 1, ncclDouble, ncclMax, g->comm, st));
-    STS_CUDA(cudaMemcpyAsync(g->h_pinned, g->d_red, sizeof(double), cudaMemcpyDeviceToHost, st));
+    launch_publish(g->d_red, 1, g->d_pinned, st);
     STS_CUDA(cudaStreamSynchronize(st));
     const double lam = g->h_pinned[0];
     *dt_out = lam > 0.0 ? 2.0 / lam : std::numeric_limits<double>::infinity();
@@ -1318,7 +1319,8 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     bool all_done = false;
     try {
       while (true) {
-        STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, is));
+        launch_publish(reinterpret_cast<const double*>(sc), (int)(sizeof(PcgScal) * ncomp / sizeof(double)),
+                       g->d_pinned, is);
         STS_CUDA(cudaStreamSynchronize(is));
         all_done = true;
         for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
@@ -1372,7 +1374,8 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       Timed t(g, STS_K_PCG_XFINAL, st);
       launch_pcg_xfinal(ncomp, (long long)N, cs, x, pb[0], pb[1], sc, st);
     }
-    STS_CUDA(cudaMemcpyAsync(hsc, sc, sizeof(PcgScal) * ncomp, cudaMemcpyDeviceToHost, st));
+    launch_publish(reinterpret_cast<const double*>(sc), (int)(sizeof(PcgScal) * ncomp / sizeof(double)),
+                   g->d_pinned, st);
     STS_CUDA(cudaStreamSynchronize(st));
     if (iters_out)
       for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;

@@ -126,7 +126,8 @@ struct sts_grid {
   double* d_red = nullptr;              // reduction partials + scalars
   size_t red_bytes = 0;
   unsigned int* d_ticket = nullptr;     // last-block tickets
-  double* h_pinned = nullptr;           // small pinned host mailbox
+  double* h_pinned = nullptr;           // small pinned, device-mapped host mailbox
+  double* d_pinned = nullptr;           // its device alias (written by launch_publish)
   // multi-GPU
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -194,6 +195,7 @@ struct PcgScal {
                     // the merged iteration also applies it to z)
   int done, iters;
 };
+static_assert(sizeof(PcgScal) % sizeof(double) == 0, "PcgScal is published as doubles");
 
 // fused final reduction of a PCG pass (pcg.cuh: fused_final_reduce)
 struct FinRed {
@@ -313,5 +315,7 @@ void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, i
                        double* sums, int phase, PcgScal* sc, double rtol2, cudaStream_t st);
 void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal* sc, double rtol2,
                        cudaStream_t st);
+// copy n doubles to mapped pinned host memory with SM stores (no copy engine)
+void launch_publish(const double* src, int n, double* dst_mapped, cudaStream_t st);
 
 }  // namespace sts
