@@ -258,30 +258,34 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
     zn = zk11;    // its z (merged PCG)
   };
 
-  double SuL = 0, TuL = 0, FuL = 0;
-  double SAl = 0, DBl = 0, DCl = 0;
-  double uc = 0.0, poc = 0.0, zc = 0.0;   // own-cell source value (pold, z) of the previous plane
   double part = 0.0, part2 = 0.0, part3 = 0.0, part4 = 0.0;
   constexpr bool kR0 = (EPI == EPI_PCG_R0);
+  // state of one cell plane carried to the next: the 2x2 sums of the source, the
+  // vertex-pair sums of the vertex plane below it, the own cell's source value (pold,
+  // z), and (R0) the L_ii part of the 4 vertices above it.  Two sets, alternated by
+  // an unroll by two, so no register moves between planes.
   // R0: L_ii = -sum over the cell's 8 vertices of W^2, W = the cell's weight in q_v =
-  // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex);
-  // the 4 vertices of the plane below are summed one step earlier (ldlo)
-  double ldlo = 0.0;
-  for (int p = ib - 1; p <= ie; ++p) {
+  // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex)
+  struct St {
+    double Su, Tu, Fu, SA, DB, DC, u, po, z, ld;
+  };
+  St SX = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, SY = SX;
+  // plane p: Q(p) landed; L = state of cell plane p-1, H receives cell plane p's
+  auto body = [&](int p, const St& L, St& H) {
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
     mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
-    double SuH, TuH, FuH, un, pon, zn;
-    usums(S, SuH, TuH, FuH, un, pon, zn);
+    usums(S, H.Su, H.Tu, H.Fu, H.u, H.po, H.z);
     double* vb = vbuf + (p & 1) * VBUF;
+    H.SA = H.DB = H.DC = H.ld = 0.0;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
       const double* E = S + Lay::E;
       const int ei = vj * EBW + vk + se;
       const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
-      const double q = er * (SuH - SuL) + et * (ig2l * TuL + ig2h * TuH) + ep * (ig2l * FuL + ig2h * FuH);
-      double ldhi = 0.0, ldnext = 0.0;
+      const double q = er * (H.Su - L.Su) + et * (ig2l * L.Tu + ig2h * H.Tu) + ep * (ig2l * L.Fu + ig2h * H.Fu);
+      double ldhi = 0.0;
       if constexpr (kR0) {
         if (own) {
           // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
             const double wl = -r_ + st4[t] * t_ * ig2l + sp4[t] * p_ * ig2l * ig3c;
             const double wh = r_ + st4[t] * t_ * ig2h + sp4[t] * p_ * ig2h * ig3c;
             ldhi += wl * wl;
-            ldnext += wh * wh;
+            H.ld += wh * wh;
           }
         }
       }
@@ -310,20 +314,20 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       vb[2 * XNT + tid] = dC;
       // consumer warps only: the vertex plane is complete
       asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
-      double SAh = 0, DBh = 0, DCh = 0;
       if (own) {
-        SAh = hA + vb[tid + 32];
-        DBh = hB - vb[XNT + tid + 32];
-        DCh = dC + vb[2 * XNT + tid + 32];
+        H.SA = hA + vb[tid + 32];
+        H.DB = hB - vb[XNT + tid + 32];
+        H.DC = dC + vb[2 * XNT + tid + 32];
       }
       if (p >= ib + 1 && own) {
-        // output cell plane il = p-1
+        // output cell plane il = p-1 (its own values are L's)
         const int il = p - 1;
         const double* O = S + Lay::O + vj * XK + vk + se;
         const double ig2c = S[Lay::MT + 0];                   // iG2 of plane p-1
-        const double Lu = -((SAl - SAh) + ig2c * (DBl + DBh) + ig2c * ig3c * (DCl + DCh));
+        const double Lu = -((L.SA - H.SA) + ig2c * (L.DB + H.DB) + ig2c * ig3c * (L.DC + H.DC));
         const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * S[Lay::MT + 2] * vtpc;
         const long long gi = (long long)il * G.plane + coff;
+        const double uc = L.u, poc = L.po, zc = L.z;
         if constexpr (EPI == EPI_F) {
           c.ea.out[gi] = Lu / WV;
         } else if constexpr (EPI == EPI_RKL2_FIRST) {
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
                          c.ea.c1 * O[OW_M0 * O_PART];
         } else if constexpr (kR0) {
           // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
-          const double Ld = -(ldlo + ldhi);
+          const double Ld = -(L.ld + ldhi);
           const double r = c.ea.dt * Lu;
           const double dinv = 1.0 / (WV - c.ea.dt * Ld);
           const double z = r * dinv;
@@ -369,20 +373,16 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           part4 += wk * y;
         }
       }
-      SAl = SAh;
-      DBl = DBh;
-      DCl = DCh;
-      ldlo = ldnext;
     }
     __syncwarp();
     if (vk == 0) mbar_arrive(empty + slot);   // this warp is done with the slot of Q(p)
-    SuL = SuH;
-    TuL = TuH;
-    FuL = FuH;
-    uc = un;
-    poc = pon;
-    zc = zn;
+  };
+  int p = ib - 1;
+  for (; p + 1 <= ie; p += 2) {
+    body(p, SX, SY);
+    body(p + 1, SY, SX);
   }
+  if (p <= ie) body(p, SX, SY);
   if constexpr (kR0) {
     __shared__ double red2[2][XNT / 32];
     double v = part, v2 = part2;
