@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) pcg_rupdate_kernel(long long n, long long
     partials[threadIdx.x * pstride + blockIdx.x] = s;
   }
   if (fin.ticket) {
-    __shared__ double fred[32];
+    __shared__ double fred[4 * MAXC * 32];
     __shared__ unsigned flag;
     fused_final_reduce(fin, partials, pstride, gridDim.x, threadIdx.x, blockDim.x, fred, &flag,
                        [] { __syncthreads(); });
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long 
     partials[threadIdx.x * pstride + blockIdx.x] = s;
   }
   if (fin.ticket) {
-    __shared__ double fred[32];
+    __shared__ double fred[4 * MAXC * 32];
     __shared__ unsigned flag;
     fused_final_reduce(fin, partials, pstride, gridDim.x, threadIdx.x, blockDim.x, fred, &flag,
                        [] { __syncthreads(); });
@@ -400,9 +400,67 @@ __global__ void pcg_scalar_kernel(const double* sums, int ncomp, int nq, int pha
   if (threadIdx.x < ncomp) pcg_phase(sums, threadIdx.x, nq, phase, sc, rtol2);
 }
 
+// Two-level deterministic reduction for large passes: block b sums slice b of every
+// row (all rows' loads in flight at once) into l2[row][b]; the last block (ticket)
+// sums l2 in a fixed order and runs the scalar phase.  One load round per thread
+// instead of the ~100 dependent rounds of a single-block reduction.
+constexpr int R2_THREADS = 256, R2_MAXROWS = 4 * MAXC;
+__global__ void __launch_bounds__(R2_THREADS) pcg_reduce2_kernel(const double* __restrict__ partials,
+                                                                 long long pstride, int nblocks, int ncomp, int nq,
+                                                                 double* __restrict__ sums, double* l2,
+                                                                 unsigned* ticket, int phase, PcgScal* sc,
+                                                                 double rtol2) {
+  __shared__ double red[R2_MAXROWS][R2_THREADS / 32];
+  __shared__ unsigned flag;
+  const int nrows = ncomp * nq, R = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long per = (nblocks + R - 1) / R;
+  const long long b0 = blockIdx.x * per, b1 = min((long long)nblocks, b0 + per);
+  double v[R2_MAXROWS];
+#pragma unroll
+  for (int r = 0; r < R2_MAXROWS; ++r) v[r] = 0.0;
+  for (long long b = b0 + tid; b < b1; b += R2_THREADS) {
+#pragma unroll
+    for (int r = 0; r < R2_MAXROWS; ++r)
+      if (r < nrows) v[r] += __ldcg(partials + r * pstride + b);
+  }
+#pragma unroll
+  for (int r = 0; r < R2_MAXROWS; ++r) {
+    if (r >= nrows) break;
+    const double w = warp_sum_d(v[r]);
+    if (lane == 0) red[r][wid] = w;
+  }
+  __syncthreads();
+  if (tid < nrows) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < R2_THREADS / 32; ++w) t += red[tid][w];
+    l2[tid * R + blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) flag = (atomicAdd(ticket, 1u) == (unsigned)(R - 1)) ? 1u : 0u;
+  __syncthreads();
+  if (!flag) return;
+  __threadfence();
+  if (tid < nrows) {
+    double t = 0.0;
+    for (int b = 0; b < R; ++b) t += __ldcg(l2 + tid * R + b);
+    sums[tid] = t;
+  }
+  __syncthreads();
+  if (phase != PH_NONE && tid < ncomp) pcg_phase(sums, tid, nq, phase, sc, rtol2);
+  if (tid == 0) *ticket = 0u;
+}
+
 void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, int ncomp, int nq, double* sums,
-                       int phase, PcgScal* sc, double rtol2, cudaStream_t st) {
-  pcg_reduce_kernel<<<1, 1024, 0, st>>>(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2);
+                       int phase, PcgScal* sc, double rtol2, cudaStream_t st, double* l2, unsigned* ticket) {
+  const int R = std::min(R2_MAXBLOCKS, (nblocks + R2_THREADS - 1) / R2_THREADS);
+  if (l2 && ticket && R >= 2 && ncomp * nq <= R2_MAXROWS) {
+    pcg_reduce2_kernel<<<R, R2_THREADS, 0, st>>>(partials, pstride, nblocks, ncomp, nq, sums, l2, ticket, phase, sc,
+                                                 rtol2);
+  } else {
+    pcg_reduce_kernel<<<1, 1024, 0, st>>>(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2);
+  }
   STS_CUDA(cudaGetLastError());
 }
 

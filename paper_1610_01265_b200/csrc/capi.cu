@@ -684,6 +684,7 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const doub
       STS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g->d_pinned), g->h_pinned, 0));
       STS_CUDA(cudaMalloc(&g->d_ticket, 64 * sizeof(unsigned int)));
       STS_CUDA(cudaMemset(g->d_ticket, 0, 64 * sizeof(unsigned int)));
+      STS_CUDA(cudaMalloc(&g->d_red2, (size_t)R2_MAXBLOCKS * 4 * MAXC * sizeof(double)));
     } catch (...) {
       sts_grid_destroy(g);
       throw;
@@ -716,6 +717,7 @@ int sts_grid_destroy(sts_grid* g) {
     if (g->ws.base) cudaFree(g->ws.base);
     if (g->d_red) cudaFree(g->d_red);
     if (g->d_ticket) cudaFree(g->d_ticket);
+    if (g->d_red2) cudaFree(g->d_red2);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     delete g;
     if (prev >= 0) cudaSetDevice(prev);
@@ -1216,12 +1218,12 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     auto reduce = [&](int nblocks, int nq, int phase) {
       Timed t(g, STS_K_PCG_REDUCE, st);
       if (g->comm) {
-        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, PH_NONE, sc, rtol2, st);
+        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, PH_NONE, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
         STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * nq, ncclDouble, ncclSum, g->comm, st));
         launch_pcg_scalar(sums, ncomp, nq, phase, sc, rtol2, st);
         g->launches += 1;
       } else {
-        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2, st);
+        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
       }
     };
 
@@ -1247,7 +1249,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       else nbs = sweep(g, {{H_Z, zb[a], ncomp}, {H_W, wb[a], ncomp}, {H_P, pb[a], ncomp}}, is, make_m, fs);
       if (!fs) {
         Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is);
+        launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
         if (g->comm) {
           STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * 4, ncclDouble, ncclSum, g->comm, is));
           launch_pcg_scalar(sums, ncomp, 4, PH_M, sc, rtol2, is);
@@ -1278,7 +1280,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       }
       if (!(fused && !g->comm && sb_s <= 4096)) {           // else finished by the S-pass's last CTA
         Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbs, ncomp, 1, sums, g->comm ? PH_NONE : PH_AP, sc, rtol2, is);
+        launch_pcg_reduce(partials, pstride, nbs, ncomp, 1, sums, g->comm ? PH_NONE : PH_AP, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
         if (g->comm) {
           STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
           launch_pcg_scalar(sums, ncomp, 1, PH_AP, sc, rtol2, is);
@@ -1293,7 +1295,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       }
       if (g->comm) {
         Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbu, ncomp, 1, sums, PH_NONE, sc, rtol2, is);
+        launch_pcg_reduce(partials, pstride, nbu, ncomp, 1, sums, PH_NONE, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
         STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
         launch_pcg_scalar(sums, ncomp, 1, PH_RZ, sc, rtol2, is);
         g->launches += 1;

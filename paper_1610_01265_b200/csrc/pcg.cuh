@@ -59,8 +59,9 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
 //   nthr threads participate; sync() is the barrier among them.
 template <class Sync>
 __device__ inline void fused_final_reduce(const FinRed& f, const double* partials, long long pstride,
-                                          unsigned long long nblk, int tid, int nthr, double* red /*[32]*/,
+                                          unsigned long long nblk, int tid, int nthr, double* red /*[4 MAXC][32]*/,
                                           unsigned* s_flag, Sync sync) {
+  constexpr int MAXROWS = 4 * MAXC;
   __threadfence();
   sync();
   if (tid == 0) *s_flag = (atomicAdd(f.ticket, 1u) == (unsigned)(nblk - 1)) ? 1u : 0u;
@@ -68,30 +69,32 @@ __device__ inline void fused_final_reduce(const FinRed& f, const double* partial
   if (*s_flag == 0u) return;
   __threadfence();
   const int lane = tid & 31, wid = tid >> 5, nw = (nthr + 31) >> 5;
-  for (int row = 0; row < f.ncomp * f.nq; ++row) {
-    const double* src = partials + row * pstride;
-    // four independent accumulators per thread (loads in flight), combined in a fixed order
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    long long b = tid;
-    for (; b + 3LL * nthr < f.ntot; b += 4LL * nthr) {
-      a0 += __ldcg(src + b);
-      a1 += __ldcg(src + b + nthr);
-      a2 += __ldcg(src + b + 2LL * nthr);
-      a3 += __ldcg(src + b + 3LL * nthr);
-    }
-    for (; b < f.ntot; b += nthr) a0 += __ldcg(src + b);
-    double a = (a0 + a1) + (a2 + a3);
+  const int nrows = f.ncomp * f.nq;
+  // every row's loads in flight at once (one strided pass over the slots), then a
+  // fixed-order combine: deterministic, independent of which CTA is last
+  double v[MAXROWS];
+#pragma unroll
+  for (int r = 0; r < MAXROWS; ++r) v[r] = 0.0;
+  for (long long b = tid; b < f.ntot; b += nthr) {
+#pragma unroll
+    for (int r = 0; r < MAXROWS; ++r)
+      if (r < nrows) v[r] += __ldcg(partials + r * pstride + b);
+  }
+#pragma unroll
+  for (int r = 0; r < MAXROWS; ++r) {
+    if (r >= nrows) break;
+    double a = v[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) red[wid] = a;
-    sync();
-    if (tid == 0) {
-      double v = 0.0;
-      for (int w = 0; w < nw; ++w) v += red[w];
-      f.sums[row] = v;
-    }
-    sync();
+    if (lane == 0) red[r * 32 + wid] = a;
   }
+  sync();
+  if (tid < nrows) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[tid * 32 + w];
+    f.sums[tid] = t;
+  }
+  sync();
   if (tid < f.ncomp) pcg_phase(f.sums, tid, f.nq, f.phase, f.sc, f.rtol2);
   if (tid == 0) *f.ticket = 0u;
 }

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
     if constexpr (FR) {
-      __shared__ double fred[32];
+      __shared__ double fred[4 * MAXC * 32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
                          (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, XNT, fred, &flag,

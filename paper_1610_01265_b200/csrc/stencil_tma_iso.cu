@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       c.ea.partials[tid * c.ea.pstride + c.ea.pbase + blk] = s;
     }
     if constexpr (FR && (kS || kM)) {
-      __shared__ double fred[32];
+      __shared__ double fred[4 * MAXC * 32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
                          (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, INT, fred, &flag,

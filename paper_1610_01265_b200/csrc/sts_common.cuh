@@ -125,7 +125,8 @@ struct sts_grid {
   sts::Workspace ws;
   double* d_red = nullptr;              // reduction partials + scalars
   size_t red_bytes = 0;
-  unsigned int* d_ticket = nullptr;     // last-block tickets
+  unsigned int* d_ticket = nullptr;     // last-block tickets ([0] stencil passes, [1] reductions)
+  double* d_red2 = nullptr;             // second level of the multi-block PCG reduction
   double* h_pinned = nullptr;           // small pinned, device-mapped host mailbox
   double* d_pinned = nullptr;           // its device alias (written by launch_publish)
   // multi-GPU
@@ -311,8 +312,11 @@ void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double*
 enum PcgPhase { PH_NONE = 0, PH_R0 = 1, PH_AP = 2, PH_RZ = 3, PH_M = 4 };
 constexpr int PW_BLOCKS = 148 * 8;   // grid of the pointwise PCG kernels
 // sums[c*nq + q] = sum_b partials[(c*nq+q)*pstride + b], then the phase's scalar update
+// (l2 [R2_MAXBLOCKS x 4 MAXC] and a zeroed ticket: the two-level multi-block reduction)
+constexpr int R2_MAXBLOCKS = 64;
 void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, int ncomp, int nq,
-                       double* sums, int phase, PcgScal* sc, double rtol2, cudaStream_t st);
+                       double* sums, int phase, PcgScal* sc, double rtol2, cudaStream_t st,
+                       double* l2 = nullptr, unsigned* ticket = nullptr);
 void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal* sc, double rtol2,
                        cudaStream_t st);
 // copy n doubles to mapped pinned host memory with SM stores (no copy engine)
