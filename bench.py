@@ -134,6 +134,8 @@ def _visc_bytes(add, s_v, it_v, fused=False, merged=False):
     add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
     add("iso_rkl2_stage", (s_v - 1) * bytes_per_cell("iso_rkl2_stage", 3))
     add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0_m" if merged else "iso_pcg_r0", 3))
+    if merged:   # metric-folded K1, K2, K3, wV once per solve (timed with the vertex coefficients)
+        add("vertex_coef", 64)
     for k in range(1, max(it_v) + 1):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
         if merged:

@@ -54,6 +54,38 @@ __global__ void face_kappa_kernel(Geo G, FieldV T, double* __restrict__ k1, doub
   }
 }
 
+// Face coefficients of the isotropic operator with the metrics folded in, for the
+// merged PCG pass (once per solve): K1 = k1 F1r F1t F1p (r face i+1/2), K2 = k2 F2r
+// F2t F2p (theta face j+1/2), K3 = k3 F2r F3t F3p (phi face k+1/2, periodic wrap),
+// WV = w Vr Vt Vp -- each product in the association the stencil kernels use, so the
+// pass computes bit-identical coefficients; zero where the face is a wall.
+__global__ void iso_premul_kernel(Geo G, const double* __restrict__ k1, const double* __restrict__ k2,
+                                  const double* __restrict__ k3, const double* __restrict__ w,
+                                  double* __restrict__ K1, double* __restrict__ K2, double* __restrict__ K3,
+                                  double* __restrict__ WV) {
+  // grid: (phi chunks of 256, theta rows, local r planes) -- no index divisions
+  const Metrics& M = G.m;
+  const bool per = G.periodic3 != 0, kself = per && G.n3 == 1;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, il = blockIdx.z;
+  if (k >= G.n3) return;
+  const long long e = (long long)il * G.plane + (long long)j * G.n3 + k;
+  const int ig = G.i0 + il;
+  const bool ip = ig + 1 < G.n1g, jp = j + 1 < G.n2, kp = !kself && (per || k + 1 < G.n3);
+  K1[e] = ip ? k1[e] * M.F1r[ig] * (M.F1t[j] * M.F1p[k]) : 0.0;
+  K2[e] = jp ? k2[e] * M.F2r[ig] * (M.F2t[j] * M.F2p[k]) : 0.0;
+  K3[e] = kp ? k3[e] * M.F2r[ig] * (M.F3t[j] * M.F3p[k]) : 0.0;
+  WV[e] = (w ? w[e] : 1.0) * M.Vr[ig] * (M.Vt[j] * M.Vp[k]);
+}
+
+void launch_iso_premul(const Geo& G, const double* k1, const double* k2, const double* k3, const double* w,
+                       double* K1, double* K2, double* K3, double* WV, cudaStream_t st) {
+  if ((long long)G.nl * G.plane == 0) return;
+  STS_REQUIRE(G.n2 <= 65535 && G.nl <= 65535, "grid too large for the coefficient pass");
+  const dim3 grid((G.n3 + 255) / 256, G.n2, G.nl);
+  iso_premul_kernel<<<grid, 256, 0, st>>>(G, k1, k2, k3, w, K1, K2, K3, WV);
+  STS_CUDA(cudaGetLastError());
+}
+
 void launch_face_kappa(const Geo& G, FieldV T, double* k1, double* k2, double* k3, double kappa0,
                        double T_cut, double fc_r0, double fc_w, const double* x1f_d, const double* x1c_d,
                        cudaStream_t st) {

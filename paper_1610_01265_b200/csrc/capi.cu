@@ -1071,14 +1071,17 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     const size_t NFr = rnd(NF), Nr = rnd(N);
     // scratch: six [ncomp][nl][plane] fields (two-pass: r, z, y, p0, p1; merged: z0, z1,
     // w0, w1, p0, p1); d [nl][plane]; vertex coefficients
-    double* base = ws_get(g, (6 * NFr + Nr + evn + rnd(sg.total)) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 6 * NFr + Nr + evn);
+    // (+ the metric-folded isotropic coefficients K1, K2, K3, wV of the merged pass)
+    const size_t npre = (mode == STS_MODE_ISO && g->tma && g->pcg_merged) ? 4 * Nr : 0;
+    double* base = ws_get(g, (6 * NFr + Nr + npre + evn + rnd(sg.total)) * sizeof(double));
+    if (sg.any_host) sg.begin(base + 6 * NFr + Nr + npre + evn);
     double* r = base;
     double* z = base + NFr;
     double* y = base + 2 * NFr;
     double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
     double* d = base + 6 * NFr;
-    double* evbase = base + 6 * NFr + Nr;
+    double* pre = npre ? base + 6 * NFr + Nr : nullptr;   // K1, K2, K3, wV ([nl][plane] each)
+    double* evbase = base + 6 * NFr + Nr + npre;
     // merged iteration buffers (ping-pong by iteration parity; the p pair is pb)
     double* zb[2] = {base, base + NFr};
     double* wb[2] = {base + 2 * NFr, base + 5 * NFr};
@@ -1113,8 +1116,21 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.ea.out3 = off(wb[1], g->slabs[0]);
       c.ea.x = off(x, g->slabs[0]);
       c.ea.dinv = off(d, g->slabs[0]);
-      merged = aniso_tma_eligible(c) || iso_tma_eligible(c);
+      if (mode == STS_MODE_ISO) {
+        c.k1.p = off(pre, g->slabs[0]);
+        c.k2.p = off(pre + Nr, g->slabs[0]);
+        c.k3.p = off(pre + 2 * Nr, g->slabs[0]);
+        c.w = off(pre + 3 * Nr, g->slabs[0]);
+        c.premul = 1;
+      }
+      merged = (mode == STS_MODE_ISO ? npre > 0 && iso_tma_eligible(c) : aniso_tma_eligible(c));
     }
+    if (merged && mode == STS_MODE_ISO)
+      for (auto& sl : g->slabs) {
+        Timed t(g, STS_K_VERTEX_COEF, st);   // (the isotropic counterpart of the frozen vertex coefficients)
+        launch_iso_premul(slab_geo(g, sl), off(k1, sl), off(k2, sl), off(k3, sl), off(w, sl), off(pre, sl),
+                          off(pre + Nr, sl), off(pre + 2 * Nr, sl), off(pre + 3 * Nr, sl), st);
+      }
     if (merged) fused = false;
     // isotropic fused S-pass: z = r d is formed inside the stencil pass from the staged
     // r and d, so neither the initial residual pass nor the U-pass stores z
@@ -1169,6 +1185,13 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
       c.ea.out3 = off(wb[b2], sl);
       c.ea.x = off(x, sl);
       c.ea.dinv = off(d, sl);
+      if (mode == STS_MODE_ISO) {   // metric-folded coefficients (the k1 halo planes stay raw)
+        c.k1.p = off(pre, sl);
+        c.k2.p = off(pre + Nr, sl);
+        c.k3.p = off(pre + 2 * Nr, sl);
+        c.w = off(pre + 3 * Nr, sl);
+        c.premul = 1;
+      }
       c.ea.first = first;
       c.ea.dt = dt;
       c.ea.partials = partials;

@@ -96,9 +96,10 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int EP = WB + T::OWN;
   static constexpr int MT = EP + nepi * T::OWN;      // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  // merged PCG at 2 CTAs per SM: the six per-column metric products live in shared
-  // memory (COL doubles per consumer thread, after the mbarriers) instead of 12 registers
-  static constexpr int COL = (EPI == EPI_PCG_M && MINB == 2) ? 6 : 0;
+  // (a variant short of registers could keep the six per-column metric products in
+  // shared memory, COL doubles per consumer thread after the mbarriers; the merged PCG
+  // pass reads metric-folded coefficients and needs none)
+  static constexpr int COL = 0;
   static constexpr int FIX = COL * T::INT * 8 + 128;
   // ring slots: 3 where MINB CTAs per SM fit (2 CTAs: <= 113 KB each), else 2
   static constexpr int NS1 = (SMEM_1CTA - 2048 - FIX) / (SLOT * 8 + 16);   // one CTA per SM: all that fit
@@ -369,7 +370,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     }
   }
   double kdn = 0.0;
-  if (own && ig0 >= 1) kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * cv[0];
+  if (own && ig0 >= 1) {
+    // merged PCG: the local planes of k1 hold the metric-folded K1 (the halo plane is raw)
+    if (kM && ib >= 1) kdn = __ldg(c.k1.p + (long long)(ib - 1) * G.plane + coff);
+    else kdn = __ldg(plane_ptr(c.k1, G, ib - 1, 0) + coff) * M.F1r[ig0 - 1] * cv[0];
+  }
   constexpr int NQ = kM ? 4 : (EPI == EPI_PCG_R0 ? 2 : 1);   // partial sums per component
   double part[NC][NQ];
 #pragma unroll
@@ -504,13 +509,13 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       mbar_wait((Lay::FORM ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
       C.K = 0.0;
       if (own) {
-        const double f1r = S[Lay::MT + 0], f23r = S[Lay::MT + 1], vr = S[Lay::MT + 2];
-        C.K = ip ? S[Lay::K1 + o8] * f1r * CV(0) : 0.0;
-        const double Kjp = jp ? S[ok2p] * f23r * CV(1) : 0.0;
-        const double Kjm = jm ? S[ok2m] * f23r * CV(2) : 0.0;
-        const double Kkp = kp ? S[ok3p] * f23r * CV(3) : 0.0;
-        const double Kkm = km ? S[ok3m] * f23r * CV(4) : 0.0;
-        C.WV = (ta.has_w ? S[Lay::WB + o8] : 1.0) * vr * CV(5);
+        // metric-folded coefficients (launch_iso_premul: zero on wall faces)
+        C.K = S[Lay::K1 + o8];
+        const double Kjp = S[ok2p];
+        const double Kjm = jm ? S[ok2m] : 0.0;
+        const double Kkp = S[ok3p];
+        const double Kkm = km ? S[ok3m] : 0.0;
+        C.WV = S[Lay::WB + o8];
         // PC1 diagonal of the own cell, the R0 pass's arithmetic (bit-identical d):
         // A_ii = wV - dt L_ii, L_ii = -(sum of the six face coefficients); r.z = z^2 A_ii
         const double Aii = C.WV - c.ea.dt * -(P.K + C.K + Kjp + Kjm + Kkp + Kkm);
@@ -612,7 +617,7 @@ bool iso_tma_eligible(const StencilCall& c) {
   if (!al16(c.u.p) || !al16(c.u2.p) || !al16(c.k1.p) || !al16(c.k2.p) || !al16(c.k3.p) || !al16(c.w)) return false;
   if (!al16(c.ea.ym2) || !al16(c.ea.y0) || !al16(c.ea.m0) || !al16(c.ea.x)) return false;
   if (c.epi == EPI_PCG_S && (!c.u3.p || !al16(c.u3.p))) return false;
-  if (c.epi == EPI_PCG_M && (!al16(c.u3.p) || !c.ea.x || !c.ea.out3)) return false;
+  if (c.epi == EPI_PCG_M && (!al16(c.u3.p) || !c.ea.x || !c.ea.out3 || !c.premul || !c.w)) return false;
   if (c.epi == EPI_PCG_R0 && (!c.ea.out4 || c.ea.sc)) return false;
   return true;
 }

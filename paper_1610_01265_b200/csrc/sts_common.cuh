@@ -238,6 +238,8 @@ struct StencilCall {
                                // EPI_PCG_M: pold
   const double* w;             // [nl][plane] or nullptr
   const double* ev = nullptr;  // ANISO fast path: vertex coefficients [3][nl+1][n2][n3+2] (see ev_pitch)
+  int premul = 0;              // ISO EPI_PCG_M: k1.p, k2.p, k3.p, w hold the metric-folded K1, K2, K3, wV
+                               // (launch_iso_premul); k1.lo / k1.hi stay the raw halo planes
   EpiArgs ea;
   int ib, ie;                  // local plane range [ib, ie)
 };
@@ -305,6 +307,9 @@ void launch_pcg_xfinal(int ncomp, long long n, long long cstride, double* x, con
                        const PcgScal* sc, cudaStream_t st);
 
 // pointwise / auxiliary kernels (aux.cu)
+// metric-folded isotropic face coefficients and wV of one slab (merged PCG pass)
+void launch_iso_premul(const Geo& G, const double* k1, const double* k2, const double* k3, const double* w,
+                       double* K1, double* K2, double* K3, double* WV, cudaStream_t st);
 void launch_face_kappa(const Geo& geo, FieldV T, double* k1, double* k2, double* k3, double kappa0,
                        double T_cut, double fc_r0, double fc_w, const double* x1f_d, const double* x1c_d,
                        cudaStream_t st);
