@@ -40,10 +40,12 @@ constexpr int SMEM_1CTA = 232448;         // max dynamic shared memory of one CT
 //  * IJ = 7, 2 CTAs per SM: 8 warps per CTA -> 4 warps per SM sub-partition, so the
 //    64K-register file allows 128 registers per thread (8 consumer warps would drop
 //    that to 96 and the 3-component PCG S-pass spills);
-//  * IJ = 11, 1 CTA per SM (the 3-component merged PCG pass, whose three staged
-//    fields make a 7-row slot too large for three ring slots at 2 CTAs per SM):
-//    12 warps -> 3 per sub-partition -> 168 registers (no spills), 3 slots of 63 KB.
-//    (14 rows would put 4 warps on a sub-partition again: 128 registers, spills.)
+//  * ISO_M3_ROWS (13) rows, 1 CTA per SM, for the 3-component merged PCG pass, whose
+//    three staged fields make a 7-row slot too large for three ring slots at 2 CTAs
+//    per SM: 13 consumer + producer + former warps, 128 registers (the pass reads
+//    metric-folded coefficients), three 72 KB slots.  Measured c4 fraction of the
+//    copy peak by rows: 7: 0.79, 8: 0.77, 9: 0.85, 11: 0.83, 12: 0.82, 13: 0.86
+//    (14 rows no longer fit three slots).
 template <int IJ_>
 struct IsoTile {
   static constexpr int IJ = IJ_;
@@ -59,7 +61,7 @@ struct IsoTile {
 
 // rows of the tile and resident CTAs per SM of one (epilogue, ncomp) variant (host and device)
 #ifndef ISO_M3_ROWS
-#define ISO_M3_ROWS 9
+#define ISO_M3_ROWS 13
 #endif
 __host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? ISO_M3_ROWS : 7; }
 __host__ __device__ constexpr int iso_minb(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 1 : 2; }
