@@ -93,27 +93,40 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         # (the isotropic pass recomputes d from the staged face coefficients)
         "iso_pcg_m": (32 * c + 32) if first else (64 * c + 32),
         "iso_pcg_r0_m": 8 * c + 32 + 24 * c + 8,
+        # RKL2 stage in deviation form (D_j = Y_j - Y0): D_{j-1}, D_{j-2}, M0 (+ e / k, w) in; D_j out
+        "aniso_rkl2_dstage": 8 + 24 + 16 + 8,
+        "iso_rkl2_dstage": 24 * c + 32 + 8 * c,
     }
     return table[kind]
 
 
-def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False, merged_c=False, merged_v=False):
+def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False, merged_c=False, merged_v=False,
+                      dev_c=False, dev_v=False):
     """Total algorithmic bytes per class for one step on `ncells` local cells."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
-        _cond_bytes(add, s_c, it_c, fused_c, merged_c)
+        _cond_bytes(add, s_c, it_c, fused_c, merged_c, dev_c)
     if s_v:
-        _visc_bytes(add, s_v, it_v, fused_v, merged_v)
+        _visc_bytes(add, s_v, it_v, fused_v, merged_v, dev_v)
     return B
 
 
-def _cond_bytes(add, s_c, it_c, fused, merged=False):
+def _rkl2_stage_bytes(add, kind, s, dev, c=1):
+    """Stages 2..s: Fig. 2 form, or deviation form for stages 2..s-1 (the last one adds Y0 back)."""
+    if dev and s >= 3:
+        add(kind + "_dstage", (s - 2) * bytes_per_cell(kind + "_dstage", c))
+        add(kind + "_stage", bytes_per_cell(kind + "_stage", c))
+    else:
+        add(kind + "_stage", (s - 1) * bytes_per_cell(kind + "_stage", c))
+
+
+def _cond_bytes(add, s_c, it_c, fused, merged=False, dev=False):
     add("face_kappa", bytes_per_cell("face_kappa"))
     add("vertex_coef", 2 * bytes_per_cell("vertex_coef"))   # once per RKL2 advance and per PCG solve
     add("aniso_gersh", bytes_per_cell("aniso_gersh"))
     add("aniso_rkl2_first", bytes_per_cell("aniso_rkl2_first"))
-    add("aniso_rkl2_stage", (s_c - 1) * bytes_per_cell("aniso_rkl2_stage"))
+    _rkl2_stage_bytes(add, "aniso_rkl2", s_c, dev)
     add("aniso_pcg_r0", bytes_per_cell("aniso_pcg_r0"))
     for k in range(1, it_c + 1):
         if merged:
@@ -129,10 +142,10 @@ def _cond_bytes(add, s_c, it_c, fused, merged=False):
         add("pcg_xfinal", bytes_per_cell("pcg_xfinal", 1))
 
 
-def _visc_bytes(add, s_v, it_v, fused=False, merged=False):
+def _visc_bytes(add, s_v, it_v, fused=False, merged=False, dev=False):
     add("iso_gersh", bytes_per_cell("iso_gersh"))
     add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
-    add("iso_rkl2_stage", (s_v - 1) * bytes_per_cell("iso_rkl2_stage", 3))
+    _rkl2_stage_bytes(add, "iso_rkl2", s_v, dev, 3)
     add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0_m" if merged else "iso_pcg_r0", 3))
     if merged:   # metric-folded K1, K2, K3, wV once per solve (timed with the vertex coefficients)
         add("vertex_coef", 64)
@@ -576,9 +589,11 @@ def main():
     fused_v = timing.get("iso_pcg_s", (0, 0.0))[0] > 0
     merged_c = timing.get("aniso_pcg_m", (0, 0.0))[0] > 0
     merged_v = timing.get("iso_pcg_m", (0, 0.0))[0] > 0
+    dev_c = timing.get("aniso_rkl2_dstage", (0, 0.0))[0] > 0
+    dev_v = timing.get("iso_rkl2_dstage", (0, 0.0))[0] > 0
     for i in pinfos:
         for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
-                                      fused_c, fused_v, merged_c, merged_v).items():
+                                      fused_c, fused_v, merged_c, merged_v, dev_c, dev_v).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
     kernels = {}
     for k, (n, kms) in timing.items():
@@ -603,7 +618,8 @@ def main():
     n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
              "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
              "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"]),
-             "aniso_pcg_m": launches_dom["it_cond"], "iso_pcg_m": max(launches_dom["it_visc"])}.get(dom)
+             "aniso_pcg_m": launches_dom["it_cond"], "iso_pcg_m": max(launches_dom["it_visc"]),
+             "aniso_rkl2_dstage": launches_dom["s_cond"] - 2, "iso_rkl2_dstage": launches_dom["s_visc"] - 2}.get(dom)
     bpl = (Bytes[dom] / len(pinfos) / n_eff) if n_eff else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,

@@ -151,7 +151,9 @@ int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_
 #define STS_K_ISO_PCG_S 20       /* fused PCG S-pass of the isotropic operator, TMA path      */
 #define STS_K_ANISO_PCG_M 21     /* one-pass (merged) PCG iteration, anisotropic, TMA path    */
 #define STS_K_ISO_PCG_M 22       /* one-pass (merged) PCG iteration, isotropic, TMA path      */
-#define STS_K_NCLASSES 23
+#define STS_K_ANISO_RKL2_DSTAGE 23  /* RKL2 stage in deviation form, anisotropic, TMA path */
+#define STS_K_ISO_RKL2_DSTAGE 24    /* RKL2 stage in deviation form, isotropic, TMA path    */
+#define STS_K_NCLASSES 25
 int sts_grid_set_timing(sts_grid* g, int enable);
 
 /*
@@ -180,6 +182,16 @@ int sts_grid_set_graphs(sts_grid* g, int enable);
  * iterates equal Fig. 1's in exact arithmetic.  0: the two-pass S / U iteration.
  */
 int sts_grid_set_pcg_merged(sts_grid* g, int enable);
+
+/*
+ * RKL2 stage form (A-B measurement / testing).  enable != 0 (the default): where
+ * the TMA kernels are eligible, stages 2..s-1 advance the deviation D_j = Y_j - Y0,
+ *   D_j = mu_j D_{j-1} + nu_j D_{j-2} + mu~_j dt M D_{j-1} + (mu~_j + gamma~_j) dt M Y0,
+ * D_0 = 0, D_1 = mu~_1 dt M Y0, and the last stage returns Y0 + D_s -- Fig. 2
+ * rewritten with M linear, so an intermediate stage streams
+ * three solution-sized arrays instead of four.  0: Fig. 2 as printed.
+ */
+int sts_grid_set_rkl2_deviation(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
 

@@ -336,13 +336,14 @@ static std::vector<const double*> build_vertex_coefs(sts_grid* g, int mode, doub
 // one stencil pass: the TMA pipelined kernel where eligible, else the cp.async kernels
 static void launch_pass(sts_grid* g, const StencilCall& c, cudaStream_t st) {
   const bool aniso = c.mode == STS_MODE_ANISO;
-  const int kind = (c.epi == EPI_PCG_S)   ? (aniso ? STS_K_ANISO_PCG_S : STS_K_ISO_PCG_S)
-                   : (c.epi == EPI_PCG_M) ? (aniso ? STS_K_ANISO_PCG_M : STS_K_ISO_PCG_M)
-                                          : stencil_kind(c.mode, c.epi);
+  const int kind = (c.epi == EPI_PCG_S)         ? (aniso ? STS_K_ANISO_PCG_S : STS_K_ISO_PCG_S)
+                   : (c.epi == EPI_PCG_M)       ? (aniso ? STS_K_ANISO_PCG_M : STS_K_ISO_PCG_M)
+                   : (c.epi == EPI_RKL2_DSTAGE) ? (aniso ? STS_K_ANISO_RKL2_DSTAGE : STS_K_ISO_RKL2_DSTAGE)
+                                                : stencil_kind(c.mode, c.epi);
   Timed t(g, kind, st);
   if (g->tma && (launch_aniso_tma(c, st) || launch_iso_tma(c, st))) return;
-  if (c.epi == EPI_PCG_S || c.epi == EPI_PCG_M)
-    throw Error{STS_ERR_STATE, "fused PCG pass launched without a TMA-eligible call"};
+  if (c.epi == EPI_PCG_S || c.epi == EPI_PCG_M || c.epi == EPI_RKL2_DSTAGE)
+    throw Error{STS_ERR_STATE, "TMA-only pass launched without a TMA-eligible call"};
   launch_stencil(c, st);
 }
 
@@ -575,7 +576,23 @@ static void rkl2_core(sts_grid* g, int mode, int ncomp, const double* u0, double
                       const double* k2, const double* k3, const double* bb, const double* w, double dt, int s,
                       const std::vector<const double*>& ev, double* M0, double* A, double* B, cudaStream_t st) {
   const Rkl2Coef co = rkl2_coefs(s);
-  // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0
+  // deviation form (sts_grid_set_rkl2_deviation): D_j = Y_j - Y0 for the stages before
+  // the last, where the TMA kernels take both stage forms
+  bool dev = false;
+  if (g->tma && g->rkl2_dev && s >= 3) {
+    StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_RKL2_DSTAGE, A, k1, k2, k3, bb, w);
+    c.ev = ev[0];
+    c.ea.out = off(B, g->slabs[0]);
+    c.ea.ym2 = off(B, g->slabs[0]);
+    c.ea.m0 = off(M0, g->slabs[0]);
+    StencilCall f = make_call(g, g->slabs[0], mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
+    f.ev = ev[0];
+    f.ea.out = off(A, g->slabs[0]);
+    f.ea.out2 = off(M0, g->slabs[0]);
+    dev = mode == STS_MODE_ANISO ? aniso_tma_eligible(c) && aniso_tma_eligible(f)
+                                 : iso_tma_eligible(c) && iso_tma_eligible(f);
+  }
+  // stage 1: M0 = F(Y0), Y1 = Y0 + mu~_1 dt M0 (deviation form: D1 = mu~_1 dt M0)
   sweep(g, {{H_U, u0, ncomp}}, st, [&](size_t si) {
     const Slab& sl = g->slabs[si];
     StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, u0, k1, k2, k3, bb, w);
@@ -583,29 +600,40 @@ static void rkl2_core(sts_grid* g, int mode, int ncomp, const double* u0, double
     c.ea.out = off(A, sl);
     c.ea.out2 = off(M0, sl);
     c.ea.c0 = co.mut[1] * dt;
+    c.ea.a0 = dev ? 0.0 : 1.0;
     return c;
   });
-  // stages 2..s (buffer rotation: Y_{j-1} in `cur`, Y_{j-2} in `prev`)
-  const double* prev = u0;
+  // stages 2..s (buffer rotation: Y_{j-1} (D_{j-1}) in `cur`, Y_{j-2} (D_{j-2}) in `prev`;
+  // prev == nullptr stands for D_0 = 0)
+  const double* prev = dev ? nullptr : u0;
   double* cur = A;
   for (int j = 2; j <= s; ++j) {
     double* dst;
     if (j == s) dst = u1;
-    else if (prev == u0) dst = B;                       // never overwrite Y0
+    else if (prev == u0 || prev == nullptr) dst = B;    // never overwrite Y0
     else dst = const_cast<double*>(prev);               // in place over Y_{j-2}
+    const bool dstage = dev && j < s;
     sweep(g, {{H_U, cur, ncomp}}, st, [&](size_t si) {
       const Slab& sl = g->slabs[si];
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_STAGE, cur, k1, k2, k3, bb, w);
+      StencilCall c = make_call(g, sl, mode, ncomp, dstage ? EPI_RKL2_DSTAGE : EPI_RKL2_STAGE, cur, k1, k2, k3, bb,
+                                w);
       c.ev = ev[si];
       c.ea.out = off(dst, sl);
-      c.ea.ym2 = off(prev, sl);
+      c.ea.ym2 = off(prev ? prev : cur, sl);             // (D_0 = 0: nu multiplies a finite dummy)
       c.ea.y0 = off(u0, sl);
       c.ea.m0 = off(M0, sl);
       c.ea.mu = co.mu[j];
-      c.ea.nu = co.nu[j];
-      c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
+      c.ea.nu = prev ? co.nu[j] : 0.0;
       c.ea.c0 = co.mut[j] * dt;
-      c.ea.c1 = co.gt[j] * dt;
+      if (dev) {
+        // D_j = mu D_{j-1} + nu D_{j-2} + mu~ dt M D_{j-1} + (mu~ + gamma~) dt M0; the last
+        // stage adds Y0 back (c2 = 1)
+        c.ea.c1 = (co.mut[j] + co.gt[j]) * dt;
+        c.ea.c2 = 1.0;
+      } else {
+        c.ea.c1 = co.gt[j] * dt;
+        c.ea.c2 = 1.0 - co.mu[j] - co.nu[j];
+      }
       return c;
     });
     prev = cur;
@@ -764,6 +792,13 @@ int sts_grid_set_pcg_merged(sts_grid* g, int enable) {
   return guard([&] {
     STS_REQUIRE(g, "NULL grid");
     g->pcg_merged = enable != 0;
+  });
+}
+
+int sts_grid_set_rkl2_deviation(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->rkl2_dev = enable != 0;
   });
 }
 

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(NT, 3) aniso_kernel(StencilCall c, int ic, uns
     } else if constexpr (EPI == EPI_RKL2_FIRST) {
       const double F = Lu / WV;
       c.ea.out2[gi] = F;
-      c.ea.out[gi] = uc + c.ea.c0 * F;
+      c.ea.out[gi] = c.ea.a0 * uc + c.ea.c0 * F;
     } else if constexpr (EPI == EPI_RKL2_STAGE) {
       const double F = Lu / WV;
       const double ym2 = c.ea.ym2[gi], y0 = c.ea.y0[gi], m0 = c.ea.m0[gi];
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
       } else if constexpr (EPI == EPI_RKL2_FIRST) {
         const double F = Lu / WV;
         c.ea.out2[gi] = F;
-        c.ea.out[gi] = uc + c.ea.c0 * F;
+        c.ea.out[gi] = c.ea.a0 * uc + c.ea.c0 * F;
       } else if constexpr (EPI == EPI_RKL2_STAGE) {
         const double F = Lu / WV;
         c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * ym2c + c.ea.c2 * y0c + c.ea.c0 * F + c.ea.c1 * m0c;
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(NT, 4) iso_kernel(StencilCall c, int ic, unsig
         } else if constexpr (EPI == EPI_RKL2_FIRST) {
           const double F = Lu / WV;
           c.ea.out2[go] = F;
-          c.ea.out[go] = uc[q] + c.ea.c0 * F;
+          c.ea.out[go] = c.ea.a0 * uc[q] + c.ea.c0 * F;
         } else if constexpr (EPI == EPI_RKL2_STAGE) {
           const double F = Lu / WV;
           c.ea.out[go] = c.ea.mu * uc[q] + c.ea.nu * c.ea.ym2[go] + c.ea.c2 * c.ea.y0[go] + c.ea.c0 * F +
@@ -1003,7 +1003,7 @@ __global__ void __launch_bounds__(NT, (NC >= 3 ? 2 : 3)) iso_fast_kernel(Stencil
           } else if constexpr (EPI == EPI_RKL2_FIRST) {
             const double F = Lu / WV;
             c.ea.out2[go] = F;
-            c.ea.out[go] = u0 + c.ea.c0 * F;
+            c.ea.out[go] = c.ea.a0 * u0 + c.ea.c0 * F;
           } else if constexpr (EPI == EPI_RKL2_STAGE) {
             const double F = Lu / WV;
             c.ea.out[go] = c.ea.mu * u0 + c.ea.nu * ym2[q] + c.ea.c2 * y0v[q] + c.ea.c0 * F + c.ea.c1 * m0v[q];

@@ -84,12 +84,15 @@ constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : 3; 
 
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
+enum { OW_DM2 = 0, OW_DM0 = 1 };              // RKL2 stage, deviation form
 enum { OW_X = 0, OW_D = 1 };                 // PCG S-pass (x) / merged pass (x, d)
 // slot layout of one (epilogue, has-w) variant
 template <int EPI, bool W>
 struct TmaLay {
   static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
-  static constexpr int nepi = (EPI == EPI_RKL2_STAGE) ? 3 : (EPI == EPI_PCG_S ? 1 : (EPI == EPI_PCG_M ? 2 : 0));
+  static constexpr int nepi = (EPI == EPI_RKL2_STAGE)
+                                  ? 3
+                                  : ((EPI == EPI_RKL2_DSTAGE || EPI == EPI_PCG_M) ? 2 : (EPI == EPI_PCG_S ? 1 : 0));
   static constexpr int nown = nepi + (W ? 1 : 0);             // w is the last own box
   static constexpr int E = nsrc * U_FIELD;
   static constexpr int O = E + E_PART;
@@ -333,11 +336,14 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
         } else if constexpr (EPI == EPI_RKL2_FIRST) {
           const double F = Lu / WV;
           c.ea.out2[gi] = F;
-          c.ea.out[gi] = uc + c.ea.c0 * F;
+          c.ea.out[gi] = c.ea.a0 * uc + c.ea.c0 * F;
         } else if constexpr (EPI == EPI_RKL2_STAGE) {
           const double F = Lu / WV;
           c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_YM2 * O_PART] + c.ea.c2 * O[OW_Y0 * O_PART] + c.ea.c0 * F +
                          c.ea.c1 * O[OW_M0 * O_PART];
+        } else if constexpr (EPI == EPI_RKL2_DSTAGE) {
+          const double F = Lu / WV;
+          c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_DM2 * O_PART] + c.ea.c0 * F + c.ea.c1 * O[OW_DM0 * O_PART];
         } else if constexpr (kR0) {
           // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
           const double Ld = -(L.ld + ldhi);
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
 // ============================================================================
 static bool has_tma(int epi) {
   return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0 ||
-         epi == EPI_PCG_M;
+         epi == EPI_PCG_M || epi == EPI_RKL2_DSTAGE;
 }
 
 bool aniso_tma_eligible(const StencilCall& c) {
@@ -543,6 +549,9 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     owns[nown++] = c.ea.ym2;
     owns[nown++] = c.ea.y0;
     owns[nown++] = c.ea.m0;
+  } else if (c.epi == EPI_RKL2_DSTAGE) {
+    owns[nown++] = c.ea.ym2;
+    owns[nown++] = c.ea.m0;
   } else if (c.epi == EPI_PCG_S) {
     owns[nown++] = c.ea.x;
   } else if (c.epi == EPI_PCG_M) {
@@ -555,6 +564,7 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_F: launch_w<EPI_F>(c, grid, ic, ta, st); break;
     case EPI_RKL2_FIRST: launch_w<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
     case EPI_RKL2_STAGE: launch_w<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_DSTAGE: launch_w<EPI_RKL2_DSTAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_w<EPI_PCG_S>(c, grid, ic, ta, st); break;
     case EPI_PCG_R0: launch_w<EPI_PCG_R0>(c, grid, ic, ta, st); break;
     case EPI_PCG_M: launch_w<EPI_PCG_M>(c, grid, ic, ta, st); break;

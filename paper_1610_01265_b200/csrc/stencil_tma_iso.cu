@@ -81,7 +81,8 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x (d is recomputed from
   // the staged face coefficients: A_ii = wV - dt L_ii, d = 1 / A_ii as in the R0 pass)
   static constexpr int nepi =
-      (EPI == EPI_RKL2_STAGE) ? 3 * NC : ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) ? NC : 0);
+      (EPI == EPI_RKL2_STAGE) ? 3 * NC
+                              : (EPI == EPI_RKL2_DSTAGE ? 2 * NC : ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) ? NC : 0));
   // one block per staged field: NC main boxes, then the NC x 2 wrap boxes, so a
   // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
   static constexpr int WRP = NC * T::S_MAIN;                          // wrap boxes within a field block
@@ -439,11 +440,15 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           } else if constexpr (EPI == EPI_RKL2_FIRST) {
             const double F = Lu / WV;
             o2[go] = F;
-            o1[go] = u0 + c.ea.c0 * F;
+            o1[go] = c.ea.a0 * u0 + c.ea.c0 * F;
           } else if constexpr (EPI == EPI_RKL2_STAGE) {
             const double F = Lu / WV;
             o1[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c2 * S[Lay::EP + (NC + q) * OWN + o8] +
                      c.ea.c0 * F + c.ea.c1 * S[Lay::EP + (2 * NC + q) * OWN + o8];
+          } else if constexpr (EPI == EPI_RKL2_DSTAGE) {
+            const double F = Lu / WV;
+            o1[go] = c.ea.mu * u0 + c.ea.nu * S[Lay::EP + q * OWN + o8] + c.ea.c0 * F +
+                     c.ea.c1 * S[Lay::EP + (NC + q) * OWN + o8];
           } else if constexpr (kR0) {
             // r0 = b - A x0 = dt L u (x0 = u^n); z0 = r0 d; partials r.z and b.P^-1 b
             const double r = c.ea.dt * Lu;
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 // ============================================================================
 static bool iso_has_tma(int epi) {
   return epi == EPI_F || epi == EPI_RKL2_FIRST || epi == EPI_RKL2_STAGE || epi == EPI_PCG_S || epi == EPI_PCG_R0 ||
-         epi == EPI_PCG_M;
+         epi == EPI_PCG_M || epi == EPI_RKL2_DSTAGE;
 }
 
 bool iso_tma_eligible(const StencilCall& c) {
@@ -708,6 +713,9 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     map_plain(&ta.epi[0], c.ea.ym2, G, npl, IK, IJ);
     map_plain(&ta.epi[1], c.ea.y0, G, npl, IK, IJ);
     map_plain(&ta.epi[2], c.ea.m0, G, npl, IK, IJ);
+  } else if (c.epi == EPI_RKL2_DSTAGE) {
+    map_plain(&ta.epi[0], c.ea.ym2, G, npl, IK, IJ);
+    map_plain(&ta.epi[1], c.ea.m0, G, npl, IK, IJ);
   } else if (c.epi == EPI_PCG_S) {
     map_plain(&ta.epi[0], c.ea.x, G, npl, IK, IJ);
     map_plain(&ta.dm, c.u3.p, G, G.nl, SBW, SBH);
@@ -719,6 +727,7 @@ bool launch_iso_tma(const StencilCall& c, cudaStream_t st) {
     case EPI_F: launch_iso_nc<EPI_F>(c, grid, ic, ta, st); break;
     case EPI_RKL2_FIRST: launch_iso_nc<EPI_RKL2_FIRST>(c, grid, ic, ta, st); break;
     case EPI_RKL2_STAGE: launch_iso_nc<EPI_RKL2_STAGE>(c, grid, ic, ta, st); break;
+    case EPI_RKL2_DSTAGE: launch_iso_nc<EPI_RKL2_DSTAGE>(c, grid, ic, ta, st); break;
     case EPI_PCG_S: launch_iso_nc<EPI_PCG_S>(c, grid, ic, ta, st); break;
     case EPI_PCG_R0: launch_iso_nc<EPI_PCG_R0>(c, grid, ic, ta, st); break;
     case EPI_PCG_M: launch_iso_nc<EPI_PCG_M>(c, grid, ic, ta, st); break;

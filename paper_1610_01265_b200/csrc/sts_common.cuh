@@ -140,6 +140,7 @@ struct sts_grid {
   bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
   bool graphs = true;                   // CUDA-graph replay of PCG iteration pairs (sts_grid_set_graphs)
   bool pcg_merged = true;               // one-pass PCG iteration where eligible (sts_grid_set_pcg_merged)
+  bool rkl2_dev = true;                 // RKL2 stages in deviation form where eligible (sts_grid_set_rkl2_deviation)
   cudaStream_t graph_stream = nullptr;  // non-blocking stream for capture / replay
   cudaEvent_t ev_c = nullptr;
   // per-kernel-class event timing (sts_grid_set_timing)
@@ -187,6 +188,7 @@ enum Epi : int {
   EPI_PCG_S,        // p = z + beta pold; x += ax pold; y = wV p - dt L p; partial p.y  (fused S-pass)
   EPI_PCG_M,        // merged iteration: z = zold - ax wold; p = z + beta pold; x += ax pold;
                     // y = wV p - dt L p; w = d y; partials z.z/d, p.y, z.y, w.y
+  EPI_RKL2_DSTAGE,  // deviation form D_j = Y_j - Y0: dj = mu*u + nu*dm2 + c0*F(u) + c1*M0 (no Y0 operand)
 };
 
 // PCG per-component scalars (device)
@@ -217,6 +219,7 @@ struct EpiArgs {
   const double* y0 = nullptr;  // Y_0
   const double* m0 = nullptr;  // M0 = F(Y_0)
   double mu = 0, nu = 0, c0 = 0, c1 = 0, c2 = 0, dt = 0;
+  double a0 = 1.0;             // EPI_RKL2_FIRST: out = a0*u + c0*F (deviation form: a0 = 0, D_1 = c0 M0)
   double* partials = nullptr;  // [value q][pstride]: per-CTA partial sums
   long long pstride = 0;       // stride between partial-value rows
   long long pbase = 0;         // this launch's first CTA slot

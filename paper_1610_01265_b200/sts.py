@@ -26,7 +26,8 @@ UID_BYTES = 128
 KERNEL_CLASSES = ["face_kappa", "aniso_F", "aniso_rkl2_first", "aniso_rkl2_stage", "aniso_pcg_r0",
                   "aniso_pcg_ap", "aniso_gersh", "iso_F", "iso_rkl2_first", "iso_rkl2_stage", "iso_pcg_r0",
                   "iso_pcg_ap", "iso_gersh", "pcg_update", "pcg_pupdate", "pcg_reduce", "halo",
-                  "vertex_coef", "aniso_pcg_s", "pcg_xfinal", "iso_pcg_s", "aniso_pcg_m", "iso_pcg_m"]
+                  "vertex_coef", "aniso_pcg_s", "pcg_xfinal", "iso_pcg_s", "aniso_pcg_m", "iso_pcg_m",
+                  "aniso_rkl2_dstage", "iso_rkl2_dstage"]
 
 _lib = None
 
@@ -60,6 +61,7 @@ def lib():
         "sts_grid_set_tma": (I, [P, I]),
         "sts_grid_set_graphs": (I, [P, I]),
         "sts_grid_set_pcg_merged": (I, [P, I]),
+        "sts_grid_set_rkl2_deviation": (I, [P, I]),
         "sts_grid_timing_reset": (I, [P]),
         "sts_grid_timing": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
         "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
@@ -195,6 +197,10 @@ class Grid:
     def set_pcg_merged(self, enable=True):
         """One fused pass + one reduction per PCG iteration (default) or the two-pass S / U iteration."""
         _check("sts_grid_set_pcg_merged", lib().sts_grid_set_pcg_merged(self._h, int(bool(enable))))
+
+    def set_rkl2_deviation(self, enable=True):
+        """RKL2 stages 2..s-1 on the deviation D_j = Y_j - Y0 (default) or on Y_j as Fig. 2 prints them."""
+        _check("sts_grid_set_rkl2_deviation", lib().sts_grid_set_rkl2_deviation(self._h, int(bool(enable))))
 
     def timing_reset(self):
         _check("sts_grid_timing_reset", lib().sts_grid_timing_reset(self._h))

@@ -169,14 +169,17 @@ def _gpu_rkl2_run(G, T0, cfg, ratio, nsteps, b, inplace=False):
     return T, ss
 
 
-@pytest.mark.parametrize("tma", [True, False])
+@pytest.mark.parametrize("tma,deviation", [(True, True), (True, False), (False, False)])
 @pytest.mark.parametrize("nsteps,tol", [(1, 1e-11), (20, 1e-9)])
-def test_rkl2_spitzer_parity(dev, nsteps, tol, tma):
+def test_rkl2_spitzer_parity(dev, nsteps, tol, tma, deviation):
+    """Fig. 2 on the lagged Spitzer operator: TMA kernels with the stages in deviation
+    form (default) or as printed, and the cp.async kernels."""
     cfg = W.make_config("c1_spitzer64", shape=(20, 19, 70))
     g = cfg["grid"]
     ref, s_ref = _oracle_rkl2_run(g, cfg["T"].numpy(), cfg, 100.0, nsteps, cfg["b"].numpy())
     G = sts().Grid.from_grid(g)
     G.set_tma(tma)
+    G.set_rkl2_deviation(deviation)
     out, s_gpu = _gpu_rkl2_run(G, cfg["T"].to(dev), cfg, 100.0, nsteps, cfg["b"].to(dev))
     assert s_gpu == s_ref
     assert rel_l2(cpu(out), ref) <= tol
@@ -205,7 +208,8 @@ def test_rkl2_config0_parity(dev):
     assert abs(float(u.sum()) - float(cfg["u"].sum())) <= 1e-12 * float(cfg["u"].abs().sum())
 
 
-def test_rkl2_viscosity_parity(dev):
+@pytest.mark.parametrize("deviation", [True, False])
+def test_rkl2_viscosity_parity(dev, deviation):
     cfg = W.make_config("c2_visc64", shape=(20, 19, 70))
     g = cfg["grid"]
     k = [f.numpy() for f in cfg["visc_faces"]]
@@ -215,6 +219,7 @@ def test_rkl2_viscosity_parity(dev):
     s = O.rkl2_num_stages(dt, dte)
     ref = O.rkl2_advance(lambda x: op.apply(x), cfg["v"].numpy(), dt, s)
     G = sts().Grid.from_grid(g)
+    G.set_rkl2_deviation(deviation)
     kd = [f.to(dev) for f in cfg["visc_faces"]]
     rho = cfg["rho"].to(dev)
     assert abs(G.dt_euler("iso", kd, None, rho) - dte) <= 1e-13 * dte
