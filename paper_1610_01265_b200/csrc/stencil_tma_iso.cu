@@ -104,10 +104,10 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   // pass reads metric-folded coefficients and needs none)
   static constexpr int COL = 0;
   static constexpr int FIX = COL * T::INT * 8 + 128;
-  // ring slots: 3 where MINB CTAs per SM fit (2 CTAs: <= 113 KB each), else 2
+  // ring slots: as many as MINB CTAs per SM fit (2 CTAs: <= 113 KB each), 2..4 (1 CTA: up to 6)
   static constexpr int NS1 = (SMEM_1CTA - 2048 - FIX) / (SLOT * 8 + 16);   // one CTA per SM: all that fit
-  static constexpr int NS = (MINB == 2) ? ((3 * (SLOT * 8 + 16) + FIX <= 113 * 1024) ? 3 : 2)
-                                        : (NS1 > 6 ? 6 : NS1);
+  static constexpr int NS2 = (113 * 1024 - FIX) / (SLOT * 8 + 16);   // two CTAs per SM
+  static constexpr int NS = (MINB == 2) ? (NS2 > 4 ? 4 : (NS2 < 2 ? 2 : NS2)) : (NS1 > 6 ? 6 : NS1);
   static constexpr size_t SMEM =
       (size_t)NS * SLOT * sizeof(double) + 3 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
   static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
