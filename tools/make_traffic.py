@@ -21,6 +21,8 @@ CLASSES = [
     (r"^void iso_tma_kernel<2,", "iso_rkl2_stage"),
     (r"^void iso_tma_kernel<5,", "iso_pcg_s"),
     (r"^void aniso_tma_kernel<6,", "aniso_pcg_m"),
+    (r"^void aniso_tma_kernel<7,", "aniso_rkl2_dstage"),
+    (r"^void iso_tma_kernel<7,", "iso_rkl2_dstage"),
     (r"^void iso_tma_kernel<6,", "iso_pcg_m"),
     (r"^void pcg_rupdate_kernel<3>", "pcg_update_c3"),
     (r"^void pcg_rupdate_kernel<1>", "pcg_update"),

@@ -4,7 +4,7 @@ set -x
 mkdir -p gpurun_out
 CMD="python tools/profile_step.py --config c3_spitzer256 --visc"
 $CMD > gpurun_out/plain_prof.log 2>&1 || exit 1
-KLIST=${KERNELS:-"aniso_tma_kernel<.int.2,..bool.0,..bool.0> aniso_tma_kernel<.int.6,..bool.0, iso_tma_kernel<.int.2,..int.3,..bool.0,..bool.0> iso_tma_kernel<.int.6,..int.3,..bool.0,"}
+KLIST=${KERNELS:-"aniso_tma_kernel<.int.7,..bool.0,..bool.0> aniso_tma_kernel<.int.6,..bool.0, iso_tma_kernel<.int.7,..int.3,..bool.0,..bool.0> iso_tma_kernel<.int.6,..int.3,..bool.0,"}
 for k in $KLIST; do
   tag=$(echo "$k" | tr -c 'a-zA-Z0-9_\n' '_')
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s 2 -c 1 \
