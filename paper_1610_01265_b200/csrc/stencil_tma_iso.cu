@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       if constexpr (kR0) {
         // PC1: d = 1/A_ii, A = wV - dt L, L_ii = -(sum of the face coefficients)
         const double Ldiag = -(kdn + Kup + Kjp + Kjm + Kkp + Kkm);
-        dinv = 1.0 / (WV - c.ea.dt * Ldiag);
+        dinv = rcp_pos(WV - c.ea.dt * Ldiag);   // (the merged pass recomputes it the same way)
         o4[gi] = dinv;
       }
 #pragma unroll
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         // PC1 diagonal of the own cell, the R0 pass's arithmetic (bit-identical d):
         // A_ii = wV - dt L_ii, L_ii = -(sum of the six face coefficients); r.z = z^2 A_ii
         const double Aii = C.WV - c.ea.dt * -(P.K + C.K + Kjp + Kjm + Kkp + Kkm);
-        C.dc = 1.0 / Aii;
+        C.dc = rcp_pos(Aii);
         const double idcell = Aii;
         const long long gi = (long long)il * pl + coff;
 #pragma unroll
