@@ -483,8 +483,8 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     // memory (the neighbour slab's halo plane at a slab boundary).
     // per-plane state carried to the next plane; two sets, unrolled by two (no moves)
     struct St {
-      double L[NC], u[NC], z[NC];   // L p without the r-up term, p, z of the own cell
-      double WV, dc, K;              // wV, d of the own cell, r-up face coefficient
+      double L[NC], u[NC], z[NC];   // off-diagonal face sum without the r-up term, p, z of the own cell
+      double A, dc, K;               // A_ii, d of the own cell, r-up face coefficient
     };
     St SA, SB;
 #pragma unroll
@@ -492,15 +492,16 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       SA.u[q] = udn[q];              // plane ib-1 (the down neighbour of plane ib)
       SA.L[q] = SA.z[q] = 0.0;
     }
-    SA.WV = SA.dc = 0.0;
+    SA.A = SA.dc = 0.0;
     SA.K = kdn;
     auto finish = [&](int il, const St& P, const double* uup) {   // y-dependent outputs of plane il
       const long long gi = (long long)il * pl + coff;
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
         if (skip[q]) continue;
-        const double Lu = P.L[q] + P.K * (uup[q] - P.u[q]);
-        const double y = P.WV * P.u[q] - c.ea.dt * Lu;
+        // y = A p = A_ii p - dt sum_f K_f p_f (the matrix row as assembled: diagonal + the
+        // six off-diagonal face couplings)
+        const double y = P.A * P.u[q] - c.ea.dt * fma(P.K, uup[q], P.L[q]);
         const double wk = P.dc * y;
         o3[gi + q * cs] = wk;
         part[q][1] += P.u[q] * y;
@@ -522,10 +523,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         const double Kjm = jm ? S[ok2m] : 0.0;
         const double Kkp = S[ok3p];
         const double Kkm = km ? S[ok3m] : 0.0;
-        C.WV = S[Lay::WB + o8];
+        const double WV = S[Lay::WB + o8];
         // PC1 diagonal of the own cell, the R0 pass's arithmetic (bit-identical d):
         // A_ii = wV - dt L_ii, L_ii = -(sum of the six face coefficients); r.z = z^2 A_ii
-        const double Aii = C.WV - c.ea.dt * -(P.K + C.K + Kjp + Kjm + Kkp + Kkm);
+        const double Aii = WV - c.ea.dt * -(P.K + C.K + Kjp + Kjm + Kkp + Kkm);
+        C.A = Aii;
         C.dc = rcp_pos(Aii);
         const double idcell = Aii;
         const long long gi = (long long)il * pl + coff;
@@ -536,7 +538,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           const double u0 = kF ? S[oq + Lay::FS] : (kP ? fma(sbeta[q], S[oq + 2 * Lay::FS], zk) : zk);
           const double ujm = sv(S, oq - SBW, 0, q), ujp = sv(S, oq + SBW, 0, q);
           const double ukm = sv(S, okm0 + q * okms, 0, q), ukp = sv(S, okp0 + q * okps, 0, q);
-          C.L[q] = P.K * (P.u[q] - u0) + Kjm * (ujm - u0) + Kjp * (ujp - u0) + Kkm * (ukm - u0) + Kkp * (ukp - u0);
+          C.L[q] = P.K * P.u[q] + Kjm * ujm + Kjp * ujp + Kkm * ukm + Kkp * ukp;
           C.u[q] = u0;
           C.z[q] = zk;
           if (!skip[q]) {
