@@ -200,14 +200,15 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
 
   // ======================= consumer warps =======================
   const int vj = tid >> 5, vk = tid & 31;
-#define beta sbx[0]
-#define ax sbx[1]
-#define ig3a sg3[vj]       /* vertex row jv = j0-1+vj */
-#define ig3b sg3[vj + 1]   /* and jv+1 (= the own cell row j) */
+  // references into shared memory (read where used; they hold no registers)
+  const double& beta = sbx[0];
+  const double& ax = sbx[1];
+  const double& ig3a = sg3[vj];       // vertex row jv = j0-1+vj
+  const double& ig3b = sg3[vj + 1];   // and jv+1 (= the own cell row j)
+  const double& ig3c = sg3[vj + 1];   // (own cells only)
   const int j = j0 + vj, k = k0 + vk;
   const bool own = vj < XOJ && vk < XOK && j < G.n2 && k < G.n3;
   const long long coff = own ? (long long)j * G.n3 + k : 0;
-#define ig3c sg3[vj + 1]   /* own cells only */
   const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
   // offset (within a staged field block) of the cell at tile row r (global j0-1+r)
   // and tile col t (global k0-1+t)
@@ -438,11 +439,6 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   }
 }
 
-#undef beta
-#undef ax
-#undef ig3a
-#undef ig3b
-#undef ig3c
 
 // ============================================================================
 // host side

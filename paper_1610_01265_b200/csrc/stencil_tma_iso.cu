@@ -99,17 +99,13 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int EP = WB + T::OWN;
   static constexpr int MT = EP + nepi * T::OWN;      // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  // (a variant short of registers could keep the six per-column metric products in
-  // shared memory, COL doubles per consumer thread after the mbarriers; the merged PCG
-  // pass reads metric-folded coefficients and needs none)
-  static constexpr int COL = 0;
-  static constexpr int FIX = COL * T::INT * 8 + 128;
+  static constexpr int FIX = 128;
   // ring slots: as many as MINB CTAs per SM fit (2 CTAs: <= 113 KB each), 2..4 (1 CTA: up to 6)
   static constexpr int NS1 = (SMEM_1CTA - 2048 - FIX) / (SLOT * 8 + 16);   // one CTA per SM: all that fit
   static constexpr int NS2 = (113 * 1024 - FIX) / (SLOT * 8 + 16);   // two CTAs per SM
   static constexpr int NS = (MINB == 2) ? (NS2 > 4 ? 4 : (NS2 < 2 ? 2 : NS2)) : (NS1 > 6 ? 6 : NS1);
   static constexpr size_t SMEM =
-      (size_t)NS * SLOT * sizeof(double) + 3 * NS * sizeof(uint64_t) + (size_t)COL * T::INT * sizeof(double) + 128;
+      (size_t)NS * SLOT * sizeof(double) + 3 * NS * sizeof(uint64_t) + 128;
   static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
 };
 
@@ -278,16 +274,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     cv[4] = km ? M.F3t[j] * M.F3p[kmw] : 0.0;
     cv[5] = M.Vt[j] * M.Vp[k];
   }
-  double* const colc = reinterpret_cast<double*>(formed + NS);
-  if constexpr (Lay::COL > 0) {
-#pragma unroll
-    for (int t = 0; t < 6; ++t) colc[t * INT + tid] = cv[t];   // read back by this thread only
-  }
-  // column constant t: a register, or (merged PCG) this thread's shared-memory copy
-  auto CV = [&](int t) -> double {
-    if constexpr (Lay::COL > 0) return colc[t * INT + tid];
-    return cv[t];
-  };
+  auto CV = [&](int t) -> double { return cv[t]; };   // per-column metric products
   // smem offsets (relative to the slot) of the own cell, its in-plane neighbours per
   // component (periodic phi wrap: cell n3-1 / 0 from the 2-column wrap boxes)
   const int oc = (tj + 1) * SBW + tk + 2;
