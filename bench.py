@@ -656,7 +656,10 @@ def main():
         hunits = sum(i["units"] for i in hinfos)
         e2e = {"value": ncells_total * hunits / (hms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": hstep.h2d * ws, "d2h_bytes_per_step": hstep.d2h * ws,
-               "steps": args.e2e_steps, "ms_per_step": hms / args.e2e_steps}
+               "steps": args.e2e_steps, "ms_per_step": hms / args.e2e_steps,
+               "mode": "host arrays uploaded and results downloaded every step on two copy streams, "
+                       "pipelined with the computation (next step's conduction inputs during this step's "
+                       "viscosity; first upload and last download exposed)"}
         del host_inp, hstep
 
     cpu_base = None
