@@ -24,8 +24,13 @@
 //   vertex coeffs e   : 34 x 8 per component from (even(k0), j0), vertex plane p-1
 //                       (padded e layout: zero row / wrap column built in)
 //   epilogue operands : 32 x 7 from (even(k0), j0), cell plane p-1
-// Epilogues: RKL2 first stage / stage recurrence (Fig. 2) and the fused
-// PCG S-pass  p = z + beta pold, x += ax pold, y = A p, partial p.y  (Fig. 1).
+// Ring depth: 4 slots (3 for the merged PCG pass, whose three staged fields make a
+// larger slot; 3 CTAs per SM either way).
+// Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
+// deviation form D_j = Y_j - Y0), the PCG initial residual with the Jacobi diagonal,
+// the two-pass PCG S-pass  p = z + beta pold, x += ax pold, y = A p, partial p.y, and
+// the merged one-pass PCG iteration (z = zold - ax wold, p = z + beta pold, y = A p,
+// w = d y, four partial sums; Fig. 1 reorganised).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>

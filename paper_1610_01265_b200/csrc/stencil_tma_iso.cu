@@ -5,20 +5,26 @@
 //   (L u)_i = sum_faces K_f (u_nb - u_i),   K_f = kappa_f A_f / h_f,   F = L u / (w V)
 // with exactly the arithmetic of iso_fast_kernel (stencil.cu).
 //
-// Warp-specialised: 7 consumer warps own a 7 x 32 (theta x phi) tile of cell
+// Warp-specialised: IJ consumer warps own an IJ x 32 (theta x phi) tile of cell
 // columns and march along r; one producer warp streams one "package" per r-plane
-// into a 3-slot shared-memory ring with cp.async.bulk.tensor (TMA):
-//   per component of each staged source field: 36 x 9 box from (k0-2, j0-1)
+// into a ring of shared-memory slots with cp.async.bulk.tensor (TMA):
+//   per component of each staged source field: 36 x (IJ+2) box from (k0-2, j0-1)
 //        (+ 2-column periodic-wrap boxes on the edge tiles),
-//   theta-face diffusivity k2: 32 x 8 from (k0, j0-1); phi-face k3: 34 x 7 from
-//   (k0-2, j0) (+ wrap), r-face k1 and w: 32 x 7, epilogue operands: 32 x 7 each.
+//   theta-face coefficient: 32 x (IJ+1) from (k0, j0-1); phi-face: 34 x IJ from
+//   (k0-2, j0) (+ wrap), r-face and w: 32 x IJ, epilogue operands: 32 x IJ each.
 // Every box origin column is even (16 B aligned, see tma.cuh).  A full mbarrier per
 // slot signals "landed", an empty mbarrier (one arrival per consumer warp) signals
-// "free"; there is no CTA-wide barrier in the march.  The r-neighbours of the own
-// column (planes il +- 1, possibly the neighbour slab's halo plane) come from
-// registers, prefetched two planes ahead with plain loads.
-// Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2), and the
-// fused PCG S-pass p = z + beta pold, x += ax pold, y = A p, p.y (Fig. 1).
+// "free"; there is no CTA-wide barrier in the march.
+// Tiles (IsoTile / IsoLay): 7 rows at two CTAs per SM for every pass but the
+// 3-component merged PCG pass, which runs 13 rows at one CTA per SM with an extra
+// "former" warp (see IsoLay::FORM).
+// Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
+// deviation form D_j = Y_j - Y0), the PCG initial residual (R0), the two-pass PCG
+// S-pass, and the merged one-pass PCG iteration (Fig. 1 reorganised,
+// DESIGN.md §5.3): z = zold - alpha wold, p = z + beta pold, x += alpha pold,
+// y = A p, w = d y and the four partial sums.  Passes other than the merged one take
+// the own column's r-neighbours from registers prefetched two planes ahead; the
+// merged pass takes the r-up neighbour from the next plane's slot instead.
 #include "sts_common.cuh"
 #include "tma.cuh"
 #include "pcg.cuh"
