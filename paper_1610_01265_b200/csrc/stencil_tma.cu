@@ -6,8 +6,8 @@
 // needs for one r-plane -- the staged source plane(s) with their theta/phi halo,
 // the three vertex coefficients, and the pointwise epilogue operands -- arrives
 // as ONE "package" of cp.async.bulk.tensor (TMA) boxes completing on one
-// mbarrier.  A 3-slot ring keeps two packages in flight while the CTA computes
-// on the third, so the bytes in flight per SM no longer depend on registers or
+// mbarrier.  A ring of slots keeps packages in flight while the CTA computes on
+// the oldest, so the bytes in flight per SM no longer depend on registers or
 // on how far each thread can prefetch (the limit ncu showed for the cp.async
 // fast path: 27-29 % of DRAM peak, long-scoreboard bound).
 //
