@@ -506,8 +506,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4_scale512", choices=list(RATIO))
     ap.add_argument("--impl", default="sts", choices=["sts", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3,
-                    help="end-to-end steps from pinned host memory (pipelined across steps)")
+    ap.add_argument("--e2e-steps", type=int, default=-1,
+                    help="end-to-end steps from pinned host memory, pipelined across steps "
+                         "(default: as many as --steps; 0 skips the leg)")
     ap.add_argument("--timing-steps", type=int, default=2,
                     help="instrumented steps (after the timed region) for the per-kernel breakdown")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -628,6 +629,8 @@ def main():
 
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
+    if args.e2e_steps < 0:
+        args.e2e_steps = args.steps
     if args.e2e_steps > 0:
         del step
         torch.cuda.empty_cache()
