@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b,
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
   const int R0 = blockIdx.y * VCJ, C0 = blockIdx.x * VCK;        // padded row / col origin
-  const int vlo = -1 + blockIdx.z * ic;                          // vertex planes [vlo, vhi)
+  const int vlo = -1 + (int)blockIdx.z * ic;                     // vertex planes [vlo, vhi)
   const int vhi = min(vlo + ic, G.nl);
   const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3), es = (long long)(G.nl + 1) * pp;
   // stage cell plane il (-1..nl) into ring slot sl: cells rows R0-1+r (r < 9), cols C0-1+c (c < 33)

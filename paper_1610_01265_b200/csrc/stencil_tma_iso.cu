@@ -505,8 +505,6 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     auto mbody = [&](int il, const St& P, St& C) {
       const int slot = (il - ib) % NS;
       const double* S = ring + slot * Lay::SLOT;
-      const int ig = G.i0 + il;
-      const bool ip = ig + 1 < G.n1g;
       mbar_wait((Lay::FORM ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
       C.K = 0.0;
       if (own) {
