@@ -374,7 +374,10 @@ def test_tma_kernels_match_oracle_and_cpasync(dev, shape, periodic, nv):
 
 
 ISO_CASES = [((20, 19, 70), True, 1, 3), ((13, 17, 64), False, 1, 3), ((5, 9, 2), True, 1, 2), ((9, 16, 96), True, 1, 1),
-             ((21, 19, 62), True, 3, 3), ((12, 8, 40), False, 2, 2), ((7, 23, 33), True, 1, 3)]
+             ((21, 19, 62), True, 3, 3), ((12, 8, 40), False, 2, 2), ((7, 23, 33), True, 1, 3),
+             # the 3-component merged pass's 13-row tile: one partial tile row, n3 = 2, and
+             # virtual slabs of 2, 1, 1 planes
+             ((6, 5, 8), True, 1, 3), ((5, 9, 2), True, 2, 3), ((4, 11, 16), False, 3, 3)]
 
 
 @pytest.mark.parametrize("shape,periodic,nv,nc", ISO_CASES)
