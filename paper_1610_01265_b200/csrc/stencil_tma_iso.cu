@@ -48,10 +48,11 @@ constexpr int SMEM_1CTA = 232448;         // max dynamic shared memory of one CT
 //    that to 96 and the 3-component PCG S-pass spills);
 //  * ISO_M3_ROWS (13) rows, 1 CTA per SM, for the 3-component merged PCG pass, whose
 //    three staged fields make a 7-row slot too large for three ring slots at 2 CTAs
-//    per SM: 13 consumer + producer + former warps, 128 registers (the pass reads
-//    metric-folded coefficients), three 72 KB slots.  Measured c4 fraction of the
-//    copy peak by rows: 7: 0.79, 8: 0.77, 9: 0.85, 11: 0.83, 12: 0.82, 13: 0.86
-//    (14 rows no longer fit three slots).
+//    per SM: 13 consumer + producer + ISO_FORMERS (2) former warps, 128 registers
+//    (the pass reads metric-folded coefficients), three 72 KB slots.  Measured c4
+//    fraction of the copy peak by rows (one former warp): 7: 0.79, 8: 0.77, 9: 0.85,
+//    11: 0.83, 12: 0.82, 13: 0.86 (14 rows no longer fit three slots); two former
+//    warps 0.874 at 13 rows (12 rows with three: 0.874, 11 with three: 0.81).
 template <int IJ_>
 struct IsoTile {
   static constexpr int IJ = IJ_;
@@ -81,7 +82,11 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   // once per staged position, instead of every consumer re-forming its 5-point
   // neighbourhood; consumers wait on a per-slot "formed" mbarrier
   static constexpr bool FORM = (EPI == EPI_PCG_M) && MINB == 1;
-  static constexpr int THREADS = T::INT + 32 + (FORM ? 32 : 0);
+#ifndef ISO_FORMERS
+#define ISO_FORMERS 2
+#endif
+  static constexpr int NFORM = FORM ? ISO_FORMERS : 0;   // former warps
+  static constexpr int THREADS = T::INT + 32 + 32 * NFORM;
   // staged fields: u | PCG S-pass r, pold | merged PCG zold, wold, pold
   static constexpr int nsrcf = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
   // own-box operands: RKL2 ym2, y0, M0 | S-pass x | merged x (d is recomputed from
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, IJ);
-      mbar_init(formed + s, 1);
+      mbar_init(formed + s, Lay::NFORM > 0 ? Lay::NFORM : 1);
     }
     mbar_fence_init();
   }
@@ -186,6 +191,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   // ======================= former warp (merged PCG) =======================
   if (Lay::FORM && tid >= INT + 32) {
     const int lane = tid & 31;
+    const int fl = tid - (INT + 32), fn = 32 * Lay::NFORM;   // this thread among the former warps
     for (int p = ib; p < ie; ++p) {
       const int slot = (p - ib) % NS;
       mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
@@ -198,9 +204,9 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         };
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-          for (int o = lane; o < SBW * SBH; o += 32) form(q * S_MAIN + o, q);
+          for (int o = fl; o < SBW * SBH; o += fn) form(q * S_MAIN + o, q);
           if (wrapL || wrapR)
-            for (int o = lane; o < 2 * S_W; o += 32) form(Lay::WRP + q * 2 * S_W + o, q);
+            for (int o = fl; o < 2 * S_W; o += fn) form(Lay::WRP + q * 2 * S_W + o, q);
         }
       }
       __syncwarp();
