@@ -17,7 +17,7 @@
 // "free"; there is no CTA-wide barrier in the march.
 // Tiles (IsoTile / IsoLay): 7 rows at two CTAs per SM for every pass but the
 // 3-component merged PCG pass, which runs 13 rows at one CTA per SM with an extra
-// "former" warp (see IsoLay::FORM).
+// "former" warps (see IsoLay::FORM).
 // Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
 // deviation form D_j = Y_j - Y0), the PCG initial residual (R0), the two-pass PCG
 // S-pass, and the merged one-pass PCG iteration (Fig. 1 reorganised,
@@ -77,10 +77,11 @@ template <int EPI, int NC>
 struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   using T = IsoTile<iso_rows(EPI, NC)>;
   static constexpr int MINB = iso_minb(EPI, NC);   // CTAs per SM (launch bounds)
-  // merged PCG, one CTA per SM: a "former" warp turns each landed slot's zold, wold,
+  // merged PCG, one CTA per SM: "former" warps turn each landed slot's zold, wold,
   // pold into z_k = zold - alpha wold (field 0) and p_k = z_k + beta pold (field 1)
   // once per staged position, instead of every consumer re-forming its 5-point
-  // neighbourhood; consumers wait on a per-slot "formed" mbarrier
+  // neighbourhood; consumers wait on a per-slot "formed" mbarrier (one arrival per
+  // former warp)
   static constexpr bool FORM = (EPI == EPI_PCG_M) && MINB == 1;
 #ifndef ISO_FORMERS
 #define ISO_FORMERS 2
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   double* ring = smi;
   uint64_t* full = reinterpret_cast<uint64_t*>(smi + NS * Lay::SLOT);
   uint64_t* empty = full + NS;
-  uint64_t* formed = empty + NS;     // (merged PCG with a former warp)
+  uint64_t* formed = empty + NS;     // (merged PCG with former warps)
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 
   // ======================= producer warp =======================
   constexpr bool kF = Lay::FORM && kP;   // consumers read formed z_k / p_k
-  // ======================= former warp (merged PCG) =======================
+  // ======================= former warps (merged PCG) =======================
   if (Lay::FORM && tid >= INT + 32) {
     const int lane = tid & 31;
     const int fl = tid - (INT + 32), fn = 32 * Lay::NFORM;   // this thread among the former warps
