@@ -16,7 +16,7 @@
 // slot signals "landed", an empty mbarrier (one arrival per consumer warp) signals
 // "free"; there is no CTA-wide barrier in the march.
 // Tiles (IsoTile / IsoLay): 7 rows at two CTAs per SM for every pass but the
-// 3-component merged PCG pass, which runs 13 rows at one CTA per SM with an extra
+// 3-component merged PCG pass, which runs 13 rows at one CTA per SM with two
 // "former" warps (see IsoLay::FORM).
 // Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
 // deviation form D_j = Y_j - Y0), the PCG initial residual (R0), the two-pass PCG
