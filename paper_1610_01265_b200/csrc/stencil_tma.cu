@@ -375,10 +375,13 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           const double y = WV * uc - c.ea.dt * Lu;
           const double dd = O[OW_D * O_PART];
           const double wk = dd * y;
-          c.ea.out[gi] = zc;
-          c.ea.out2[gi] = uc;
-          c.ea.out3[gi] = wk;
-          if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);
+          // streaming stores (evict-first in L2): the outputs are read again only by the
+          // next pass, after far more than L2 has streamed through; L2 keeps the input
+          // halo rows the neighbouring tiles re-read instead
+          __stcs(c.ea.out + gi, zc);
+          __stcs(c.ea.out2 + gi, uc);
+          __stcs(c.ea.out3 + gi, wk);
+          if (!first) __stcs(c.ea.x + gi, fma(ax, poc, O[OW_X * O_PART]));
           part += zc * zc * rcp_pos(dd);
           part2 += uc * y;
           part3 += zc * y;

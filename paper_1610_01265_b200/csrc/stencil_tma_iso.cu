@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         // six off-diagonal face couplings)
         const double y = P.A * P.u[q] - c.ea.dt * fma(P.K, uup[q], P.L[q]);
         const double wk = P.dc * y;
-        o3[gi + q * cs] = wk;
+        __stcs(o3 + gi + q * cs, wk);   // (streaming stores: see the aniso merged pass)
         part[q][1] += P.u[q] * y;
         part[q][2] += P.z[q] * y;
         part[q][3] += wk * y;
@@ -541,9 +541,9 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           C.z[q] = zk;
           if (!skip[q]) {
             const long long go = gi + q * cs;
-            o1[go] = zk;
-            o2[go] = u0;
-            if constexpr (kP) ox[go] = fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
+            __stcs(o1 + go, zk);
+            __stcs(o2 + go, u0);
+            if constexpr (kP) __stcs(ox + go, fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]));
             part[q][0] += zk * zk * idcell;
           }
         }

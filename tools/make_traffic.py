@@ -1,10 +1,11 @@
 """DRAM traffic per cell of the hot kernels from `ncu --set full` captures.
 
-  python tools/make_traffic.py gpurun_out/prof_*.ncu-rep > profiles/ncu_traffic.json
+  python tools/make_traffic.py [--cells N] gpurun_out/prof_*.ncu-rep > profiles/ncu_traffic.json
 
 The captures come from tools/prof_kernels.sh (tools/profile_step.py: the c4 recipe
-at the c3 size 256 x 256 x 512, one launch per kernel).  bench.py multiplies the
-per-cell figure by its local cell count to fill roofline.traffic.
+at the c3 size 256 x 256 x 512, one launch per kernel; --cells 268435456 for captures
+of the full c4 grid).  bench.py multiplies the per-cell figure by its local cell count
+to fill roofline.traffic.
 """
 import csv
 import io
@@ -16,7 +17,7 @@ import sys
 CELLS = 256 * 256 * 512
 # demangled kernel name -> bench.py kernel class
 CLASSES = [
-    (r"^void aniso_tma_kernel<2,", "aniso_rkl2_stage"),
+    (r"^void (sts::)?aniso_tma_kernel<(\(int\))?2,", "aniso_rkl2_stage"),
     (r"^void aniso_tma_kernel<5,", "aniso_pcg_s"),
     (r"^void iso_tma_kernel<2,", "iso_rkl2_stage"),
     (r"^void iso_tma_kernel<5,", "iso_pcg_s"),
@@ -30,8 +31,8 @@ CLASSES = [
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def main(paths):
-    out = {"cells": CELLS, "source": "ncu --set full --clock-control none, tools/prof_kernels.sh",
+def main(paths, cells=CELLS):
+    out = {"cells": cells, "source": "ncu --set full --clock-control none, tools/prof_kernels.sh",
            "dram_bytes_per_cell": {}, "dram_pct": {}, "duration_us": {}}
     for p in paths:
         txt = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"],
@@ -48,7 +49,7 @@ def main(paths):
                 continue
             rd = float(d["dram__bytes_read.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_read.sum")]]
             wr = float(d["dram__bytes_write.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_write.sum")]]
-            out["dram_bytes_per_cell"][cls] = round((rd + wr) / CELLS, 3)
+            out["dram_bytes_per_cell"][cls] = round((rd + wr) / cells, 3)
             out["dram_pct"][cls] = float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"].replace(",", ""))
             dur = float(d["gpu__time_duration.sum"].replace(",", ""))
             unit = u[h.index("gpu__time_duration.sum")]
@@ -57,4 +58,8 @@ def main(paths):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:])
+    args = sys.argv[1:]
+    cells = CELLS
+    if args and args[0] == "--cells":
+        cells, args = int(args[1]), args[2:]
+    main(args, cells)
