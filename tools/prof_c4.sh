@@ -1,3 +1,6 @@
+# ncu --set full captures of the four hot kernels on the FULL c4 grid (512 x 512 x 1024,
+# the bench workload), one launch each; run only after the same command exited 0.
+#   bash tools/prof_c4.sh && python tools/make_traffic.py --cells 268435456 gpurun_out/c4prof_*.ncu-rep
 mkdir -p gpurun_out
 python tools/profile_step.py --config c4_scale512 --visc > gpurun_out/pp.log 2>&1 || exit 1
 for K in "sts::aniso_tma_kernel<.int.6" "sts::iso_tma_kernel<.int.6" "sts::aniso_tma_kernel<.int.7" "sts::iso_tma_kernel<.int.7"; do
