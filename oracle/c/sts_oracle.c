@@ -94,6 +94,7 @@ static void face_geo(const grid_t* g, int d, int i, int j, int k, double* A, dou
 void oc_face_kappa(const grid_t* g, const double* T, double kappa0, double T_cut, double fc_r0, double fc_w,
                    double* k1, double* k2, double* k3) {
   double* K[3] = {k1, k2, k3};
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < g->n1; ++i)
     for (int j = 0; j < g->n2; ++j)
       for (int k = 0; k < g->n3; ++k)
@@ -408,4 +409,153 @@ int oc_be_pcg(const grid_t* g, int mode, int ncomp, const double* k1, const doub
   }
   free(WV); free(diag); free(r); free(z); free(p); free(y); free(Lx); free(rhs);
   return last;
+}
+
+/* ---------------------------------------------------------------------------
+ * Full-grid checker (test infrastructure for the production-size parity tests).
+ * Row c of L assembled on its own, matrix-free, from the same vertex / face
+ * definitions as assemble_rows (DESIGN R2) -- the "gather" view of the same sum:
+ *   anisotropic: L_cq = -sum over the vertices v that contain cell c (the upper
+ *                corners of the cells c - (a, b, e), a, b, e in {0, 1}) of
+ *                C_v w_{v,p} w_{v,q}, p the slot(s) of c in v;
+ *   isotropic  : L_cc = -sum K_f, L_co = +K_f over the faces f between c and o != c.
+ * No n x 27 row table is held, so it runs at the 268M-cell configs[4] size, one
+ * OpenMP thread per r-plane range (rows are independent; nothing is shared).
+ * ------------------------------------------------------------------------- */
+static void row_gather(const grid_t* g, int mode, const double* const kap[3], const double* b, int i, int j, int k,
+                       row_t* R) {
+  const long c = idx(g, i, j, k);
+  R->cnt = 0;
+  if (mode == 0) {
+    for (int d = 0; d < 3; ++d) {
+      int ii, jj, kk;
+      double A, h;
+      /* the + face of c */
+      if (plus(g, d, i, j, k, &ii, &jj, &kk) && idx(g, ii, jj, kk) != c) {
+        face_geo(g, d, i, j, k, &A, &h);
+        const double K = kap[d][c] * A / h;
+        row_add(R, c, -K);
+        row_add(R, idx(g, ii, jj, kk), K);
+      }
+      /* the + face of the - neighbour m (whose + neighbour is c) */
+      int mi = i, mj = j, mk = k, ok = 1;
+      if (d == 0) { if (i == 0) ok = 0; else mi = i - 1; }
+      else if (d == 1) { if (j == 0) ok = 0; else mj = j - 1; }
+      else { if (k > 0) mk = k - 1; else if (g->periodic3) mk = g->n3 - 1; else ok = 0; }
+      if (ok && idx(g, mi, mj, mk) != c) {
+        face_geo(g, d, mi, mj, mk, &A, &h);
+        const double K = kap[d][idx(g, mi, mj, mk)] * A / h;
+        row_add(R, c, -K);
+        row_add(R, idx(g, mi, mj, mk), K);
+      }
+    }
+    return;
+  }
+  long seen[8];
+  int nseen = 0;
+  for (int s = 0; s < 8; ++s) {
+    int bi = i - ((s >> 2) & 1), bj = j - ((s >> 1) & 1), bk = k - (s & 1);
+    if (bi < 0 || bj < 0) continue;
+    if (bk < 0) {
+      if (!g->periodic3) continue;
+      bk += g->n3;
+    }
+    const long base = idx(g, bi, bj, bk);
+    int dup = 0;
+    for (int t = 0; t < nseen; ++t) dup |= (seen[t] == base);
+    if (dup) continue;   /* (n3 = 1 periodic: both phi offsets name the same vertex) */
+    seen[nseen++] = base;
+    vertex_t v;
+    if (!vertex(g, kap, b, bi, bj, bk, &v)) continue;
+    for (int p = 0; p < 8; ++p) {
+      if (v.id[p] != c) continue;
+      for (int q = 0; q < 8; ++q) row_add(R, v.id[q], -v.C * v.w[p] * v.w[q]);
+    }
+  }
+}
+
+/*
+ * For the backward-Euler system A = wV - dt L, rhs = wV un (Eq. 4,
+ * DESIGN R7) and a candidate solution x, per component c:
+ *   out[4c+0] = sum_i r_i^2 / A_ii      (r = rhs - A x; the stopping-test norm of DESIGN R8)
+ *   out[4c+1] = sum_i rhs_i^2 / A_ii
+ *   out[4c+2] = max_i |r_i| / max_i |rhs_i|
+ *   out[4c+3] = 0
+ * and *lam = max_i sum_q |L_iq| / (w V)_i (the Appendix B Gershgorin bound).
+ * x may be NULL (then only *lam is computed).
+ */
+void oc_check_full(const grid_t* g, int mode, int ncomp, const double* k1, const double* k2, const double* k3,
+                   const double* b, const double* w, const double* un, const double* x, double dt, double* out,
+                   double* lam) {
+  const double* kap[3] = {k1, k2, k3};
+  const long n = (long)g->n1 * g->n2 * g->n3;
+  double acc[3][4] = {{0}};
+  double lmax = 0.0;
+  for (int c = 0; c < ncomp; ++c) acc[c][0] = acc[c][1] = acc[c][2] = acc[c][3] = 0.0;
+#pragma omp parallel
+  {
+    double a[3][4] = {{0}};
+    double lm = 0.0;
+    row_t R;
+#pragma omp for schedule(dynamic, 1) collapse(2)
+    for (int i = 0; i < g->n1; ++i)
+      for (int j = 0; j < g->n2; ++j)
+        for (int k = 0; k < g->n3; ++k) {
+          const long q = idx(g, i, j, k);
+          row_gather(g, mode, kap, b, i, j, k, &R);
+          const double wv = (w ? w[q] : 1.0) * volume(g, i, j, k);
+          double s = 0.0;
+          for (int t = 0; t < R.cnt; ++t) s += fabs(R.val[t]);
+          if (s / wv > lm) lm = s / wv;
+          if (!x) continue;
+          const double Aii = wv - dt * row_diag(&R, q);
+          for (int c = 0; c < ncomp; ++c) {
+            const double* xc = x + c * n;
+            double Lx = 0.0;
+            for (int t = 0; t < R.cnt; ++t) Lx += R.val[t] * xc[R.id[t]];
+            const double rhs = wv * un[c * n + q];
+            const double r = rhs - (wv * xc[q] - dt * Lx);
+            a[c][0] += r * r / Aii;
+            a[c][1] += rhs * rhs / Aii;
+            if (fabs(r) > a[c][2]) a[c][2] = fabs(r);
+            if (fabs(rhs) > a[c][3]) a[c][3] = fabs(rhs);
+          }
+        }
+#pragma omp critical
+    {
+      if (lm > lmax) lmax = lm;
+      for (int c = 0; c < ncomp; ++c) {
+        acc[c][0] += a[c][0];
+        acc[c][1] += a[c][1];
+        if (a[c][2] > acc[c][2]) acc[c][2] = a[c][2];
+        if (a[c][3] > acc[c][3]) acc[c][3] = a[c][3];
+      }
+    }
+  }
+  for (int c = 0; c < ncomp; ++c) {
+    out[4 * c + 0] = acc[c][0];
+    out[4 * c + 1] = acc[c][1];
+    out[4 * c + 2] = acc[c][3] > 0.0 ? acc[c][2] / acc[c][3] : acc[c][2];
+    out[4 * c + 3] = 0.0;
+  }
+  *lam = lmax;
+}
+
+/* OpenMP threads of the checker (bench.py's cpu_baseline pins the oracle to 1) */
+void oc_set_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+int oc_max_threads(void) {
+#ifdef _OPENMP
+  extern int omp_get_max_threads(void);
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
 }

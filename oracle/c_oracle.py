@@ -17,9 +17,10 @@ _lib = None
 
 
 def build(force=False):
-    """Compile the C oracle (gcc -O2, plain C11; no CUDA)."""
+    """Compile the C oracle (gcc -O2, plain C11, OpenMP for the full-grid checker; no CUDA)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.run(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", LIB + ".tmp", SRC, "-lm"], check=True)
+        subprocess.run(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC", "-o", LIB + ".tmp", SRC, "-lm"],
+                       check=True)
         os.replace(LIB + ".tmp", LIB)
     return LIB
 
@@ -45,6 +46,9 @@ def lib():
         L.oc_rkl2_advance.argtypes = [G, I, I, P, P, P, P, P, P, D, I, P]
         L.oc_be_pcg.argtypes = [G, I, I, P, P, P, P, P, P, D, D, I, P, P]
         L.oc_be_pcg.restype = I
+        L.oc_check_full.argtypes = [G, I, I, P, P, P, P, P, P, P, D, P, P]
+        L.oc_set_threads.argtypes = [I]
+        L.oc_max_threads.restype = I
         _lib = L
     return _lib
 
@@ -124,3 +128,29 @@ def be_pcg_solve(g, un, kap, b, w, dt, rtol=1e-12, kmax=100000):
     lib().oc_be_pcg(G.ptr, mode, ncomp, *[_p(a) for a in kap], _p(b), _p(w), _p(un), float(dt), float(rtol),
                     int(kmax), _p(x), it)
     return x, list(it)
+
+
+def set_threads(n):
+    """OpenMP threads of the oracle's parallel loops (face kappa, full-grid checker)."""
+    lib().oc_set_threads(int(n))
+
+
+def max_threads():
+    return lib().oc_max_threads()
+
+
+def check_full(g, un, kap, b, w, x, dt):
+    """Matrix-free full-grid check of a backward-Euler iterate (oc_check_full): per
+    component (sum r^2/A_ii, sum rhs^2/A_ii, max|r|/max|rhs|) for A = wV - dt L,
+    rhs = wV un, r = rhs - A x, and the Gershgorin lambda_max of M = L/(wV).
+    x None: only lambda_max.  Returns (list of per-component tuples, lambda_max)."""
+    G = CGrid(g)
+    kap, b, w, mode = _args(kap, b, w)
+    un = _c(un)
+    ncomp = 1 if un is None or un.ndim == 3 else un.shape[0]
+    x = _c(x)
+    out = np.zeros(4 * ncomp)
+    lam = ctypes.c_double()
+    lib().oc_check_full(G.ptr, mode, ncomp, *[_p(a) for a in kap], _p(b), _p(w), _p(un), _p(x), float(dt),
+                        _p(out), ctypes.byref(lam))
+    return [tuple(out[4 * c:4 * c + 3]) for c in range(ncomp)], lam.value

@@ -87,3 +87,57 @@ def test_c_stage_count_brute_force():
         smin = next(t for t in range(2, 100000) if (t * t + t - 2) / 4.0 >= r * (1 - 1e-15))
         assert C.rkl2_num_stages(r, 1.0) == smin
     assert (C.rkl2_num_stages(1, 1), C.rkl2_num_stages(100, 1), C.rkl2_num_stages(500, 1)) == (2, 20, 45)
+
+
+@pytest.mark.parametrize("case", GRIDS)
+def test_c_oracle_fc_branch_matches_numpy(case):
+    """The f_c(r) factor of the C oracle's face diffusivity, with the
+    half-value radius placed inside the grid, against the numpy oracle (itself pinned by
+    hand values in test_oracle_operator.py::test_fc_*)."""
+    g = _grid(*case)
+    T, _, _, _ = _inputs(g, 3, False)
+    r0 = float(np.median(g.x1c))
+    kc = C.face_kappa(g, T, 1e-9, 5e5, r0, 0.3)
+    ko = O.spitzer_face_kappa(g, T, 1e-9, 5e5, r0, 0.3)
+    off = O.spitzer_face_kappa(g, T, 1e-9, 5e5)
+    for a, e, o in zip(kc, ko, off):
+        np.testing.assert_allclose(a, e, rtol=1e-13, atol=0)
+    if g.geom == "spherical":
+        assert any(np.any(e != o) for e, o in zip(ko, off))   # the profile is active
+
+
+@pytest.mark.parametrize("case", GRIDS)
+@pytest.mark.parametrize("aniso", [False, True])
+def test_full_grid_checker_matches_assembled_system(case, aniso):
+    """oc_check_full (row c of L gathered matrix-free from the vertices / faces around c)
+    against the numpy oracle's assembled sparse system: the Gershgorin bound of App. B
+     and the preconditioned residual norms of the BE system (DESIGN R7, R8)
+    for a perturbed iterate, for the direct solution (residual at rounding level) and
+    for 3 components."""
+    g = _grid(*case)
+    T, kap, b, w = _inputs(g, 11, aniso)
+    op = O.Operator(g, kap, b, w)
+    dte = O.dt_euler(op)
+    dt = 30.0 * dte
+    A = O.be_system(op, dt)
+    D = A.diagonal()
+    rng = np.random.default_rng(5)
+    x = T * (1.0 + 1e-3 * rng.normal(size=g.shape))
+    res, lam = C.check_full(g, T, kap, b, w, x, dt)
+    assert abs(2.0 / lam - dte) <= 1e-13 * dte
+    rhs = op.WV * T.ravel()
+    r = rhs - A @ x.ravel()
+    num, den, mx = res[0]
+    assert abs(num - float(r @ (r / D))) <= 1e-10 * float(r @ (r / D))
+    assert abs(den - float(rhs @ (rhs / D))) <= 1e-13 * den
+    assert abs(mx - np.abs(r).max() / np.abs(rhs).max()) <= 1e-10 * mx
+    import scipy.sparse.linalg as spl
+    xe = spl.spsolve(A.tocsc(), rhs).reshape(g.shape)
+    (num_e, den_e, _), = C.check_full(g, T, kap, b, w, xe, dt)[0]
+    assert num_e <= 1e-26 * den_e
+    v = np.stack([T, x, xe])
+    res3, lam3 = C.check_full(g, v, kap, b, w, np.stack([xe, xe, x]), dt)
+    assert lam3 == lam and res3[0][0] <= 1e-26 * res3[0][1]
+    for q, xq in ((1, xe), (2, x)):
+        rq = op.WV * v[q].ravel() - A @ xq.ravel()
+        assert abs(res3[q][0] - float(rq @ (rq / D))) <= 1e-9 * float(rq @ (rq / D)) + 1e-26 * res3[q][1]

@@ -61,6 +61,45 @@ def test_spitzer_kappa_closed_form():
     assert abs(O.beta_tcut(Tc * (1 - 1e-12), Tc) - 1.0) < 1e-11
 
 
+# tanh(1), written out (not computed): 0.76159415595576488812 (Abramowitz & Stegun Table 4.11)
+TANH1 = 0.7615941559557649
+
+
+def test_fc_profile_hand_values():
+    """PAPER.md:183 f_c(r) = 0.5 (1 - tanh[(r - 10 R_sun) / 0.5 R_sun]) at hand-evaluated
+    points: the half-value radius, one width either side, far inside / outside, the
+    f_c + f_nc = 1 symmetry about 10 R_sun, monotone decrease, and f_c = 1 when off."""
+    f = lambda r: float(O.f_c(np.array([r]), 10.0, 0.5)[0])  # noqa: E731
+    assert f(10.0) == 0.5
+    assert abs(f(10.5) - 0.5 * (1.0 - TANH1)) <= 1e-16
+    assert abs(f(9.5) - 0.5 * (1.0 + TANH1)) <= 1e-16
+    # the logistic form 0.5 (1 - tanh x) = 1 / (1 + e^{2x}), x = (r - 10)/0.5, far from the
+    # half-value radius (r << 10: f_c -> 1, e^{-36} below 1 at r = 1; r >> 10: f_c -> 0)
+    for r, x in ((1.0, -18.0), (8.0, -4.0), (12.0, 4.0), (15.0, 10.0), (19.5, 19.0)):
+        assert abs(f(r) - 1.0 / (1.0 + math.exp(2.0 * x))) <= 1e-12 * f(r) + 4.5e-16, r
+    r = np.linspace(1.0, 20.0, 2001)
+    fc = O.f_c(r, 10.0, 0.5)
+    assert np.all(np.diff(fc) <= 0.0)
+    np.testing.assert_allclose(O.f_c(10.0 + (r - 1.0), 10.0, 0.5) + O.f_c(10.0 - (r - 1.0), 10.0, 0.5), 1.0,
+                               rtol=0, atol=2e-16)
+    assert np.all(O.f_c(r, 10.0, 0.0) == 1.0)
+
+
+def test_fc_face_kappa_evaluation_radius():
+    """The f_c factor of the lagged face diffusivity (PAPER.md:173 boxed term) is taken at
+    the face's own radius: r_{i+1/2} for r-faces, the cell centre r_i for theta / phi faces
+    (DESIGN R3).  A grid with an r-face exactly at 10 R_sun and a cell centred at 10.5."""
+    x1f = np.array([9.0, 9.5, 10.0, 11.0, 12.0])      # centres 9.25, 9.75, 10.5, 11.5
+    g = W.Grid("spherical", x1f, np.linspace(0.5, 2.5, 4), np.linspace(0.0, 1.0, 4), False)
+    T = np.full(g.shape, 1.0e6)
+    on = O.spitzer_face_kappa(g, T, 1.0, 5e5, 10.0, 0.5)
+    off = O.spitzer_face_kappa(g, T, 1.0, 5e5, 10.0, 0.0)
+    assert on[0][1, 0, 0] == 0.5 * off[0][1, 0, 0]                             # r-face at r = 10
+    assert abs(on[1][2, 0, 0] / off[1][2, 0, 0] - 0.5 * (1 - TANH1)) <= 1e-15  # theta face, r_c = 10.5
+    assert abs(on[2][2, 1, 0] / off[2][2, 1, 0] - 0.5 * (1 - TANH1)) <= 1e-15  # phi face, r_c = 10.5
+    assert abs(on[0][0, 0, 0] / off[0][0, 0, 0] - 0.5 * (1 + TANH1)) <= 1e-15  # r-face at 9.5
+
+
 # ------------------------------------------------------------------ spectral pin
 @pytest.mark.parametrize("shape,h,periodic", [((6, 7, 8), (1.0, 0.5, 2.0), False),
                                               ((5, 4, 9), (0.3, 0.3, 0.7), True)])
