@@ -61,6 +61,9 @@ typedef struct sts_grid sts_grid;
 #define STS_ERR_NOT_CONVERGED (-4)/* PCG hit kmax; outputs hold the last iterate    */
 #define STS_ERR_STATE (-5)        /* call not valid in the grid's current state     */
 #define STS_ERR_ALLOC (-6)        /* device allocation failed                       */
+#define STS_ERR_BREAKDOWN (-7)    /* PCG breakdown: p.A p <= 0 or a non-finite scalar
+                                     (A not SPD, or NaN / inf input); outputs hold the
+                                     last iterate                                   */
 
 #define STS_GEOM_CARTESIAN 0
 #define STS_GEOM_SPHERICAL 1
@@ -266,6 +269,9 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
  *   n_euler explicit Euler steps  u <- u + dte F(u),  dte = euler_frac dt / n_euler,
  *   then n_sub RKL2 super-steps of dtr = (1 - euler_frac) dt / n_sub, each with
  *   s = rkl2_num_stages(dtr, dt_exp, 0) stages (Fig. 2).
+ *  n_euler < 0 selects the default ceil(euler_frac dt / (dt_exp/2)) (0 if euler_frac = 0):
+ *  sub-steps of at most dt_exp/2, the step 1 + (dt_exp/2)(-2/dt_exp) = 0 that annihilates
+ *  the highest mode (DESIGN R11).
  *  Requirements: 0 <= euler_frac < 1; n_euler > 0 exactly when euler_frac > 0;
  *  dte <= dt_exp (explicit stability); n_sub >= 1.
  *  stages_out: host int[2] = {n_euler, s} (may be NULL).  u1 may alias u0.
@@ -283,7 +289,9 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
  *   stop when r.z <= rtol^2 (b . P^-1 b), independently per component.
  *  un, un1 [ncomp][nl][n2][n3] (may alias); iters_out: host int[ncomp] receives
  *  the A p products each component used (may be NULL).  kmax >= 1.
- *  Returns STS_ERR_NOT_CONVERGED (un1 = last iterate) if a component hits kmax.
+ *  Returns STS_ERR_NOT_CONVERGED (un1 = last iterate) if a component hits kmax,
+ *  STS_ERR_BREAKDOWN if a component's p.A p is not positive or a PCG scalar is not
+ *  finite (A not SPD, NaN / inf in the inputs; that component stops, un1 = last iterate).
  *  Synchronises `stream` (the host polls the device-side convergence flags
  *  once per batch of iterations).  By default each iteration is one fused
  *  stencil pass and one reduction (sts_grid_set_pcg_merged; the convergence

@@ -13,10 +13,19 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
 def nccl_flags():
-    # NCCL headers/libraries: system copy (same ABI as the torch-bundled one that
-    # is already loaded when the library is opened from Python)
-    inc, libdir = "/usr/include", "/usr/lib/x86_64-linux-gnu"
-    return [f"-I{inc}", f"-L{libdir}", "-lnccl"]
+    """NCCL headers and library: the copy bundled with torch (nvidia-nccl wheel), which is
+    the one already loaded in every Python process that imports torch, so the headers the
+    library is compiled against match the runtime; the rpath makes a plain C program
+    (examples/c_abi_demo.c) load the same copy.  Falls back to the system NCCL."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        inc, libdir = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(libdir, "libnccl.so.2")):
+            return [f"-I{inc}", f"-L{libdir}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}"]
+    except ImportError:
+        pass
+    return ["-I/usr/include", "-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
 
 
 def build(force=False, verbose=True):

@@ -354,18 +354,20 @@ void launch_pcg_pnew(int ncomp, long long n, long long cs, double* pnew, const d
 
 // grid of the U-pass: exactly the resident capacity (blocks per SM x 148, at most
 // PW_BLOCKS), so the grid-stride loop has no partial last wave
+// (cached per device ordinal: devices may differ in SM count)
 template <class K>
 static int resident_grid(K kernel) {
-  static int cached = 0;
-  if (!cached) {
-    int per_sm = 0;
+  static std::atomic<int> cached[64];
+  const int dev = current_device() & 63;
+  int v = cached[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    int per_sm = 0, sms = 148;
     STS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
-    int dev = 0, sms = 148;
-    STS_CUDA(cudaGetDevice(&dev));
-    STS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    cached = std::max(1, std::min(PW_BLOCKS, per_sm * sms));
+    STS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()));
+    v = std::max(1, std::min(PW_BLOCKS, per_sm * sms));
+    cached[dev].store(v, std::memory_order_relaxed);
   }
-  return cached;
+  return v;
 }
 
 template <int NC>

@@ -176,6 +176,9 @@ static bool needs_halos(const sts_grid* g) {
 //  * neighbouring ranks: ncclSend / ncclRecv of one plane per component
 static void exchange(sts_grid* g, int slot, const double* arr, int ncomp, cudaStream_t st) {
   if (!needs_halos(g)) return;
+  if (g->comm == nullptr && g->n_virtual == 1)
+    throw Error{STS_ERR_STATE, "this handle is an r-slab of a distributed grid (i0 > 0 or i0 + nl < n1): "
+                               "call sts_comm_init before any operator"};
   ensure_halos(g);
   Timed t(g, STS_K_HALO, st, false);
   const long long P = g->plane;
@@ -1018,7 +1021,9 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
     check_mode(mode, ncomp, b);
     STS_REQUIRE(std::isfinite(dt) && dt >= 0.0 && std::isfinite(dt_exp) && dt_exp > 0.0, "bad dt / dt_exp");
     STS_REQUIRE(euler_frac >= 0.0 && euler_frac < 1.0, "euler_frac must be in [0, 1)");
-    STS_REQUIRE(n_sub >= 1 && n_euler >= 0, "n_sub >= 1, n_euler >= 0");
+    STS_REQUIRE(n_sub >= 1, "n_sub must be >= 1");
+    if (n_euler < 0)   // default (DESIGN R11): sub-steps of dt_exp/2, which annihilate the highest mode
+      n_euler = euler_frac == 0.0 ? 0 : (int)std::ceil(euler_frac * dt / (0.5 * dt_exp) - 1e-12);
     STS_REQUIRE((n_euler == 0) == (euler_frac == 0.0), "n_euler > 0 exactly when euler_frac > 0");
     const double dte = n_euler ? euler_frac * dt / n_euler : 0.0;
     STS_REQUIRE(dte <= dt_exp * (1.0 + 1e-12), "explicit Euler sub-step exceeds dt_exp");
@@ -1377,6 +1382,7 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     int launched = 0;
     int batch = 4;
     bool all_done = false;
+    bool capturing = false;
     try {
       while (true) {
         launch_publish(reinterpret_cast<const double*>(sc), (int)(sizeof(PcgScal) * ncomp / sizeof(double)),
@@ -1396,8 +1402,10 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
               const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
               cudaGraph_t graph;
               STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
+              capturing = true;
               iteration(k, is);
               iteration(k + 1, is);
+              capturing = false;
               STS_CUDA(cudaStreamEndCapture(is, &graph));
               STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
               STS_CUDA(cudaGraphDestroy(graph));
@@ -1422,6 +1430,11 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
         batch = std::min(batch * 2, 64);
       }
     } catch (...) {
+      if (capturing) {   // leave the library's stream usable: close the capture, drop the graph
+        cudaGraph_t broken = nullptr;
+        if (cudaStreamEndCapture(is, &broken) == cudaSuccess && broken) cudaGraphDestroy(broken);
+        cudaGetLastError();
+      }
       if (pair_exec) cudaGraphExecDestroy(pair_exec);
       throw;
     }
@@ -1439,8 +1452,13 @@ int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1
     STS_CUDA(cudaStreamSynchronize(st));
     if (iters_out)
       for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;
+    bool broke = false;
+    for (int c = 0; c < ncomp; ++c) broke = broke || (hsc[c].flags & PCG_BREAKDOWN);
     sg.end({un1});
-    if (!all_done) {
+    if (broke) {
+      status = STS_ERR_BREAKDOWN;
+      set_error("be_pcg_solve: PCG breakdown (p.A p <= 0 or a non-finite scalar: A not SPD or non-finite input)");
+    } else if (!all_done) {
       status = STS_ERR_NOT_CONVERGED;
       set_error("be_pcg_solve: kmax reached before convergence");
     }

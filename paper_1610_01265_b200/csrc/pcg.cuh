@@ -6,6 +6,14 @@
 
 namespace sts {
 
+// stop the component: A is not SPD (p.A p <= 0) or a scalar is not finite (NaN / inf
+// input); the host reports STS_ERR_BREAKDOWN, x holds the last iterate
+__device__ inline void pcg_breakdown(PcgScal& s) {
+  s.done = 1;
+  s.flags |= PCG_BREAKDOWN;
+  s.ax = 0.0;
+}
+
 // scalar recurrences of Fig. 1 (one thread per component)
 __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal* sc, double rtol2) {
   PcgScal& s = sc[c];
@@ -13,12 +21,16 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.rz = sums[c * nq + 0];
     s.thresh = rtol2 * sums[c * nq + 1];
     s.iters = 0;
+    s.flags = 0;
     s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
     s.beta = 0.0;
     s.ax = 0.0;
+    // r.P^-1 r and b.P^-1 b are >= 0 for an SPD Jacobi P (A_ii > 0); NaN fails both tests
+    if (!(s.rz >= 0.0) || !(s.thresh >= 0.0) || !isfinite(s.rz) || !isfinite(s.thresh)) pcg_breakdown(s);
   } else if (phase == PH_AP) {
     if (s.done) return;
     s.pAp = sums[c * nq];
+    if (!(s.pAp > 0.0) || !isfinite(s.pAp)) return pcg_breakdown(s);
     s.alpha = s.rz / s.pAp;                // alpha_k = r_r / (p_k . y_k)
   } else if (phase == PH_RZ) {
     if (s.done) return;
@@ -37,13 +49,28 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     // not accumulate across iterations).  The pass forms z_{k+1} = z_k - alpha_k d y_k.
     if (s.done) return;
     const double rz = sums[c * nq + 0];
+    if (rz <= s.thresh) {
+      // the pass's own r_k.z_k meets the test: reached only after an extrapolated value
+      // below its own rounding (below); x_k is complete (the pass applied alpha_{k-1})
+      s.done = 1;
+      s.ax = 0.0;
+      s.rz = rz;
+      return;
+    }
     s.pAp = sums[c * nq + 1];
+    if (!(s.pAp > 0.0) || !isfinite(s.pAp) || !isfinite(rz)) return pcg_breakdown(s);
     s.alpha = rz / s.pAp;
     s.rz_old = rz;
     s.rz = rz - 2.0 * s.alpha * sums[c * nq + 2] + s.alpha * s.alpha * sums[c * nq + 3];
     s.iters += 1;
     s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k (next pass / final pass)
-    if (s.rz <= s.thresh) s.done = 1;
+    // The expansion cancels to ~4 eps r_k.z_k.  A negative value means the true one is
+    // below that rounding: it decides convergence only if the rounding itself is under
+    // the threshold; otherwise restart the direction (beta = 0) and let the next pass's
+    // own r.z sum decide (the test above).
+    const double fuzz = 4.0 * 2.220446049250313e-16 * rz;
+    if (s.rz < 0.0 && fuzz > s.thresh) s.beta = 0.0;
+    else if (s.rz <= s.thresh) s.done = 1;
     else s.beta = s.rz / rz;               // beta_{k+1} = r_{k+1}.z_{k+1} / r_k.z_k
   }
 }

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NT, 3) aniso_kernel(StencilCall c, int ic, uns
 // anisotropic operator, fast path (F / RKL2 stages / PCG A p)
 // ----------------------------------------------------------------------------
 // The vertex coefficients are frozen over an advance (lagged diffusivity,
-// PAPER.md:33), so vertex_coef_kernel folds b, kappa and the metrics into three
+// PAPER.md:33), so vertex_coef_tiled_kernel folds b, kappa and the metrics into three
 // numbers per vertex ONCE per advance:  e_a = sqrt(V_v kappa_v) * b_{v,a} / (4 h_a)
 // (h_th, h_ph without their cell-dependent r / sin(theta) factors).  Then
 //   Q_v D_a = (e_v . d_v) e_{v,a},   d_v = the 4-difference sums of u,
@@ -343,55 +343,6 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool o
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// e for every vertex plane il = -1 .. nl-1 of a slab (vertex between cell planes
-// il and il+1), in the padded layout of ev_row/ev_plane (sts_common.cuh): column
-// kv+1 holds vertex kv, column 0 the periodic wrap copy of kv = n3-1, zero where
-// the vertex has a missing cell.  One thread per padded entry; b / kappa gathered
-// through L1/L2.
-__global__ void __launch_bounds__(256) vertex_coef_kernel(Geo G, FieldV b, FieldV k1, FieldV k2, FieldV k3,
-                                                          double* __restrict__ ev) {
-  const Metrics& M = G.m;
-  const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3);
-  const long long nv = (long long)(G.nl + 1) * pp;
-  const long long es = nv;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nv; e += (long long)gridDim.x * blockDim.x) {
-    const int il = (int)(e / pp) - 1;
-    const long long rem = e - (long long)(il + 1) * pp;
-    const int jv = (int)(rem / row) - 1;
-    int kv = (int)(rem - (long long)(jv + 1) * row) - 1;
-    if (kv == -1 && G.periodic3) kv = G.n3 - 1;
-    const int iv = G.i0 + il;
-    bool ok = kv >= 0 && kv < G.n3 && iv >= 0 && iv + 1 < G.n1g && jv >= 0 && jv + 1 < G.n2 &&
-              (G.periodic3 || kv + 1 < G.n3);
-    double er = 0.0, et = 0.0, ep = 0.0;
-    if (ok) {
-      const int kv1 = (kv + 1 < G.n3) ? kv + 1 : 0;
-      const long long o00 = (long long)jv * G.n3 + kv, o01 = (long long)jv * G.n3 + kv1;
-      const long long o10 = o00 + G.n3, o11 = o01 + G.n3;
-      const double* bl0 = plane_ptr(b, G, il, 0); const double* bh0 = plane_ptr(b, G, il + 1, 0);
-      const double* bl1 = plane_ptr(b, G, il, 1); const double* bh1 = plane_ptr(b, G, il + 1, 1);
-      const double* bl2 = plane_ptr(b, G, il, 2); const double* bh2 = plane_ptr(b, G, il + 1, 2);
-      const double br = 0.125 * ((bl0[o00] + bl0[o01]) + (bl0[o10] + bl0[o11]) + ((bh0[o00] + bh0[o01]) + (bh0[o10] + bh0[o11])));
-      const double bt = 0.125 * ((bl1[o00] + bl1[o01]) + (bl1[o10] + bl1[o11]) + ((bh1[o00] + bh1[o01]) + (bh1[o10] + bh1[o11])));
-      const double bp = 0.125 * ((bl2[o00] + bl2[o01]) + (bl2[o10] + bl2[o11]) + ((bh2[o00] + bh2[o01]) + (bh2[o10] + bh2[o11])));
-      const double* K1l = plane_ptr(k1, G, il, 0);
-      const double* K2l = plane_ptr(k2, G, il, 0); const double* K2h = plane_ptr(k2, G, il + 1, 0);
-      const double* K3l = plane_ptr(k3, G, il, 0); const double* K3h = plane_ptr(k3, G, il + 1, 0);
-      const double kap = (1.0 / 12.0) * (((K1l[o00] + K1l[o01]) + (K1l[o10] + K1l[o11])) +
-                                         ((K2l[o00] + K2l[o01]) + (K3l[o00] + K3l[o10])) +
-                                         ((K2h[o00] + K2h[o01]) + (K3h[o00] + K3h[o10])));
-      const double C = 0.125 * (M.Vr[iv] + M.Vr[iv + 1]) * (M.Vt[jv] + M.Vt[jv + 1]) * (M.Vp[kv] + M.Vp[kv1]) * kap;
-      const double sq = sqrt(C);
-      er = sq * 0.25 * br * M.iH1[iv];
-      et = sq * 0.25 * bt * M.iH2[jv];
-      ep = sq * 0.25 * bp * M.iH3[kv];
-    }
-    ev[e] = er;
-    ev[es + e] = et;
-    ev[2 * es + e] = ep;
-  }
-}
 
 template <int EPI>
 __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fast_kernel(StencilCall c, int ic) {
@@ -588,11 +539,14 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
   }
 }
 
-// Tiled variant: a CTA owns 8 x 32 padded vertex positions (rows jv+1, cols kv+1) and
+// A CTA owns 8 x 32 padded vertex positions (rows jv+1, cols kv+1) and
 // marches along r; each cell plane of b (3 comps) and the three face diffusivities is
 // staged once in shared memory (2-plane ring, 9 x 33 cells with halo and periodic wrap)
-// and shared by the 8 vertices around every cell -- same arithmetic as
-// vertex_coef_kernel, coalesced loads instead of 36 gathers per vertex.
+// and shared by the 8 vertices around every cell (coalesced loads instead of 36
+// gathers per vertex).  e for every vertex plane il = -1 .. nl-1 of a slab (vertex
+// between cell planes il and il+1) in the padded layout of ev_row/ev_plane
+// (sts_common.cuh): column kv+1 holds vertex kv, column 0 the periodic wrap copy of
+// kv = n3-1, zero where the vertex has a missing cell.
 constexpr int VCJ = 8, VCK = 32, VCR = VCJ + 1, VCC = VCK + 1, VCN = VCR * VCC;   // 9 x 33 cells
 __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b, FieldV k1, FieldV k2, FieldV k3,
                                                                 double* __restrict__ ev, int ic) {
@@ -1061,12 +1015,8 @@ int stencil_blocks(int mode, int epi, const Geo& G, int ib, int ie) {
 
 template <int EPI, int NC>
 static void launch_iso_fast(const StencilCall& c, dim3 grid, int ic, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(iso_fast_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)IsoSmem<NC>::bytes));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_smem_attr(iso_fast_kernel<EPI, NC>, (int)IsoSmem<NC>::bytes, attr);
   iso_fast_kernel<EPI, NC><<<grid, NT, IsoSmem<NC>::bytes, st>>>(c, ic);
 }
 
@@ -1077,21 +1027,13 @@ static void launch_epi(const StencilCall& c, cudaStream_t st, unsigned long long
   if (grid.x == 0) return;
   if (c.mode == STS_MODE_ANISO) {
     if constexpr (EPI == EPI_F || EPI == EPI_RKL2_FIRST || EPI == EPI_RKL2_STAGE || EPI == EPI_PCG_AP) {
-      static bool attr_fast = false;
-      if (!attr_fast) {
-        STS_CUDA(cudaFuncSetAttribute(aniso_fast_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)FAST_SMEM));
-        attr_fast = true;
-      }
+      static std::atomic<unsigned long long> attr_fast{0};
+      ensure_smem_attr(aniso_fast_kernel<EPI>, (int)FAST_SMEM, attr_fast);
       if (!c.ev) throw Error{STS_ERR_STATE, "vertex coefficients missing for the anisotropic fast path"};
       aniso_fast_kernel<EPI><<<grid, FNT, FAST_SMEM, st>>>(c, ic);
     } else {
-      static bool attr_set = false;
-      if (!attr_set) {
-        STS_CUDA(cudaFuncSetAttribute(aniso_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)ANISO_SMEM));
-        attr_set = true;
-      }
+      static std::atomic<unsigned long long> attr_set{0};
+      ensure_smem_attr(aniso_kernel<EPI>, (int)ANISO_SMEM, attr_set);
       aniso_kernel<EPI><<<grid, NT, ANISO_SMEM, st>>>(c, ic, dmax);
     }
   } else {

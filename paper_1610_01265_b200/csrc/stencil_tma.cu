@@ -493,12 +493,8 @@ int aniso_tma_blocks(const StencilCall& c) {
 
 template <int EPI, bool W, bool FR>
 static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(aniso_tma_kernel<EPI, W, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)TmaLay<EPI, W>::SMEM));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_smem_attr(aniso_tma_kernel<EPI, W, FR>, (int)TmaLay<EPI, W>::SMEM, attr);
   aniso_tma_kernel<EPI, W, FR><<<grid, XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
 }
 

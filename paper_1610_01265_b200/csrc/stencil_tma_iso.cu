@@ -652,12 +652,8 @@ int iso_tma_blocks(const StencilCall& c) {
 
 template <int EPI, int NC, bool FST, bool FR>
 static void launch_iso_g(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    STS_CUDA(cudaFuncSetAttribute(iso_tma_kernel<EPI, NC, FST, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)IsoLay<EPI, NC>::SMEM));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  ensure_smem_attr(iso_tma_kernel<EPI, NC, FST, FR>, (int)IsoLay<EPI, NC>::SMEM, attr);
   iso_tma_kernel<EPI, NC, FST, FR><<<grid, IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
 }
 

@@ -8,6 +8,7 @@
 
 #include <cstddef>
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -173,6 +174,24 @@ __device__ __forceinline__ double rcp_pos(double x) {
 }
 
 Geo slab_geo(const sts_grid* g, const Slab& s);
+
+// current CUDA device ordinal (the handle's DeviceGuard has selected it)
+inline int current_device() {
+  int dev = 0;
+  STS_CUDA(cudaGetDevice(&dev));
+  return dev;
+}
+
+// Once per (call site, device): the >48 KB dynamic shared-memory opt-in of `kernel`.
+// `done` is a per-call-site bit mask over device ordinals; setting the attribute twice
+// from racing threads is harmless (idempotent), so a lock-free fetch_or suffices.
+template <class K>
+inline void ensure_smem_attr(K kernel, int bytes, std::atomic<unsigned long long>& done) {
+  const unsigned long long bit = 1ull << (current_device() & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  STS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.fetch_or(bit, std::memory_order_release);
+}
 double* ws_get(sts_grid* g, size_t bytes);  // scratch of at least `bytes`, reused across calls
 
 // ----------------------------------------------------------------------------
@@ -197,7 +216,9 @@ struct PcgScal {
   double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update;
                     // the merged iteration also applies it to z)
   int done, iters;
+  int flags, pad;   // flags: PCG_BREAKDOWN (p.A p <= 0 or a non-finite scalar: A not SPD / NaN input)
 };
+constexpr int PCG_BREAKDOWN = 1;
 static_assert(sizeof(PcgScal) % sizeof(double) == 0, "PcgScal is published as doubles");
 
 // fused final reduction of a PCG pass (pcg.cuh: fused_final_reduce)

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libsts_b200.so")
 
 STS_OK = 0
 STS_ERR_NOT_CONVERGED = -4
+STS_ERR_BREAKDOWN = -7
 GEOM = {"cartesian": 0, "spherical": 1}
 MODE = {"iso": 0, "aniso": 1}
 UID_BYTES = 128
@@ -258,11 +259,11 @@ class Grid:
 
     def rkl2_advance_hybrid(self, mode, u0, k, b=None, w=None, dt=0.0, dt_exp=1.0, euler_frac=0.25,
                             n_euler=None, n_sub=1, out=None, stream=None):
-        """PAPER.md:341 remedies: explicit-Euler prefix over euler_frac*dt (default sub-step
-        dt_exp/2, which annihilates the highest mode) + n_sub RKL2 sub-cycles.
-        Returns (u1, (n_euler, s))."""
+        """PAPER.md:341 remedies: explicit-Euler prefix over euler_frac*dt (n_euler None: the
+        library's default sub-step dt_exp/2, which annihilates the highest mode) + n_sub RKL2
+        sub-cycles.  Returns (u1, (n_euler, s))."""
         if n_euler is None:
-            n_euler = 0 if euler_frac == 0 else int(math.ceil(euler_frac * dt / (0.5 * dt_exp) - 1e-12))
+            n_euler = -1
         ncomp = 1 if u0.dim() == 3 else u0.shape[0]
         out = self._alloc(ncomp, u0) if out is None else out
         st = (ctypes.c_int * 2)()
