@@ -20,11 +20,26 @@
  *    wrap face between k = n3-1 and k = 0.
  *  - The unit field b is [3][nl][n2][n3] (components along the grid's own unit
  *    vectors).  w (viscosity: rho) is [nl][n2][n3]; NULL means w = 1.
- *  - Array arguments may be DEVICE pointers (no copy) or HOST pointers
- *    (pinned or pageable; the library stages them through its own device
- *    buffers with cudaMemcpyAsync on `stream` and copies outputs back before
- *    returning).  The caller owns every array it passes; the library never
- *    frees or retains caller pointers past the call.
+ *  - Array arguments may be DEVICE pointers (no copy) or HOST pointers.  Host
+ *    arrays are staged through device buffers the handle owns: uploads run on the
+ *    handle's own host-to-device copy stream and downloads on its device-to-host
+ *    copy stream, so the copies of one call overlap the computation of the calls
+ *    enqueued before and after it; `stream` waits only for the call's own inputs.
+ *      PINNED (page-locked) host arrays make the call asynchronous, like
+ *      cudaMemcpyAsync: it returns once the work is enqueued; the caller must not
+ *      modify its inputs nor read its outputs before sts_grid_join(g, s) has been
+ *      issued on a stream s and s has been synchronized (or sts_grid_synchronize).
+ *      PAGEABLE host arrays make the call synchronous: it returns with the outputs
+ *      written back.
+ *    The caller owns every array it passes; the library never frees caller
+ *    pointers, and retains DEVICE coefficient pointers only while they are bound
+ *    (sts_grid_bind_coeffs).
+ *  - Coefficient arrays (k1, k2, k3, b, w) all NULL: the call uses the coefficients
+ *    bound to its mode (sts_grid_bind_coeffs, sts_face_kappa_spitzer with NULL
+ *    outputs), and the data the library derives from them -- the frozen vertex
+ *    coefficients of STS_MODE_ANISO, the metric-folded face coefficients of the
+ *    merged isotropic PCG pass, the Gershgorin bound -- is built once per binding
+ *    instead of once per call.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Entry points
  *    that return host-visible values (dt, iteration counts) synchronise the
  *    stream; the others are asynchronous.
@@ -168,9 +183,10 @@ int sts_grid_set_timing(sts_grid* g, int enable);
 int sts_grid_set_tma(sts_grid* g, int enable);
 
 /*
- * enable != 0 (the default): single-process PCG solves replay one captured CUDA
- * graph per pair of iterations (k, k+1 >= 2); 0 launches every kernel directly.
- * Graphs are never used while per-launch timing is on or with an NCCL communicator.
+ * enable != 0 (the default): single-process PCG solves run iterations k >= 4 as the
+ * body (one iteration pair) of a device-side WHILE loop in a CUDA graph; 0 launches
+ * every kernel directly from a host-polled loop.  Graphs are never used while
+ * per-launch timing is on or with an NCCL communicator.
  */
 int sts_grid_set_graphs(sts_grid* g, int enable);
 
@@ -211,12 +227,41 @@ int sts_nccl_unique_id(void* out, size_t nbytes);
 int sts_comm_init(sts_grid* g, int nranks, int rank, const void* uid, size_t nbytes);
 
 /*
+ * Resident coefficients.  sts_grid_bind_coeffs binds the coefficient arrays of one
+ * operator mode to the handle (one binding per mode: conduction and viscosity can be
+ * resident together).  Each non-NULL array replaces the mode's current one; NULL keeps
+ * it.  DEVICE arrays are referenced (the caller keeps them allocated and unchanged
+ * while bound); HOST arrays are uploaded into library-owned device copies on the H2D
+ * copy stream (two copies per array, used in turn, so an upload overlaps the work still
+ * reading the previous binding).  b is STS_MODE_ANISO only; w NULL means w = 1.
+ * Calls that pass k1 = k2 = k3 = b = w = NULL then use the binding (see "Coefficient
+ * arrays" above).  sts_grid_unbind_coeffs synchronizes the device and releases the
+ * mode's binding and library-owned copies.
+ * Errors: STS_ERR_ARG for a bad mode; STS_ERR_STATE when a call selects a binding that
+ * lacks an array it needs.
+ */
+int sts_grid_bind_coeffs(sts_grid* g, int mode, const double* k1, const double* k2, const double* k3,
+                         const double* b, const double* w, void* stream);
+int sts_grid_unbind_coeffs(sts_grid* g, int mode);
+
+/*
+ * sts_grid_join makes `stream` wait for every copy the handle has enqueued so far on its
+ * copy streams (the uploads and the result downloads of host arrays): after it, work on
+ * `stream` -- and a synchronization of `stream` -- also covers the host outputs.
+ * sts_grid_synchronize blocks until all of the handle's internal streams are idle.
+ */
+int sts_grid_join(sts_grid* g, void* stream);
+int sts_grid_synchronize(sts_grid* g);
+
+/*
  * A3 — lagged Spitzer face diffusivity (DESIGN R3)
  *   k_d[f] = kappa0 * f_c(r_f) * beta_Tcut(Tf) * Tf^(5/2),  Tf = (T_L + T_R)/2,
  *   beta_Tcut(T) = (T/T_cut)^(5/2) if T < T_cut else 1  (T_cut <= 0: beta = 1),
  *   f_c(r) = 0.5 (1 - tanh((r - fc_r0)/fc_w))            (fc_w <= 0: f_c = 1).
  *  T[nl][n2][n3] (> 0) in; k1, k2, k3 [nl][n2][n3] out (faces leaving the
  *  domain are written as 0).  Distributed grids exchange T's boundary planes.
+ *  k1 = k2 = k3 = NULL: the face diffusivities are written into library-owned device
+ *  arrays and bound as the STS_MODE_ANISO coefficients (the binding's b is kept).
  */
 int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2, double* k3,
                            double kappa0, double T_cut, double fc_r0, double fc_w,
@@ -292,16 +337,36 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
  *  Returns STS_ERR_NOT_CONVERGED (un1 = last iterate) if a component hits kmax,
  *  STS_ERR_BREAKDOWN if a component's p.A p is not positive or a PCG scalar is not
  *  finite (A not SPD, NaN / inf in the inputs; that component stops, un1 = last iterate).
- *  Synchronises `stream` (the host polls the device-side convergence flags
- *  once per batch of iterations).  By default each iteration is one fused
- *  stencil pass and one reduction (sts_grid_set_pcg_merged; the convergence
- *  test uses r.z of the next iterate from the expansion of (r - alpha y).d(r -
- *  alpha y), so the count can differ from Fig. 1's by one at a tie).
+ *  Synchronises `stream` before returning.  Single-process solves run the
+ *  iteration loop on the device (a conditional WHILE node of a CUDA graph, one
+ *  iteration pair per trip, the condition set by a kernel from the device-side
+ *  convergence flags), so the host never polls; with per-launch timing, graphs
+ *  disabled or an NCCL communicator the host polls the flags once per batch of
+ *  iterations, the batch sized from the observed convergence rate so that at most
+ *  one or two no-op iterations follow convergence.  By default each iteration is
+ *  one fused stencil pass and one reduction (sts_grid_set_pcg_merged; the
+ *  convergence test uses r.z of the next iterate from the expansion of
+ *  (r - alpha y).d(r - alpha y), so the count can differ from Fig. 1's by one at
+ *  a tie).
  */
 int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1,
                  const double* k1, const double* k2, const double* k3,
                  const double* b, const double* w, double dt, double rtol, int kmax,
                  int* iters_out, void* stream);
+
+/*
+ * A7, asynchronous — be_pcg_solve without waiting for the solve: where the loop runs on
+ * the device (single process, graphs enabled, per-launch timing off) and no array is in
+ * pageable host memory, the call returns once the solve is enqueued; iters_out[ncomp]
+ * and *status_out (STS_OK, STS_ERR_NOT_CONVERGED or STS_ERR_BREAKDOWN) are written by the
+ * host when `stream` reaches the end of the solve, so both must stay valid until then
+ * (either may be NULL).  Otherwise it behaves like be_pcg_solve and writes both before
+ * returning.  The return value reports enqueue-time errors only (argument, CUDA, state).
+ */
+int be_pcg_solve_async(sts_grid* g, int mode, int ncomp, const double* un, double* un1,
+                       const double* k1, const double* k2, const double* k3,
+                       const double* b, const double* w, double dt, double rtol, int kmax,
+                       int* iters_out, int* status_out, void* stream);
 
 #ifdef __cplusplus
 }

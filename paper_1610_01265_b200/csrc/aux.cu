@@ -504,6 +504,40 @@ void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal
   STS_CUDA(cudaGetLastError());
 }
 
+// per-solve initialisation of the PCG scalars: the iteration limit, cleared flags, and
+// the counter of executed iteration-pair bodies of the device-driven loop
+__global__ void pcg_init_kernel(PcgScal* sc, int ncomp, int kmax, int* body_count) {
+  const int c = threadIdx.x;
+  if (c < ncomp) {
+    sc[c].kmax = kmax;
+    sc[c].flags = 0;
+    sc[c].done = 0;
+    sc[c].iters = 0;
+  }
+  if (c == 0 && body_count) *body_count = 0;
+}
+
+void launch_pcg_init(PcgScal* sc, int ncomp, int kmax, int* body_count, cudaStream_t st) {
+  pcg_init_kernel<<<1, 32, 0, st>>>(sc, ncomp, kmax, body_count);
+  STS_CUDA(cudaGetLastError());
+}
+
+// the loop condition of the device-driven PCG (a WHILE conditional graph node): run
+// another iteration pair while any component is neither converged nor stopped
+__global__ void pcg_continue_kernel(cudaGraphConditionalHandle h, const PcgScal* sc, int ncomp, int* body_count,
+                                    int count) {
+  int more = 0;
+  for (int c = 0; c < ncomp; ++c) more |= !sc[c].done;
+  if (count) *body_count += 1;
+  cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+void launch_pcg_continue(cudaGraphConditionalHandle h, const PcgScal* sc, int ncomp, int* body_count, bool count,
+                         cudaStream_t st) {
+  pcg_continue_kernel<<<1, 1, 0, st>>>(h, sc, ncomp, body_count, count ? 1 : 0);
+  STS_CUDA(cudaGetLastError());
+}
+
 // small device results to mapped pinned host memory by SM stores: the host reads
 // them after a stream sync without a DMA copy, which would queue behind large
 // transfers a caller runs on the copy engines (e.g. the previous result's download)

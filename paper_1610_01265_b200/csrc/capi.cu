@@ -134,16 +134,6 @@ static void ensure_red(sts_grid* g, size_t bytes) {
   g->red_bytes = bytes;
 }
 
-static bool is_device_ptr(const void* p) {
-  if (!p) return true;
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
 // ----------------------------------------------------------------------------
 // halo buffers and exchange
 // ----------------------------------------------------------------------------
@@ -218,56 +208,172 @@ static FieldV view(const sts_grid* g, const Slab& s, int slot, const double* arr
 }
 
 // ----------------------------------------------------------------------------
-// argument staging (host pointers -> device scratch)
+// host-array path (include/sts_b200.h "Array arguments"): every host array is staged
+// through a device buffer of the handle's staging pool.  Uploads run on the handle's
+// H2D copy stream and downloads on its D2H copy stream, so a call's copies overlap the
+// compute of the calls enqueued before / after it; the compute stream waits only for
+// its own inputs.  Pinned host arrays make the call asynchronous (like cudaMemcpyAsync:
+// the caller keeps inputs unchanged and reads outputs after sts_grid_join /
+// sts_grid_synchronize); a pageable array makes it synchronous.
 // ----------------------------------------------------------------------------
-struct Stage {
+enum class Mem { Device, Pinned, Pageable };
+
+static Mem mem_kind(const void* p) {
+  if (!p) return Mem::Device;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return Mem::Pageable;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Mem::Device;
+  return a.type == cudaMemoryTypeHost ? Mem::Pinned : Mem::Pageable;
+}
+
+static bool is_device_ptr(const void* p) { return mem_kind(p) == Mem::Device; }
+
+static cudaStream_t copy_stream(sts_grid* g, bool h2d) {
+  cudaStream_t& s = h2d ? g->h2d_stream : g->d2h_stream;
+  cudaEvent_t& e = h2d ? g->ev_h2d_last : g->ev_d2h_last;
+  if (!s) STS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (!e) STS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return s;
+}
+
+static void pool_reclaim(sts_grid* g) {
+  for (auto& b : g->stage_pool) {
+    if (!b.pending || b.claimed) continue;
+    const cudaError_t q = cudaEventQuery(b.ev);
+    if (q == cudaSuccess) b.pending = false;
+    else if (q != cudaErrorNotReady) STS_CUDA(q);
+  }
+}
+
+static void pool_free_idle(sts_grid* g) {
+  for (auto it = g->stage_pool.begin(); it != g->stage_pool.end();) {
+    if (!it->pending && !it->claimed) {
+      cudaFree(it->p);
+      cudaEventDestroy(it->ev);
+      g->stage_bytes -= it->bytes;
+      it = g->stage_pool.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// a staging buffer of >= bytes that no enqueued work still uses; allocates when none is
+// free, releasing idle buffers (then waiting for in-flight ones) if the device is full
+static StageBuf* stage_acquire(sts_grid* g, size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  pool_reclaim(g);
+  StageBuf* best = nullptr;
+  for (auto& b : g->stage_pool)
+    if (!b.pending && !b.claimed && b.bytes >= bytes && (!best || b.bytes < best->bytes)) best = &b;
+  for (int attempt = 0; !best && attempt < 3; ++attempt) {
+    double* p = nullptr;
+    if (cudaMalloc(&p, bytes) == cudaSuccess) {
+      StageBuf nb;
+      nb.p = p;
+      nb.bytes = bytes;
+      STS_CUDA(cudaEventCreateWithFlags(&nb.ev, cudaEventDisableTiming));
+      g->stage_pool.push_back(nb);
+      g->stage_bytes += bytes;
+      best = &g->stage_pool.back();
+      break;
+    }
+    cudaGetLastError();
+    if (attempt == 1)   // wait for every in-flight staging buffer
+      for (auto& b : g->stage_pool)
+        if (b.pending && !b.claimed) STS_CUDA(cudaEventSynchronize(b.ev));
+    pool_reclaim(g);
+    pool_free_idle(g);
+  }
+  if (!best) throw Error{STS_ERR_ALLOC, "cudaMalloc of " + std::to_string(bytes) + " bytes of host-array staging failed"};
+  best->claimed = true;
+  return best;
+}
+
+struct HostIO {
   sts_grid* g;
   cudaStream_t st;
-  std::vector<std::pair<const double*, size_t>> in;  // host src, count
-  std::vector<double**> in_dst;
-  std::vector<std::pair<double*, size_t>> out;       // host dst, count
-  std::vector<double**> out_dev;
-  size_t total = 0;
-  bool any_host = false;
+  struct Arr {
+    const double* host;
+    double** slot;    // the call's pointer variable, rewritten to the staging buffer
+    size_t n;
+    StageBuf* buf;
+  };
+  std::vector<Arr> ins, outs;
+  bool sync = false;  // a pageable array: the call returns with its outputs written back
+  bool ended = false;
 
-  void input(const double*& p, size_t count) {
-    if (p && !is_device_ptr(p)) {
-      in.push_back({p, count});
-      in_dst.push_back(const_cast<double**>(&p));
-      total += (count + 31) / 32 * 32;
-      any_host = true;
+  HostIO(sts_grid* g_, cudaStream_t st_) : g(g_), st(st_) {}
+  void input(const double*& p, size_t n) {
+    const Mem k = mem_kind(p);
+    if (k == Mem::Device) return;
+    sync = sync || k == Mem::Pageable;
+    ins.push_back({p, const_cast<double**>(&p), n, nullptr});
+  }
+  void output(double*& p, size_t n) {
+    const Mem k = mem_kind(p);
+    if (k == Mem::Device) return;
+    sync = sync || k == Mem::Pageable;
+    outs.push_back({p, &p, n, nullptr});
+  }
+  bool any() const { return !ins.empty() || !outs.empty(); }
+  // claim staging buffers, start the uploads, make the compute stream wait for them
+  void begin() {
+    if (!ins.empty()) {
+      cudaStream_t cs = copy_stream(g, true);
+      for (auto& a : ins) {
+        a.buf = stage_acquire(g, a.n * sizeof(double));
+        STS_CUDA(cudaMemcpyAsync(a.buf->p, a.host, a.n * sizeof(double), cudaMemcpyHostToDevice, cs));
+        *a.slot = a.buf->p;
+      }
+      STS_CUDA(cudaEventRecord(g->ev_h2d_last, cs));
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_h2d_last, 0));
+      g->h2d_used = true;
+    }
+    for (auto& a : outs) {
+      a.buf = stage_acquire(g, a.n * sizeof(double));
+      *a.slot = a.buf->p;
     }
   }
-  // output (may alias an input: then the input's staged copy is used in place)
-  void output(double*& p, size_t count, const double* alias_in = nullptr, const double* alias_host = nullptr) {
-    if (p && !is_device_ptr(p)) {
-      out.push_back({p, count});
-      out_dev.push_back(&p);
-      total += (count + 31) / 32 * 32;
-      any_host = true;
+  // after the call's kernels: release the inputs (free once the kernels ran), download
+  // the outputs on the D2H stream (free once downloaded)
+  void end() {
+    ended = true;
+    for (auto& a : ins) release(a.buf, st);
+    if (!outs.empty()) {
+      cudaStream_t cs = copy_stream(g, false);
+      StageBuf* first = outs[0].buf;
+      STS_CUDA(cudaEventRecord(first->ev, st));   // (reused below as the D2H buffer's own event)
+      STS_CUDA(cudaStreamWaitEvent(cs, first->ev, 0));
+      for (auto& a : outs) {
+        STS_CUDA(cudaMemcpyAsync(const_cast<double*>(a.host), a.buf->p, a.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                 cs));
+        release(a.buf, cs);
+      }
+      STS_CUDA(cudaEventRecord(g->ev_d2h_last, cs));
+      g->d2h_used = true;
+      if (sync) STS_CUDA(cudaStreamSynchronize(cs));
     }
-    (void)alias_in;
-    (void)alias_host;
+    if (sync) STS_CUDA(cudaStreamSynchronize(st));
   }
-  // carve staging out of `base` (count doubles), issue H2D copies; rewrite pointers
-  void begin(double* base) {
-    size_t off = 0;
-    for (size_t i = 0; i < in.size(); ++i) {
-      double* d = base + off;
-      STS_CUDA(cudaMemcpyAsync(d, in[i].first, in[i].second * sizeof(double), cudaMemcpyHostToDevice, st));
-      *in_dst[i] = d;
-      off += (in[i].second + 31) / 32 * 32;
-    }
-    for (size_t i = 0; i < out.size(); ++i) {
-      double* d = base + off;
-      *out_dev[i] = d;
-      off += (out[i].second + 31) / 32 * 32;
-    }
+  static void release(StageBuf* b, cudaStream_t s) {
+    if (!b) return;
+    STS_CUDA(cudaEventRecord(b->ev, s));
+    b->pending = true;
+    b->claimed = false;
   }
-  void end(const std::vector<double*>& dev_out) {
-    for (size_t i = 0; i < out.size(); ++i)
-      STS_CUDA(cudaMemcpyAsync(out[i].first, dev_out[i], out[i].second * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (!out.empty()) STS_CUDA(cudaStreamSynchronize(st));
+  ~HostIO() {
+    if (ended) return;   // an error path: whatever was enqueued may still read the buffers
+    for (auto* v : {&ins, &outs})
+      for (auto& a : *v)
+        if (a.buf) {
+          if (cudaEventRecord(a.buf->ev, st) == cudaSuccess) a.buf->pending = true;
+          a.buf->claimed = false;
+        }
+    cudaGetLastError();
   }
 };
 
@@ -276,6 +382,100 @@ static void check_mode(int mode, int ncomp, const double* b) {
   STS_REQUIRE(ncomp >= 1 && ncomp <= MAXC, "ncomp must be 1..3");
   STS_REQUIRE(mode == STS_MODE_ISO || ncomp == 1, "STS_MODE_ANISO supports ncomp == 1");
   STS_REQUIRE(mode == STS_MODE_ISO || b != nullptr, "STS_MODE_ANISO requires b");
+}
+
+// ----------------------------------------------------------------------------
+// resident coefficients (sts_grid_bind_coeffs): one slot per operator mode
+// ----------------------------------------------------------------------------
+static int slot_index(int mode) { return mode == STS_MODE_ANISO ? 1 : 0; }
+
+static void slot_invalidate(CoefSlot& s) {
+  s.ev_ok = s.pre_ok = false;
+  s.lam = -1.0;
+}
+
+static void slot_free(CoefSlot& s) {
+  for (int i = 0; i < 5; ++i)
+    for (int c = 0; c < 2; ++c) {
+      if (s.own[i][c]) cudaFree(s.own[i][c]);
+      s.own[i][c] = nullptr;
+      s.own_n[i][c] = 0;
+    }
+  for (int d = 0; d < 3; ++d) {
+    if (s.kfk[d]) cudaFree(s.kfk[d]);
+    s.kfk[d] = nullptr;
+  }
+  if (s.derived) cudaFree(s.derived);
+  s.derived = nullptr;
+  s.derived_bytes = 0;
+  for (int i = 0; i < 5; ++i)
+    for (int c = 0; c < 2; ++c) {
+      if (s.own_ev[i][c]) cudaEventDestroy(s.own_ev[i][c]);
+      s.own_ev[i][c] = nullptr;
+      s.own_ev_set[i][c] = false;
+    }
+  s.k[0] = s.k[1] = s.k[2] = s.b = s.w = nullptr;
+  s.bound = false;
+  slot_invalidate(s);
+}
+
+static double* dev_alloc(size_t n, const char* what) {
+  double* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{STS_ERR_ALLOC, std::string("cudaMalloc of ") + what + " failed"};
+  }
+  return p;
+}
+
+// slot-owned derived buffer of at least n doubles (written by kernels on the compute
+// stream, so in stream order with every earlier reader)
+static double* slot_derived(CoefSlot& s, size_t n) {
+  if (s.derived_bytes < n * sizeof(double)) {
+    if (s.derived) STS_CUDA(cudaFree(s.derived));
+    s.derived = nullptr;
+    s.derived = dev_alloc(n, "resident derived coefficients");
+    s.derived_bytes = n * sizeof(double);
+  }
+  return s.derived;
+}
+
+// The coefficient arrays one call uses (device pointers): the caller's arrays (staged
+// if on the host), or the mode's resident binding when k1 = k2 = k3 = NULL.
+struct Coefs {
+  const double *k1 = nullptr, *k2 = nullptr, *k3 = nullptr, *b = nullptr, *w = nullptr;
+  CoefSlot* slot = nullptr;
+};
+
+// (io keeps pointers to c's fields: c must outlive io.begin())
+static void resolve_coefs(Coefs& c, sts_grid* g, int mode, const double* k1, const double* k2, const double* k3,
+                          const double* b, const double* w, HostIO& io, size_t N) {
+  if (!k1 && !k2 && !k3) {
+    CoefSlot& s = g->slot[slot_index(mode)];
+    STS_REQUIRE(s.bound && s.k[0] && s.k[1] && s.k[2],
+                "k1 = k2 = k3 = NULL selects the resident coefficients, but none are bound for this mode "
+                "(sts_grid_bind_coeffs / sts_face_kappa_spitzer with NULL outputs)");
+    STS_REQUIRE(!b && !w, "with resident coefficients (k = NULL) b and w must be NULL too (they are bound)");
+    STS_REQUIRE(mode == STS_MODE_ISO || s.b, "the resident STS_MODE_ANISO coefficients have no b bound");
+    c.k1 = s.k[0];
+    c.k2 = s.k[1];
+    c.k3 = s.k[2];
+    c.b = mode == STS_MODE_ANISO ? s.b : nullptr;
+    c.w = s.w;
+    c.slot = &s;
+    return;
+  }
+  STS_REQUIRE(k1 && k2 && k3, "k1, k2, k3 must all be given (or all NULL for the resident coefficients)");
+  c.k1 = k1;
+  c.k2 = k2;
+  c.k3 = k3;
+  c.b = mode == STS_MODE_ANISO ? b : nullptr;
+  c.w = w;
+  io.input(c.k1, N);
+  io.input(c.k2, N);
+  io.input(c.k3, N);
+  if (mode == STS_MODE_ANISO) io.input(c.b, 3 * N);
+  io.input(c.w, N);
 }
 
 // coefficient halos for the operator (once per call)
@@ -644,6 +844,499 @@ static void rkl2_core(sts_grid* g, int mode, int ncomp, const double* u0, double
   }
 }
 
+// frozen vertex coefficients of one call (ANISO): the binding's, built once per binding,
+// or built into `scratch` (vertex_coef_doubles(g, mode) doubles) from the call's arrays
+static std::vector<const double*> call_vertex_coefs(sts_grid* g, int mode, const Coefs& cf, double* scratch,
+                                                    cudaStream_t st) {
+  if (mode != STS_MODE_ANISO) return std::vector<const double*>(g->slabs.size(), nullptr);
+  if (!cf.slot) return build_vertex_coefs(g, mode, scratch, cf.k1, cf.k2, cf.k3, cf.b, st);
+  CoefSlot& s = *cf.slot;
+  double* base = slot_derived(s, vertex_coef_doubles(g, mode));
+  if (!s.ev_ok) {
+    build_vertex_coefs(g, mode, base, cf.k1, cf.k2, cf.k3, cf.b, st);
+    s.ev_ok = true;
+  }
+  std::vector<const double*> out;
+  size_t o = 0;
+  for (auto& sl : g->slabs) {
+    out.push_back(base + o);
+    o += rnd(3 * (size_t)ev_cstride(sl.nl, g->n2, g->n3));
+  }
+  return out;
+}
+
+// scratch doubles a call needs for its vertex coefficients
+static size_t call_ev_doubles(const sts_grid* g, int mode, const Coefs& cf) {
+  return cf.slot ? 0 : vertex_coef_doubles(g, mode);
+}
+
+// metric-folded face coefficients K1, K2, K3 and wV of the merged isotropic PCG pass
+// ([4][nl][plane] at stride Nr): the binding's (once per binding) or built into `scratch`
+static double* call_premul(sts_grid* g, const Coefs& cf, double* scratch, size_t Nr, cudaStream_t st) {
+  double* pre = scratch;
+  if (cf.slot) {
+    pre = slot_derived(*cf.slot, 4 * Nr);
+    if (cf.slot->pre_ok) return pre;
+  }
+  for (auto& sl : g->slabs) {
+    Timed t(g, STS_K_VERTEX_COEF, st);   // (the isotropic counterpart of the frozen vertex coefficients)
+    launch_iso_premul(slab_geo(g, sl), off(cf.k1, sl), off(cf.k2, sl), off(cf.k3, sl), off(cf.w, sl), off(pre, sl),
+                      off(pre + Nr, sl), off(pre + 2 * Nr, sl), off(pre + 3 * Nr, sl), st);
+  }
+  if (cf.slot) cf.slot->pre_ok = true;
+  return pre;
+}
+
+// ----------------------------------------------------------------------------
+// BE + Jacobi-PCG (Fig. 1): one solve, enqueued on `st`.
+// Single-process solves with graphs enabled run the iteration loop on the device: the
+// first three iterations directly, then a WHILE conditional graph node whose body is one
+// iteration pair (k even, k odd: the ping-pong buffers swap back) and whose condition
+// kernel continues while any component is neither converged nor stopped at kmax -- no
+// host polling, so the call need not wait for the solve.  Instrumented (timing) and NCCL
+// solves poll device-side convergence flags from the host in batches sized by the
+// observed convergence rate.  Results (iterations, status) are published to the handle's
+// mapped mailbox at the end of the solve; `done` is called with them on the host.
+// ----------------------------------------------------------------------------
+struct PcgResult {
+  int iters[MAXC];
+  int status;
+};
+
+static void CUDART_CB pcg_mailbox_cb(void* p);
+
+struct PcgCallback {
+  sts_grid* g;
+  int ncomp;
+  int* iters_out;
+  int* status_out;
+  long long body_launches, body_local, body_global;
+};
+
+static int mailbox_status(const PcgScal* hsc, int ncomp) {
+  bool broke = false, kmax = false;
+  for (int c = 0; c < ncomp; ++c) {
+    broke = broke || (hsc[c].flags & PCG_BREAKDOWN);
+    kmax = kmax || (hsc[c].flags & PCG_KMAX) || !hsc[c].done;
+  }
+  return broke ? STS_ERR_BREAKDOWN : (kmax ? STS_ERR_NOT_CONVERGED : STS_OK);
+}
+
+static void CUDART_CB pcg_mailbox_cb(void* p) {
+  auto* cb = static_cast<PcgCallback*>(p);
+  const auto* hsc = reinterpret_cast<const PcgScal*>(cb->g->h_pinned);
+  const int bodies = reinterpret_cast<const int*>(cb->g->h_pinned + (sizeof(PcgScal) * MAXC) / sizeof(double))[0];
+  if (cb->iters_out)
+    for (int c = 0; c < cb->ncomp; ++c) cb->iters_out[c] = hsc[c].iters;
+  if (cb->status_out) *cb->status_out = mailbox_status(hsc, cb->ncomp);
+  cb->g->launches_async += bodies * cb->body_launches;
+  cb->g->comm_async[0] += bodies * cb->body_local;
+  cb->g->comm_async[1] += bodies * cb->body_global;
+  delete cb;
+}
+
+// one BE + Jacobi-PCG solve; returns true if it ran synchronously (results already in
+// the mailbox and written to iters_out / status_out)
+static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const Coefs& cf, double dt,
+                     double rtol, int kmax, cudaStream_t st, bool write_x0, int* iters_out, int* status_out,
+                     int* sync_status, bool allow_async, HostIO& io) {
+  const size_t N = (size_t)g->nl * g->plane;
+  const size_t NF = N * ncomp;
+  const size_t NFr = rnd(NF), Nr = rnd(N);
+  const double *k1 = cf.k1, *k2 = cf.k2, *k3 = cf.k3, *w = cf.w;
+  const double* bb = mode == STS_MODE_ANISO ? cf.b : nullptr;
+  // scratch: six [ncomp][nl][plane] fields (two-pass: r, z, y, p0, p1; merged: z0, z1,
+  // w0, w1, p0, p1); d [nl][plane]; vertex coefficients (unless resident)
+  // (+ the metric-folded isotropic coefficients K1, K2, K3, wV of the merged pass, unless resident)
+  const bool want_pre = mode == STS_MODE_ISO && g->tma && g->pcg_merged;
+  const size_t npre = (want_pre && !cf.slot) ? 4 * Nr : 0;
+  const size_t evn = call_ev_doubles(g, mode, cf);
+  double* base = ws_get(g, (6 * NFr + Nr + npre + evn) * sizeof(double));
+  double* r = base;
+  double* z = base + NFr;
+  double* y = base + 2 * NFr;
+  double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
+  double* d = base + 6 * NFr;
+  double* evbase = base + 6 * NFr + Nr + npre;
+  double* zb[2] = {base, base + NFr};
+  double* wb[2] = {base + 2 * NFr, base + 5 * NFr};
+  double* x = un1;
+  const double rtol2 = rtol * rtol;
+  const long long cs = (long long)g->nl * g->plane;
+
+  exchange_coeffs(g, mode, k1, k2, k3, bb, st);
+  const auto ev = call_vertex_coefs(g, mode, cf, evbase, st);
+  // the S-pass (p update + x update + A p) is ONE fused TMA kernel where eligible
+  bool fused = false;
+  if (g->tma) {
+    StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
+    c.u2 = view(g, g->slabs[0], H_P, pb[0]);
+    c.ev = ev[0];
+    c.ea.out = off(y, g->slabs[0]);
+    c.ea.out2 = off(pb[1], g->slabs[0]);
+    c.ea.x = off(x, g->slabs[0]);
+    c.u3 = view(g, g->slabs[0], H_D, d);
+    fused = aniso_tma_eligible(c) || iso_tma_eligible(c);
+  }
+  // merged iteration (one pass + one reduction per iteration, sts_grid_set_pcg_merged);
+  // eligibility does not depend on the coefficient values, so it is decided before the
+  // isotropic coefficients are folded
+  bool merged = false;
+  double* pre = nullptr;
+  if (g->tma && g->pcg_merged) {
+    StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_M, zb[0], k1, k2, k3, bb, w);
+    c.u2 = view(g, g->slabs[0], H_W, wb[0]);
+    c.u3 = view(g, g->slabs[0], H_P, pb[0]);
+    c.ev = ev[0];
+    c.ea.out = off(zb[1], g->slabs[0]);
+    c.ea.out2 = off(pb[1], g->slabs[0]);
+    c.ea.out3 = off(wb[1], g->slabs[0]);
+    c.ea.x = off(x, g->slabs[0]);
+    c.ea.dinv = off(d, g->slabs[0]);
+    if (mode == STS_MODE_ISO) {
+      // (any 16 B-aligned stand-in: the folded arrays are laid out like the scratch fields)
+      double* probe = cf.slot ? slot_derived(*cf.slot, 4 * Nr) : base + 6 * NFr + Nr;
+      c.k1.p = off(probe, g->slabs[0]);
+      c.k2.p = off(probe + Nr, g->slabs[0]);
+      c.k3.p = off(probe + 2 * Nr, g->slabs[0]);
+      c.w = off(probe + 3 * Nr, g->slabs[0]);
+      c.premul = 1;
+    }
+    merged = (mode == STS_MODE_ISO ? want_pre && iso_tma_eligible(c) : aniso_tma_eligible(c));
+  }
+  if (merged && mode == STS_MODE_ISO) pre = call_premul(g, cf, base + 6 * NFr + Nr, Nr, st);
+  if (merged) fused = false;
+  // isotropic fused S-pass: z = r d is formed inside the stencil pass from the staged
+  // r and d, so neither the initial residual pass nor the U-pass stores z
+  const bool zd = fused && mode == STS_MODE_ISO;
+  double* partials = nullptr;
+  long long pstride = 0;
+  PcgScal* sc = nullptr;
+  int k_cur = 1;   // iteration whose S-pass is being built
+  auto make_r0 = [&](size_t si) {
+    const Slab& sl = g->slabs[si];
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
+    c.ev = ev[si];
+    c.ea.out = merged ? off(wb[0], sl) : off(r, sl);   // (merged: r0 itself is not needed)
+    c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
+    c.ea.out3 = merged ? off(zb[0], sl) : (zd ? nullptr : off(z, sl));
+    c.ea.out4 = off(d, sl);
+    c.ea.dt = dt;
+    c.ea.partials = partials;
+    c.ea.pstride = pstride;
+    return c;
+  };
+  auto make_s = [&](size_t si) {   // fused S-pass (TMA)
+    const Slab& sl = g->slabs[si];
+    const int first = (k_cur == 1);
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, zd ? r : z, k1, k2, k3, bb, w);
+    c.u = view(g, sl, H_Z, zd ? r : z);
+    c.u2 = first ? FieldV{} : view(g, sl, H_P, pb[(k_cur - 1) & 1]);
+    if (zd) c.u3 = view(g, sl, H_D, d);
+    c.ev = ev[si];
+    c.ea.out = off(y, sl);
+    c.ea.out2 = off(pb[k_cur & 1], sl);
+    c.ea.x = off(x, sl);
+    c.ea.first = first;
+    c.ea.dt = dt;
+    c.ea.partials = partials;
+    c.ea.pstride = pstride;
+    c.ea.sc = sc;
+    return c;
+  };
+  auto make_m = [&](size_t si) {   // merged iteration k_cur (TMA)
+    const Slab& sl = g->slabs[si];
+    const int first = (k_cur == 1);
+    const int a = (k_cur - 1) & 1, b2 = k_cur & 1;
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_M, zb[a], k1, k2, k3, bb, w);
+    c.u = view(g, sl, H_Z, zb[a]);
+    c.u2 = first ? FieldV{} : view(g, sl, H_W, wb[a]);
+    c.u3 = first ? FieldV{} : view(g, sl, H_P, pb[a]);
+    c.ev = ev[si];
+    c.ea.out = off(zb[b2], sl);
+    c.ea.out2 = off(pb[b2], sl);
+    c.ea.out3 = off(wb[b2], sl);
+    c.ea.x = off(x, sl);
+    c.ea.dinv = off(d, sl);
+    if (mode == STS_MODE_ISO) {   // metric-folded coefficients (the k1 halo planes stay raw)
+      c.k1.p = off(pre, sl);
+      c.k2.p = off(pre + Nr, sl);
+      c.k3.p = off(pre + 2 * Nr, sl);
+      c.w = off(pre + 3 * Nr, sl);
+      c.premul = 1;
+    }
+    c.ea.first = first;
+    c.ea.dt = dt;
+    c.ea.partials = partials;
+    c.ea.pstride = pstride;
+    c.ea.sc = sc;
+    return c;
+  };
+  auto make_ap = [&](size_t si) {  // A p of the unfused S-pass
+    const Slab& sl = g->slabs[si];
+    double* pnew = pb[k_cur & 1];
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, pnew, k1, k2, k3, bb, w);
+    c.ev = ev[si];
+    c.ea.out = off(y, sl);
+    c.ea.dt = dt;
+    c.ea.partials = partials;
+    c.ea.pstride = pstride;
+    c.ea.sc = sc;
+    return c;
+  };
+  const int sb_r0 = sweep_blocks(g, true, make_r0);
+  const int sb_s = merged ? sweep_blocks(g, true, make_m)
+                          : (fused ? sweep_blocks(g, true, make_s) : sweep_blocks(g, true, make_ap));
+  pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
+  // partial rows: ncomp x (2 for R0, 1 per two-pass phase, 4 for the merged pass); then
+  // the sums, the per-component scalars and the loop-body counter
+  const size_t nsc = (sizeof(PcgScal) * MAXC) / sizeof(double);
+  const size_t red_doubles = (size_t)4 * ncomp * pstride + 16 + nsc + 8;
+  ensure_red(g, red_doubles * sizeof(double));
+  partials = g->d_red;
+  double* sums = partials + 4 * ncomp * pstride;
+  sc = reinterpret_cast<PcgScal*>(sums + 16);
+  int* body_count = reinterpret_cast<int*>(sums + 16 + nsc);
+  const int npub = (int)nsc + 1;   // published: the scalars of MAXC components + the body counter
+
+  // fused final reductions (single process): the last CTA of the S-pass / U-pass sums
+  // the partials and runs the scalar phase, saving two launches per iteration
+  FinRed fin_s;
+  fin_s.ticket = g->d_ticket;
+  fin_s.sums = sums;
+  fin_s.sc = sc;
+  fin_s.ncomp = ncomp;
+  fin_s.nq = 1;
+  fin_s.phase = PH_AP;
+  fin_s.rtol2 = rtol2;
+  FinRed fin_u = fin_s;
+  fin_u.phase = PH_RZ;
+  FinRed fin_m = fin_s;
+  fin_m.nq = 4;
+  fin_m.phase = PH_M;
+  fin_u.ntot = PW_BLOCKS;   // set to the launched grid by launch_pcg_rupdate
+  auto reduce = [&](int nblocks, int nq, int phase) {
+    Timed t(g, STS_K_PCG_REDUCE, st);
+    if (g->comm) {
+      launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, PH_NONE, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
+      STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * nq, ncclDouble, ncclSum, g->comm, st));
+      launch_pcg_scalar(sums, ncomp, nq, phase, sc, rtol2, st);
+      g->launches += 1;
+    } else {
+      launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
+    }
+  };
+
+  launch_pcg_init(sc, ncomp, kmax, body_count, st);
+  g->launches += 1;
+  // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
+  reduce(sweep(g, {{H_U, un, ncomp}}, st, make_r0), 2, PH_R0);
+  if (needs_halos(g)) g->comm_global += 1;
+  if (zd) exchange(g, H_D, d, 1, st);   // d is fixed for the whole solve: its halo once
+  // merged iteration k: ONE pass (z_k, p_k, y_k = A p_k, w_k = d y_k, x_k; partials
+  // r_k.z_k, p_k.y_k, z_k.y_k, w_k.y_k) and ONE reduction (alpha_k, r_{k+1}.z_{k+1},
+  // convergence, beta_{k+1}: pcg.cuh PH_M)
+  auto iteration_m = [&](int k, cudaStream_t is) {
+    k_cur = k;
+    if (needs_halos(g)) g->comm_global += 1;
+    const int a = (k - 1) & 1;
+    const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_m;
+    int nbs;
+    if (k == 1) nbs = sweep(g, {{H_Z, zb[0], ncomp}}, is, make_m, fs);
+    else nbs = sweep(g, {{H_Z, zb[a], ncomp}, {H_W, wb[a], ncomp}, {H_P, pb[a], ncomp}}, is, make_m, fs);
+    if (!fs) {
+      Timed t(g, STS_K_PCG_REDUCE, is);
+      launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is, g->d_red2,
+                        g->d_ticket + 1);
+      if (g->comm) {
+        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * 4, ncclDouble, ncclSum, g->comm, is));
+        launch_pcg_scalar(sums, ncomp, 4, PH_M, sc, rtol2, is);
+        g->launches += 1;
+      }
+    }
+  };
+  // two-pass iteration k (Fig. 1 with the x update deferred one iteration):
+  //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
+  //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
+  auto iteration = [&](int k, cudaStream_t is) {
+    if (merged) return iteration_m(k, is);
+    k_cur = k;
+    if (needs_halos(g)) g->comm_global += 2;   // p.y (alpha) and r.z (beta + convergence)
+    double* pold = pb[(k - 1) & 1];
+    double* pnew = pb[k & 1];
+    int nbs;
+    if (fused) {
+      // (the last CTA finishes the reduction when the pass has few CTAs; large passes
+      // keep the 1024-thread reduction kernel, which sums ~1e4 partials faster)
+      const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_s;
+      const double* zr = zd ? r : z;
+      if (k == 1) nbs = sweep(g, {{H_Z, zr, ncomp}}, is, make_s, fs);
+      else nbs = sweep(g, {{H_Z, zr, ncomp}, {H_P, pold, ncomp}}, is, make_s, fs);
+    } else {
+      {
+        Timed t(g, STS_K_PCG_PUPDATE, is);
+        launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, k == 1, is);
+      }
+      nbs = sweep(g, {{H_U, pnew, ncomp}}, is, make_ap);
+    }
+    if (!(fused && !g->comm && sb_s <= 4096)) {           // else finished by the S-pass's last CTA
+      Timed t(g, STS_K_PCG_REDUCE, is);
+      launch_pcg_reduce(partials, pstride, nbs, ncomp, 1, sums, g->comm ? PH_NONE : PH_AP, sc, rtol2, is, g->d_red2,
+                        g->d_ticket + 1);
+      if (g->comm) {
+        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
+        launch_pcg_scalar(sums, ncomp, 1, PH_AP, sc, rtol2, is);
+        g->launches += 1;
+      }
+    }
+    int nbu;
+    {
+      Timed t(g, STS_K_PCG_UPDATE, is);
+      nbu = launch_pcg_rupdate(ncomp, (long long)N, cs, r, zd ? nullptr : z, y, d, sc, partials, pstride,
+                               g->comm ? FinRed{} : fin_u, is);
+    }
+    if (g->comm) {
+      Timed t(g, STS_K_PCG_REDUCE, is);
+      launch_pcg_reduce(partials, pstride, nbu, ncomp, 1, sums, PH_NONE, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
+      STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
+      launch_pcg_scalar(sums, ncomp, 1, PH_RZ, sc, rtol2, is);
+      g->launches += 1;
+    }
+  };
+
+  auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
+  const bool device_loop = g->graphs && !g->timing && g->comm == nullptr;
+  long long body_launches = 0, body_local = 0, body_global = 0;
+  if (device_loop) {
+    // iterations 1..3 directly (iteration 1 is its own pass variant; every kernel variant
+    // then has had its one-time attribute setup outside graph capture), then the loop
+    cudaStream_t is = graph_stream(g);
+    STS_CUDA(cudaEventRecord(g->ev_c, st));
+    STS_CUDA(cudaStreamWaitEvent(is, g->ev_c, 0));
+    for (int k = 1; k <= 3; ++k) iteration(k, is);
+    cudaGraph_t cg = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool capturing = false;
+    try {
+      STS_CUDA(cudaGraphCreate(&cg, 0));
+      cudaGraphConditionalHandle h;
+      STS_CUDA(cudaGraphConditionalHandleCreate(&h, cg, 0, cudaGraphCondAssignDefault));
+      // node 1: the first evaluation of the condition
+      STS_CUDA(cudaStreamBeginCaptureToGraph(is, cg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      launch_pcg_continue(h, sc, ncomp, body_count, false, is);
+      capturing = false;
+      STS_CUDA(cudaStreamEndCapture(is, &cg));
+      size_t nn = 1;
+      cudaGraphNode_t first = nullptr;
+      STS_CUDA(cudaGraphGetNodes(cg, &first, &nn));
+      // node 2: WHILE (condition) { iteration pair; condition }
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t loop;
+      STS_CUDA(cudaGraphAddNode(&loop, cg, &first, 1, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
+      STS_CUDA(cudaStreamBeginCaptureToGraph(is, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      iteration(4, is);
+      iteration(5, is);
+      launch_pcg_continue(h, sc, ncomp, body_count, true, is);
+      g->launches += 1;
+      capturing = false;
+      STS_CUDA(cudaStreamEndCapture(is, &body));
+      body_launches = g->launches - l0;
+      body_local = g->comm_local - cl0;
+      body_global = g->comm_global - cg0;
+      g->launches = l0 + 1;   // the condition node itself
+      g->comm_local = cl0;
+      g->comm_global = cg0;
+      STS_CUDA(cudaGraphInstantiate(&exec, cg, 0));
+      STS_CUDA(cudaGraphLaunch(exec, is));
+      // (an executable graph destroyed while in flight is released when it completes)
+      STS_CUDA(cudaGraphExecDestroy(exec));
+      exec = nullptr;
+      STS_CUDA(cudaGraphDestroy(cg));
+      cg = nullptr;
+    } catch (...) {
+      if (capturing) {   // leave the library's stream usable: close the capture, drop the graph
+        cudaGraph_t broken = nullptr;
+        if (cudaStreamEndCapture(is, &broken) == cudaSuccess && broken && broken != cg) cudaGraphDestroy(broken);
+      }
+      if (exec) cudaGraphExecDestroy(exec);
+      if (cg) cudaGraphDestroy(cg);
+      cudaGetLastError();
+      throw;
+    }
+    STS_CUDA(cudaEventRecord(g->ev_c, is));
+    STS_CUDA(cudaStreamWaitEvent(st, g->ev_c, 0));
+  } else {
+    // host-polled loop: batches sized from the observed convergence rate so that no more
+    // than ~1-2 no-op iterations (which still exchange halos and all-reduce under NCCL)
+    // follow convergence
+    int launched = 0;
+    int batch = 4;
+    std::vector<double> rz_prev(ncomp, 0.0);
+    while (true) {
+      launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, st);
+      g->launches += 1;
+      STS_CUDA(cudaStreamSynchronize(st));
+      bool all_done = true;
+      for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
+      if (all_done || launched >= kmax) break;
+      if (launched > 0) {
+        // remaining iterations ~ log(thresh / rz) / log(rate), rate per iteration from the last batch
+        int need = 1;
+        for (int c = 0; c < ncomp; ++c) {
+          if (hsc[c].done) continue;
+          const double rz = hsc[c].rz, th = hsc[c].thresh, r0 = rz_prev[c];
+          int n = 64;
+          if (rz > 0.0 && r0 > rz && th > 0.0) {
+            const double lrate = std::log(rz / r0) / batch;
+            n = (int)std::ceil(std::log(th / rz) / lrate);
+          }
+          need = std::max(need, std::max(1, std::min(64, n)));
+        }
+        batch = need;
+      }
+      for (int c = 0; c < ncomp; ++c) rz_prev[c] = hsc[c].rz;
+      const int nb = std::min(batch, kmax - launched);
+      for (int it = 0; it < nb; ++it) iteration(launched + it + 1, st);
+      launched += nb;
+      batch = nb;
+    }
+  }
+  {
+    Timed t(g, STS_K_PCG_XFINAL, st);
+    launch_pcg_xfinal(ncomp, (long long)N, cs, x, pb[0], pb[1], sc, st);
+  }
+  launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, st);
+  g->launches += 1;
+  io.end();
+  const bool async = allow_async && device_loop && !io.sync;
+  if (async) {
+    auto* cb = new PcgCallback{g, ncomp, iters_out, status_out, body_launches, body_local, body_global};
+    const cudaError_t e = cudaLaunchHostFunc(st, pcg_mailbox_cb, cb);
+    if (e != cudaSuccess) {
+      delete cb;
+      STS_CUDA(e);
+    }
+    return false;
+  }
+  STS_CUDA(cudaStreamSynchronize(st));
+  const int bodies = reinterpret_cast<const int*>(g->h_pinned + nsc)[0];
+  g->launches += bodies * body_launches;
+  g->comm_local += bodies * body_local;
+  g->comm_global += bodies * body_global;
+  if (iters_out)
+    for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;
+  *sync_status = mailbox_status(hsc, ncomp);
+  return true;
+}
+
 }  // namespace sts
 
 using namespace sts;
@@ -682,6 +1375,8 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const doub
     }
     DeviceGuard dg(device);
     auto* g = new sts_grid();
+    g->comm_async[0] = 0;
+    g->comm_async[1] = 0;
     g->device = device;
     g->geom = geom;
     g->n1g = n1;
@@ -744,6 +1439,17 @@ int sts_grid_destroy(sts_grid* g) {
       cudaEventDestroy(r.b);
     }
     for (auto e : g->free_events) cudaEventDestroy(e);
+    if (g->h2d_stream || g->d2h_stream || !g->stage_pool.empty()) cudaDeviceSynchronize();
+    for (auto& b : g->stage_pool) {
+      cudaFree(b.p);
+      cudaEventDestroy(b.ev);
+    }
+    g->stage_pool.clear();
+    for (auto& sl : g->slot) slot_free(sl);
+    if (g->h2d_stream) cudaStreamDestroy(g->h2d_stream);
+    if (g->d2h_stream) cudaStreamDestroy(g->d2h_stream);
+    if (g->ev_h2d_last) cudaEventDestroy(g->ev_h2d_last);
+    if (g->ev_d2h_last) cudaEventDestroy(g->ev_d2h_last);
     if (g->d_metrics) cudaFree(g->d_metrics);
     if (g->ws.base) cudaFree(g->ws.base);
     if (g->d_red) cudaFree(g->d_red);
@@ -765,15 +1471,15 @@ int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes) {
 int sts_grid_kernel_launches(const sts_grid* g, long long* count) {
   return guard([&] {
     STS_REQUIRE(g && count, "NULL argument");
-    *count = g->launches;
+    *count = g->launches + g->launches_async.load();
   });
 }
 
 int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_) {
   return guard([&] {
     STS_REQUIRE(g && local && global_, "NULL argument");
-    *local = g->comm_local;
-    *global_ = g->comm_global;
+    *local = g->comm_local + g->comm_async[0].load();
+    *global_ = g->comm_global + g->comm_async[1].load();
   });
 }
 
@@ -869,16 +1575,26 @@ int sts_comm_init(sts_grid* g, int nranks, int rank, const void* uid, size_t nby
 int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2, double* k3, double kappa0,
                            double T_cut, double fc_r0, double fc_w, void* stream) {
   return guard([&] {
-    STS_REQUIRE(g && T && k1 && k2 && k3, "NULL argument");
+    STS_REQUIRE(g && T, "NULL argument");
+    const bool resident = !k1 && !k2 && !k3;
+    STS_REQUIRE(resident || (k1 && k2 && k3), "k1, k2, k3 must all be given (or all NULL: resident output)");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
-    Stage sg{g, st};
-    sg.input(T, N);
-    sg.output(k1, N);
-    sg.output(k2, N);
-    sg.output(k3, N);
-    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
+    CoefSlot& s = g->slot[slot_index(STS_MODE_ANISO)];
+    if (resident) {
+      for (int d = 0; d < 3; ++d)
+        if (!s.kfk[d]) s.kfk[d] = dev_alloc(N, "resident face diffusivities");
+      k1 = s.kfk[0];
+      k2 = s.kfk[1];
+      k3 = s.kfk[2];
+    }
+    HostIO io(g, st);
+    io.input(T, N);
+    io.output(k1, N);
+    io.output(k2, N);
+    io.output(k3, N);
+    io.begin();
     exchange(g, H_AUX, T, 1, st);
     Slab whole;
     whole.i0 = g->i0;
@@ -893,71 +1609,156 @@ int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2,
       Timed t(g, STS_K_FACE_KAPPA, st);
       launch_face_kappa(G, Tv, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, d_x1f(g), d_x1c(g), st);
     }
-    sg.end({k1, k2, k3});
+    io.end();
+    if (resident) {   // bind them (b and w of the binding are kept)
+      for (int d = 0; d < 3; ++d) s.k[d] = s.kfk[d];
+      s.bound = true;
+      slot_invalidate(s);
+    }
+  });
+}
+
+int sts_grid_bind_coeffs(sts_grid* g, int mode, const double* k1, const double* k2, const double* k3,
+                         const double* b, const double* w, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    STS_REQUIRE(mode == STS_MODE_ISO || mode == STS_MODE_ANISO, "mode must be STS_MODE_ISO or STS_MODE_ANISO");
+    STS_REQUIRE(mode == STS_MODE_ANISO || !b, "b is bound for STS_MODE_ANISO only");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t N = (size_t)g->nl * g->plane;
+    CoefSlot& s = g->slot[slot_index(mode)];
+    const double* src[5] = {k1, k2, k3, b, w};
+    const size_t cnt[5] = {N, N, N, 3 * N, N};
+    const double** dst[5] = {&s.k[0], &s.k[1], &s.k[2], &s.b, &s.w};
+    bool uploaded = false;
+    for (int i = 0; i < 5; ++i) {
+      if (!src[i]) continue;
+      const Mem kind = mem_kind(src[i]);
+      if (kind == Mem::Device) {
+        *dst[i] = src[i];
+        continue;
+      }
+      // host array: into the library-owned copy the previous upload superseded, once the
+      // work enqueued before that supersession has run
+      const int c = s.own_next[i];
+      s.own_next[i] ^= 1;
+      if (s.own_n[i][c] < cnt[i]) {
+        if (s.own[i][c]) STS_CUDA(cudaFree(s.own[i][c]));
+        s.own[i][c] = nullptr;
+        s.own[i][c] = dev_alloc(cnt[i], "resident coefficients");
+        s.own_n[i][c] = cnt[i];
+      }
+      cudaStream_t cs = copy_stream(g, true);
+      if (s.own_ev_set[i][c]) STS_CUDA(cudaStreamWaitEvent(cs, s.own_ev[i][c], 0));
+      STS_CUDA(cudaMemcpyAsync(s.own[i][c], src[i], cnt[i] * sizeof(double), cudaMemcpyHostToDevice, cs));
+      if (kind == Mem::Pageable) STS_CUDA(cudaStreamSynchronize(cs));
+      // the other copy is superseded now: work reading it was enqueued before this point
+      if (!s.own_ev[i][1 - c]) STS_CUDA(cudaEventCreateWithFlags(&s.own_ev[i][1 - c], cudaEventDisableTiming));
+      STS_CUDA(cudaEventRecord(s.own_ev[i][1 - c], st));
+      s.own_ev_set[i][1 - c] = true;
+      *dst[i] = s.own[i][c];
+      uploaded = true;
+    }
+    if (uploaded) {
+      STS_CUDA(cudaEventRecord(g->ev_h2d_last, g->h2d_stream));
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_h2d_last, 0));
+      g->h2d_used = true;
+    }
+    s.bound = true;
+    slot_invalidate(s);
+  });
+}
+
+int sts_grid_unbind_coeffs(sts_grid* g, int mode) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    STS_REQUIRE(mode == STS_MODE_ISO || mode == STS_MODE_ANISO, "mode must be STS_MODE_ISO or STS_MODE_ANISO");
+    DeviceGuard dg(g->device);
+    STS_CUDA(cudaDeviceSynchronize());   // enqueued work may still read the binding
+    slot_free(g->slot[slot_index(mode)]);
+  });
+}
+
+int sts_grid_join(sts_grid* g, void* stream) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (g->h2d_used) STS_CUDA(cudaStreamWaitEvent(st, g->ev_h2d_last, 0));
+    if (g->d2h_used) STS_CUDA(cudaStreamWaitEvent(st, g->ev_d2h_last, 0));
+  });
+}
+
+int sts_grid_synchronize(sts_grid* g) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    DeviceGuard dg(g->device);
+    for (cudaStream_t s : {g->h2d_stream, g->d2h_stream, g->graph_stream, g->comm_stream})
+      if (s) STS_CUDA(cudaStreamSynchronize(s));
   });
 }
 
 int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out, const double* k1,
                  const double* k2, const double* k3, const double* b, const double* w, void* stream) {
   return guard([&] {
-    STS_REQUIRE(g && u && out && k1 && k2 && k3, "NULL argument");
-    check_mode(mode, ncomp, b);
-    STS_REQUIRE((const void*)u != (const void*)out, "u and out must not alias");
+    STS_REQUIRE(g && u && out, "NULL argument");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
-    Stage sg{g, st};
-    sg.input(u, N * ncomp);
-    sg.input(k1, N);
-    sg.input(k2, N);
-    sg.input(k3, N);
-    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
-    sg.input(w, N);
-    sg.output(out, N * ncomp);
-    const size_t evn = vertex_coef_doubles(g, mode);
-    double* base = ws_get(g, (rnd(sg.total) + evn) * sizeof(double));
-    if (sg.any_host) sg.begin(base + evn);
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, base, k1, k2, k3, b, st);
+    HostIO io(g, st);
+    Coefs cf;
+    resolve_coefs(cf, g, mode, k1, k2, k3, b, w, io, N);
+    check_mode(mode, ncomp, cf.b);
+    STS_REQUIRE((const void*)u != (const void*)out, "u and out must not alias");
+    io.input(u, N * ncomp);
+    io.output(out, N * ncomp);
+    io.begin();
+    double* base = ws_get(g, (call_ev_doubles(g, mode, cf) + 1) * sizeof(double));
+    exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, cf.b, st);
+    const auto ev = call_vertex_coefs(g, mode, cf, base, st);
     sweep(g, {{H_U, u, ncomp}}, st, [&](size_t si) {
       const Slab& s = g->slabs[si];
-      StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
+      StencilCall c = make_call(g, s, mode, ncomp, EPI_F, u, cf.k1, cf.k2, cf.k3, cf.b, cf.w);
       c.ev = ev[si];
       c.ea.out = off(out, s);
       return c;
     });
-    sg.end({out});
+    io.end();
   });
 }
 
 int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, const double* k3, const double* b,
                  const double* w, double* dt_out, void* stream) {
   return guard([&] {
-    STS_REQUIRE(g && k1 && k2 && k3 && dt_out, "NULL argument");
-    check_mode(mode, 1, b);
+    STS_REQUIRE(g && dt_out, "NULL argument");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
-    Stage sg{g, st};
-    sg.input(k1, N);
-    sg.input(k2, N);
-    sg.input(k3, N);
-    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
-    sg.input(w, N);
-    if (sg.any_host) sg.begin(ws_get(g, sg.total * sizeof(double)));
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    ensure_red(g, 4096);
-    auto* dmax = reinterpret_cast<unsigned long long*>(g->d_red);
-    STS_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-    for (auto& s : g->slabs) {
-      StencilCall c = make_call(g, s, mode, 1, 0, nullptr, k1, k2, k3, mode == STS_MODE_ANISO ? b : nullptr, w);
-      Timed t(g, mode == STS_MODE_ANISO ? STS_K_ANISO_GERSH : STS_K_ISO_GERSH, st);
-      launch_gershgorin(c, dmax, st);
+    HostIO io(g, st);
+    Coefs cf;
+    resolve_coefs(cf, g, mode, k1, k2, k3, b, w, io, N);
+    check_mode(mode, 1, cf.b);
+    double lam = cf.slot ? cf.slot->lam : -1.0;
+    if (lam < 0.0) {   // (resident coefficients: computed once per binding)
+      io.begin();
+      exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, cf.b, st);
+      ensure_red(g, 4096);
+      auto* dmax = reinterpret_cast<unsigned long long*>(g->d_red);
+      STS_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+      for (auto& s : g->slabs) {
+        StencilCall c = make_call(g, s, mode, 1, 0, nullptr, cf.k1, cf.k2, cf.k3, cf.b, cf.w);
+        Timed t(g, mode == STS_MODE_ANISO ? STS_K_ANISO_GERSH : STS_K_ISO_GERSH, st);
+        launch_gershgorin(c, dmax, st);
+      }
+      if (g->comm) STS_NCCL(ncclAllReduce(g->d_red, g->d_red, 1, ncclDouble, ncclMax, g->comm, st));
+      launch_publish(g->d_red, 1, g->d_pinned, st);
+      g->launches += 1;
+      io.end();
+      STS_CUDA(cudaStreamSynchronize(st));
+      lam = g->h_pinned[0];
+      if (cf.slot) cf.slot->lam = lam;
     }
-    if (g->comm) STS_NCCL(ncclAllReduce(g->d_red, g->d_red, 1, ncclDouble, ncclMax, g->comm, st));
-    launch_publish(g->d_red, 1, g->d_pinned, st);
-    STS_CUDA(cudaStreamSynchronize(st));
-    const double lam = g->h_pinned[0];
     *dt_out = lam > 0.0 ? 2.0 / lam : std::numeric_limits<double>::infinity();
   });
 }
@@ -982,34 +1783,30 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
                  const double* k2, const double* k3, const double* b, const double* w, double dt, int s,
                  void* stream) {
   return guard([&] {
-    STS_REQUIRE(g && u0 && u1 && k1 && k2 && k3, "NULL argument");
-    check_mode(mode, ncomp, b);
+    STS_REQUIRE(g && u0 && u1, "NULL argument");
     STS_REQUIRE(s >= 2, "s must be >= 2");
     STS_REQUIRE(std::isfinite(dt) && dt >= 0.0, "dt must be finite and >= 0");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
     const size_t NF = N * ncomp;
-    Stage sg{g, st};
-    sg.input(u0, NF);
-    sg.input(k1, N);
-    sg.input(k2, N);
-    sg.input(k3, N);
-    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
-    sg.input(w, N);
-    // host arrays (even an in-place u0 == u1) are staged separately: the result
-    // goes to its own device buffer and back; a device in-place advance is safe
-    // because Y0 is only read pointwise after stage 1
-    sg.output(u1, NF);
-    const size_t evn = vertex_coef_doubles(g, mode);
+    HostIO io(g, st);
+    Coefs cf;
+    resolve_coefs(cf, g, mode, k1, k2, k3, b, w, io, N);
+    check_mode(mode, ncomp, cf.b);
+    io.input(u0, NF);
+    // host arrays (even an in-place u0 == u1) are staged separately: the result goes to
+    // its own device buffer and back; a device in-place advance is safe because Y0 is
+    // only read pointwise after stage 1
+    io.output(u1, NF);
+    io.begin();
     const size_t NFr = rnd(NF);
-    double* base = ws_get(g, (rnd(sg.total) + 3 * NFr + evn) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 3 * NFr + evn);
-    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, base + 3 * NFr, k1, k2, k3, b, st);
-    rkl2_core(g, mode, ncomp, u0, u1, k1, k2, k3, bb, w, dt, s, ev, base, base + NFr, base + 2 * NFr, st);
-    sg.end({u1});
+    double* base = ws_get(g, (3 * NFr + call_ev_doubles(g, mode, cf)) * sizeof(double));
+    exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, cf.b, st);
+    const auto ev = call_vertex_coefs(g, mode, cf, base + 3 * NFr, st);
+    rkl2_core(g, mode, ncomp, u0, u1, cf.k1, cf.k2, cf.k3, cf.b, cf.w, dt, s, ev, base, base + NFr, base + 2 * NFr,
+              st);
+    io.end();
   });
 }
 
@@ -1017,8 +1814,7 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
                         const double* k2, const double* k3, const double* b, const double* w, double dt,
                         double dt_exp, double euler_frac, int n_euler, int n_sub, int* stages_out, void* stream) {
   return guard([&] {
-    STS_REQUIRE(g && u0 && u1 && k1 && k2 && k3, "NULL argument");
-    check_mode(mode, ncomp, b);
+    STS_REQUIRE(g && u0 && u1, "NULL argument");
     STS_REQUIRE(std::isfinite(dt) && dt >= 0.0 && std::isfinite(dt_exp) && dt_exp > 0.0, "bad dt / dt_exp");
     STS_REQUIRE(euler_frac >= 0.0 && euler_frac < 1.0, "euler_frac must be in [0, 1)");
     STS_REQUIRE(n_sub >= 1, "n_sub must be >= 1");
@@ -1034,23 +1830,20 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
     const size_t NF = N * ncomp;
-    Stage sg{g, st};
-    sg.input(u0, NF);
-    sg.input(k1, N);
-    sg.input(k2, N);
-    sg.input(k3, N);
-    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
-    sg.input(w, N);
-    sg.output(u1, NF);
-    const size_t evn = vertex_coef_doubles(g, mode);
+    HostIO io(g, st);
+    Coefs cf;
+    resolve_coefs(cf, g, mode, k1, k2, k3, b, w, io, N);
+    check_mode(mode, ncomp, cf.b);
+    io.input(u0, NF);
+    io.output(u1, NF);
+    io.begin();
     const size_t NFr = rnd(NF);
     // scratch: M0, A, B (RKL2 stages), E0, E1 (sub-step ping-pong), vertex coefficients
-    double* base = ws_get(g, (rnd(sg.total) + 5 * NFr + evn) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 5 * NFr + evn);
+    double* base = ws_get(g, (5 * NFr + call_ev_doubles(g, mode, cf)) * sizeof(double));
     double* E[2] = {base + 3 * NFr, base + 4 * NFr};
-    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, base + 5 * NFr, k1, k2, k3, b, st);
+    const double* bb = cf.b;
+    exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, bb, st);
+    const auto ev = call_vertex_coefs(g, mode, cf, base + 5 * NFr, st);
     // explicit Euler prefix: u <- u + dte F(u), n_euler times
     const double* cur = u0;
     int e = 0;
@@ -1059,7 +1852,7 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
       e ^= 1;
       sweep(g, {{H_U, cur, ncomp}}, st, [&](size_t si) {
         const Slab& sl = g->slabs[si];
-        StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, cur, k1, k2, k3, bb, w);
+        StencilCall c = make_call(g, sl, mode, ncomp, EPI_RKL2_FIRST, cur, cf.k1, cf.k2, cf.k3, bb, cf.w);
         c.ev = ev[si];
         c.ea.out = off(dst, sl);
         c.ea.out2 = off(base, sl);   // F(u) (unused scratch)
@@ -1072,398 +1865,64 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
     for (int m = 1; m <= n_sub; ++m) {
       double* dst = (m == n_sub) ? u1 : E[e];
       if (m < n_sub) e ^= 1;
-      rkl2_core(g, mode, ncomp, cur, dst, k1, k2, k3, bb, w, dtr, s, ev, base, base + NFr, base + 2 * NFr, st);
+      rkl2_core(g, mode, ncomp, cur, dst, cf.k1, cf.k2, cf.k3, bb, cf.w, dtr, s, ev, base, base + NFr, base + 2 * NFr,
+                st);
       cur = dst;
     }
     if (stages_out) {
       stages_out[0] = n_euler;
       stages_out[1] = s;
     }
-    sg.end({u1});
+    io.end();
   });
 }
 
-int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const double* k1,
-                 const double* k2, const double* k3, const double* b, const double* w, double dt, double rtol,
-                 int kmax, int* iters_out, void* stream) {
+static int pcg_entry(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const double* k1,
+                     const double* k2, const double* k3, const double* b, const double* w, double dt, double rtol,
+                     int kmax, int* iters_out, int* status_out, void* stream, bool allow_async) {
   int status = STS_OK;
+  bool synchronous = true;
   int rc = guard([&] {
-    STS_REQUIRE(g && un && un1 && k1 && k2 && k3, "NULL argument");
-    check_mode(mode, ncomp, b);
+    STS_REQUIRE(g && un && un1, "NULL argument");
     STS_REQUIRE(kmax >= 1, "kmax must be >= 1");
     STS_REQUIRE(std::isfinite(dt) && dt >= 0.0 && std::isfinite(rtol) && rtol >= 0.0, "bad dt / rtol");
     DeviceGuard dg(g->device);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t N = (size_t)g->nl * g->plane;
     const size_t NF = N * ncomp;
+    HostIO io(g, st);
+    Coefs cf;
+    resolve_coefs(cf, g, mode, k1, k2, k3, b, w, io, N);
+    check_mode(mode, ncomp, cf.b);
     const bool alias = (const void*)un == (const void*)un1;
     // same DEVICE array for un and un1: x0 is already in place; otherwise write it
     const bool write_x0 = !(alias && is_device_ptr(un1));
-    Stage sg{g, st};
-    sg.input(un, NF);
-    sg.input(k1, N);
-    sg.input(k2, N);
-    sg.input(k3, N);
-    if (mode == STS_MODE_ANISO) sg.input(b, 3 * N);
-    sg.input(w, N);
-    sg.output(un1, NF);
-    const size_t evn = vertex_coef_doubles(g, mode);
-    const size_t NFr = rnd(NF), Nr = rnd(N);
-    // scratch: six [ncomp][nl][plane] fields (two-pass: r, z, y, p0, p1; merged: z0, z1,
-    // w0, w1, p0, p1); d [nl][plane]; vertex coefficients
-    // (+ the metric-folded isotropic coefficients K1, K2, K3, wV of the merged pass)
-    const size_t npre = (mode == STS_MODE_ISO && g->tma && g->pcg_merged) ? 4 * Nr : 0;
-    double* base = ws_get(g, (6 * NFr + Nr + npre + evn + rnd(sg.total)) * sizeof(double));
-    if (sg.any_host) sg.begin(base + 6 * NFr + Nr + npre + evn);
-    double* r = base;
-    double* z = base + NFr;
-    double* y = base + 2 * NFr;
-    double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
-    double* d = base + 6 * NFr;
-    double* pre = npre ? base + 6 * NFr + Nr : nullptr;   // K1, K2, K3, wV ([nl][plane] each)
-    double* evbase = base + 6 * NFr + Nr + npre;
-    // merged iteration buffers (ping-pong by iteration parity; the p pair is pb)
-    double* zb[2] = {base, base + NFr};
-    double* wb[2] = {base + 2 * NFr, base + 5 * NFr};
-    double* x = un1;
-    const double* bb = mode == STS_MODE_ANISO ? b : nullptr;
-    const double rtol2 = rtol * rtol;
-    const long long cs = (long long)g->nl * g->plane;
-
-    exchange_coeffs(g, mode, k1, k2, k3, b, st);
-    const auto ev = build_vertex_coefs(g, mode, evbase, k1, k2, k3, b, st);
-    // the S-pass (p update + x update + A p) is ONE fused TMA kernel where eligible
-    bool fused = false;
-    if (g->tma) {
-      StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_S, z, k1, k2, k3, bb, w);
-      c.u2 = view(g, g->slabs[0], H_P, pb[0]);
-      c.ev = ev[0];
-      c.ea.out = off(y, g->slabs[0]);
-      c.ea.out2 = off(pb[1], g->slabs[0]);
-      c.ea.x = off(x, g->slabs[0]);
-      c.u3 = view(g, g->slabs[0], H_D, d);
-      fused = aniso_tma_eligible(c) || iso_tma_eligible(c);
-    }
-    // merged iteration (one pass + one reduction per iteration, sts_grid_set_pcg_merged)
-    bool merged = false;
-    if (g->tma && g->pcg_merged) {
-      StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_M, zb[0], k1, k2, k3, bb, w);
-      c.u2 = view(g, g->slabs[0], H_W, wb[0]);
-      c.u3 = view(g, g->slabs[0], H_P, pb[0]);
-      c.ev = ev[0];
-      c.ea.out = off(zb[1], g->slabs[0]);
-      c.ea.out2 = off(pb[1], g->slabs[0]);
-      c.ea.out3 = off(wb[1], g->slabs[0]);
-      c.ea.x = off(x, g->slabs[0]);
-      c.ea.dinv = off(d, g->slabs[0]);
-      if (mode == STS_MODE_ISO) {
-        c.k1.p = off(pre, g->slabs[0]);
-        c.k2.p = off(pre + Nr, g->slabs[0]);
-        c.k3.p = off(pre + 2 * Nr, g->slabs[0]);
-        c.w = off(pre + 3 * Nr, g->slabs[0]);
-        c.premul = 1;
-      }
-      merged = (mode == STS_MODE_ISO ? npre > 0 && iso_tma_eligible(c) : aniso_tma_eligible(c));
-    }
-    if (merged && mode == STS_MODE_ISO)
-      for (auto& sl : g->slabs) {
-        Timed t(g, STS_K_VERTEX_COEF, st);   // (the isotropic counterpart of the frozen vertex coefficients)
-        launch_iso_premul(slab_geo(g, sl), off(k1, sl), off(k2, sl), off(k3, sl), off(w, sl), off(pre, sl),
-                          off(pre + Nr, sl), off(pre + 2 * Nr, sl), off(pre + 3 * Nr, sl), st);
-      }
-    if (merged) fused = false;
-    // isotropic fused S-pass: z = r d is formed inside the stencil pass from the staged
-    // r and d, so neither the initial residual pass nor the U-pass stores z
-    const bool zd = fused && mode == STS_MODE_ISO;
-    // the passes (make(si) -> StencilCall of slab si; sweep() sets the plane range and pbase)
-    double* partials = nullptr;
-    long long pstride = 0;
-    PcgScal* sc = nullptr;
-    int k_cur = 1;   // iteration whose S-pass is being built
-    auto make_r0 = [&](size_t si) {
-      const Slab& sl = g->slabs[si];
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_R0, un, k1, k2, k3, bb, w);
-      c.ev = ev[si];
-      c.ea.out = merged ? off(wb[0], sl) : off(r, sl);   // (merged: r0 itself is not needed)
-      c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-      c.ea.out3 = merged ? off(zb[0], sl) : (zd ? nullptr : off(z, sl));
-      c.ea.out4 = off(d, sl);
-      c.ea.dt = dt;
-      c.ea.partials = partials;
-      c.ea.pstride = pstride;
-      return c;
-    };
-    auto make_s = [&](size_t si) {   // fused S-pass (TMA)
-      const Slab& sl = g->slabs[si];
-      const int first = (k_cur == 1);
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_S, zd ? r : z, k1, k2, k3, bb, w);
-      c.u = view(g, sl, H_Z, zd ? r : z);
-      c.u2 = first ? FieldV{} : view(g, sl, H_P, pb[(k_cur - 1) & 1]);
-      if (zd) c.u3 = view(g, sl, H_D, d);
-      c.ev = ev[si];
-      c.ea.out = off(y, sl);
-      c.ea.out2 = off(pb[k_cur & 1], sl);
-      c.ea.x = off(x, sl);
-      c.ea.first = first;
-      c.ea.dt = dt;
-      c.ea.partials = partials;
-      c.ea.pstride = pstride;
-      c.ea.sc = sc;
-      return c;
-    };
-    auto make_m = [&](size_t si) {   // merged iteration k_cur (TMA)
-      const Slab& sl = g->slabs[si];
-      const int first = (k_cur == 1);
-      const int a = (k_cur - 1) & 1, b2 = k_cur & 1;
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_M, zb[a], k1, k2, k3, bb, w);
-      c.u = view(g, sl, H_Z, zb[a]);
-      c.u2 = first ? FieldV{} : view(g, sl, H_W, wb[a]);
-      c.u3 = first ? FieldV{} : view(g, sl, H_P, pb[a]);
-      c.ev = ev[si];
-      c.ea.out = off(zb[b2], sl);
-      c.ea.out2 = off(pb[b2], sl);
-      c.ea.out3 = off(wb[b2], sl);
-      c.ea.x = off(x, sl);
-      c.ea.dinv = off(d, sl);
-      if (mode == STS_MODE_ISO) {   // metric-folded coefficients (the k1 halo planes stay raw)
-        c.k1.p = off(pre, sl);
-        c.k2.p = off(pre + Nr, sl);
-        c.k3.p = off(pre + 2 * Nr, sl);
-        c.w = off(pre + 3 * Nr, sl);
-        c.premul = 1;
-      }
-      c.ea.first = first;
-      c.ea.dt = dt;
-      c.ea.partials = partials;
-      c.ea.pstride = pstride;
-      c.ea.sc = sc;
-      return c;
-    };
-    auto make_ap = [&](size_t si) {  // A p of the unfused S-pass
-      const Slab& sl = g->slabs[si];
-      double* pnew = pb[k_cur & 1];
-      StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_AP, pnew, k1, k2, k3, bb, w);
-      c.ev = ev[si];
-      c.ea.out = off(y, sl);
-      c.ea.dt = dt;
-      c.ea.partials = partials;
-      c.ea.pstride = pstride;
-      c.ea.sc = sc;
-      return c;
-    };
-    const int sb_r0 = sweep_blocks(g, true, make_r0);
-    const int sb_s = merged ? sweep_blocks(g, true, make_m)
-                            : (fused ? sweep_blocks(g, true, make_s) : sweep_blocks(g, true, make_ap));
-    pstride = std::max(std::max(sb_r0, sb_s), PW_BLOCKS);
-    // partial rows: ncomp x (2 for R0, 1 per two-pass phase, 4 for the merged pass)
-    const size_t red_doubles = (size_t)4 * ncomp * pstride + 16 + (sizeof(PcgScal) * MAXC) / sizeof(double) + 8;
-    ensure_red(g, red_doubles * sizeof(double));
-    partials = g->d_red;
-    double* sums = partials + 4 * ncomp * pstride;
-    sc = reinterpret_cast<PcgScal*>(sums + 16);
-
-    // fused final reductions (single process): the last CTA of the S-pass / U-pass sums
-    // the partials and runs the scalar phase, saving two launches per iteration
-    FinRed fin_s;
-    fin_s.ticket = g->d_ticket;
-    fin_s.sums = sums;
-    fin_s.sc = sc;
-    fin_s.ncomp = ncomp;
-    fin_s.nq = 1;
-    fin_s.phase = PH_AP;
-    fin_s.rtol2 = rtol2;
-    FinRed fin_u = fin_s;
-    fin_u.phase = PH_RZ;
-    FinRed fin_m = fin_s;
-    fin_m.nq = 4;
-    fin_m.phase = PH_M;
-    fin_u.ntot = PW_BLOCKS;   // set to the launched grid by launch_pcg_rupdate
-    auto reduce = [&](int nblocks, int nq, int phase) {
-      Timed t(g, STS_K_PCG_REDUCE, st);
-      if (g->comm) {
-        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, PH_NONE, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
-        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * nq, ncclDouble, ncclSum, g->comm, st));
-        launch_pcg_scalar(sums, ncomp, nq, phase, sc, rtol2, st);
-        g->launches += 1;
-      } else {
-        launch_pcg_reduce(partials, pstride, nblocks, ncomp, nq, sums, phase, sc, rtol2, st, g->d_red2, g->d_ticket + 1);
-      }
-    };
-
-    // r0 = b - A x0 = dt L un ; d = 1/diag(A) ; x = un ; z0 = r0 d ; r0.z0, b.P^-1 b
-    reduce(sweep(g, {{H_U, un, ncomp}}, st, make_r0), 2, PH_R0);
-    if (needs_halos(g)) g->comm_global += 1;
-    if (zd) exchange(g, H_D, d, 1, st);   // d is fixed for the whole solve: its halo once
-    // iteration k (Fig. 1 with the x update deferred one iteration):
-    //   S: p_k = z_k + beta_{k-1} p_{k-1};  x_k = x_{k-1} + alpha_{k-1} p_{k-1};  y = A p_k;  alpha_k
-    //   U: r_{k+1} = r_k - alpha_k y;  z_{k+1} = r_{k+1} d;  r.z -> convergence, beta_k
-    auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
-    // one PCG iteration k on stream `is`
-    // merged iteration k: ONE pass (z_k, p_k, y_k = A p_k, w_k = d y_k, x_k; partials
-    // r_k.z_k, p_k.y_k, z_k.y_k, w_k.y_k) and ONE reduction (alpha_k, r_{k+1}.z_{k+1},
-    // convergence, beta_{k+1}: pcg.cuh PH_M)
-    auto iteration_m = [&](int k, cudaStream_t is) {
-      k_cur = k;
-      if (needs_halos(g)) g->comm_global += 1;
-      const int a = (k - 1) & 1;
-      const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_m;
-      int nbs;
-      if (k == 1) nbs = sweep(g, {{H_Z, zb[0], ncomp}}, is, make_m, fs);
-      else nbs = sweep(g, {{H_Z, zb[a], ncomp}, {H_W, wb[a], ncomp}, {H_P, pb[a], ncomp}}, is, make_m, fs);
-      if (!fs) {
-        Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
-        if (g->comm) {
-          STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp * 4, ncclDouble, ncclSum, g->comm, is));
-          launch_pcg_scalar(sums, ncomp, 4, PH_M, sc, rtol2, is);
-          g->launches += 1;
-        }
-      }
-    };
-    auto iteration = [&](int k, cudaStream_t is) {
-      if (merged) return iteration_m(k, is);
-      k_cur = k;
-      if (needs_halos(g)) g->comm_global += 2;   // p.y (alpha) and r.z (beta + convergence)
-      double* pold = pb[(k - 1) & 1];
-      double* pnew = pb[k & 1];
-      int nbs;
-      if (fused) {
-        // (the last CTA finishes the reduction when the pass has few CTAs; large passes
-        // keep the 1024-thread reduction kernel, which sums ~1e4 partials faster)
-        const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_s;
-        const double* zr = zd ? r : z;
-        if (k == 1) nbs = sweep(g, {{H_Z, zr, ncomp}}, is, make_s, fs);
-        else nbs = sweep(g, {{H_Z, zr, ncomp}, {H_P, pold, ncomp}}, is, make_s, fs);
-      } else {
-        {
-          Timed t(g, STS_K_PCG_PUPDATE, is);
-          launch_pcg_pnew(ncomp, (long long)N, cs, pnew, z, pold, x, sc, k == 1, is);
-        }
-        nbs = sweep(g, {{H_U, pnew, ncomp}}, is, make_ap);
-      }
-      if (!(fused && !g->comm && sb_s <= 4096)) {           // else finished by the S-pass's last CTA
-        Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbs, ncomp, 1, sums, g->comm ? PH_NONE : PH_AP, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
-        if (g->comm) {
-          STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
-          launch_pcg_scalar(sums, ncomp, 1, PH_AP, sc, rtol2, is);
-          g->launches += 1;
-        }
-      }
-      int nbu;
-      {
-        Timed t(g, STS_K_PCG_UPDATE, is);
-        nbu = launch_pcg_rupdate(ncomp, (long long)N, cs, r, zd ? nullptr : z, y, d, sc, partials, pstride,
-                                 g->comm ? FinRed{} : fin_u, is);
-      }
-      if (g->comm) {
-        Timed t(g, STS_K_PCG_REDUCE, is);
-        launch_pcg_reduce(partials, pstride, nbu, ncomp, 1, sums, PH_NONE, sc, rtol2, is, g->d_red2, g->d_ticket + 1);
-        STS_NCCL(ncclAllReduce(sums, sums, (size_t)ncomp, ncclDouble, ncclSum, g->comm, is));
-        launch_pcg_scalar(sums, ncomp, 1, PH_RZ, sc, rtol2, is);
-        g->launches += 1;
-      }
-    };
-    // Iterations k >= 2 come in identical pairs (k even, k odd: the p buffers swap back),
-    // so a single process replays one captured CUDA graph per pair: no host launch work
-    // and minimal launch gaps per iteration.  Instrumented runs (per-launch events) and
-    // NCCL runs launch directly.  The graph runs on the library's own non-blocking
-    // stream (capture is not allowed on the legacy default stream), forked from and
-    // joined back to the caller's stream.
-    const bool use_graph = g->graphs && !g->timing && g->comm == nullptr;
-    cudaStream_t is = st;
-    cudaGraphExec_t pair_exec = nullptr;
-    long long pair_launches = 0, pair_local = 0, pair_global = 0;
-    if (use_graph) {
-      is = graph_stream(g);
-      STS_CUDA(cudaEventRecord(g->ev_c, st));
-      STS_CUDA(cudaStreamWaitEvent(is, g->ev_c, 0));
-    }
-    int launched = 0;
-    int batch = 4;
-    bool all_done = false;
-    bool capturing = false;
-    try {
-      while (true) {
-        launch_publish(reinterpret_cast<const double*>(sc), (int)(sizeof(PcgScal) * ncomp / sizeof(double)),
-                       g->d_pinned, is);
-        STS_CUDA(cudaStreamSynchronize(is));
-        all_done = true;
-        for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
-        if (all_done || launched >= kmax) break;
-        const int nb = std::min(batch, kmax - launched);
-        int it = 0;
-        while (it < nb) {
-          const int k = launched + it + 1;
-          // (the first pair, k = 2, 3, runs directly: every kernel variant it uses has then
-          // had its one-time attribute setup outside the capture)
-          if (use_graph && k >= 4 && (k % 2) == 0 && it + 2 <= nb) {
-            if (!pair_exec) {
-              const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
-              cudaGraph_t graph;
-              STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
-              capturing = true;
-              iteration(k, is);
-              iteration(k + 1, is);
-              capturing = false;
-              STS_CUDA(cudaStreamEndCapture(is, &graph));
-              STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
-              STS_CUDA(cudaGraphDestroy(graph));
-              pair_launches = g->launches - l0;
-              pair_local = g->comm_local - cl0;
-              pair_global = g->comm_global - cg0;
-              g->launches = l0;
-              g->comm_local = cl0;
-              g->comm_global = cg0;
-            }
-            STS_CUDA(cudaGraphLaunch(pair_exec, is));
-            g->launches += pair_launches;
-            g->comm_local += pair_local;
-            g->comm_global += pair_global;
-            it += 2;
-          } else {
-            iteration(k, is);
-            it += 1;
-          }
-        }
-        launched += nb;
-        batch = std::min(batch * 2, 64);
-      }
-    } catch (...) {
-      if (capturing) {   // leave the library's stream usable: close the capture, drop the graph
-        cudaGraph_t broken = nullptr;
-        if (cudaStreamEndCapture(is, &broken) == cudaSuccess && broken) cudaGraphDestroy(broken);
-        cudaGetLastError();
-      }
-      if (pair_exec) cudaGraphExecDestroy(pair_exec);
-      throw;
-    }
-    if (pair_exec) STS_CUDA(cudaGraphExecDestroy(pair_exec));
-    if (use_graph) {
-      STS_CUDA(cudaEventRecord(g->ev_c, is));
-      STS_CUDA(cudaStreamWaitEvent(st, g->ev_c, 0));
-    }
-    {
-      Timed t(g, STS_K_PCG_XFINAL, st);
-      launch_pcg_xfinal(ncomp, (long long)N, cs, x, pb[0], pb[1], sc, st);
-    }
-    launch_publish(reinterpret_cast<const double*>(sc), (int)(sizeof(PcgScal) * ncomp / sizeof(double)),
-                   g->d_pinned, st);
-    STS_CUDA(cudaStreamSynchronize(st));
-    if (iters_out)
-      for (int c = 0; c < ncomp; ++c) iters_out[c] = hsc[c].iters;
-    bool broke = false;
-    for (int c = 0; c < ncomp; ++c) broke = broke || (hsc[c].flags & PCG_BREAKDOWN);
-    sg.end({un1});
-    if (broke) {
-      status = STS_ERR_BREAKDOWN;
-      set_error("be_pcg_solve: PCG breakdown (p.A p <= 0 or a non-finite scalar: A not SPD or non-finite input)");
-    } else if (!all_done) {
-      status = STS_ERR_NOT_CONVERGED;
-      set_error("be_pcg_solve: kmax reached before convergence");
-    }
+    io.input(un, NF);
+    io.output(un1, NF);
+    io.begin();
+    synchronous = pcg_core(g, mode, ncomp, un, un1, cf, dt, rtol, kmax, st, write_x0, iters_out, status_out,
+                           &status, allow_async, io);
   });
-  return rc != STS_OK ? rc : status;
+  if (rc != STS_OK) return rc;
+  if (!synchronous) return STS_OK;   // results arrive with the stream (status_out)
+  if (status_out) *status_out = status;
+  if (status == STS_ERR_BREAKDOWN)
+    set_error("be_pcg_solve: PCG breakdown (p.A p <= 0 or a non-finite scalar: A not SPD or non-finite input)");
+  else if (status == STS_ERR_NOT_CONVERGED)
+    set_error("be_pcg_solve: kmax reached before convergence");
+  return status;
+}
+
+int be_pcg_solve(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const double* k1,
+                 const double* k2, const double* k3, const double* b, const double* w, double dt, double rtol,
+                 int kmax, int* iters_out, void* stream) {
+  return pcg_entry(g, mode, ncomp, un, un1, k1, k2, k3, b, w, dt, rtol, kmax, iters_out, nullptr, stream, false);
+}
+
+int be_pcg_solve_async(sts_grid* g, int mode, int ncomp, const double* un, double* un1, const double* k1,
+                       const double* k2, const double* k3, const double* b, const double* w, double dt, double rtol,
+                       int kmax, int* iters_out, int* status_out, void* stream) {
+  return pcg_entry(g, mode, ncomp, un, un1, k1, k2, k3, b, w, dt, rtol, kmax, iters_out, status_out, stream, true);
 }
 
 }  // extern "C"

@@ -14,6 +14,16 @@ __device__ inline void pcg_breakdown(PcgScal& s) {
   s.ax = 0.0;
 }
 
+// the iteration limit: a component that has run kmax iterations without converging
+// stops (its last alpha still reaches x through the final pass); the host reports
+// STS_ERR_NOT_CONVERGED
+__device__ inline void pcg_kmax(PcgScal& s) {
+  if (!s.done && s.iters >= s.kmax) {
+    s.done = 1;
+    s.flags |= PCG_KMAX;
+  }
+}
+
 // scalar recurrences of Fig. 1 (one thread per component)
 __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, PcgScal* sc, double rtol2) {
   PcgScal& s = sc[c];
@@ -21,7 +31,7 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.rz = sums[c * nq + 0];
     s.thresh = rtol2 * sums[c * nq + 1];
     s.iters = 0;
-    s.flags = 0;
+    s.flags = 0;                           // (kmax was set by launch_pcg_init)
     s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
     s.beta = 0.0;
     s.ax = 0.0;
@@ -40,6 +50,7 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.ax = s.alpha;                        // x_{k+1} = x_k + alpha_k p_k, applied by the next p pass / final pass
     if (s.rz <= s.thresh) s.done = 1;      // check r_r for convergence
     else s.beta = s.rz / s.rz_old;         // beta_k = r_r / r_old
+    pcg_kmax(s);
   } else if (phase == PH_M) {
     // merged iteration k (one pass, one reduction): sums of the pass
     // are r_k.z_k (= z_k^2 / d), p_k.y_k, z_k.y_k and (d y_k).y_k with y_k = A p_k.
@@ -72,6 +83,7 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     if (s.rz < 0.0 && fuzz > s.thresh) s.beta = 0.0;
     else if (s.rz <= s.thresh) s.done = 1;
     else s.beta = s.rz / rz;               // beta_{k+1} = r_{k+1}.z_{k+1} / r_k.z_k
+    pcg_kmax(s);
   }
 }
 

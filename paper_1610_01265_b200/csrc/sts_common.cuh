@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <list>
 #include <string>
 #include <vector>
 
@@ -109,6 +110,42 @@ struct Workspace {
   size_t bytes = 0;
 };
 
+// Device staging buffer of the host-array path (capi.cu HostIO): free for reuse once
+// `ev` (recorded after its last use: the consuming kernels of an input, the download of
+// an output) has completed.
+struct StageBuf {
+  double* p = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;     // ev recorded and possibly not complete
+  bool claimed = false;     // held by the call being enqueued
+};
+
+// Coefficients of one operator mode kept resident across calls (sts_grid_bind_coeffs):
+// the arrays in use (caller device arrays, or library-owned copies of host arrays and
+// face-kappa outputs) and the data derived from them once per binding: the frozen vertex
+// coefficients (ANISO), the metric-folded face coefficients of the merged PCG pass (ISO)
+// and the Gershgorin bound.
+struct CoefSlot {
+  bool bound = false;
+  const double* k[3] = {nullptr, nullptr, nullptr};
+  const double* b = nullptr;
+  const double* w = nullptr;
+  // library-owned device copies of host arrays (k1, k2, k3, b, w), two per array used in
+  // turn: an upload writes the copy the previous upload superseded, once the work enqueued
+  // before that supersession is done (own_ev) -- so uploads overlap the current binding's work
+  double* own[5][2] = {};
+  size_t own_n[5][2] = {};
+  int own_next[5] = {0, 0, 0, 0, 0};
+  cudaEvent_t own_ev[5][2] = {};
+  bool own_ev_set[5][2] = {};
+  double* kfk[3] = {nullptr, nullptr, nullptr};   // face diffusivities written by sts_face_kappa_spitzer
+  double* derived = nullptr;          // ANISO: vertex coefficients of every slab; ISO: K1, K2, K3, wV
+  size_t derived_bytes = 0;
+  bool ev_ok = false, pre_ok = false; // derived data current for the bound arrays
+  double lam = -1.0;                  // cached Gershgorin max row sum (< 0: not computed)
+};
+
 }  // namespace sts
 
 struct sts_grid {
@@ -136,6 +173,8 @@ struct sts_grid {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   long long launches = 0;
+  std::atomic<long long> launches_async{0};    // added by completion callbacks of asynchronous solves
+  std::atomic<long long> comm_async[2];        // (local, global) likewise
   long long comm_local = 0, comm_global = 0;   // sts_grid_comm_counts
   size_t halo_bytes = 0;
   bool tma = true;                      // TMA pipelined kernels where eligible (sts_grid_set_tma)
@@ -151,6 +190,14 @@ struct sts_grid {
   std::vector<cudaEvent_t> free_events;
   double acc_ms[STS_K_NCLASSES] = {};
   long long acc_n[STS_K_NCLASSES] = {};
+  // host-array path: copy streams (H2D / D2H engines run concurrently with the compute
+  // stream), staging buffers, and the events a caller's stream joins (sts_grid_join)
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::list<sts::StageBuf> stage_pool;  // (stable addresses: a call holds pointers into it)
+  size_t stage_bytes = 0;
+  cudaEvent_t ev_h2d_last = nullptr, ev_d2h_last = nullptr;
+  bool h2d_used = false, d2h_used = false;
+  sts::CoefSlot slot[2];                // resident coefficients per mode (STS_MODE_ISO, STS_MODE_ANISO)
 };
 
 namespace sts {
@@ -216,9 +263,11 @@ struct PcgScal {
   double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update;
                     // the merged iteration also applies it to z)
   int done, iters;
-  int flags, pad;   // flags: PCG_BREAKDOWN (p.A p <= 0 or a non-finite scalar: A not SPD / NaN input)
+  int flags;        // PCG_BREAKDOWN (p.A p <= 0 or a non-finite scalar: A not SPD / NaN input), PCG_KMAX
+  int kmax;         // iteration limit (set by launch_pcg_init): reaching it stops the component
 };
 constexpr int PCG_BREAKDOWN = 1;
+constexpr int PCG_KMAX = 2;
 static_assert(sizeof(PcgScal) % sizeof(double) == 0, "PcgScal is published as doubles");
 
 // fused final reduction of a PCG pass (pcg.cuh: fused_final_reduce)
@@ -348,6 +397,11 @@ void launch_pcg_reduce(const double* partials, long long pstride, int nblocks, i
                        double* l2 = nullptr, unsigned* ticket = nullptr);
 void launch_pcg_scalar(const double* sums, int ncomp, int nq, int phase, PcgScal* sc, double rtol2,
                        cudaStream_t st);
+// per-solve PCG scalar initialisation (iteration limit, flags, loop body counter)
+void launch_pcg_init(PcgScal* sc, int ncomp, int kmax, int* body_count, cudaStream_t st);
+// condition kernel of the device-driven PCG loop (sets the WHILE node's handle)
+void launch_pcg_continue(cudaGraphConditionalHandle h, const PcgScal* sc, int ncomp, int* body_count, bool count,
+                         cudaStream_t st);
 // copy n doubles to mapped pinned host memory with SM stores (no copy engine)
 void launch_publish(const double* src, int n, double* dst_mapped, cudaStream_t st);
 

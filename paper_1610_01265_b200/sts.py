@@ -74,6 +74,11 @@ def lib():
         "rkl2_advance": (I, [P, I, I, P, P, P, P, P, P, P, D, I, P]),
         "rkl2_advance_hybrid": (I, [P, I, I, P, P, P, P, P, P, P, D, D, D, I, I, ctypes.POINTER(I), P]),
         "be_pcg_solve": (I, [P, I, I, P, P, P, P, P, P, P, D, D, I, ctypes.POINTER(I), P]),
+        "be_pcg_solve_async": (I, [P, I, I, P, P, P, P, P, P, P, D, D, I, ctypes.POINTER(I), ctypes.POINTER(I), P]),
+        "sts_grid_bind_coeffs": (I, [P, I, P, P, P, P, P, P]),
+        "sts_grid_unbind_coeffs": (I, [P, I]),
+        "sts_grid_join": (I, [P, P]),
+        "sts_grid_synchronize": (I, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -97,6 +102,29 @@ def _ptr(t):
     if t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError("arrays must be contiguous float64 tensors")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _kptrs(k):
+    """k = (k1, k2, k3) tensors, or None for the resident (bound) coefficients."""
+    if k is None:
+        return (None, None, None)
+    return tuple(_ptr(x) for x in k)
+
+
+class PcgResult:
+    """Iterations / status of an asynchronous solve, written when the stream reaches its end."""
+
+    def __init__(self, ncomp):
+        self._iters = (ctypes.c_int * ncomp)(*([-1] * ncomp))
+        self._status = ctypes.c_int(1)
+
+    @property
+    def iters(self):
+        return list(self._iters)
+
+    @property
+    def status(self):
+        return self._status.value
 
 
 def _np_ptr(a):
@@ -146,6 +174,9 @@ class Grid:
         self.i0, self.nl = i0, nl
         self.shape = (nl, n2, n3)
         self.device = torch.device("cuda", device)
+        # False: calls with host (CPU) tensors return with their outputs written back; True:
+        # they return once enqueued (pinned memory) -- then join() + synchronize first
+        self.async_host = False
 
     @classmethod
     def from_grid(cls, g, i0=0, nl=None, n_virtual=1, device=0):
@@ -216,6 +247,43 @@ class Grid:
             out[name] = (n.value, ms.value)
         return out
 
+    def bind_coeffs(self, mode, k=None, b=None, w=None, stream=None):
+        """Bind `mode`'s coefficients (resident across calls; None keeps the bound array).
+        Ops called with k=None then use them (include/sts_b200.h "Resident coefficients")."""
+        k = k if k is not None else (None, None, None)
+        self._bound = getattr(self, "_bound", {})
+        keep = self._bound.setdefault(mode, {})   # device tensors are referenced: keep them alive
+        for name, t in (("k1", k[0]), ("k2", k[1]), ("k3", k[2]), ("b", b), ("w", w)):
+            if t is not None:
+                keep[name] = t
+        _check("sts_grid_bind_coeffs", lib().sts_grid_bind_coeffs(
+            self._h, MODE[mode], *_kptrs(k), _ptr(b), _ptr(w), _stream(stream)))
+
+    def unbind_coeffs(self, mode):
+        _check("sts_grid_unbind_coeffs", lib().sts_grid_unbind_coeffs(self._h, MODE[mode]))
+        getattr(self, "_bound", {}).pop(mode, None)
+
+    def join(self, stream=None):
+        """Make `stream` wait for the handle's outstanding host-array copies."""
+        _check("sts_grid_join", lib().sts_grid_join(self._h, _stream(stream)))
+
+    def synchronize(self):
+        _check("sts_grid_synchronize", lib().sts_grid_synchronize(self._h))
+
+    def _host_done(self, stream, *arrays):
+        """Host (CPU) tensors make the C call asynchronous (pinned) -- unless the Grid is in
+        async_host mode, wait here so that the outputs can be read on return."""
+        if self.async_host:
+            return
+        if any(isinstance(a, torch.Tensor) and a.device.type == "cpu" for a in arrays if a is not None):
+            self.join(stream)
+            if stream is None:
+                torch.cuda.current_stream(self.device).synchronize()
+            elif hasattr(stream, "synchronize"):
+                stream.synchronize()
+            else:
+                torch.cuda.synchronize(self.device)
+
     def comm_init(self, nranks, rank, uid: bytes):
         buf = ctypes.create_string_buffer(uid, UID_BYTES)
         _check("sts_comm_init", lib().sts_comm_init(self._h, int(nranks), int(rank), buf, UID_BYTES))
@@ -228,33 +296,41 @@ class Grid:
             return torch.empty(shape, dtype=torch.float64, pin_memory=torch.cuda.is_available())
         return torch.empty(shape, dtype=torch.float64, device=dev)
 
-    def face_kappa_spitzer(self, T, kappa0, T_cut, fc_r0=10.0, fc_w=0.0, out=None, stream=None):
-        out = out or tuple(self._alloc(1, T) for _ in range(3))
+    def face_kappa_spitzer(self, T, kappa0, T_cut, fc_r0=10.0, fc_w=0.0, out=None, stream=None, resident=False):
+        """Face diffusivities into `out` (allocated if None) -- or, resident=True, into
+        library-owned arrays bound as the "aniso" coefficients (returns None)."""
+        if resident:
+            out = (None, None, None)
+        else:
+            out = out or tuple(self._alloc(1, T) for _ in range(3))
         _check("sts_face_kappa_spitzer", lib().sts_face_kappa_spitzer(
             self._h, _ptr(T), *[_ptr(o) for o in out], float(kappa0), float(T_cut), float(fc_r0),
             float(fc_w), _stream(stream)))
-        return out
+        self._host_done(stream, T, *(out if not resident else ()))
+        return None if resident else out
 
     def op_apply(self, mode, u, k, b=None, w=None, out=None, stream=None):
         ncomp = 1 if u.dim() == 3 else u.shape[0]
         out = self._alloc(ncomp, u) if out is None else out
         _check("sts_op_apply", lib().sts_op_apply(
-            self._h, MODE[mode], ncomp, _ptr(u), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            self._h, MODE[mode], ncomp, _ptr(u), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
             _stream(stream)))
+        self._host_done(stream, u, out, b, w, *(k or ()))
         return out
 
     def dt_euler(self, mode, k, b=None, w=None, stream=None):
         dt = ctypes.c_double()
         _check("sts_dt_euler", lib().sts_dt_euler(
-            self._h, MODE[mode], *[_ptr(x) for x in k], _ptr(b), _ptr(w), ctypes.byref(dt), _stream(stream)))
+            self._h, MODE[mode], *_kptrs(k), _ptr(b), _ptr(w), ctypes.byref(dt), _stream(stream)))
         return dt.value
 
     def rkl2_advance(self, mode, u0, k, b=None, w=None, dt=0.0, s=2, out=None, stream=None):
         ncomp = 1 if u0.dim() == 3 else u0.shape[0]
         out = self._alloc(ncomp, u0) if out is None else out
         _check("rkl2_advance", lib().rkl2_advance(
-            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
             float(dt), int(s), _stream(stream)))
+        self._host_done(stream, u0, out, b, w, *(k or ()))
         return out
 
     def rkl2_advance_hybrid(self, mode, u0, k, b=None, w=None, dt=0.0, dt_exp=1.0, euler_frac=0.25,
@@ -268,8 +344,9 @@ class Grid:
         out = self._alloc(ncomp, u0) if out is None else out
         st = (ctypes.c_int * 2)()
         _check("rkl2_advance_hybrid", lib().rkl2_advance_hybrid(
-            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            self._h, MODE[mode], ncomp, _ptr(u0), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
             float(dt), float(dt_exp), float(euler_frac), int(n_euler), int(n_sub), st, _stream(stream)))
+        self._host_done(stream, u0, out, b, w, *(k or ()))
         return out, (st[0], st[1])
 
     def be_pcg_solve(self, mode, un, k, b=None, w=None, dt=0.0, rtol=1e-12, kmax=100000, out=None,
@@ -278,10 +355,24 @@ class Grid:
         out = self._alloc(ncomp, un) if out is None else out
         iters = (ctypes.c_int * ncomp)()
         _check("be_pcg_solve", lib().be_pcg_solve(
-            self._h, MODE[mode], ncomp, _ptr(un), _ptr(out), *[_ptr(x) for x in k], _ptr(b), _ptr(w),
+            self._h, MODE[mode], ncomp, _ptr(un), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
             float(dt), float(rtol), int(kmax), iters, _stream(stream)),
             allow=(STS_ERR_NOT_CONVERGED,) if allow_not_converged else ())
+        self._host_done(stream, un, out, b, w, *(k or ()))
         return out, list(iters)
+
+    def be_pcg_solve_async(self, mode, un, k, b=None, w=None, dt=0.0, rtol=1e-12, kmax=100000, out=None,
+                           stream=None):
+        """Enqueue a solve without waiting (include/sts_b200.h be_pcg_solve_async).  Returns
+        (out, result): result.iters / result.status are valid once the stream has passed the
+        solve (e.g. after join + synchronize)."""
+        ncomp = 1 if un.dim() == 3 else un.shape[0]
+        out = self._alloc(ncomp, un) if out is None else out
+        res = PcgResult(ncomp)
+        _check("be_pcg_solve_async", lib().be_pcg_solve_async(
+            self._h, MODE[mode], ncomp, _ptr(un), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
+            float(dt), float(rtol), int(kmax), res._iters, ctypes.byref(res._status), _stream(stream)))
+        return out, res
 
 
 def inf():

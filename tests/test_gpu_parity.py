@@ -675,3 +675,85 @@ def test_pcg_breakdown_and_slab_state_errors(dev):
     assert e.value.code == -5
     with pytest.raises(S.StsError, match="sts_comm_init"):
         Gs.face_kappa_spitzer(T, 1e-9, 5e5)
+
+
+@pytest.mark.parametrize("mode", ["aniso", "iso"])
+def test_resident_coefficients_match_explicit(dev, mode):
+    """Coefficients bound once (device arrays referenced, host arrays uploaded, face kappa
+    written in place) give bit-identical results to passing the arrays every call, for
+    every entry point; the derived data (vertex coefficients, folded face coefficients,
+    Gershgorin bound) is rebuilt after a rebind."""
+    S = sts()
+    if mode == "aniso":
+        cfg = W.make_config("c1_spitzer64", shape=(13, 17, 40))
+        T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+        u, ratio, w = T, 100.0, None
+    else:
+        cfg = W.make_config("c2_visc64", shape=(13, 17, 40))
+        u, b, w, ratio = cfg["v"].to(dev), None, cfg["rho"].to(dev), 500.0
+    g = cfg["grid"]
+    G = S.Grid.from_grid(g)
+    Gr = S.Grid.from_grid(g)
+    if mode == "aniso":
+        k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+        Gr.bind_coeffs("aniso", None, b=b.cpu().pin_memory())          # b from pinned host memory
+        assert Gr.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"], resident=True) is None
+    else:
+        k = [f.to(dev) for f in cfg["visc_faces"]]
+        Gr.bind_coeffs("iso", k, w=w.cpu())                             # w from pageable host memory
+    dte = G.dt_euler(mode, k, b, w)
+    assert Gr.dt_euler(mode, None) == dte and Gr.dt_euler(mode, None) == dte     # (cached)
+    dt = ratio * dte
+    s = S.rkl2_num_stages(dt, dte)
+    assert torch.equal(G.op_apply(mode, u, k, b, w), Gr.op_apply(mode, u, None))
+    assert torch.equal(G.rkl2_advance(mode, u, k, b, w, dt, s), Gr.rkl2_advance(mode, u, None, dt=dt, s=s))
+    x1, i1 = G.be_pcg_solve(mode, u, k, b, w, dt, 1e-12, 10000)
+    x2, i2 = Gr.be_pcg_solve(mode, u, None, dt=dt, rtol=1e-12, kmax=10000)
+    assert i1 == i2 and torch.equal(x1, x2)
+    # rebind different coefficients: the derived data follows
+    k2 = [x * 1.5 for x in k]
+    Gr.bind_coeffs(mode, k2)
+    assert Gr.dt_euler(mode, None) == G.dt_euler(mode, k2, b, w)
+    assert torch.equal(G.op_apply(mode, u, k2, b, w), Gr.op_apply(mode, u, None))
+    x3, i3 = Gr.be_pcg_solve(mode, u, None, dt=dt, rtol=1e-12, kmax=10000)
+    x4, i4 = G.be_pcg_solve(mode, u, k2, b, w, dt, 1e-12, 10000)
+    assert i3 == i4 and torch.equal(x3, x4)
+    with pytest.raises(S.StsError, match="must be NULL"):
+        Gr.op_apply(mode, u, None, b=b if b is not None else w)
+    Gr.unbind_coeffs(mode)
+    with pytest.raises(S.StsError, match="none are bound"):
+        Gr.op_apply(mode, u, None)
+
+
+def test_async_host_path_and_async_solve(dev):
+    """The asynchronous host-array path (pinned arrays, outputs read after join +
+    synchronize) and be_pcg_solve_async (iterations and status written when the stream
+    reaches the end of the solve) return what the synchronous device path returns."""
+    S = sts()
+    cfg = W.make_config("c1_spitzer64", shape=(13, 17, 40))
+    g = cfg["grid"]
+    T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+    G = S.Grid.from_grid(g)
+    k = G.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G.dt_euler("aniso", k, b)
+    s = S.rkl2_num_stages(100 * dte, dte)
+    ref_rk = G.rkl2_advance("aniso", T, k, b, None, 100 * dte, s)
+    ref_be, ref_it = G.be_pcg_solve("aniso", T, k, b, None, 100 * dte, 1e-12, 10000)
+    Ga = S.Grid.from_grid(g)
+    Ga.async_host = True
+    Ga.bind_coeffs("aniso", [x.cpu().pin_memory() for x in k], b.cpu().pin_memory())
+    Th = cfg["T"].clone().pin_memory()
+    outs = []
+    for rep in range(3):                                   # staging buffers are reused across calls
+        rk = Ga.rkl2_advance("aniso", Th, None, dt=100 * dte, s=s)
+        be, res = Ga.be_pcg_solve_async("aniso", Th, None, dt=100 * dte, rtol=1e-12, kmax=10000)
+        outs.append((rk, be, res))
+    Ga.join()
+    torch.cuda.synchronize()
+    for rk, be, res in outs:
+        assert torch.equal(rk, ref_rk.cpu()) and torch.equal(be, ref_be.cpu())
+        assert res.iters == ref_it and res.status == 0
+    # a device solve through the async entry point, stopped at kmax: status, not an exception
+    x, res = G.be_pcg_solve_async("aniso", T, k, b, None, 100 * dte, 1e-12, 3)
+    torch.cuda.synchronize()
+    assert res.iters == [3] and res.status == S.STS_ERR_NOT_CONVERGED
