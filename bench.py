@@ -71,7 +71,7 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         "aniso_pcg_ap": 8 + 24 + 8,
         # fused S-pass: z, pold, x, e in; p, y, x out (first iteration: z, e in; p, y out)
         "aniso_pcg_s": (8 + 24 + 16) if first else (24 + 24 + 24),
-        "aniso_gersh": 48,
+        "aniso_gersh": 24,                   # row sums from the frozen vertex coefficients e
         "iso_rkl2_first": 8 * c + 32 + 16 * c,
         "iso_rkl2_stage": 32 * c + 32 + 8 * c,
         "iso_pcg_r0": 8 * c + 32 + 16 * c + 8,     # fused path: r, x, d (no z)
@@ -123,7 +123,7 @@ def _rkl2_stage_bytes(add, kind, s, dev, c=1):
 
 def _cond_bytes(add, s_c, it_c, fused, merged=False, dev=False):
     add("face_kappa", bytes_per_cell("face_kappa"))
-    add("vertex_coef", 2 * bytes_per_cell("vertex_coef"))   # once per RKL2 advance and per PCG solve
+    add("vertex_coef", bytes_per_cell("vertex_coef"))   # once per step (resident binding: RKL2 and PCG share it)
     add("aniso_gersh", bytes_per_cell("aniso_gersh"))
     add("aniso_rkl2_first", bytes_per_cell("aniso_rkl2_first"))
     _rkl2_stage_bytes(add, "aniso_rkl2", s_c, dev)
@@ -147,7 +147,7 @@ def _visc_bytes(add, s_v, it_v, fused=False, merged=False, dev=False):
     add("iso_rkl2_first", bytes_per_cell("iso_rkl2_first", 3))
     _rkl2_stage_bytes(add, "iso_rkl2", s_v, dev, 3)
     add("iso_pcg_r0", bytes_per_cell("iso_pcg_r0_m" if merged else "iso_pcg_r0", 3))
-    if merged:   # metric-folded K1, K2, K3, wV once per solve (timed with the vertex coefficients)
+    if merged:   # metric-folded K1, K2, K3, wV once per binding (timed with the vertex coefficients)
         add("vertex_coef", 64)
     for k in range(1, max(it_v) + 1):
         act = sum(1 for i in it_v if i >= k)          # components still iterating at iteration k
@@ -228,47 +228,48 @@ class ClockSampler:
 # the GPU step
 # ----------------------------------------------------------------------------
 class Step:
-    """One bench step on device-resident inputs: conduction then viscosity."""
+    """One bench step on device-resident inputs: conduction then viscosity, through the
+    resident-coefficient API (include/sts_b200.h "Resident coefficients"): the face
+    diffusivities are written into the handle's binding, so the frozen vertex
+    coefficients and the Gershgorin bound are built once per step and shared by the RKL2
+    super-step and the PCG solve."""
 
     def __init__(self, G, inp, ratio, dev):
         self.G, self.inp, self.ratio = G, inp, ratio
         shape = G.shape
         alloc = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)  # noqa: E731
-        self.k = tuple(alloc(*shape) for _ in range(3))
         self.T_rk, self.T_be = alloc(*shape), alloc(*shape)
         self.v_rk, self.v_be = alloc(3, *shape), alloc(3, *shape)
 
-    def cond(self, after_rkl2=None):
+    def cond(self):
         from paper_1610_01265_b200 import sts
         G, I = self.G, self.inp
         if "T" not in I:
             return 0, 0
         # conduction (anisotropic Spitzer, lagged kappa)
-        T, b = I["T"], I["b"]
-        G.face_kappa_spitzer(T, I["kappa0"], I["T_cut"], out=self.k)
-        dte = G.dt_euler("aniso", self.k, b)
+        T = I["T"]
+        G.bind_coeffs("aniso", None, b=I["b"])
+        G.face_kappa_spitzer(T, I["kappa0"], I["T_cut"], resident=True)
+        dte = G.dt_euler("aniso", None)
         dt = self.ratio * dte
         s_c = sts.rkl2_num_stages(dt, dte)
-        G.rkl2_advance("aniso", T, self.k, b, None, dt, s_c, out=self.T_rk)
-        if after_rkl2:
-            after_rkl2()
-        _, (it_c,) = G.be_pcg_solve("aniso", T, self.k, b, None, dt, RTOL, KMAX, out=self.T_be)
+        G.rkl2_advance("aniso", T, None, dt=dt, s=s_c, out=self.T_rk)
+        _, (it_c,) = G.be_pcg_solve("aniso", T, None, dt=dt, rtol=RTOL, kmax=KMAX, out=self.T_be)
         return s_c, it_c
 
-    def visc(self, after_rkl2=None):
+    def visc(self):
         from paper_1610_01265_b200 import sts
         G, I = self.G, self.inp
         if "v" not in I:
             return 0, [0]
         # viscosity (isotropic, weighted by rho, 3 components)
-        kv, rho, v = I["visc_faces"], I["rho"], I["v"]
-        dtev = G.dt_euler("iso", kv, None, rho)
+        v = I["v"]
+        G.bind_coeffs("iso", I["visc_faces"], w=I["rho"])
+        dtev = G.dt_euler("iso", None)
         dtv = self.ratio * dtev
         s_v = sts.rkl2_num_stages(dtv, dtev)
-        G.rkl2_advance("iso", v, kv, None, rho, dtv, s_v, out=self.v_rk)
-        if after_rkl2:
-            after_rkl2()
-        _, it_v = G.be_pcg_solve("iso", v, kv, None, rho, dtv, RTOL, KMAX, out=self.v_be)
+        G.rkl2_advance("iso", v, None, dt=dtv, s=s_v, out=self.v_rk)
+        _, it_v = G.be_pcg_solve("iso", v, None, dt=dtv, rtol=RTOL, kmax=KMAX, out=self.v_be)
         return s_v, it_v
 
     def __call__(self):
@@ -279,107 +280,49 @@ class Step:
 
 
 class E2EStep:
-    """The same step end to end from pinned HOST memory, as a user with host arrays
-    runs it through the public API: every step uploads that step's inputs once and
-    reads every result back into pinned host buffers; the library runs on the device
-    copies.  Copies overlap computation: H2D and D2H run on their own streams (PCIe
-    is full duplex), the viscosity inputs travel while conduction computes, each
-    result travels back as soon as it exists, and -- across consecutive steps -- the
-    NEXT step's conduction inputs travel (into the second of two input buffer sets)
-    while this step's viscosity computes.  Only the first step of a run uploads its
-    conduction inputs exposed and only the last one's final result download is
-    exposed; `start()` begins a run (no input of the run is ever uploaded before the
-    run's timed region), `__call__(prefetch)` runs one step."""
+    """The same step end to end through the library's HOST-ARRAY path: every input is a
+    pinned host tensor passed straight to the C ABI (include/sts_b200.h "Array
+    arguments"), every result lands in a pinned host tensor.  The library stages the
+    arrays on its own copy streams (uploads and downloads overlap the computation of the
+    calls around them), the coefficients are bound per step (uploaded into the handle's
+    resident copies while the previous step still computes), and the PCG solves are
+    enqueued with be_pcg_solve_async, so the host waits only where it needs a value
+    (the two dt_exp).  The caller's stream joins the handle's copies at the end."""
 
-    IN_KEYS = ("T", "b", "rho", "v")
-    COND_KEYS = ("T", "b")
-    VISC_KEYS = ("rho", "v")
-
-    def __init__(self, G, host_inp, ratio, dev):
-        self.host = host_inp
-        self.sets = []
-        for _ in range(2):
-            dinp = dict(host_inp)
-            for key in self.IN_KEYS:
-                if key in host_inp:
-                    dinp[key] = torch.empty_like(host_inp[key], device=dev)
-            if "visc_faces" in host_inp:
-                dinp["visc_faces"] = tuple(torch.empty_like(x, device=dev) for x in host_inp["visc_faces"])
-            self.sets.append(dinp)
-        self.step = Step(G, self.sets[0], ratio, dev)
-        self.h2d_s = torch.cuda.Stream(dev)
-        self.d2h_s = torch.cuda.Stream(dev)
-        pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
-        st = self.step
-        self.out_host = {"T_rk": pin(st.T_rk), "T_be": pin(st.T_be), "v_rk": pin(st.v_rk), "v_be": pin(st.v_be)}
+    def __init__(self, G, host_inp, ratio):
+        self.G, self.h, self.ratio = G, host_inp, ratio
+        pin = lambda *s: torch.empty(s, dtype=torch.float64, pin_memory=True)  # noqa: E731
+        shape = G.shape
+        self.out = [{"T_rk": pin(*shape), "T_be": pin(*shape), "v_rk": pin(3, *shape), "v_be": pin(3, *shape)}
+                    for _ in range(2)]
         nb = lambda t: t.numel() * t.element_size()  # noqa: E731
-        self.h2d = sum(nb(host_inp[k]) for k in self.IN_KEYS if k in host_inp) + \
-            sum(nb(x) for x in host_inp.get("visc_faces", ()))
-        self.d2h = sum(nb(t) for t in self.out_host.values())
-        self.ev_d2h = {}          # output name -> event after its last download
-        self.ev_used = [None, None]   # input set -> event after its last use (viscosity done)
-        self.ev_cond_in = [None, None]
+        h = host_inp
+        # uploads per step: T (face kappa, RKL2, PCG), b, v (RKL2, PCG), rho, the 3 face fields
+        self.h2d = 3 * nb(h["T"]) + nb(h["b"]) + 2 * nb(h["v"]) + nb(h["rho"]) + sum(nb(x) for x in h["visc_faces"])
+        self.d2h = sum(nb(t) for t in self.out[0].values())
         self.n = 0
 
-    def start(self):
-        self.n = 0
-        self.ev_cond_in = [None, None]
-
-    def _h2d(self, keys, faces, s, wait_ev):
-        H, D = self.host, self.sets[s]
-        with torch.cuda.stream(self.h2d_s):
-            if wait_ev is not None:
-                self.h2d_s.wait_event(wait_ev)
-            for key in keys:
-                if key in H:
-                    D[key].copy_(H[key], non_blocking=True)
-            if faces and "visc_faces" in H:
-                for d, h in zip(D["visc_faces"], H["visc_faces"]):
-                    d.copy_(h, non_blocking=True)
-            return self.h2d_s.record_event()
-
-    def _d2h(self, names, cs):
-        ev = cs.record_event()
-        with torch.cuda.stream(self.d2h_s):
-            self.d2h_s.wait_event(ev)
-            for n in names:
-                self.out_host[n].copy_(getattr(self.step, n), non_blocking=True)
-                self.ev_d2h[n] = self.d2h_s.record_event()
-
-    def _wait_out(self, cs, names):
-        for n in names:
-            if n in self.ev_d2h:
-                cs.wait_event(self.ev_d2h[n])
-
-    def __call__(self, prefetch=True):
-        st = self.step
-        cs = torch.cuda.current_stream()
-        s = self.n % 2
-        st.inp = self.sets[s]
-        if self.ev_cond_in[s] is None:            # first step of the run: its own upload
-            self.ev_cond_in[s] = self._h2d(self.COND_KEYS, False, s, self.ev_used[s])
-        ev_visc_in = self._h2d(self.VISC_KEYS, True, s, self.ev_used[s])
-        cs.wait_event(self.ev_cond_in[s])
-        self._wait_out(cs, ("T_rk", "T_be"))       # (the previous step's downloads of these)
-        s_c, it_c = st.cond(after_rkl2=lambda: self._d2h(("T_rk",), cs))
-        self._d2h(("T_be",), cs)
-        self.ev_cond_in[s] = None
-        if prefetch:                              # the next step's conduction inputs, other set
-            o = 1 - s
-            self.ev_cond_in[o] = self._h2d(self.COND_KEYS, False, o, self.ev_used[o])
-        cs.wait_event(ev_visc_in)
-        self._wait_out(cs, ("v_rk", "v_be"))
-        s_v, it_v = st.visc(after_rkl2=lambda: self._d2h(("v_rk",), cs))
-        self.ev_used[s] = cs.record_event()
-        self._d2h(("v_be",), cs)
+    def __call__(self):
+        from paper_1610_01265_b200 import sts
+        G, h, r = self.G, self.h, self.ratio
+        o = self.out[self.n % 2]
         self.n += 1
-        return {"s_cond": s_c, "it_cond": it_c, "s_visc": s_v, "it_visc": it_v,
-                "units": s_c + it_c + s_v + max(it_v)}
+        G.bind_coeffs("iso", h["visc_faces"], w=h["rho"])
+        G.bind_coeffs("aniso", None, b=h["b"])
+        G.face_kappa_spitzer(h["T"], h["kappa0"], h["T_cut"], resident=True)
+        dte = G.dt_euler("aniso", None)
+        dtev = G.dt_euler("iso", None)
+        s_c = sts.rkl2_num_stages(r * dte, dte)
+        s_v = sts.rkl2_num_stages(r * dtev, dtev)
+        G.rkl2_advance("aniso", h["T"], None, dt=r * dte, s=s_c, out=o["T_rk"])
+        G.rkl2_advance("iso", h["v"], None, dt=r * dtev, s=s_v, out=o["v_rk"])
+        _, rc = G.be_pcg_solve_async("aniso", h["T"], None, dt=r * dte, rtol=RTOL, kmax=KMAX, out=o["T_be"])
+        _, rv = G.be_pcg_solve_async("iso", h["v"], None, dt=r * dtev, rtol=RTOL, kmax=KMAX, out=o["v_be"])
+        return {"s_cond": s_c, "s_visc": s_v, "res_c": rc, "res_v": rv}
 
-    def finish(self, cs):
-        """Make `cs` wait for every outstanding download (the end of the timed region)."""
-        cs.wait_stream(self.d2h_s)
-        cs.wait_stream(self.h2d_s)
+    @staticmethod
+    def units(info):
+        return info["s_cond"] + info["res_c"].iters[0] + info["s_visc"] + max(info["res_v"].iters)
 
 
 def dist_info():
@@ -466,6 +409,8 @@ def time_oracle(name, ratio, steps=1, warmup=0):
     from threadpoolctl import threadpool_limits
     cfg = cpu_box_config(name)
     ncells = cfg["grid"].ncells
+    from oracle import c_oracle as C
+    C.set_threads(1)                 # (the C oracle's OpenMP loops: one host core, as reported)
     with threadpool_limits(limits=1):
         torch.set_num_threads(1)
         for _ in range(warmup):
@@ -499,6 +444,95 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------
+def measure_device(G, inp, ratio, args, ws, dev, ncells_local, ncells_total):
+    """Warm-up + the timed region on device-resident inputs, then instrumented steps for
+    the per-kernel-class breakdown and the roofline of the dominant kernel."""
+    step = Step(G, inp, ratio, dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 0)):
+        step()
+    launches0 = G.kernel_launches
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    barrier(ws, dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    infos = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws, dev)
+    clocks = sampler.stop()
+    ms = allreduce_max(e0.elapsed_time(e1), dev, ws)
+    launches = G.kernel_launches - launches0
+    units = sum(i["units"] for i in infos)
+    value = ncells_total * units / (ms * 1e-3) / 1e9
+
+    # per-kernel-class device time: separate instrumented steps (CUDA events around every
+    # launch on its stream), OUTSIDE the timed region above
+    G.set_timing(True)
+    G.timing_reset()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    pinfos = [step() for _ in range(max(1, min(args.steps, args.timing_steps)))]
+    p1.record(stream)
+    torch.cuda.synchronize()
+    timing = G.timing()
+    G.set_timing(False)
+    ms_prof = p0.elapsed_time(p1)
+
+    peak, peak_kind = peaks()
+    Bytes = {}
+    has = lambda k: timing.get(k, (0, 0.0))[0] > 0  # noqa: E731
+    for i in pinfos:
+        for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
+                                      has("aniso_pcg_s"), has("iso_pcg_s"), has("aniso_pcg_m"), has("iso_pcg_m"),
+                                      has("aniso_rkl2_dstage"), has("iso_rkl2_dstage")).items():
+            Bytes[k] = Bytes.get(k, 0.0) + v
+    kernels = {}
+    for k, (n, kms) in timing.items():
+        if n == 0:
+            continue
+        ent = {"launches": n, "ms": round(kms, 3), "share": round(kms / ms_prof, 4)}
+        if k in Bytes and kms > 0:
+            ent["achieved_gbs"] = round(Bytes[k] / (kms * 1e-3) / 1e9, 1)
+            ent["frac"] = round(ent["achieved_gbs"] / peak, 4)
+        kernels[k] = ent
+    dom = max((k for k in kernels if "achieved_gbs" in kernels[k]), key=lambda k: kernels[k]["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if dom in tr.get("dram_bytes_per_cell", {}) and tr.get("cells") == ncells_local:
+            traffic = tr["dram_bytes_per_cell"][dom] * ncells_local
+    except Exception:
+        pass
+    i0f = pinfos[0]
+    n_eff = {"aniso_rkl2_stage": i0f["s_cond"] - 1, "aniso_pcg_ap": i0f["it_cond"],
+             "aniso_pcg_s": i0f["it_cond"], "iso_rkl2_stage": i0f["s_visc"] - 1,
+             "iso_pcg_ap": max(i0f["it_visc"]), "iso_pcg_s": max(i0f["it_visc"]),
+             "aniso_pcg_m": i0f["it_cond"], "iso_pcg_m": max(i0f["it_visc"]),
+             "aniso_rkl2_dstage": i0f["s_cond"] - 2, "iso_rkl2_dstage": i0f["s_visc"] - 2}.get(dom)
+    bpl = (Bytes[dom] / len(pinfos) / n_eff) if n_eff else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
+                "algorithmic_bytes_per_launch": bpl}
+    return {"value": value, "ms": ms, "infos": infos, "launches": launches, "clocks": clocks, "kernels": kernels,
+            "roofline": roofline, "step": step}
+
+
+def config_block(args, gg, ratio, ws, info, ncells_total, nvirt):
+    return {"workload": args.config, "shape": list(gg.shape), "cells": ncells_total,
+            "dt_over_dt_exp": ratio, "pcg_rtol": RTOL,
+            "parallelism": f"r-slab x{ws}" + (f" (x{nvirt} virtual slabs per GPU)" if nvirt > 1 else ""),
+            "l2": f"inputs larger than L2 ({ncells_total * 8 / 1e9:.2f} GB per field)" if
+            ncells_total * 8 > 126e6 else "inputs fit L2 (no flush)",
+            "stages_cond": info["s_cond"], "pcg_iters_cond": info["it_cond"],
+            "stages_visc": info["s_visc"], "pcg_iters_visc": info["it_visc"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -507,12 +541,17 @@ def main():
     ap.add_argument("--config", default="c4_scale512", choices=list(RATIO))
     ap.add_argument("--impl", default="sts", choices=["sts", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=-1,
-                    help="end-to-end steps from pinned host memory, pipelined across steps "
-                         "(default: as many as --steps; 0 skips the leg)")
+                    help="end-to-end steps through the host-array path (default: as many as --steps; 0 skips)")
     ap.add_argument("--timing-steps", type=int, default=2,
                     help="instrumented steps (after the timed region) for the per-kernel breakdown")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shape", default=None, help="override n1,n2,n3 (debug)")
+    ap.add_argument("--ratios", default=None,
+                    help="comma-separated dt/dt_exp values: one device-timed JSON line each (e.g. the "
+                         "configs[3] sweep 10,100,1000); skips the e2e and CPU legs")
+    ap.add_argument("--virtual", type=int, default=1,
+                    help="emulate an N-way r-slab decomposition on each GPU (halo exchange through halo "
+                         "buffers, the multi-GPU schedule) to measure its overhead")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -535,99 +574,41 @@ def main():
     i0, nl = W.split_planes(n1, ws)[rank]
     cfg = W.make_config(args.config, device=dev, shape=shape, slab=(i0, nl) if ws > 1 else None)
     gg = cfg["global_grid"]
-    G = sts.Grid.from_grid(gg, i0=i0, nl=nl, device=lrank)
+    G = sts.Grid.from_grid(gg, i0=i0, nl=nl, n_virtual=args.virtual, device=lrank)
     if ws > 1:
         import torch.distributed as dist
         obj = [sts.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         G.comm_init(ws, rank, obj[0])
+        print(f"[bench] rank {rank}/{ws}: NCCL communicator initialised (r-slab planes [{i0}, {i0 + nl}) of {n1}, "
+              f"device {lrank})", file=sys.stderr, flush=True)
     ncells_local = nl * gg.shape[1] * gg.shape[2]
     ncells_total = gg.ncells
-    ratio = RATIO[args.config]
     inp = {k: cfg[k] for k in ("T", "b", "rho", "visc_faces", "v", "kappa0", "T_cut") if k in cfg}
-    step = Step(G, inp, ratio, dev)
+
+    if args.ratios:
+        for r in [float(x) for x in args.ratios.split(",")]:
+            m = measure_device(G, inp, r, args, ws, dev, ncells_local, ncells_total)
+            if rank == 0:
+                print(json.dumps({
+                    "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                    "warmup": args.warmup, "ms_per_step": m["ms"] / args.steps, "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                    "config": config_block(args, gg, r, ws, m["infos"][0], ncells_total, args.virtual),
+                    "roofline": m["roofline"], "gpu_launches": m["launches"], "clocks": m["clocks"],
+                    "kernels": m["kernels"]}), flush=True)
+            del m
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return 0
+
+    ratio = RATIO[args.config]
     stream = torch.cuda.current_stream()
+    m = measure_device(G, inp, ratio, args, ws, dev, ncells_local, ncells_total)
+    step = m.pop("step")
 
-    # ---------------- warm-up + timed region (device-resident inputs)
-    for _ in range(max(args.warmup, 0)):
-        info = step()
-    launches0 = G.kernel_launches
-    sampler = ClockSampler(lrank)
-    sampler.start()
-    barrier(ws, dev)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    infos = [step() for _ in range(args.steps)]
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier(ws, dev)
-    clocks = sampler.stop()
-    ms_local = e0.elapsed_time(e1)
-    ms = allreduce_max(ms_local, dev, ws)
-    launches = G.kernel_launches - launches0
-    units = sum(i["units"] for i in infos)
-    value = ncells_total * units / (ms * 1e-3) / 1e9
-
-    # ---------------- per-kernel-class device time: separate instrumented steps (CUDA
-    # events around every launch on its stream), OUTSIDE the timed region above
-    G.set_timing(True)
-    G.timing_reset()
-    torch.cuda.synchronize()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    pinfos = [step() for _ in range(max(1, min(args.steps, args.timing_steps)))]
-    p1.record(stream)
-    torch.cuda.synchronize()
-    timing = G.timing()
-    G.set_timing(False)
-    ms_prof = p0.elapsed_time(p1)
-
-    # ---------------- roofline of the dominant kernel (rank 0's device timing)
-    peak, peak_kind = peaks()
-    Bytes = {}
-    fused_c = timing.get("aniso_pcg_s", (0, 0.0))[0] > 0
-    fused_v = timing.get("iso_pcg_s", (0, 0.0))[0] > 0
-    merged_c = timing.get("aniso_pcg_m", (0, 0.0))[0] > 0
-    merged_v = timing.get("iso_pcg_m", (0, 0.0))[0] > 0
-    dev_c = timing.get("aniso_rkl2_dstage", (0, 0.0))[0] > 0
-    dev_v = timing.get("iso_rkl2_dstage", (0, 0.0))[0] > 0
-    for i in pinfos:
-        for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
-                                      fused_c, fused_v, merged_c, merged_v, dev_c, dev_v).items():
-            Bytes[k] = Bytes.get(k, 0.0) + v
-    kernels = {}
-    for k, (n, kms) in timing.items():
-        if n == 0:
-            continue
-        ent = {"launches": n, "ms": round(kms, 3), "share": round(kms / ms_prof, 4)}
-        if k in Bytes and kms > 0:
-            ent["achieved_gbs"] = round(Bytes[k] / (kms * 1e-3) / 1e9, 1)
-            ent["frac"] = round(ent["achieved_gbs"] / peak, 4)
-        kernels[k] = ent
-    dom = max((k for k in kernels if "achieved_gbs" in kernels[k]), key=lambda k: kernels[k]["ms"])
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        if dom in tr.get("dram_bytes_per_cell", {}):
-            traffic = tr["dram_bytes_per_cell"][dom] * ncells_local
-    except Exception:
-        pass
-    eff = [k for k in kernels if "achieved_gbs" in kernels[k]]
-    launches_dom = pinfos[0]
-    n_eff = {"aniso_rkl2_stage": launches_dom["s_cond"] - 1, "aniso_pcg_ap": launches_dom["it_cond"],
-             "aniso_pcg_s": launches_dom["it_cond"], "iso_rkl2_stage": launches_dom["s_visc"] - 1,
-             "iso_pcg_ap": max(launches_dom["it_visc"]), "iso_pcg_s": max(launches_dom["it_visc"]),
-             "aniso_pcg_m": launches_dom["it_cond"], "iso_pcg_m": max(launches_dom["it_visc"]),
-             "aniso_rkl2_dstage": launches_dom["s_cond"] - 2, "iso_rkl2_dstage": launches_dom["s_visc"] - 2}.get(dom)
-    bpl = (Bytes[dom] / len(pinfos) / n_eff) if n_eff else None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
-                "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
-                "algorithmic_bytes_per_launch": bpl}
-
-    # ---------------- end-to-end through the C ABI with host buffers
+    # ---------------- end-to-end through the C ABI's host-array path
     e2e = None
     if args.e2e_steps < 0:
         args.e2e_steps = args.steps
@@ -638,31 +619,35 @@ def main():
         for key in ("T", "b", "rho", "v"):
             host_inp[key] = inp[key].cpu().pin_memory()
         host_inp["visc_faces"] = tuple(x.cpu().pin_memory() for x in inp["visc_faces"])
-        inp.clear()            # (the device inputs of the device-timed leg: the e2e leg has its own)
+        inp.clear()            # (the device inputs of the device-timed leg: the e2e leg uploads its own)
+        G.unbind_coeffs("aniso")
+        G.unbind_coeffs("iso")
         torch.cuda.empty_cache()
-        hstep = E2EStep(G, host_inp, ratio, dev)
-        hstep.start()
-        hstep(prefetch=False)  # warm-up
-        hstep.finish(stream)
+        G.async_host = True
+        hstep = E2EStep(G, host_inp, ratio)
+        for _ in range(3):     # warm-up (staging pool, resident copies: two steps in flight)
+            hstep()
+        G.join(stream)
         barrier(ws, dev)
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        hstep.start()
-        hinfos = [hstep(prefetch=i + 1 < args.e2e_steps) for i in range(args.e2e_steps)]
-        hstep.finish(stream)
+        hinfos = [hstep() for _ in range(args.e2e_steps)]
+        G.join(stream)
         t1.record(stream)
         torch.cuda.synchronize()
         barrier(ws, dev)
         hms = allreduce_max(t0.elapsed_time(t1), dev, ws)
-        hunits = sum(i["units"] for i in hinfos)
+        assert all(i["res_c"].status == 0 and i["res_v"].status == 0 for i in hinfos)
+        hunits = sum(E2EStep.units(i) for i in hinfos)
         e2e = {"value": ncells_total * hunits / (hms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": hstep.h2d * ws, "d2h_bytes_per_step": hstep.d2h * ws,
                "steps": args.e2e_steps, "ms_per_step": hms / args.e2e_steps,
-               "mode": "host arrays uploaded and results downloaded every step on two copy streams, "
-                       "pipelined with the computation (next step's conduction inputs during this step's "
-                       "viscosity; first upload and last download exposed)"}
+               "mode": "C-ABI host-array path: pinned host tensors passed straight to the library calls "
+                       "(face kappa, coefficient binding, dt_exp, RKL2, be_pcg_solve_async); the library stages "
+                       "them on its own H2D / D2H copy streams overlapped with the computation; timed region "
+                       "ends when the caller's stream has joined the last result download"}
         del host_inp, hstep
 
     cpu_base = None
@@ -670,19 +655,13 @@ def main():
         cpu_base, _ = time_oracle(args.config, ratio, steps=1, warmup=0)
 
     if rank == 0:
-        i0f = infos[0]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": m["ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "shape": list(gg.shape), "cells": ncells_total,
-                       "dt_over_dt_exp": ratio, "pcg_rtol": RTOL, "parallelism": f"r-slab x{ws}",
-                       "l2": f"inputs larger than L2 ({ncells_total * 8 / 1e9:.2f} GB per field)" if
-                       ncells_total * 8 > 126e6 else "inputs fit L2 (no flush)",
-                       "stages_cond": i0f["s_cond"], "pcg_iters_cond": i0f["it_cond"],
-                       "stages_visc": i0f["s_visc"], "pcg_iters_visc": i0f["it_visc"]},
-            "roofline": roofline, "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "kernels": kernels,
+            "config": config_block(args, gg, ratio, ws, m["infos"][0], ncells_total, args.virtual),
+            "roofline": m["roofline"], "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": m["launches"],
+            "clocks": m["clocks"], "kernels": m["kernels"],
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -122,7 +122,8 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3,
 /* Release every device buffer, stream, event and communicator of the handle. */
 int sts_grid_destroy(sts_grid* g);
 
-/* Bytes of device workspace currently held by the handle (scratch + halos). */
+/* Bytes of device memory currently held by the handle (scratch, halos, host-array
+   staging buffers, resident coefficient copies and their derived data). */
 int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes);
 
 /* Number of kernels this handle has launched since creation (instrumentation). */

@@ -898,6 +898,25 @@ static double* call_premul(sts_grid* g, const Coefs& cf, double* scratch, size_t
 // observed convergence rate.  Results (iterations, status) are published to the handle's
 // mapped mailbox at the end of the solve; `done` is called with them on the host.
 // ----------------------------------------------------------------------------
+// destroy the loop graphs of earlier solves that have completed (all: wait for them).
+// Destroying an executable graph synchronizes the device, so this runs only when many
+// have accumulated (and in sts_grid_destroy).
+static void reap_execs(sts_grid* g, bool all) {
+  auto& v = g->retired_execs;
+  for (size_t i = 0; i < v.size();) {
+    const cudaError_t q = all ? cudaEventSynchronize(v[i].second) : cudaEventQuery(v[i].second);
+    if (q == cudaErrorNotReady) {
+      ++i;
+      continue;
+    }
+    cudaGraphExecDestroy(v[i].first);
+    cudaEventDestroy(v[i].second);
+    v[i] = v.back();
+    v.pop_back();
+  }
+  cudaGetLastError();
+}
+
 struct PcgResult {
   int iters[MAXC];
   int status;
@@ -1206,6 +1225,9 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
 
   auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
   const bool device_loop = g->graphs && !g->timing && g->comm == nullptr;
+  // (cudaGraphExecDestroy synchronizes the device: completed loop graphs are released in
+  // bulk, rarely, instead of once per solve)
+  if (g->retired_execs.size() >= 64) reap_execs(g, false);
   long long body_launches = 0, body_local = 0, body_global = 0;
   if (device_loop) {
     // iterations 1..3 directly (iteration 1 is its own pass variant; every kernel variant
@@ -1255,12 +1277,14 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
       g->comm_local = cl0;
       g->comm_global = cg0;
       STS_CUDA(cudaGraphInstantiate(&exec, cg, 0));
-      STS_CUDA(cudaGraphLaunch(exec, is));
-      // (an executable graph destroyed while in flight is released when it completes)
-      STS_CUDA(cudaGraphExecDestroy(exec));
-      exec = nullptr;
       STS_CUDA(cudaGraphDestroy(cg));
       cg = nullptr;
+      STS_CUDA(cudaGraphLaunch(exec, is));
+      cudaEvent_t done = nullptr;
+      STS_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      STS_CUDA(cudaEventRecord(done, is));
+      g->retired_execs.push_back({exec, done});
+      exec = nullptr;
     } catch (...) {
       if (capturing) {   // leave the library's stream usable: close the capture, drop the graph
         cudaGraph_t broken = nullptr;
@@ -1439,6 +1463,7 @@ int sts_grid_destroy(sts_grid* g) {
       cudaEventDestroy(r.b);
     }
     for (auto e : g->free_events) cudaEventDestroy(e);
+    reap_execs(g, true);
     if (g->h2d_stream || g->d2h_stream || !g->stage_pool.empty()) cudaDeviceSynchronize();
     for (auto& b : g->stage_pool) {
       cudaFree(b.p);
@@ -1464,7 +1489,15 @@ int sts_grid_destroy(sts_grid* g) {
 int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes) {
   return guard([&] {
     STS_REQUIRE(g && bytes, "NULL argument");
-    *bytes = g->ws.bytes + g->red_bytes + g->halo_bytes;
+    size_t slots = 0;
+    for (auto& s : g->slot) {
+      slots += s.derived_bytes;
+      for (int i = 0; i < 5; ++i)
+        for (int c = 0; c < 2; ++c) slots += s.own_n[i][c] * sizeof(double);
+      for (int d = 0; d < 3; ++d)
+        if (s.kfk[d]) slots += (size_t)g->nl * g->plane * sizeof(double);
+    }
+    *bytes = g->ws.bytes + g->red_bytes + g->halo_bytes + g->stage_bytes + slots;
   });
 }
 
@@ -1743,11 +1776,16 @@ int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, cons
     if (lam < 0.0) {   // (resident coefficients: computed once per binding)
       io.begin();
       exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, cf.b, st);
+      // ANISO: the row sums come from the frozen vertex coefficients (the binding's are
+      // then ready for the advance that follows)
+      double* scratch = ws_get(g, (call_ev_doubles(g, mode, cf) + 1) * sizeof(double));
+      const auto ev = call_vertex_coefs(g, mode, cf, scratch, st);
       ensure_red(g, 4096);
       auto* dmax = reinterpret_cast<unsigned long long*>(g->d_red);
       STS_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-      for (auto& s : g->slabs) {
-        StencilCall c = make_call(g, s, mode, 1, 0, nullptr, cf.k1, cf.k2, cf.k3, cf.b, cf.w);
+      for (size_t si = 0; si < g->slabs.size(); ++si) {
+        StencilCall c = make_call(g, g->slabs[si], mode, 1, 0, nullptr, cf.k1, cf.k2, cf.k3, cf.b, cf.w);
+        c.ev = ev[si];
         Timed t(g, mode == STS_MODE_ANISO ? STS_K_ANISO_GERSH : STS_K_ISO_GERSH, st);
         launch_gershgorin(c, dmax, st);
       }

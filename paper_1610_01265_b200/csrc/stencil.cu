@@ -1067,7 +1067,108 @@ void launch_stencil(const StencilCall& c, cudaStream_t st) {
   }
 }
 
+// ============================================================================
+// Gershgorin row sums from the frozen vertex coefficients (App. B)
+// ----------------------------------------------------------------------------
+// With e = sqrt(V_v kappa_v) b_v / (4 h) (vertex_coef_tiled_kernel), the weight of the
+// cell at corner sigma of vertex v in (b_v . g_v) is
+//   g_v(sigma) = s1 e_r + s2 e_t / r_i + s3 e_p / (r_i sin th_j),  s_a = 2 sigma_a - 1,
+// (i, j) = the cell's r / theta indices, and E_v = 1/2 (sum_sigma g_v(sigma) u_sigma)^2,
+// so L_cq = -sum over the vertices v shared by c and q of g_v(sigma_c) g_v(sigma_q).
+// A CTA owns 8 x 32 cells and marches along r; per vertex plane its threads compute the
+// 8 weights of every vertex of the tile (+ the low-side ring) once into shared memory
+// (two planes), then each cell sums its 8 vertices' 8 products into its 27 entries and
+// takes sum |L_cq| / (w V).  24 B (e) per cell streamed instead of the 48 B of b and
+// kappa plus the per-entry metric gathers of the generic kernel.  n3 >= 3 (no aliased
+// phi neighbours).
+constexpr int GJ = 8, GK = 32, GVJ = GJ + 1, GVK = GK + 1, GVC = GVJ * GVK;
+constexpr int GNT = GJ * GK;
+
+__global__ void __launch_bounds__(GNT, 3) gersh_ev_kernel(Geo G, const double* __restrict__ ev,
+                                                          const double* __restrict__ w, int ib0, int ie0, int ic,
+                                                          unsigned long long* dmax) {
+  __shared__ double gs[2][8][GVC];
+  const Metrics& M = G.m;
+  const int tid = threadIdx.x, tj = tid / GK, tk = tid % GK;
+  const int k0 = blockIdx.x * GK, j0 = blockIdx.y * GJ;
+  const int ib = ib0 + blockIdx.z * ic, ie = min(ib + ic, ie0);
+  const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3), es = ev_cstride(G.nl, G.n2, G.n3);
+  // weights of the vertices of vertex plane il (between cell planes il and il+1) -> slot
+  auto weights = [&](int il, int slot) {
+    const int iv = G.i0 + il;
+    for (int e = tid; e < GVC; e += GNT) {
+      const int vj = e / GVK, vk = e - vj * GVK;
+      const int jv = j0 - 1 + vj, kv = k0 - 1 + vk;      // padded entry (jv+1, kv+1)
+      double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (iv >= 0 && iv + 1 < G.n1g && jv >= 0 && jv + 1 < G.n2 && kv + 1 <= G.n3) {
+        const long long o = (long long)(il + 1) * pp + (long long)(jv + 1) * row + (kv + 1);
+        const double er = __ldg(ev + o), et = __ldg(ev + es + o), ep = __ldg(ev + 2 * es + o);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int s1 = (s >> 2) & 1, s2 = (s >> 1) & 1, s3 = s & 1;
+          const double ig2 = M.iG2[iv + s1], ig3 = M.iG3[jv + s2];
+          g[s] = (s1 ? er : -er) + (s2 ? et : -et) * ig2 + (s3 ? ep : -ep) * (ig2 * ig3);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) gs[slot][s][e] = g[s];
+    }
+  };
+  const int j = j0 + tj, k = k0 + tk;
+  const bool own = j < G.n2 && k < G.n3;
+  double rowmax = 0.0;
+  weights(ib - 1, (ib + 1) & 1);
+  for (int il = ib; il < ie; ++il) {
+    weights(il, il & 1);
+    __syncthreads();
+    if (own) {
+      double ent[27];
+#pragma unroll
+      for (int q = 0; q < 27; ++q) ent[q] = 0.0;
+#pragma unroll
+      for (int up = 0; up < 2; ++up) {          // up = 0: the vertex plane below (cell at sigma_1 = 1)
+        const int slot = up ? (il & 1) : ((il + 1) & 1);
+        const int c1 = up ? 0 : 1;
+#pragma unroll
+        for (int a = 0; a < 2; ++a)            // vertex row tj + a: the cell sits at sigma_2 = 1 - a
+#pragma unroll
+          for (int bq = 0; bq < 2; ++bq) {     // vertex col tk + bq: sigma_3 = 1 - bq
+            const int e = (tj + a) * GVK + tk + bq;
+            const int c2 = 1 - a, c3 = 1 - bq;
+            const double gc = gs[slot][(c1 << 2) | (c2 << 1) | c3][e];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int q1 = (q >> 2) & 1, q2 = (q >> 1) & 1, q3 = q & 1;
+              ent[(q1 - c1 + 1) * 9 + (q2 - c2 + 1) * 3 + (q3 - c3 + 1)] += gc * gs[slot][q][e];
+            }
+          }
+      }
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < 27; ++q) sum += fabs(ent[q]);
+      const int ig = G.i0 + il;
+      const double WV = (w ? __ldg(w + (long long)il * G.plane + (long long)j * G.n3 + k) : 1.0) * M.Vr[ig] *
+                        M.Vt[j] * M.Vp[k];
+      rowmax = fmax(rowmax, sum / WV);
+    }
+    __syncthreads();   // the next plane's weights overwrite the lower slot
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rowmax = fmax(rowmax, __shfl_xor_sync(0xffffffffu, rowmax, o));
+  if ((tid & 31) == 0 && rowmax > 0.0) atomicMax(dmax, (unsigned long long)__double_as_longlong(rowmax));
+}
+
 void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStream_t st) {
+  const Geo& G = c.geo;
+  if (c.mode == STS_MODE_ANISO && c.ev && G.n3 >= 3) {
+    const int nbx = (G.n3 + GK - 1) / GK, nby = (G.n2 + GJ - 1) / GJ;
+    const int np = c.ie - c.ib;
+    if (np <= 0) return;
+    const int ic = choose_chunk((long long)nbx * nby, np, 148LL * 3, 1.0, 4);
+    gersh_ev_kernel<<<dim3(nbx, nby, (np + ic - 1) / ic), GNT, 0, st>>>(G, c.ev, c.w, c.ib, c.ie, ic, d_max);
+    STS_CUDA(cudaGetLastError());
+    return;
+  }
   launch_epi<EPI_GERSH>(c, st, d_max);
 }
 

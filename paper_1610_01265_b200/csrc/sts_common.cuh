@@ -198,6 +198,9 @@ struct sts_grid {
   cudaEvent_t ev_h2d_last = nullptr, ev_d2h_last = nullptr;
   bool h2d_used = false, d2h_used = false;
   sts::CoefSlot slot[2];                // resident coefficients per mode (STS_MODE_ISO, STS_MODE_ANISO)
+  // executable PCG loop graphs still in flight: destroyed once their event has completed
+  // (destroying an in-flight executable graph would wait for it)
+  std::vector<std::pair<cudaGraphExec_t, cudaEvent_t>> retired_execs;
 };
 
 namespace sts {
