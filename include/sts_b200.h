@@ -222,7 +222,12 @@ int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
  * sts_comm_init creates the handle's NCCL communicator; the slab of `rank`
  * must be the rank-th slab in r order (rank 0 holds r_min).  Neighbour
  * exchanges (one theta x phi plane per side) use ncclSend/ncclRecv on an
- * internal communication stream, PCG dot products use ncclAllReduce.
+ * internal communication stream, overlapped with the interior planes of every
+ * stencil pass; PCG dot products use ncclAllReduce (one per merged iteration).
+ * With a communicator, be_pcg_solve polls convergence from the host in batches
+ * sized from the observed convergence rate, and replays iterations k >= 4 as one
+ * captured CUDA graph per iteration pair (NCCL calls inside the graph).
+ * nranks = 1 is allowed (a one-rank communicator: the NCCL reduction path on one GPU).
  */
 int sts_nccl_unique_id(void* out, size_t nbytes);
 int sts_comm_init(sts_grid* g, int nranks, int rank, const void* uid, size_t nbytes);

@@ -1301,13 +1301,27 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
     // host-polled loop: batches sized from the observed convergence rate so that no more
     // than ~1-2 no-op iterations (which still exchange halos and all-reduce under NCCL)
     // follow convergence
+    // With an NCCL communicator (and graphs enabled, timing off) iterations k >= 4 come
+    // in identical pairs replayed from ONE captured CUDA graph (NCCL send / recv and
+    // all-reduce are capturable): no host launch work and minimal gaps per iteration.
+    // If the capture fails the solve continues with direct launches.
+    const bool pair_graph = g->comm && g->graphs && !g->timing;
+    cudaStream_t is = st;
+    if (pair_graph) {
+      is = graph_stream(g);
+      STS_CUDA(cudaEventRecord(g->ev_c, st));
+      STS_CUDA(cudaStreamWaitEvent(is, g->ev_c, 0));
+    }
+    cudaGraphExec_t pair_exec = nullptr;
+    bool pair_failed = false;
+    long long pair_launches = 0, pair_local = 0, pair_global = 0;
     int launched = 0;
     int batch = 4;
     std::vector<double> rz_prev(ncomp, 0.0);
     while (true) {
-      launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, st);
+      launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, is);
       g->launches += 1;
-      STS_CUDA(cudaStreamSynchronize(st));
+      STS_CUDA(cudaStreamSynchronize(is));
       bool all_done = true;
       for (int c = 0; c < ncomp; ++c) all_done = all_done && hsc[c].done;
       if (all_done || launched >= kmax) break;
@@ -1328,9 +1342,63 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
       }
       for (int c = 0; c < ncomp; ++c) rz_prev[c] = hsc[c].rz;
       const int nb = std::min(batch, kmax - launched);
-      for (int it = 0; it < nb; ++it) iteration(launched + it + 1, st);
+      for (int it = 0; it < nb;) {
+        const int k = launched + it + 1;
+        if (pair_graph && !pair_failed && k >= 4 && (k % 2) == 0 && it + 2 <= nb) {
+          if (!pair_exec) {
+            const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
+            cudaGraph_t graph = nullptr;
+            bool capturing = false;
+            try {
+              STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
+              capturing = true;
+              iteration(k, is);
+              iteration(k + 1, is);
+              capturing = false;
+              STS_CUDA(cudaStreamEndCapture(is, &graph));
+              STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
+              STS_CUDA(cudaGraphDestroy(graph));
+            } catch (const Error&) {
+              if (capturing) {
+                cudaGraph_t broken = nullptr;
+                if (cudaStreamEndCapture(is, &broken) == cudaSuccess && broken) cudaGraphDestroy(broken);
+              } else if (graph) {
+                cudaGraphDestroy(graph);
+              }
+              cudaGetLastError();
+              pair_exec = nullptr;
+              pair_failed = true;
+            }
+            pair_launches = g->launches - l0;
+            pair_local = g->comm_local - cl0;
+            pair_global = g->comm_global - cg0;
+            g->launches = l0;
+            g->comm_local = cl0;
+            g->comm_global = cg0;
+            if (pair_failed) continue;   // (this pair again, launched directly)
+          }
+          STS_CUDA(cudaGraphLaunch(pair_exec, is));
+          g->launches += pair_launches;
+          g->comm_local += pair_local;
+          g->comm_global += pair_global;
+          it += 2;
+        } else {
+          iteration(k, is);
+          it += 1;
+        }
+      }
       launched += nb;
       batch = nb;
+    }
+    if (pair_exec) {
+      cudaEvent_t done = nullptr;
+      STS_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      STS_CUDA(cudaEventRecord(done, is));
+      g->retired_execs.push_back({pair_exec, done});
+    }
+    if (pair_graph) {
+      STS_CUDA(cudaEventRecord(g->ev_c, is));
+      STS_CUDA(cudaStreamWaitEvent(st, g->ev_c, 0));
     }
   }
   {
@@ -1596,12 +1664,9 @@ int sts_comm_init(sts_grid* g, int nranks, int rank, const void* uid, size_t nby
     std::memcpy(&id, uid, sizeof(id));
     g->nranks = nranks;
     g->rank = rank;
-    if (nranks > 1) {
-      STS_NCCL(ncclCommInitRank(&g->comm, nranks, id, rank));
-      STS_CUDA(cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking));
-      STS_CUDA(cudaEventCreateWithFlags(&g->ev_a, cudaEventDisableTiming));
-      STS_CUDA(cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming));
-    }
+    // (a 1-rank communicator is created too: the NCCL reduction path then runs on one GPU)
+    STS_NCCL(ncclCommInitRank(&g->comm, nranks, id, rank));
+    comm_stream(g);
   });
 }
 

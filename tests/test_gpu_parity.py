@@ -757,3 +757,42 @@ def test_async_host_path_and_async_solve(dev):
     x, res = G.be_pcg_solve_async("aniso", T, k, b, None, 100 * dte, 1e-12, 3)
     torch.cuda.synchronize()
     assert res.iters == [3] and res.status == S.STS_ERR_NOT_CONVERGED
+
+
+@pytest.mark.parametrize("mode", ["aniso", "iso"])
+@pytest.mark.parametrize("graphs", [True, False])
+def test_nccl_one_rank_path_matches_single_process(dev, mode, graphs):
+    """The NCCL path of the PCG solve (per-rank partial sums -> ncclAllReduce -> scalar
+    kernel; host-polled batches; iteration pairs replayed from a captured graph with the
+    NCCL calls inside) on a one-rank communicator equals the single-process path to the
+    rounding of the dot-product summation order; RKL2 (no reductions) bit for bit."""
+    S = sts()
+    name = "c1_spitzer64" if mode == "aniso" else "c2_visc64"
+    cfg = W.make_config(name, shape=(13, 17, 40))
+    g = cfg["grid"]
+    G1 = S.Grid.from_grid(g)
+    Gn = S.Grid.from_grid(g)
+    Gn.comm_init(1, 0, S.nccl_unique_id())
+    Gn.set_graphs(graphs)
+    if mode == "aniso":
+        u, b, w = cfg["T"].to(dev), cfg["b"].to(dev), None
+        k = G1.face_kappa_spitzer(u, cfg["kappa0"], cfg["T_cut"])
+        ratio = 100.0
+    else:
+        u, b, w = cfg["v"].to(dev), None, cfg["rho"].to(dev)
+        k = [f.to(dev) for f in cfg["visc_faces"]]
+        ratio = 500.0
+    dte = G1.dt_euler(mode, k, b, w)
+    assert Gn.dt_euler(mode, k, b, w) == dte
+    s = S.rkl2_num_stages(ratio * dte, dte)
+    assert torch.equal(G1.rkl2_advance(mode, u, k, b, w, ratio * dte, s),
+                       Gn.rkl2_advance(mode, u, k, b, w, ratio * dte, s))
+    x1, i1 = G1.be_pcg_solve(mode, u, k, b, w, ratio * dte, 1e-12, 10000)
+    l0 = Gn.kernel_launches
+    xn, i_n = Gn.be_pcg_solve(mode, u, k, b, w, ratio * dte, 1e-12, 10000)
+    assert all(abs(a - c) <= 1 for a, c in zip(i1, i_n)), (i1, i_n)
+    assert rel_l2(cpu(xn), cpu(x1)) <= 1e-12
+    # no more than a couple of no-op iterations after convergence (batches sized from the
+    # observed rate): launches per iteration are bounded
+    per_it = 4 if mode == "aniso" else 4
+    assert Gn.kernel_launches - l0 <= per_it * (max(i_n) + 3) + 40
