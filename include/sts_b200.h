@@ -187,7 +187,9 @@ int sts_grid_set_tma(sts_grid* g, int enable);
  * enable != 0 (the default): single-process PCG solves run iterations k >= 4 as the
  * body (one iteration pair) of a device-side WHILE loop in a CUDA graph; 0 launches
  * every kernel directly from a host-polled loop.  Graphs are never used while
- * per-launch timing is on or with an NCCL communicator.
+ * per-launch timing is on or with an NCCL communicator.  The environment variable
+ * STS_PCG_HOST_LOOP=1, read at sts_grid_create, selects 0 (profilers such as ncu
+ * cannot profile the kernel nodes of a graph with conditional nodes).
  */
 int sts_grid_set_graphs(sts_grid* g, int enable);
 

@@ -28,26 +28,32 @@ def nccl_flags():
     return ["-I/usr/include", "-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
 
 
-def build(force=False, verbose=True):
-    if not force and os.path.exists(OUT):
-        t = os.path.getmtime(OUT)
+def build(force=False, verbose=True, out=None, defines=()):
+    """Compile the library (out / defines: A-B variants of the compile-time knobs, e.g.
+    defines=("ISO_RASTER_H=0",), out=".../libsts_b200_v.so"; loaded with STS_LIB=path)."""
+    OUTP = out or OUT
+    if not force and os.path.exists(OUTP):
+        t = os.path.getmtime(OUTP)
         if all(os.path.getmtime(d) <= t for d in DEPS):
-            return OUT
+            return OUTP
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}",
-           *SRC, "-o", OUT + ".tmp", *nccl_flags()]
+           *[f"-D{d}" for d in defines], *SRC, "-o", OUTP + ".tmp", *nccl_flags()]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build_ptxas.log")
+    log = os.path.join(HERE, "build_ptxas.log") if out is None else OUTP + ".log"
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stderr)
         raise RuntimeError(f"nvcc failed ({r.returncode}); see {log}")
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(OUTP + ".tmp", OUTP)
+    return OUTP
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a[6:] for a in args if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, out=outs[0] if outs else None, defines=defs))

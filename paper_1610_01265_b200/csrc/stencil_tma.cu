@@ -85,6 +85,9 @@ struct TmaArgs {
 #ifndef ANISO_M_NS
 #define ANISO_M_NS 3
 #endif
+#ifndef ANISO_RASTER_H   // (theta-first bands measured worse for L2: DESIGN.md §5.4)
+#define ANISO_RASTER_H 0
+#endif
 constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : 3; }
 
 // epilogue operand slots
@@ -123,10 +126,11 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
-  const int j0 = blockIdx.y * XOJ, k0 = blockIdx.x * XOK;
-  const int ib = c.ib + blockIdx.z * ic;
+  const Tile3 tl = raster_tile(blockIdx.x, (c.geo.n3 + XOK - 1) / XOK, (c.geo.n2 + XOJ - 1) / XOJ, ANISO_RASTER_H);
+  const int j0 = tl.y * XOJ, k0 = tl.x * XOK;
+  const int ib = c.ib + tl.z * ic;
   const int ie = min(ib + ic, c.ie);
-  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  const long long blk = blockIdx.x;
 
   if constexpr (EPI == EPI_PCG_S || kM) {
     if (c.ea.sc && c.ea.sc[0].done) return;
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       __shared__ double fred[4 * MAXC * 32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
-                         (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, XNT, fred, &flag,
+                         (unsigned long long)gridDim.x, tid, XNT, fred, &flag,
                          [] { asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory"); });
     }
   }
@@ -495,7 +499,7 @@ template <int EPI, bool W, bool FR>
 static void launch_t(const StencilCall& c, dim3 grid, int ic, const TmaArgs& ta, cudaStream_t st) {
   static std::atomic<unsigned long long> attr{0};
   ensure_smem_attr(aniso_tma_kernel<EPI, W, FR>, (int)TmaLay<EPI, W>::SMEM, attr);
-  aniso_tma_kernel<EPI, W, FR><<<grid, XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
+  aniso_tma_kernel<EPI, W, FR><<<dim3(grid.x * grid.y * grid.z), XTHREADS, TmaLay<EPI, W>::SMEM, st>>>(c, ic, ta);
 }
 
 template <int EPI>

@@ -70,6 +70,9 @@ struct IsoTile {
 #ifndef ISO_M3_ROWS
 #define ISO_M3_ROWS 13
 #endif
+#ifndef ISO_RASTER_H     // (theta-first bands measured worse for L2: DESIGN.md §5.4)
+#define ISO_RASTER_H 0
+#endif
 __host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? ISO_M3_ROWS : 7; }
 __host__ __device__ constexpr int iso_minb(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 1 : 2; }
 
@@ -154,10 +157,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
-  const int j0 = blockIdx.y * IJ, k0 = blockIdx.x * IK;
-  const int ib = c.ib + blockIdx.z * ic;
+  const Tile3 tl = raster_tile(blockIdx.x, (c.geo.n3 + IK - 1) / IK, (c.geo.n2 + IJ - 1) / IJ, ISO_RASTER_H);
+  const int j0 = tl.y * IJ, k0 = tl.x * IK;
+  const int ib = c.ib + tl.z * ic;
   const int ie = min(ib + ic, c.ie);
-  const long long blk = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+  const long long blk = blockIdx.x;
   const bool per = G.periodic3 != 0;
   const bool wrapL = per && k0 == 0;
   const bool wrapR = per && (k0 + IK >= G.n3);
@@ -603,7 +607,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       __shared__ double fred[4 * MAXC * 32];
       __shared__ unsigned flag;
       fused_final_reduce(c.ea.fin, c.ea.partials, c.ea.pstride,
-                         (unsigned long long)gridDim.x * gridDim.y * gridDim.z, tid, INT, fred, &flag,
+                         (unsigned long long)gridDim.x, tid, INT, fred, &flag,
                          [] { asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory"); });
     }
   }
@@ -654,7 +658,8 @@ template <int EPI, int NC, bool FST, bool FR>
 static void launch_iso_g(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
   static std::atomic<unsigned long long> attr{0};
   ensure_smem_attr(iso_tma_kernel<EPI, NC, FST, FR>, (int)IsoLay<EPI, NC>::SMEM, attr);
-  iso_tma_kernel<EPI, NC, FST, FR><<<grid, IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+  iso_tma_kernel<EPI, NC, FST, FR>
+      <<<dim3(grid.x * grid.y * grid.z), IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
 }
 
 template <int EPI, int NC, bool FST>

@@ -15,7 +15,8 @@ import os
 import torch  # noqa: F401  (loads CUDA runtime + NCCL before the library)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsts_b200.so")
+# (STS_LIB: an A-B variant built in-tree by build.py --out=...; the default is the product build)
+LIB_PATH = os.environ.get("STS_LIB") or os.path.join(_HERE, "libsts_b200.so")
 
 STS_OK = 0
 STS_ERR_NOT_CONVERGED = -4

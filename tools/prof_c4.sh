@@ -2,6 +2,8 @@
 # the bench workload), one launch each; run only after the same command exited 0.
 #   bash tools/prof_c4.sh && python tools/make_traffic.py --cells 268435456 gpurun_out/c4prof_*.ncu-rep
 mkdir -p gpurun_out
+export STS_PCG_HOST_LOOP=1   # (ncu skips kernel nodes of conditional graphs)
+rm -f gpurun_out/c4prof_*.ncu-rep
 python tools/profile_step.py --config c4_scale512 --visc > gpurun_out/pp.log 2>&1 || exit 1
 for K in "sts::aniso_tma_kernel<.int.6" "sts::iso_tma_kernel<.int.6" "sts::aniso_tma_kernel<.int.7" "sts::iso_tma_kernel<.int.7"; do
   tag=$(echo "$K" | tr -c 'a-zA-Z0-9_\n' '_')
