@@ -24,33 +24,45 @@ __device__ __forceinline__ double fc_profile(double r, double r0, double w) {
   return w > 0.0 ? 0.5 * (1.0 - tanh((r - r0) / w)) : 1.0;
 }
 
-__global__ void face_kappa_kernel(Geo G, FieldV T, double* __restrict__ k1, double* __restrict__ k2,
-                                  double* __restrict__ k3, double kappa0, double T_cut, double fc_r0,
-                                  double fc_w, const double* __restrict__ x1f, const double* __restrict__ x1c) {
-  const long long n = (long long)G.nl * G.plane;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const int il = (int)(e / G.plane);
-    const long long rem = e - (long long)il * G.plane;
-    const int j = (int)(rem / G.n3);
-    const int k = (int)(rem - (long long)j * G.n3);
+// one thread per (theta, phi) column marching along r over planes [ib, ie): T of the
+// next plane is loaded once (it is this plane's r-face neighbour and the next plane's
+// own value), the phi neighbour comes from the next lane (lane 31 loads it), the theta
+// neighbour is a coalesced row load; streaming stores (the face fields are re-read by a
+// later pass, after far more than L2 has streamed through)
+constexpr int FK_T = 256;
+__global__ void __launch_bounds__(FK_T) face_kappa_kernel(Geo G, FieldV T, double* __restrict__ k1,
+                                                          double* __restrict__ k2, double* __restrict__ k3,
+                                                          double kappa0, double T_cut, double fc_r0, double fc_w,
+                                                          const double* __restrict__ x1f,
+                                                          const double* __restrict__ x1c, int ic) {
+  const int k = blockIdx.x * FK_T + threadIdx.x, j = blockIdx.y;
+  const int ib = blockIdx.z * ic, ie = min(ib + ic, G.nl);
+  const bool in = k < G.n3;
+  const bool jp = j + 1 < G.n2, kp = G.periodic3 || k + 1 < G.n3;
+  const int kn = (k + 1 < G.n3) ? k + 1 : 0;    // (wrap to k = 0)
+  const long long col = (long long)j * G.n3;
+  const int lane = threadIdx.x & 31;
+  // the phi neighbour is the next lane's own value unless it lies in another warp / wraps
+  const bool shfl_ok = lane < 31 && k + 1 < G.n3;
+  double Tc = (in && ib < ie) ? __ldg(T.p + (long long)ib * G.plane + col + k) : 0.0;
+  for (int il = ib; il < ie; ++il) {
+    const long long e = (long long)il * G.plane + col + k;
     const int ig = G.i0 + il;
-    const double Tc = T.p[e];
-    // r-face (i+1/2): needs T at il+1 (hi halo on the last local plane)
-    double v1 = 0.0;
-    if (ig + 1 < G.n1g) {
-      const double Tn = (il + 1 < G.nl) ? T.p[e + G.plane] : T.hi[rem];
-      v1 = spitzer(0.5 * (Tc + Tn), kappa0, T_cut) * fc_profile(x1f[ig + 1], fc_r0, fc_w);
+    double Tn = 0.0;
+    if (in && ig + 1 < G.n1g) Tn = (il + 1 < G.nl) ? __ldg(T.p + e + G.plane) : T.hi[col + k];
+    const double Tk_s = __shfl_down_sync(0xffffffffu, Tc, 1);
+    if (in) {
+      const double Tk = shfl_ok ? Tk_s : __ldg(T.p + (long long)il * G.plane + col + kn);
+      const double fcc = fc_profile(x1c[ig], fc_r0, fc_w);
+      const double v1 = (ig + 1 < G.n1g) ? spitzer(0.5 * (Tc + Tn), kappa0, T_cut) * fc_profile(x1f[ig + 1], fc_r0, fc_w)
+                                         : 0.0;
+      const double v2 = jp ? spitzer(0.5 * (Tc + __ldg(T.p + e + G.n3)), kappa0, T_cut) * fcc : 0.0;
+      const double v3 = kp ? spitzer(0.5 * (Tc + Tk), kappa0, T_cut) * fcc : 0.0;
+      __stcs(k1 + e, v1);
+      __stcs(k2 + e, v2);
+      __stcs(k3 + e, v3);
     }
-    double v2 = 0.0;
-    if (j + 1 < G.n2) v2 = spitzer(0.5 * (Tc + T.p[e + G.n3]), kappa0, T_cut) * fc_profile(x1c[ig], fc_r0, fc_w);
-    double v3 = 0.0;
-    if (G.periodic3 || k + 1 < G.n3) {
-      const long long en = (k + 1 < G.n3) ? e + 1 : e - k;  // wrap to k = 0
-      v3 = spitzer(0.5 * (Tc + T.p[en]), kappa0, T_cut) * fc_profile(x1c[ig], fc_r0, fc_w);
-    }
-    k1[e] = v1;
-    k2[e] = v2;
-    k3[e] = v3;
+    Tc = Tn;
   }
 }
 
@@ -89,11 +101,17 @@ void launch_iso_premul(const Geo& G, const double* k1, const double* k2, const d
 void launch_face_kappa(const Geo& G, FieldV T, double* k1, double* k2, double* k3, double kappa0,
                        double T_cut, double fc_r0, double fc_w, const double* x1f_d, const double* x1c_d,
                        cudaStream_t st) {
-  const long long n = (long long)G.nl * G.plane;
-  if (n == 0) return;
-  long long nb = (n + 255) / 256;
-  if (nb > 148 * 16) nb = 148 * 16;
-  face_kappa_kernel<<<(int)nb, 256, 0, st>>>(G, T, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, x1f_d, x1c_d);
+  if ((long long)G.nl * G.plane == 0) return;
+  STS_REQUIRE(G.n2 <= 65535, "grid too large for the face-kappa pass");
+  const int nbx = (G.n3 + FK_T - 1) / FK_T;
+  // ~8 resident blocks per SM x 148 SMs x 4 waves of columns, chunks of >= 8 planes
+  const long long cols = (long long)nbx * G.n2;
+  int nch = (int)std::max(1LL, std::min<long long>((148LL * 8 * 4 + cols - 1) / cols, (G.nl + 7) / 8));
+  nch = std::min(nch, 65535);
+  const int ic = (G.nl + nch - 1) / nch;
+  nch = (G.nl + ic - 1) / ic;
+  face_kappa_kernel<<<dim3(nbx, G.n2, nch), FK_T, 0, st>>>(G, T, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, x1f_d,
+                                                           x1c_d, ic);
   STS_CUDA(cudaGetLastError());
 }
 

@@ -85,6 +85,9 @@ struct TmaArgs {
 #ifndef ANISO_M_NS
 #define ANISO_M_NS 3
 #endif
+#ifndef ANISO_M_DREAD    // 0: the merged PCG pass recomputes d from the staged e (8 B/cell fewer)
+#define ANISO_M_DREAD 1       // measured 42 % slower (L1 / register bound, spills): reads d
+#endif
 #ifndef ANISO_RASTER_H   // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ANISO_RASTER_H 0
 #endif
@@ -93,14 +96,17 @@ constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : 3; 
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
 enum { OW_DM2 = 0, OW_DM0 = 1 };              // RKL2 stage, deviation form
-enum { OW_X = 0, OW_D = 1 };                 // PCG S-pass (x) / merged pass (x, d)
+enum { OW_X = 0 };                           // PCG S-pass / merged pass (x)
 // slot layout of one (epilogue, has-w) variant
 template <int EPI, bool W>
 struct TmaLay {
   static constexpr int nsrc = (EPI == EPI_PCG_S) ? 2 : (EPI == EPI_PCG_M ? 3 : 1);
+  // (merged PCG pass: x and d; ANISO_M_DREAD = 0 recomputes d from the staged e instead)
   static constexpr int nepi = (EPI == EPI_RKL2_STAGE)
                                   ? 3
-                                  : ((EPI == EPI_RKL2_DSTAGE || EPI == EPI_PCG_M) ? 2 : (EPI == EPI_PCG_S ? 1 : 0));
+                                  : (EPI == EPI_RKL2_DSTAGE || (EPI == EPI_PCG_M && ANISO_M_DREAD)
+                                         ? 2
+                                         : ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) ? 1 : 0));
   static constexpr int nown = nepi + (W ? 1 : 0);             // w is the last own box
   static constexpr int E = nsrc * U_FIELD;
   static constexpr int O = E + E_PART;
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
       const double q = er * (H.Su - L.Su) + et * (ig2l * L.Tu + ig2h * H.Tu) + ep * (ig2l * L.Fu + ig2h * H.Fu);
       double ldhi = 0.0;
-      if constexpr (kR0) {
+      if constexpr (kR0 || (kM && !ANISO_M_DREAD)) {
         if (own) {
           // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
           // the own cell (j, k) sits at (st, sp) = (+,+) in vertex (vj,vk), (+,-) in (vj,vk+1),
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
           const double Ld = -(L.ld + ldhi);
           const double r = c.ea.dt * Lu;
-          const double dinv = 1.0 / (WV - c.ea.dt * Ld);
+          const double dinv = rcp_pos(WV - c.ea.dt * Ld);
           const double z = r * dinv;
           const double bb = WV * uc;
           c.ea.out[gi] = r;
@@ -377,7 +383,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           // y_k = A p_k, w_k = d y_k; z_k, p_k, w_k to the other buffers, x in place;
           // partials r_k.z_k = z_k^2 / d, p_k.y_k, z_k.y_k, w_k.y_k
           const double y = WV * uc - c.ea.dt * Lu;
-          const double dd = O[OW_D * O_PART];
+          // the Jacobi diagonal A_ii = wV - dt L_ii of the R0 pass (same arithmetic), d = 1/A_ii
+          const double Aii = ANISO_M_DREAD ? rcp_pos(O[1 * O_PART]) : WV - c.ea.dt * (-(L.ld + ldhi));
+          const double dd = ANISO_M_DREAD ? O[1 * O_PART] : rcp_pos(Aii);
           const double wk = dd * y;
           // streaming stores (evict-first in L2): the outputs are read again only by the
           // next pass, after far more than L2 has streamed through; L2 keeps the input
@@ -386,7 +394,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           __stcs(c.ea.out2 + gi, uc);
           __stcs(c.ea.out3 + gi, wk);
           if (!first) __stcs(c.ea.x + gi, fma(ax, poc, O[OW_X * O_PART]));
-          part += zc * zc * rcp_pos(dd);
+          part += zc * zc * Aii;
           part2 += uc * y;
           part3 += zc * y;
           part4 += wk * y;
@@ -560,7 +568,7 @@ bool launch_aniso_tma(const StencilCall& c, cudaStream_t st) {
     owns[nown++] = c.ea.x;
   } else if (c.epi == EPI_PCG_M) {
     owns[nown++] = c.ea.x;
-    owns[nown++] = c.ea.dinv;
+    if (ANISO_M_DREAD) owns[nown++] = c.ea.dinv;
   }
   if (c.w) owns[nown++] = c.w;
   for (int q = 0; q < nown; ++q) map_plain(&ta.own[q], owns[q], G, G.nl, XK, XOJ);
