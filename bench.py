@@ -287,7 +287,8 @@ class E2EStep:
     calls around them), the coefficients are bound per step (uploaded into the handle's
     resident copies while the previous step still computes), and the PCG solves are
     enqueued with be_pcg_solve_async, so the host waits only where it needs a value
-    (the two dt_exp).  The caller's stream joins the handle's copies at the end."""
+    (the two dt_exp, each behind the previous step's solve of the same operator only).
+    The caller's stream joins the handle's copies at the end."""
 
     def __init__(self, G, host_inp, ratio):
         self.G, self.h, self.ratio = G, host_inp, ratio
@@ -307,16 +308,21 @@ class E2EStep:
         G, h, r = self.G, self.h, self.ratio
         o = self.out[self.n % 2]
         self.n += 1
-        G.bind_coeffs("iso", h["visc_faces"], w=h["rho"])
+        # conduction: its binding work waits for the previous step's conduction solve only
+        # (the library orders it after the binding's last readers), so it overlaps the
+        # previous step's viscosity
         G.bind_coeffs("aniso", None, b=h["b"])
         G.face_kappa_spitzer(h["T"], h["kappa0"], h["T_cut"], resident=True)
         dte = G.dt_euler("aniso", None)
-        dtev = G.dt_euler("iso", None)
         s_c = sts.rkl2_num_stages(r * dte, dte)
-        s_v = sts.rkl2_num_stages(r * dtev, dtev)
         G.rkl2_advance("aniso", h["T"], None, dt=r * dte, s=s_c, out=o["T_rk"])
-        G.rkl2_advance("iso", h["v"], None, dt=r * dtev, s=s_v, out=o["v_rk"])
         _, rc = G.be_pcg_solve_async("aniso", h["T"], None, dt=r * dte, rtol=RTOL, kmax=KMAX, out=o["T_be"])
+        # viscosity: likewise behind the previous step's viscosity, while this step's
+        # conduction computes
+        G.bind_coeffs("iso", h["visc_faces"], w=h["rho"])
+        dtev = G.dt_euler("iso", None)
+        s_v = sts.rkl2_num_stages(r * dtev, dtev)
+        G.rkl2_advance("iso", h["v"], None, dt=r * dtev, s=s_v, out=o["v_rk"])
         _, rv = G.be_pcg_solve_async("iso", h["v"], None, dt=r * dtev, rtol=RTOL, kmax=KMAX, out=o["v_be"])
         return {"s_cond": s_c, "s_visc": s_v, "res_c": rc, "res_v": rv}
 

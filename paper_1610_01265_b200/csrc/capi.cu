@@ -262,17 +262,29 @@ static void pool_free_idle(sts_grid* g) {
   }
 }
 
-// a staging buffer of >= bytes that no enqueued work still uses; allocates when none is
-// free, releasing idle buffers (then waiting for in-flight ones) if the device is full
+// (a staging allocation leaves STAGE_HEADROOM bytes of the device free for everything else)
+constexpr size_t STAGE_HEADROOM = 6ull << 30;
+static double* try_alloc(size_t bytes, bool headroom = true) {
+  double* p = nullptr;
+  size_t fr = 0, tot = 0;
+  if (headroom && cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr < bytes + STAGE_HEADROOM) return nullptr;
+  if (cudaMalloc(&p, bytes) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+// a staging buffer of >= bytes that no enqueued work still uses: a free one; else a new
+// one; else (device full) the OLDEST in-flight one large enough, waited for -- which
+// bounds the pool without a device-wide synchronization; only when no buffer is large
+// enough are all of them waited for and the idle ones released (cudaFree synchronizes)
 static StageBuf* stage_acquire(sts_grid* g, size_t bytes) {
   bytes = (bytes + 255) / 256 * 256;
   pool_reclaim(g);
   StageBuf* best = nullptr;
   for (auto& b : g->stage_pool)
     if (!b.pending && !b.claimed && b.bytes >= bytes && (!best || b.bytes < best->bytes)) best = &b;
-  for (int attempt = 0; !best && attempt < 3; ++attempt) {
-    double* p = nullptr;
-    if (cudaMalloc(&p, bytes) == cudaSuccess) {
+  if (!best) {
+    if (double* p = try_alloc(bytes)) {
       StageBuf nb;
       nb.p = p;
       nb.bytes = bytes;
@@ -280,19 +292,40 @@ static StageBuf* stage_acquire(sts_grid* g, size_t bytes) {
       g->stage_pool.push_back(nb);
       g->stage_bytes += bytes;
       best = &g->stage_pool.back();
-      break;
     }
-    cudaGetLastError();
-    if (attempt == 1)   // wait for every in-flight staging buffer
-      for (auto& b : g->stage_pool)
-        if (b.pending && !b.claimed) STS_CUDA(cudaEventSynchronize(b.ev));
+  }
+  if (!best) {
+    StageBuf* old = nullptr;
+    for (auto& b : g->stage_pool)
+      if (b.pending && !b.claimed && b.bytes >= bytes && (!old || b.seq < old->seq)) old = &b;
+    if (old) {
+      STS_CUDA(cudaEventSynchronize(old->ev));
+      old->pending = false;
+      best = old;
+    }
+  }
+  if (!best) {
+    for (auto& b : g->stage_pool)
+      if (b.pending && !b.claimed) STS_CUDA(cudaEventSynchronize(b.ev));
     pool_reclaim(g);
     pool_free_idle(g);
+    if (double* p = try_alloc(bytes, false)) {
+      StageBuf nb;
+      nb.p = p;
+      nb.bytes = bytes;
+      STS_CUDA(cudaEventCreateWithFlags(&nb.ev, cudaEventDisableTiming));
+      g->stage_pool.push_back(nb);
+      g->stage_bytes += bytes;
+      best = &g->stage_pool.back();
+    }
   }
   if (!best) throw Error{STS_ERR_ALLOC, "cudaMalloc of " + std::to_string(bytes) + " bytes of host-array staging failed"};
   best->claimed = true;
   return best;
 }
+
+// mapped-mailbox word of the Gershgorin maximum (the PCG scalars use the words before it)
+constexpr int DT_MAILBOX = 64;
 
 struct HostIO {
   sts_grid* g;
@@ -360,11 +393,12 @@ struct HostIO {
     }
     if (sync) STS_CUDA(cudaStreamSynchronize(st));
   }
-  static void release(StageBuf* b, cudaStream_t s) {
+  void release(StageBuf* b, cudaStream_t s) {
     if (!b) return;
     STS_CUDA(cudaEventRecord(b->ev, s));
     b->pending = true;
     b->claimed = false;
+    b->seq = ++g->stage_seq;
   }
   ~HostIO() {
     if (ended) return;   // an error path: whatever was enqueued may still read the buffers
@@ -390,31 +424,29 @@ static void check_mode(int mode, int ncomp, const double* b) {
 // ----------------------------------------------------------------------------
 static int slot_index(int mode) { return mode == STS_MODE_ANISO ? 1 : 0; }
 
+// the bound arrays changed: the derived data must be rebuilt
 static void slot_invalidate(CoefSlot& s) {
   s.ev_ok = s.pre_ok = false;
   s.lam = -1.0;
 }
 
 static void slot_free(CoefSlot& s) {
-  for (int i = 0; i < 5; ++i)
-    for (int c = 0; c < 2; ++c) {
-      if (s.own[i][c]) cudaFree(s.own[i][c]);
-      s.own[i][c] = nullptr;
-      s.own_n[i][c] = 0;
-    }
+  for (int i = 0; i < 5; ++i) {
+    if (s.own[i]) cudaFree(s.own[i]);
+    s.own[i] = nullptr;
+    s.own_n[i] = 0;
+  }
   for (int d = 0; d < 3; ++d) {
     if (s.kfk[d]) cudaFree(s.kfk[d]);
     s.kfk[d] = nullptr;
   }
-  if (s.derived) cudaFree(s.derived);
-  s.derived = nullptr;
-  s.derived_bytes = 0;
-  for (int i = 0; i < 5; ++i)
-    for (int c = 0; c < 2; ++c) {
-      if (s.own_ev[i][c]) cudaEventDestroy(s.own_ev[i][c]);
-      s.own_ev[i][c] = nullptr;
-      s.own_ev_set[i][c] = false;
-    }
+  if (s.dbuf) cudaFree(s.dbuf);
+  s.dbuf = nullptr;
+  s.dbytes = 0;
+  if (s.last_use) cudaEventDestroy(s.last_use);
+  s.last_use = nullptr;
+  s.use_set = false;
+  s.user_dev = false;
   s.k[0] = s.k[1] = s.k[2] = s.b = s.w = nullptr;
   s.bound = false;
   slot_invalidate(s);
@@ -429,16 +461,50 @@ static double* dev_alloc(size_t n, const char* what) {
   return p;
 }
 
-// slot-owned derived buffer of at least n doubles (written by kernels on the compute
-// stream, so in stream order with every earlier reader)
-static double* slot_derived(CoefSlot& s, size_t n) {
-  if (s.derived_bytes < n * sizeof(double)) {
-    if (s.derived) STS_CUDA(cudaFree(s.derived));
-    s.derived = nullptr;
-    s.derived = dev_alloc(n, "resident derived coefficients");
-    s.derived_bytes = n * sizeof(double);
+// the binding's derived-data buffer, at least n doubles
+static double* slot_dbuf(CoefSlot& s, size_t n) {
+  if (s.dbytes < n * sizeof(double)) {
+    if (s.dbuf) STS_CUDA(cudaFree(s.dbuf));
+    s.dbuf = nullptr;
+    s.dbuf = dev_alloc(n, "resident derived coefficients");
+    s.dbytes = n * sizeof(double);
   }
-  return s.derived;
+  return s.dbuf;
+}
+
+// `ws`, a stream about to overwrite the binding's arrays, waits for their last readers
+static void slot_wait_readers(CoefSlot& s, cudaStream_t ws) {
+  if (s.use_set) STS_CUDA(cudaStreamWaitEvent(ws, s.last_use, 0));
+}
+
+// a call on stream `st` has enqueued its reads of the binding
+static void slot_used(CoefSlot* s, cudaStream_t st) {
+  if (!s) return;
+  if (!s->last_use) STS_CUDA(cudaEventCreateWithFlags(&s->last_use, cudaEventDisableTiming));
+  STS_CUDA(cudaEventRecord(s->last_use, st));
+  s->use_set = true;
+}
+
+// a bound array the caller owns (written on the caller's stream, not by the library)
+static bool slot_user_array(const CoefSlot& s, const double* p) {
+  if (!p) return false;
+  for (int i = 0; i < 5; ++i)
+    if (p == s.own[i]) return false;
+  for (int d = 0; d < 3; ++d)
+    if (p == s.kfk[d]) return false;
+  return true;
+}
+
+static void slot_update_user_dev(CoefSlot& s) {
+  s.user_dev = slot_user_array(s, s.k[0]) || slot_user_array(s, s.k[1]) || slot_user_array(s, s.k[2]) ||
+               slot_user_array(s, s.b) || slot_user_array(s, s.w);
+}
+
+static cudaStream_t coef_stream(sts_grid* g) {
+  if (!g->coef_stream) STS_CUDA(cudaStreamCreateWithFlags(&g->coef_stream, cudaStreamNonBlocking));
+  if (!g->ev_coef) STS_CUDA(cudaEventCreateWithFlags(&g->ev_coef, cudaEventDisableTiming));
+  if (!g->ev_pos) STS_CUDA(cudaEventCreateWithFlags(&g->ev_pos, cudaEventDisableTiming));
+  return g->coef_stream;
 }
 
 // The coefficient arrays one call uses (device pointers): the caller's arrays (staged
@@ -848,13 +914,16 @@ static void rkl2_core(sts_grid* g, int mode, int ncomp, const double* u0, double
 // frozen vertex coefficients of one call (ANISO): the binding's, built once per binding,
 // or built into `scratch` (vertex_coef_doubles(g, mode) doubles) from the call's arrays
 static std::vector<const double*> call_vertex_coefs(sts_grid* g, int mode, const Coefs& cf, double* scratch,
-                                                    cudaStream_t st) {
+                                                    cudaStream_t st, cudaStream_t build_stream = nullptr) {
   if (mode != STS_MODE_ANISO) return std::vector<const double*>(g->slabs.size(), nullptr);
   if (!cf.slot) return build_vertex_coefs(g, mode, scratch, cf.k1, cf.k2, cf.k3, cf.b, st);
   CoefSlot& s = *cf.slot;
-  double* base = slot_derived(s, vertex_coef_doubles(g, mode));
+  const size_t n = vertex_coef_doubles(g, mode);
+  cudaStream_t bs = build_stream ? build_stream : st;
+  double* base = slot_dbuf(s, n);
   if (!s.ev_ok) {
-    build_vertex_coefs(g, mode, base, cf.k1, cf.k2, cf.k3, cf.b, st);
+    if (bs != st) slot_wait_readers(s, bs);   // (on the compute stream the readers are earlier)
+    build_vertex_coefs(g, mode, base, cf.k1, cf.k2, cf.k3, cf.b, bs);
     s.ev_ok = true;
   }
   std::vector<const double*> out;
@@ -873,11 +942,17 @@ static size_t call_ev_doubles(const sts_grid* g, int mode, const Coefs& cf) {
 
 // metric-folded face coefficients K1, K2, K3 and wV of the merged isotropic PCG pass
 // ([4][nl][plane] at stride Nr): the binding's (once per binding) or built into `scratch`
-static double* call_premul(sts_grid* g, const Coefs& cf, double* scratch, size_t Nr, cudaStream_t st) {
+static double* call_premul(sts_grid* g, const Coefs& cf, double* scratch, size_t Nr, cudaStream_t st,
+                           cudaStream_t build_stream = nullptr) {
   double* pre = scratch;
   if (cf.slot) {
-    pre = slot_derived(*cf.slot, 4 * Nr);
-    if (cf.slot->pre_ok) return pre;
+    CoefSlot& s = *cf.slot;
+    pre = slot_dbuf(s, 4 * Nr);
+    if (s.pre_ok) return pre;
+    if (build_stream && build_stream != st) {
+      slot_wait_readers(s, build_stream);
+      st = build_stream;
+    }
   }
   for (auto& sl : g->slabs) {
     Timed t(g, STS_K_VERTEX_COEF, st);   // (the isotropic counterpart of the frozen vertex coefficients)
@@ -1015,7 +1090,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
     c.ea.dinv = off(d, g->slabs[0]);
     if (mode == STS_MODE_ISO) {
       // (any 16 B-aligned stand-in: the folded arrays are laid out like the scratch fields)
-      double* probe = cf.slot ? slot_derived(*cf.slot, 4 * Nr) : base + 6 * NFr + Nr;
+      double* probe = base;
       c.k1.p = off(probe, g->slabs[0]);
       c.k2.p = off(probe + Nr, g->slabs[0]);
       c.k3.p = off(probe + 2 * Nr, g->slabs[0]);
@@ -1408,6 +1483,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
   }
   launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, st);
   g->launches += 1;
+  slot_used(cf.slot, st);
   io.end();
   const bool async = allow_async && device_loop && !io.sync;
   if (async) {
@@ -1507,6 +1583,7 @@ int sts_grid_create(sts_grid** out, int geom, int n1, int n2, int n3, const doub
       STS_CUDA(cudaMalloc(&g->d_ticket, 64 * sizeof(unsigned int)));
       STS_CUDA(cudaMemset(g->d_ticket, 0, 64 * sizeof(unsigned int)));
       STS_CUDA(cudaMalloc(&g->d_red2, (size_t)R2_MAXBLOCKS * 4 * MAXC * sizeof(double)));
+      STS_CUDA(cudaMalloc(&g->d_gmax, 64));
     } catch (...) {
       sts_grid_destroy(g);
       throw;
@@ -1552,6 +1629,10 @@ int sts_grid_destroy(sts_grid* g) {
     if (g->d_red) cudaFree(g->d_red);
     if (g->d_ticket) cudaFree(g->d_ticket);
     if (g->d_red2) cudaFree(g->d_red2);
+    if (g->d_gmax) cudaFree(g->d_gmax);
+    if (g->coef_stream) cudaStreamDestroy(g->coef_stream);
+    if (g->ev_coef) cudaEventDestroy(g->ev_coef);
+    if (g->ev_pos) cudaEventDestroy(g->ev_pos);
     if (g->h_pinned) cudaFreeHost(g->h_pinned);
     delete g;
     if (prev >= 0) cudaSetDevice(prev);
@@ -1563,9 +1644,8 @@ int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes) {
     STS_REQUIRE(g && bytes, "NULL argument");
     size_t slots = 0;
     for (auto& s : g->slot) {
-      slots += s.derived_bytes;
-      for (int i = 0; i < 5; ++i)
-        for (int c = 0; c < 2; ++c) slots += s.own_n[i][c] * sizeof(double);
+      slots += s.dbytes;
+      for (int i = 0; i < 5; ++i) slots += s.own_n[i] * sizeof(double);
       for (int d = 0; d < 3; ++d)
         if (s.kfk[d]) slots += (size_t)g->nl * g->plane * sizeof(double);
     }
@@ -1691,6 +1771,20 @@ int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2,
       k2 = s.kfk[1];
       k3 = s.kfk[2];
     }
+    // a resident output on a single-slab grid is computed on the coefficient stream: it
+    // waits only for its input (the upload of a host T, the caller's stream for a device
+    // T) and for the last readers of the binding it overwrites
+    const bool on_cs = resident && !needs_halos(g);
+    const bool dev_T = is_device_ptr(T);
+    const cudaStream_t cst = st;
+    if (on_cs) {
+      st = coef_stream(g);
+      slot_wait_readers(s, st);
+      if (dev_T) {
+        STS_CUDA(cudaEventRecord(g->ev_pos, cst));
+        STS_CUDA(cudaStreamWaitEvent(st, g->ev_pos, 0));
+      }
+    }
     HostIO io(g, st);
     io.input(T, N);
     io.output(k1, N);
@@ -1712,10 +1806,15 @@ int sts_face_kappa_spitzer(sts_grid* g, const double* T, double* k1, double* k2,
       launch_face_kappa(G, Tv, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, d_x1f(g), d_x1c(g), st);
     }
     io.end();
+    if (on_cs) {   // later work on the caller's stream sees the new diffusivities
+      STS_CUDA(cudaEventRecord(g->ev_coef, st));
+      STS_CUDA(cudaStreamWaitEvent(cst, g->ev_coef, 0));
+    }
     if (resident) {   // bind them (b and w of the binding are kept)
       for (int d = 0; d < 3; ++d) s.k[d] = s.kfk[d];
       s.bound = true;
       slot_invalidate(s);
+      slot_update_user_dev(s);
     }
   });
 }
@@ -1741,25 +1840,20 @@ int sts_grid_bind_coeffs(sts_grid* g, int mode, const double* k1, const double* 
         *dst[i] = src[i];
         continue;
       }
-      // host array: into the library-owned copy the previous upload superseded, once the
-      // work enqueued before that supersession has run
-      const int c = s.own_next[i];
-      s.own_next[i] ^= 1;
-      if (s.own_n[i][c] < cnt[i]) {
-        if (s.own[i][c]) STS_CUDA(cudaFree(s.own[i][c]));
-        s.own[i][c] = nullptr;
-        s.own[i][c] = dev_alloc(cnt[i], "resident coefficients");
-        s.own_n[i][c] = cnt[i];
+      // host array: into the library-owned copy, once the binding's last readers (calls on
+      // the compute stream, binding work on the coefficient stream) have run
+      if (s.own_n[i] < cnt[i]) {
+        if (s.own[i]) STS_CUDA(cudaFree(s.own[i]));
+        s.own[i] = nullptr;
+        s.own[i] = dev_alloc(cnt[i], "resident coefficients");
+        s.own_n[i] = cnt[i];
       }
       cudaStream_t cs = copy_stream(g, true);
-      if (s.own_ev_set[i][c]) STS_CUDA(cudaStreamWaitEvent(cs, s.own_ev[i][c], 0));
-      STS_CUDA(cudaMemcpyAsync(s.own[i][c], src[i], cnt[i] * sizeof(double), cudaMemcpyHostToDevice, cs));
+      slot_wait_readers(s, cs);
+      if (g->coef_stream) STS_CUDA(cudaStreamWaitEvent(cs, g->ev_coef, 0));
+      STS_CUDA(cudaMemcpyAsync(s.own[i], src[i], cnt[i] * sizeof(double), cudaMemcpyHostToDevice, cs));
       if (kind == Mem::Pageable) STS_CUDA(cudaStreamSynchronize(cs));
-      // the other copy is superseded now: work reading it was enqueued before this point
-      if (!s.own_ev[i][1 - c]) STS_CUDA(cudaEventCreateWithFlags(&s.own_ev[i][1 - c], cudaEventDisableTiming));
-      STS_CUDA(cudaEventRecord(s.own_ev[i][1 - c], st));
-      s.own_ev_set[i][1 - c] = true;
-      *dst[i] = s.own[i][c];
+      *dst[i] = s.own[i];
       uploaded = true;
     }
     if (uploaded) {
@@ -1769,6 +1863,7 @@ int sts_grid_bind_coeffs(sts_grid* g, int mode, const double* k1, const double* 
     }
     s.bound = true;
     slot_invalidate(s);
+    slot_update_user_dev(s);
   });
 }
 
@@ -1826,6 +1921,7 @@ int sts_op_apply(sts_grid* g, int mode, int ncomp, const double* u, double* out,
       c.ea.out = off(out, s);
       return c;
     });
+    slot_used(cf.slot, st);
     io.end();
   });
 }
@@ -1843,14 +1939,29 @@ int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, cons
     check_mode(mode, 1, cf.b);
     double lam = cf.slot ? cf.slot->lam : -1.0;
     if (lam < 0.0) {   // (resident coefficients: computed once per binding)
+      // Resident coefficients on a single-slab grid: the binding's work (vertex /
+      // folded coefficients into the other generation, the Gershgorin pass) runs on the
+      // coefficient stream, which waits only for the binding's uploads (and the caller's
+      // stream if a bound array is the caller's) -- so the host gets dt_exp while the
+      // previous binding's solves still compute.  Otherwise on the caller's stream.
+      const bool on_cs = cf.slot && !needs_halos(g) && !g->comm;
+      const cudaStream_t cst = st;
+      if (on_cs) {
+        st = coef_stream(g);
+        if (cf.slot->user_dev) {
+          STS_CUDA(cudaEventRecord(g->ev_pos, cst));
+          STS_CUDA(cudaStreamWaitEvent(st, g->ev_pos, 0));
+        }
+        if (g->h2d_used) STS_CUDA(cudaStreamWaitEvent(st, g->ev_h2d_last, 0));
+      }
+      io.st = st;
       io.begin();
       exchange_coeffs(g, mode, cf.k1, cf.k2, cf.k3, cf.b, st);
       // ANISO: the row sums come from the frozen vertex coefficients (the binding's are
       // then ready for the advance that follows)
-      double* scratch = ws_get(g, (call_ev_doubles(g, mode, cf) + 1) * sizeof(double));
-      const auto ev = call_vertex_coefs(g, mode, cf, scratch, st);
-      ensure_red(g, 4096);
-      auto* dmax = reinterpret_cast<unsigned long long*>(g->d_red);
+      double* scratch = on_cs ? nullptr : ws_get(g, (call_ev_doubles(g, mode, cf) + 1) * sizeof(double));
+      const auto ev = call_vertex_coefs(g, mode, cf, scratch, cst, st);
+      auto* dmax = reinterpret_cast<unsigned long long*>(g->d_gmax);
       STS_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
       for (size_t si = 0; si < g->slabs.size(); ++si) {
         StencilCall c = make_call(g, g->slabs[si], mode, 1, 0, nullptr, cf.k1, cf.k2, cf.k3, cf.b, cf.w);
@@ -1858,12 +1969,22 @@ int sts_dt_euler(sts_grid* g, int mode, const double* k1, const double* k2, cons
         Timed t(g, mode == STS_MODE_ANISO ? STS_K_ANISO_GERSH : STS_K_ISO_GERSH, st);
         launch_gershgorin(c, dmax, st);
       }
-      if (g->comm) STS_NCCL(ncclAllReduce(g->d_red, g->d_red, 1, ncclDouble, ncclMax, g->comm, st));
-      launch_publish(g->d_red, 1, g->d_pinned, st);
+      if (g->comm) STS_NCCL(ncclAllReduce(g->d_gmax, g->d_gmax, 1, ncclDouble, ncclMax, g->comm, st));
+      // (the isotropic binding's folded coefficients of the merged PCG pass, while here)
+      if (on_cs && mode == STS_MODE_ISO && g->tma && g->pcg_merged)
+        call_premul(g, cf, nullptr, rnd((size_t)g->nl * g->plane), cst, st);
+      launch_publish(g->d_gmax, 1, g->d_pinned + DT_MAILBOX, st);
       g->launches += 1;
       io.end();
-      STS_CUDA(cudaStreamSynchronize(st));
-      lam = g->h_pinned[0];
+      if (on_cs) {
+        STS_CUDA(cudaEventRecord(g->ev_coef, st));
+        STS_CUDA(cudaStreamWaitEvent(cst, g->ev_coef, 0));
+        STS_CUDA(cudaEventSynchronize(g->ev_coef));
+      } else {
+        slot_used(cf.slot, st);
+        STS_CUDA(cudaStreamSynchronize(st));
+      }
+      lam = g->h_pinned[DT_MAILBOX];
       if (cf.slot) cf.slot->lam = lam;
     }
     *dt_out = lam > 0.0 ? 2.0 / lam : std::numeric_limits<double>::infinity();
@@ -1913,6 +2034,7 @@ int rkl2_advance(sts_grid* g, int mode, int ncomp, const double* u0, double* u1,
     const auto ev = call_vertex_coefs(g, mode, cf, base + 3 * NFr, st);
     rkl2_core(g, mode, ncomp, u0, u1, cf.k1, cf.k2, cf.k3, cf.b, cf.w, dt, s, ev, base, base + NFr, base + 2 * NFr,
               st);
+    slot_used(cf.slot, st);
     io.end();
   });
 }
@@ -1980,6 +2102,7 @@ int rkl2_advance_hybrid(sts_grid* g, int mode, int ncomp, const double* u0, doub
       stages_out[0] = n_euler;
       stages_out[1] = s;
     }
+    slot_used(cf.slot, st);
     io.end();
   });
 }

@@ -119,6 +119,7 @@ struct StageBuf {
   cudaEvent_t ev = nullptr;
   bool pending = false;     // ev recorded and possibly not complete
   bool claimed = false;     // held by the call being enqueued
+  unsigned long long seq = 0;   // release order (oldest first when the pool must wait)
 };
 
 // Coefficients of one operator mode kept resident across calls (sts_grid_bind_coeffs):
@@ -131,17 +132,18 @@ struct CoefSlot {
   const double* k[3] = {nullptr, nullptr, nullptr};
   const double* b = nullptr;
   const double* w = nullptr;
-  // library-owned device copies of host arrays (k1, k2, k3, b, w), two per array used in
-  // turn: an upload writes the copy the previous upload superseded, once the work enqueued
-  // before that supersession is done (own_ev) -- so uploads overlap the current binding's work
-  double* own[5][2] = {};
-  size_t own_n[5][2] = {};
-  int own_next[5] = {0, 0, 0, 0, 0};
-  cudaEvent_t own_ev[5][2] = {};
-  bool own_ev_set[5][2] = {};
+  double* own[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // k1, k2, k3, b, w copies of host arrays
+  size_t own_n[5] = {0, 0, 0, 0, 0};
   double* kfk[3] = {nullptr, nullptr, nullptr};   // face diffusivities written by sts_face_kappa_spitzer
-  double* derived = nullptr;          // ANISO: vertex coefficients of every slab; ISO: K1, K2, K3, wV
-  size_t derived_bytes = 0;
+  double* dbuf = nullptr;             // ANISO: vertex coefficients of every slab; ISO: K1, K2, K3, wV
+  size_t dbytes = 0;
+  // Every call that reads the binding records last_use on its (compute) stream; work
+  // that OVERWRITES the binding's arrays on another stream (uploads on the H2D stream,
+  // face kappa / derived data on the coefficient stream) waits for it -- exactly the
+  // previous binding's readers, not everything enqueued on the compute stream.
+  cudaEvent_t last_use = nullptr;
+  bool use_set = false;
+  bool user_dev = false;              // a bound array is a caller device array (written on the caller's stream)
   bool ev_ok = false, pre_ok = false; // derived data current for the bound arrays
   double lam = -1.0;                  // cached Gershgorin max row sum (< 0: not computed)
 };
@@ -195,9 +197,14 @@ struct sts_grid {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   std::list<sts::StageBuf> stage_pool;  // (stable addresses: a call holds pointers into it)
   size_t stage_bytes = 0;
+  unsigned long long stage_seq = 0;
   cudaEvent_t ev_h2d_last = nullptr, ev_d2h_last = nullptr;
   bool h2d_used = false, d2h_used = false;
   sts::CoefSlot slot[2];                // resident coefficients per mode (STS_MODE_ISO, STS_MODE_ANISO)
+  cudaStream_t coef_stream = nullptr;   // binding work (face kappa, derived data, Gershgorin) of host bindings
+  cudaEvent_t ev_coef = nullptr;        // after the last binding work on coef_stream
+  cudaEvent_t ev_pos = nullptr;         // scratch: a position on the caller's stream
+  double* d_gmax = nullptr;             // Gershgorin maximum (its own word: concurrent with PCG reductions)
   // executable PCG loop graphs still in flight: destroyed once their event has completed
   // (destroying an in-flight executable graph would wait for it)
   std::vector<std::pair<cudaGraphExec_t, cudaEvent_t>> retired_execs;
