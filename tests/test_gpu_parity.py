@@ -796,3 +796,38 @@ def test_nccl_one_rank_path_matches_single_process(dev, mode, graphs):
     # observed rate): launches per iteration are bounded
     per_it = 4 if mode == "aniso" else 4
     assert Gn.kernel_launches - l0 <= per_it * (max(i_n) + 3) + 40
+
+
+def test_host_path_pageable_and_virtual_slab_bindings(dev):
+    """Pageable host arrays make a call synchronous (outputs written back on return, no
+    join); resident bindings on a virtual-slab grid (binding work on the compute stream,
+    halos of the coefficients exchanged every call) equal the single domain bit for bit;
+    an asynchronous solve on host arrays in pageable memory falls back to synchronous."""
+    S = sts()
+    cfg = W.make_config("c1_spitzer64", shape=(13, 17, 40))
+    g = cfg["grid"]
+    T, b = cfg["T"].to(dev), cfg["b"].to(dev)
+    G1 = S.Grid.from_grid(g)
+    k = G1.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
+    dte = G1.dt_euler("aniso", k, b)
+    s = S.rkl2_num_stages(60 * dte, dte)
+    ref = G1.rkl2_advance("aniso", T, k, b, None, 60 * dte, s)
+    ref_x, ref_it = G1.be_pcg_solve("aniso", T, k, b, None, 60 * dte, 1e-12, 10000)
+    Gp = S.Grid.from_grid(g)
+    Gp.async_host = True                       # no join in the binding: pageable => synchronous
+    Th, kh, bh = cfg["T"].clone(), [x.cpu() for x in k], cfg["b"].clone()
+    assert not Th.is_pinned()
+    out = torch.empty_like(Th)
+    Gp.rkl2_advance("aniso", Th, kh, bh, None, 60 * dte, s, out=out)
+    assert torch.equal(out, ref.cpu())
+    xo = torch.empty_like(Th)
+    _, res = Gp.be_pcg_solve_async("aniso", Th, kh, bh, None, 60 * dte, 1e-12, 10000, out=xo)
+    assert res.status == 0 and res.iters == ref_it and torch.equal(xo, ref_x.cpu())
+    for nv in (1, 3):
+        Gv = S.Grid.from_grid(g, n_virtual=nv)
+        Gv.bind_coeffs("aniso", None, b=b)
+        Gv.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"], resident=True)
+        assert Gv.dt_euler("aniso", None) == dte
+        assert torch.equal(Gv.rkl2_advance("aniso", T, None, dt=60 * dte, s=s), ref)
+        xv, iv = Gv.be_pcg_solve("aniso", T, None, dt=60 * dte, rtol=1e-12, kmax=10000)
+        assert abs(iv[0] - ref_it[0]) <= 1 and rel_l2(cpu(xv), cpu(ref_x)) <= 1e-12
