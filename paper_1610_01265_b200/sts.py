@@ -370,6 +370,9 @@ class Grid:
         ncomp = 1 if un.dim() == 3 else un.shape[0]
         out = self._alloc(ncomp, un) if out is None else out
         res = PcgResult(ncomp)
+        # the library writes res when the stream reaches the end of the solve: keep it alive
+        # until then even if the caller drops it (the last 256 results are held)
+        self._inflight = getattr(self, "_inflight", [])[-255:] + [res]
         _check("be_pcg_solve_async", lib().be_pcg_solve_async(
             self._h, MODE[mode], ncomp, _ptr(un), _ptr(out), *_kptrs(k), _ptr(b), _ptr(w),
             float(dt), float(rtol), int(kmax), res._iters, ctypes.byref(res._status), _stream(stream)))
