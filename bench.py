@@ -101,14 +101,22 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
 
 
 def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False, merged_c=False, merged_v=False,
-                      dev_c=False, dev_v=False):
-    """Total algorithmic bytes per class for one step on `ncells` local cells."""
+                      dev_c=False, dev_v=False, xm_c=None, xm_v=None):
+    """Total algorithmic bytes per class for one step on `ncells` local cells.
+    xm_c / xm_v: (skipped, caught_up) x-update passes per component of the merged PCG
+    solves (DESIGN.md §5.3 "x in pairs"): a skipped pass moves 16 B/cell/component less
+    (no x read / write), a catch-up pass 8 B more (the own z_{k-1} of the isotropic pass is
+    re-read from memory; the anisotropic pass has it staged)."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
         _cond_bytes(add, s_c, it_c, fused_c, merged_c, dev_c)
+        if merged_c and xm_c:
+            add("aniso_pcg_m", -16 * sum(xm_c[0]))
     if s_v:
         _visc_bytes(add, s_v, it_v, fused_v, merged_v, dev_v)
+        if merged_v and xm_v:
+            add("iso_pcg_m", -16 * sum(xm_v[0]) + 8 * sum(xm_v[1]))
     return B
 
 
@@ -255,6 +263,7 @@ class Step:
         s_c = sts.rkl2_num_stages(dt, dte)
         G.rkl2_advance("aniso", T, None, dt=dt, s=s_c, out=self.T_rk)
         _, (it_c,) = G.be_pcg_solve("aniso", T, None, dt=dt, rtol=RTOL, kmax=KMAX, out=self.T_be)
+        self.xm_c = G.pcg_xmodes(1)
         return s_c, it_c
 
     def visc(self):
@@ -270,13 +279,15 @@ class Step:
         s_v = sts.rkl2_num_stages(dtv, dtev)
         G.rkl2_advance("iso", v, None, dt=dtv, s=s_v, out=self.v_rk)
         _, it_v = G.be_pcg_solve("iso", v, None, dt=dtv, rtol=RTOL, kmax=KMAX, out=self.v_be)
+        self.xm_v = G.pcg_xmodes(3)
         return s_v, it_v
 
     def __call__(self):
+        self.xm_c, self.xm_v = ([0], [0]), ([0, 0, 0], [0, 0, 0])
         s_c, it_c = self.cond()
         s_v, it_v = self.visc()
         return {"s_cond": s_c, "it_cond": it_c, "s_visc": s_v, "it_visc": it_v,
-                "units": s_c + it_c + s_v + max(it_v)}
+                "units": s_c + it_c + s_v + max(it_v), "xm_c": self.xm_c, "xm_v": self.xm_v}
 
 
 class E2EStep:
@@ -494,7 +505,8 @@ def measure_device(G, inp, ratio, args, ws, dev, ncells_local, ncells_total):
     for i in pinfos:
         for k, v in algorithmic_bytes(ncells_local, i["s_cond"], i["it_cond"], i["s_visc"], i["it_visc"],
                                       has("aniso_pcg_s"), has("iso_pcg_s"), has("aniso_pcg_m"), has("iso_pcg_m"),
-                                      has("aniso_rkl2_dstage"), has("iso_rkl2_dstage")).items():
+                                      has("aniso_rkl2_dstage"), has("iso_rkl2_dstage"), i.get("xm_c"),
+                                      i.get("xm_v")).items():
             Bytes[k] = Bytes.get(k, 0.0) + v
     kernels = {}
     for k, (n, kms) in timing.items():

@@ -130,6 +130,14 @@ int sts_grid_workspace_bytes(const sts_grid* g, size_t* bytes);
 int sts_grid_kernel_launches(const sts_grid* g, long long* count);
 
 /*
+ * Merged-PCG x-update profile of the most recent SYNCHRONOUS be_pcg_solve on the
+ * handle (instrumentation; DESIGN.md §5.3 "x in pairs"): per component, the passes
+ * that skipped the x update and the passes that caught it up (the others updated x
+ * every pass).  ncomp 1..3.
+ */
+int sts_grid_pcg_xmodes(const sts_grid* g, int ncomp, int* skipped, int* caught_up);
+
+/*
  * Communication profile (Sec. 2.4 and the boxed terms of Figs. 1-2):
  * `local` counts neighbour (halo) exchange events -- one per operator application
  * that reads across slab boundaries -- and `global` counts all-rank reductions

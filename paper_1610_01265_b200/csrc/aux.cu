@@ -334,15 +334,22 @@ template <int NC>
 __global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long cs, double* __restrict__ x,
                                                          const double* __restrict__ p0, const double* __restrict__ p1,
                                                          const PcgScal* __restrict__ sc) {
-  double ax[NC];
-  const double* pp[NC];
-  bool act[NC];
+  // what x still owes after the last iteration k = iters (PcgScal::xmf): alpha_k p_k;
+  // after a skipped pass also alpha_{k-1} p_{k-1} (X_FIN_TWO), or only that (X_FIN_PREV,
+  // a skipped pass that converged on its own r.z): p_k in p[k % 2], p_{k-1} in the other
+  double ax[NC], axp[NC];
+  const double *pp[NC], *pq[NC];
+  bool act[NC], two[NC];
   bool any = false;
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    act[q] = sc[q].iters > 0;
-    ax[q] = sc[q].ax;
-    pp[q] = (sc[q].iters & 1) ? p1 : p0;
+    const int it = sc[q].iters, f = sc[q].xmf;
+    act[q] = it > 0 || f == X_FIN_PREV;
+    two[q] = f == X_FIN_TWO || f == X_FIN_PREV;
+    ax[q] = f == X_FIN_PREV ? 0.0 : sc[q].ax;
+    axp[q] = sc[q].axp;
+    pp[q] = (it & 1) ? p1 : p0;
+    pq[q] = (f == X_FIN_PREV) ? pp[q] : ((it & 1) ? p0 : p1);   // p_{k-1}
     any = any || act[q];
   }
   if (!any) return;
@@ -351,7 +358,9 @@ __global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long 
     for (int q = 0; q < NC; ++q) {
       if (!act[q]) continue;
       const long long o = e + q * cs;
-      x[o] = fma(ax[q], pp[q][o], x[o]);
+      double xv = x[o];
+      if (two[q]) xv = fma(axp[q], pq[q][o], xv);
+      x[o] = fma(ax[q], pp[q][o], xv);
     }
   }
 }

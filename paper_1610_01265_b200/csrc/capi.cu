@@ -1660,6 +1660,17 @@ int sts_grid_kernel_launches(const sts_grid* g, long long* count) {
   });
 }
 
+int sts_grid_pcg_xmodes(const sts_grid* g, int ncomp, int* skipped, int* caught_up) {
+  return guard([&] {
+    STS_REQUIRE(g && skipped && caught_up && ncomp >= 1 && ncomp <= MAXC, "bad arguments");
+    const auto* hsc = reinterpret_cast<const PcgScal*>(g->h_pinned);
+    for (int c = 0; c < ncomp; ++c) {
+      skipped[c] = hsc[c].nskip;
+      caught_up[c] = hsc[c].ncatch;
+    }
+  });
+}
+
 int sts_grid_comm_counts(const sts_grid* g, long long* local, long long* global_) {
   return guard([&] {
     STS_REQUIRE(g && local && global_, "NULL argument");

@@ -11,6 +11,13 @@ namespace sts {
 __device__ inline void pcg_breakdown(PcgScal& s) {
   s.done = 1;
   s.flags |= PCG_BREAKDOWN;
+  // (a skipped pass still owes x its alpha_{k-1} p_{k-1}: the final pass adds it)
+  if (s.xm == X_SKIP) {
+    s.xmf = X_FIN_PREV;
+    s.axp = s.ax;
+  } else {
+    s.xmf = X_FIN_ONE;
+  }
   s.ax = 0.0;
 }
 
@@ -32,6 +39,10 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.thresh = rtol2 * sums[c * nq + 1];
     s.iters = 0;
     s.flags = 0;                           // (kmax was set by launch_pcg_init)
+    s.xm = X_NORMAL;
+    s.xmf = X_FIN_ONE;
+    s.cxp = s.cxz = s.axp = 0.0;
+    s.nskip = s.ncatch = 0;
     s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
     s.beta = 0.0;
     s.ax = 0.0;
@@ -59,17 +70,25 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     // (exact in exact arithmetic; r_k.z_k is the pass's own sum, so rounding does
     // not accumulate across iterations).  The pass forms z_{k+1} = z_k - alpha_k d y_k.
     if (s.done) return;
+    const int mk = s.xm;                   // x mode of the pass that just ran
     const double rz = sums[c * nq + 0];
     if (rz <= s.thresh) {
       // the pass's own r_k.z_k meets the test: reached only after an extrapolated value
-      // below its own rounding (below); x_k is complete (the pass applied alpha_{k-1})
+      // below its own rounding (below); x_k is complete unless the pass skipped x
       s.done = 1;
+      if (mk == X_SKIP) {
+        s.xmf = X_FIN_PREV;
+        s.axp = s.ax;
+      } else {
+        s.xmf = X_FIN_ONE;
+      }
       s.ax = 0.0;
       s.rz = rz;
       return;
     }
     s.pAp = sums[c * nq + 1];
     if (!(s.pAp > 0.0) || !isfinite(s.pAp) || !isfinite(rz)) return pcg_breakdown(s);
+    const double a_prev = s.ax, b_prev = s.beta;   // alpha_{k-1}, beta_k (used by this pass)
     s.alpha = rz / s.pAp;
     s.rz_old = rz;
     s.rz = rz - 2.0 * s.alpha * sums[c * nq + 2] + s.alpha * s.alpha * sums[c * nq + 3];
@@ -84,6 +103,28 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     else if (s.rz <= s.thresh) s.done = 1;
     else s.beta = s.rz / rz;               // beta_{k+1} = r_{k+1}.z_{k+1} / r_k.z_k
     pcg_kmax(s);
+    // x in pairs: after a skipped pass the next one catches up; otherwise the next pass
+    // may skip if the catch-up after it divides by a safe beta_{k+1}
+    if (s.done) {
+      if (mk == X_SKIP) {                  // x still owes alpha_{k-1} p_{k-1} + alpha_k p_k
+        s.xmf = X_FIN_TWO;
+        s.axp = a_prev;
+      } else {
+        s.xmf = X_FIN_ONE;
+      }
+    } else if (mk == X_SKIP) {
+      s.xm = X_CATCHUP;
+      s.cxz = a_prev / b_prev;
+      s.cxp = s.alpha + s.cxz;
+      s.ncatch += 1;
+    } else if (s.beta >= X_SKIP_BETA) {
+      s.xm = X_SKIP;
+      s.nskip += 1;
+    } else {
+      s.xm = X_NORMAL;
+      s.cxp = s.alpha;
+      s.cxz = 0.0;
+    }
   }
 }
 

@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   // warp-uniform values in shared memory (broadcast loads instead of registers):
   // 1/g3 of the vertex rows j0-1 .. j0+XJ-1 (row vj of a warp and the one above it)
   // and the PCG scalars beta_k, alpha_{k-1}
-  __shared__ double sg3[XJ + 1], sbx[2];
+  // (merged PCG: the x mode of this pass and its catch-up coefficients, pcg.cuh)
+  __shared__ double sg3[XJ + 1], sbx[4];
+  __shared__ int sxm;
   if (tid <= XJ) {
     const int r = j0 - 1 + tid;
     sg3[tid] = (r >= 0 && r < G.n2) ? M.iG3[r] : 0.0;
@@ -160,6 +162,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
     const bool kPcg = (EPI == EPI_PCG_S || kM) && !first;
     sbx[0] = kPcg ? c.ea.sc[0].beta : 0.0;
     sbx[1] = kPcg ? c.ea.sc[0].ax : 0.0;
+    sbx[2] = (kM && kPcg) ? c.ea.sc[0].cxp : 0.0;
+    sbx[3] = (kM && kPcg) ? c.ea.sc[0].cxz : 0.0;
+    sxm = (kM && kPcg) ? c.ea.sc[0].xm : X_NORMAL;
   }
   if (tid == 0) {
     for (int s = 0; s < XTS; ++s) {
@@ -174,6 +179,8 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   if (tid >= XNT) {
     if (tid != XNT) return;
     const int nsrc_now = ((EPI == EPI_PCG_S || kM) && first) ? 1 : Lay::nsrc;
+    // merged PCG: no x box when the pass does not touch x (first pass, skipped x update)
+    const bool no_x = kM && (first || sxm == X_SKIP);
     for (int p = ib - 1; p <= ie; ++p) {
       const int slot = (p - ib + 1) % XTS, n = (p - ib + 1) / XTS;
       if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
@@ -187,7 +194,11 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       if (wrapL) bytes += nsrc_now * 2 * UBH * 8;
       if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
       if (has_e) bytes += E_PART * 8;
-      if (has_own) bytes += Lay::nown * XOJ * XK * 8;
+      // (merged PCG: the x box is of the package's OWN plane p -- the x update uses only
+      // values of plane p's slot -- the other epilogue boxes are of plane p-1)
+      const bool x_here = kM && !no_x && p >= ib && p < ie;
+      if (has_own) bytes += (Lay::nown - (kM ? 1 : 0)) * XOJ * XK * 8;
+      if (x_here) bytes += XOJ * XK * 8;
       // per-plane metrics (plain stores: the mbarrier arrive below releases them to the
       // consumers' acquiring wait): iG2 of cell planes p-1 and p, Vr of plane p-1
       {
@@ -208,7 +219,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
         for (int a = 0; a < 3; ++a) tma3(S + Lay::E + a * E_COMP, &ta.e, oe, j0, a * (G.nl + 1) + p, bar);
       if (has_own)
 #pragma unroll
-        for (int q = 0; q < Lay::nown; ++q) tma3(S + Lay::O + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
+        for (int q = 0; q < Lay::nown; ++q)
+          if (!(kM && q == OW_X)) tma3(S + Lay::O + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
+      if (x_here) tma3(S + Lay::O + OW_X * O_PART, &ta.own[OW_X], oe, j0, p, bar);
     }
     return;
   }
@@ -289,12 +302,24 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
     double Su, Tu, Fu, SA, DB, DC, u, po, z, ld;
   };
   St SX = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, SY = SX;
+  const int xm = kM ? sxm : X_NORMAL;
   // plane p: Q(p) landed; L = state of cell plane p-1, H receives cell plane p's
   auto body = [&](int p, const St& L, St& H) {
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
     mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
     usums(S, H.Su, H.Tu, H.Fu, H.u, H.po, H.z);
+    if constexpr (kM) {
+      // x of the own cell of plane p, from this slot alone (pcg.cuh "x in pairs"):
+      // x_k = x_{k-1} + alpha_{k-1} p_{k-1}, skipped, or the catch-up
+      // x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (raw staged z_{k-1})
+      if (!first && xm != X_SKIP && own && p >= ib && p < ie) {
+        const double* Ox = S + Lay::O + OW_X * O_PART + vj * XK + vk + se;
+        double xn = fma(xm == X_CATCHUP ? sbx[2] : ax, H.po, *Ox);
+        if (xm == X_CATCHUP) xn = fma(-sbx[3], S[o11], xn);
+        __stcs(c.ea.x + (long long)p * G.plane + coff, xn);
+      }
+    }
     double* vb = vbuf + (p & 1) * VBUF;
     H.SA = H.DB = H.DC = H.ld = 0.0;
     if (p >= ib) {
@@ -393,7 +418,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           __stcs(c.ea.out + gi, zc);
           __stcs(c.ea.out2 + gi, uc);
           __stcs(c.ea.out3 + gi, wk);
-          if (!first) __stcs(c.ea.x + gi, fma(ax, poc, O[OW_X * O_PART]));
+          // (x of this plane was updated when its slot landed, above)
           part += zc * zc * Aii;
           part2 += uc * y;
           part3 += zc * y;

@@ -176,10 +176,15 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   if ((kS || kM) && all) return;
 
   // PCG scalars of this iteration, broadcast from shared memory (keeps them out of registers)
-  __shared__ double sbeta[NC], sax[NC];
+  // (merged PCG: each component's x mode of this pass and catch-up coefficients, pcg.cuh)
+  __shared__ double sbeta[NC], sax[NC], scxp[NC], scxz[NC];
+  __shared__ int sxm[NC];
   if (tid < NC) {
     sbeta[tid] = kP ? c.ea.sc[tid].beta : 0.0;
     sax[tid] = kP ? c.ea.sc[tid].ax : 0.0;
+    scxp[tid] = (kM && kP) ? c.ea.sc[tid].cxp : 0.0;
+    scxz[tid] = (kM && kP) ? c.ea.sc[tid].cxz : 0.0;
+    sxm[tid] = (kM && kP) ? c.ea.sc[tid].xm : X_NORMAL;
   }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -227,7 +232,16 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     if (wrapL) bytes += nsrcf_now * NC * 2 * SBH * 8 + 2 * K3H * 8;
     if (wrapR) bytes += nsrcf_now * NC * 2 * SBH * 8;
     if (ta.has_w) bytes += OWN * 8;
+    // merged PCG: the x box of a component whose x the pass does not touch (first pass,
+    // skipped x update) is not loaded
+    bool no_x[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) no_x[q] = kM && (!kP || sxm[q] == X_SKIP);
     bytes += Lay::nepi * OWN * 8;
+    if constexpr (kM)
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        if (no_x[q]) bytes -= OWN * 8;
     if (Lay::nd) {
       bytes += SBW * SBH * 8;
       if (wrapL) bytes += 2 * SBH * 8;
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       if (ta.has_w) tma3(S + Lay::WB, &ta.w, k0, j0, p, bar);
 #pragma unroll
       for (int q = 0; q < Lay::nepi; ++q)
-        tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+        if (!(kM && no_x[q % NC])) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
     }
     return;
   }
@@ -547,7 +561,17 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
             const long long go = gi + q * cs;
             __stcs(o1 + go, zk);
             __stcs(o2 + go, u0);
-            if constexpr (kP) __stcs(ox + go, fma(sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]));
+            if constexpr (kP) {
+              // x in pairs (pcg.cuh): x_k = x_{k-1} + alpha_{k-1} p_{k-1}; skipped; or the
+              // catch-up x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (z_{k-1}: the raw staged
+              // value was formed in place, so it is read from global memory)
+              const int m = sxm[q];
+              if (m != X_SKIP) {
+                double xn = fma(m == X_CATCHUP ? scxp[q] : sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
+                if (m == X_CATCHUP) xn = fma(-scxz[q], __ldcs(c.u.p + go), xn);
+                __stcs(ox + go, xn);
+              }
+            }
             part[q][0] += zk * zk * idcell;
           }
         }

@@ -300,10 +300,25 @@ struct PcgScal {
   double rz, rz_old, pAp, alpha, beta, thresh;
   double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update;
                     // the merged iteration also applies it to z)
+  // merged iteration, x updated every other pass (DESIGN.md §5.3 "x in pairs"): the pass's
+  // x mode xm -- X_NORMAL: x_k = x_{k-1} + ax p_{k-1}; X_SKIP: x not touched;
+  // X_CATCHUP: x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (p_{k-2} = (p_{k-1} - z_{k-1}) / beta_{k-1});
+  // xmf / axp: what the final pass still owes x after the last iteration (X_FIN_*)
+  double cxp, cxz, axp;
   int done, iters;
   int flags;        // PCG_BREAKDOWN (p.A p <= 0 or a non-finite scalar: A not SPD / NaN input), PCG_KMAX
   int kmax;         // iteration limit (set by launch_pcg_init): reaching it stops the component
+  int xm, xmf;
+  int nskip, ncatch;   // passes run with a skipped x update / a catch-up (instrumentation)
 };
+enum { X_NORMAL = 0, X_SKIP = 1, X_CATCHUP = 2 };
+enum { X_FIN_ONE = 0, X_FIN_TWO = 4, X_FIN_PREV = 5 };   // final x += ax p_k | + axp p_{k-1} | axp p_{k-1} only
+// a pass skips the x update only if the next pass's catch-up divides by a beta at least this
+// large (its rounding is amplified by ~1 + 1/beta; CG's beta is ~0.8-1 in slow convergence)
+#ifndef STS_X_SKIP_BETA   // (A-B: a value > 1 disables the skipped x updates)
+#define STS_X_SKIP_BETA 0.1
+#endif
+constexpr double X_SKIP_BETA = STS_X_SKIP_BETA;
 constexpr int PCG_BREAKDOWN = 1;
 constexpr int PCG_KMAX = 2;
 static_assert(sizeof(PcgScal) % sizeof(double) == 0, "PcgScal is published as doubles");

@@ -59,6 +59,7 @@ def lib():
         "sts_grid_workspace_bytes": (I, [P, ctypes.POINTER(ctypes.c_size_t)]),
         "sts_grid_kernel_launches": (I, [P, ctypes.POINTER(ctypes.c_longlong)]),
         "sts_grid_comm_counts": (I, [P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
+        "sts_grid_pcg_xmodes": (I, [P, I, ctypes.POINTER(I), ctypes.POINTER(I)]),
         "sts_grid_set_timing": (I, [P, I]),
         "sts_grid_set_tma": (I, [P, I]),
         "sts_grid_set_graphs": (I, [P, I]),
@@ -209,6 +210,12 @@ class Grid:
         a, b = ctypes.c_longlong(), ctypes.c_longlong()
         _check("sts_grid_comm_counts", lib().sts_grid_comm_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    def pcg_xmodes(self, ncomp=1):
+        """(skipped, caught_up) x-update passes per component of the last synchronous solve."""
+        a, b = (ctypes.c_int * ncomp)(), (ctypes.c_int * ncomp)()
+        _check("sts_grid_pcg_xmodes", lib().sts_grid_pcg_xmodes(self._h, int(ncomp), a, b))
+        return list(a), list(b)
 
     @property
     def workspace_bytes(self):
