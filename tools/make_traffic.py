@@ -34,6 +34,8 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def main(paths, cells=CELLS):
     out = {"cells": cells, "source": "ncu --set full --clock-control none, tools/prof_kernels.sh",
            "dram_bytes_per_cell": {}, "dram_pct": {}, "duration_us": {}}
+    acc = {}   # class -> [(bytes/cell, dram %, us)] over the captured launches (averaged: the merged
+    #            PCG passes alternate a skipped and a catch-up x update)
     for p in paths:
         txt = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"],
                              capture_output=True, text=True).stdout
@@ -49,11 +51,15 @@ def main(paths, cells=CELLS):
                 continue
             rd = float(d["dram__bytes_read.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_read.sum")]]
             wr = float(d["dram__bytes_write.sum"].replace(",", "")) * SCALE[u[h.index("dram__bytes_write.sum")]]
-            out["dram_bytes_per_cell"][cls] = round((rd + wr) / cells, 3)
-            out["dram_pct"][cls] = float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"].replace(",", ""))
+            pct = float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"].replace(",", ""))
             dur = float(d["gpu__time_duration.sum"].replace(",", ""))
             unit = u[h.index("gpu__time_duration.sum")]
-            out["duration_us"][cls] = dur * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1.0)
+            acc.setdefault(cls, []).append(((rd + wr) / cells, pct, dur * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1.0)))
+    for cls, v in acc.items():
+        out["dram_bytes_per_cell"][cls] = round(sum(x[0] for x in v) / len(v), 3)
+        out["dram_pct"][cls] = round(sum(x[1] for x in v) / len(v), 3)
+        out["duration_us"][cls] = round(sum(x[2] for x in v) / len(v), 3)
+        out.setdefault("launches_averaged", {})[cls] = len(v)
     print(json.dumps(out, indent=1))
 
 
