@@ -105,8 +105,8 @@ def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False,
     """Total algorithmic bytes per class for one step on `ncells` local cells.
     xm_c / xm_v: (skipped, caught_up) x-update passes per component of the merged PCG
     solves (DESIGN.md §5.3 "x in pairs"): a skipped pass moves 16 B/cell/component less
-    (no x read / write), a catch-up pass 8 B more (the own z_{k-1} of the isotropic pass is
-    re-read from memory; the anisotropic pass has it staged)."""
+    (no x read / write); a catch-up pass moves what a normal pass does (its own z_{k-1}
+    is staged)."""
     B = {}
     add = lambda k, v: B.__setitem__(k, B.get(k, 0.0) + v * ncells)  # noqa: E731
     if s_c:
@@ -116,7 +116,7 @@ def algorithmic_bytes(ncells, s_c, it_c, s_v, it_v, fused_c=True, fused_v=False,
     if s_v:
         _visc_bytes(add, s_v, it_v, fused_v, merged_v, dev_v)
         if merged_v and xm_v:
-            add("iso_pcg_m", -16 * sum(xm_v[0]) + 8 * sum(xm_v[1]))
+            add("iso_pcg_m", -16 * sum(xm_v[0]))
     return B
 
 

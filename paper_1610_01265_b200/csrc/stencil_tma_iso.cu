@@ -207,9 +207,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
       if constexpr (kF) {
         double* S = ring + slot * Lay::SLOT;
+        // p_k = (zold - alpha wold) + beta pold over wold; zold stays raw (the own cell's
+        // z_k = p_k - beta pold is re-formed by its consumer, and the x catch-up reads the
+        // raw z_{k-1})
         auto form = [&](int o, int q) {
           const double z = fma(-sax[q], S[o + Lay::FS], S[o]);
-          S[o] = z;
           S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
         };
 #pragma unroll
@@ -550,7 +552,8 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
           const int oq = q * S_MAIN + oc;
-          const double zk = zm(S, oq, q);
+          // (formed slot: field 1 holds p_k, field 0 the raw z_{k-1}: z_k = p_k - beta p_{k-1})
+          const double zk = kF ? fma(-sbeta[q], S[oq + 2 * Lay::FS], S[oq + Lay::FS]) : zm(S, oq, q);
           const double u0 = kF ? S[oq + Lay::FS] : (kP ? fma(sbeta[q], S[oq + 2 * Lay::FS], zk) : zk);
           const double ujm = sv(S, oq - SBW, 0, q), ujp = sv(S, oq + SBW, 0, q);
           const double ukm = sv(S, okm0 + q * okms, 0, q), ukp = sv(S, okp0 + q * okps, 0, q);
@@ -563,12 +566,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
             __stcs(o2 + go, u0);
             if constexpr (kP) {
               // x in pairs (pcg.cuh): x_k = x_{k-1} + alpha_{k-1} p_{k-1}; skipped; or the
-              // catch-up x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (z_{k-1}: the raw staged
-              // value was formed in place, so it is read from global memory)
+              // catch-up x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (the raw staged z_{k-1})
               const int m = sxm[q];
               if (m != X_SKIP) {
                 double xn = fma(m == X_CATCHUP ? scxp[q] : sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
-                if (m == X_CATCHUP) xn = fma(-scxz[q], __ldcs(c.u.p + go), xn);
+                if (m == X_CATCHUP) xn = fma(-scxz[q], S[oq], xn);
                 __stcs(ox + go, xn);
               }
             }
