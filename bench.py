@@ -87,11 +87,11 @@ def bytes_per_cell(kind, ncomp=1, active=None, first=False):
         # p pass of the unfused S-pass: z, pold, x in; p, x out (first: z in, p out)
         "pcg_pupdate": 16 * c if first else 40 * c,
         "pcg_xfinal": 24 * c,
-        # merged iteration (one pass): zold, wold, pold, x (+ e, d) in; z, p, w, x out
-        # (first: z0 (+ e, d) in; z, p, w out); R0 of the merged path also writes z0
-        "aniso_pcg_m": (8 + 24 + 8 + 24) if first else (32 + 24 + 8 + 32),
+        # merged iteration (one pass): p_{k-2}, w_{k-1}, p_{k-1}, x (+ e, d) in; p, w, x out
+        # (first: z0 (+ e, d) in; p, w out); z is never stored; R0 of the merged path writes z0
+        "aniso_pcg_m": (8 + 24 + 8 + 16) if first else (32 + 24 + 8 + 24),
         # (the isotropic pass recomputes d from the staged face coefficients)
-        "iso_pcg_m": (32 * c + 32) if first else (64 * c + 32),
+        "iso_pcg_m": (24 * c + 32) if first else (56 * c + 32),
         "iso_pcg_r0_m": 8 * c + 32 + 24 * c + 8,
         # RKL2 stage in deviation form (D_j = Y_j - Y0): D_{j-1}, D_{j-2}, M0 (+ e / k, w) in; D_j out
         "aniso_rkl2_dstage": 8 + 24 + 16 + 8,

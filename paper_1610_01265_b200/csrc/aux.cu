@@ -332,11 +332,13 @@ __global__ void __launch_bounds__(256) pcg_rupdate_v2_kernel(long long n2, long 
 
 template <int NC>
 __global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long cs, double* __restrict__ x,
-                                                         const double* __restrict__ p0, const double* __restrict__ p1,
+                                                         const double* __restrict__ pk0, const double* __restrict__ pk1,
+                                                         const double* __restrict__ pk2, const double* __restrict__ pk3,
                                                          const PcgScal* __restrict__ sc) {
   // what x still owes after the last iteration k = iters (PcgScal::xmf): alpha_k p_k;
   // after a skipped pass also alpha_{k-1} p_{k-1} (X_FIN_TWO), or only that (X_FIN_PREV,
-  // a skipped pass that converged on its own r.z): p_k in p[k % 2], p_{k-1} in the other
+  // a skipped pass that converged on its own r.z: iters = k-1); p_j in pk[j % 4]
+  const double* pk[4] = {pk0, pk1, pk2, pk3};
   double ax[NC], axp[NC];
   const double *pp[NC], *pq[NC];
   bool act[NC], two[NC];
@@ -348,8 +350,8 @@ __global__ void __launch_bounds__(256) pcg_xfinal_kernel(long long n, long long 
     two[q] = f == X_FIN_TWO || f == X_FIN_PREV;
     ax[q] = f == X_FIN_PREV ? 0.0 : sc[q].ax;
     axp[q] = sc[q].axp;
-    pp[q] = (it & 1) ? p1 : p0;
-    pq[q] = (f == X_FIN_PREV) ? pp[q] : ((it & 1) ? p0 : p1);   // p_{k-1}
+    pp[q] = pk[it & 3];
+    pq[q] = (f == X_FIN_PREV) ? pk[it & 3] : pk[(it + 3) & 3];   // p_{k-1}
     any = any || act[q];
   }
   if (!any) return;
@@ -428,9 +430,9 @@ int launch_pcg_rupdate(int ncomp, long long n, long long cs, double* r, double* 
   return nb;
 }
 
-void launch_pcg_xfinal(int ncomp, long long n, long long cs, double* x, const double* p0, const double* p1,
+void launch_pcg_xfinal(int ncomp, long long n, long long cs, double* x, const double* const pk[4],
                        const PcgScal* sc, cudaStream_t st) {
-  STS_NC_SWITCH(ncomp, pcg_xfinal_kernel, n, cs, x, p0, p1, sc);
+  STS_NC_SWITCH(ncomp, pcg_xfinal_kernel, n, cs, x, pk[0], pk[1], pk[2], pk[3], sc);
   STS_CUDA(cudaGetLastError());
 }
 

@@ -1053,7 +1053,9 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
   double* pb[2] = {base + 3 * NFr, base + 4 * NFr};
   double* d = base + 6 * NFr;
   double* evbase = base + 6 * NFr + Nr + npre;
-  double* zb[2] = {base, base + NFr};
+  // merged iteration buffers: p_k in p4[k % 4] (the pass reads p_{k-2} and p_{k-1}, writes
+  // p_k; z is never stored), w_k in wb[k % 2]; R0 leaves z0 in p4[0]
+  double* p4[4] = {base, base + NFr, base + 3 * NFr, base + 4 * NFr};
   double* wb[2] = {base + 2 * NFr, base + 5 * NFr};
   double* x = un1;
   const double rtol2 = rtol * rtol;
@@ -1079,12 +1081,11 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
   bool merged = false;
   double* pre = nullptr;
   if (g->tma && g->pcg_merged) {
-    StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_M, zb[0], k1, k2, k3, bb, w);
+    StencilCall c = make_call(g, g->slabs[0], mode, ncomp, EPI_PCG_M, p4[0], k1, k2, k3, bb, w);
     c.u2 = view(g, g->slabs[0], H_W, wb[0]);
-    c.u3 = view(g, g->slabs[0], H_P, pb[0]);
+    c.u3 = view(g, g->slabs[0], H_P, p4[1]);
     c.ev = ev[0];
-    c.ea.out = off(zb[1], g->slabs[0]);
-    c.ea.out2 = off(pb[1], g->slabs[0]);
+    c.ea.out2 = off(p4[2], g->slabs[0]);
     c.ea.out3 = off(wb[1], g->slabs[0]);
     c.ea.x = off(x, g->slabs[0]);
     c.ea.dinv = off(d, g->slabs[0]);
@@ -1114,7 +1115,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
     c.ev = ev[si];
     c.ea.out = merged ? off(wb[0], sl) : off(r, sl);   // (merged: r0 itself is not needed)
     c.ea.out2 = write_x0 ? off(x, sl) : nullptr;
-    c.ea.out3 = merged ? off(zb[0], sl) : (zd ? nullptr : off(z, sl));
+    c.ea.out3 = merged ? off(p4[0], sl) : (zd ? nullptr : off(z, sl));
     c.ea.out4 = off(d, sl);
     c.ea.dt = dt;
     c.ea.partials = partials;
@@ -1139,18 +1140,20 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
     c.ea.sc = sc;
     return c;
   };
-  auto make_m = [&](size_t si) {   // merged iteration k_cur (TMA)
+  auto make_m = [&](size_t si) {   // merged iteration k_cur (TMA): fields p_{k-2}, w_{k-1}, p_{k-1}
     const Slab& sl = g->slabs[si];
     const int first = (k_cur == 1);
-    const int a = (k_cur - 1) & 1, b2 = k_cur & 1;
-    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_M, zb[a], k1, k2, k3, bb, w);
-    c.u = view(g, sl, H_Z, zb[a]);
-    c.u2 = first ? FieldV{} : view(g, sl, H_W, wb[a]);
-    c.u3 = first ? FieldV{} : view(g, sl, H_P, pb[a]);
+    const int k = k_cur;
+    // (first: z0 as field 0; k = 2: p_0 = z0 stands in for p_{k-2}, its coefficient beta_1 = 0)
+    double* f0 = first ? p4[0] : p4[(k - 2) & 3];
+    StencilCall c = make_call(g, sl, mode, ncomp, EPI_PCG_M, f0, k1, k2, k3, bb, w);
+    c.u = view(g, sl, H_Z, f0);
+    c.u2 = first ? FieldV{} : view(g, sl, H_W, wb[(k - 1) & 1]);
+    c.u3 = first ? FieldV{} : view(g, sl, H_P, p4[(k - 1) & 3]);
     c.ev = ev[si];
-    c.ea.out = off(zb[b2], sl);
-    c.ea.out2 = off(pb[b2], sl);
-    c.ea.out3 = off(wb[b2], sl);
+    c.ea.out = nullptr;
+    c.ea.out2 = off(p4[k & 3], sl);
+    c.ea.out3 = off(wb[k & 1], sl);
     c.ea.x = off(x, sl);
     c.ea.dinv = off(d, sl);
     if (mode == STS_MODE_ISO) {   // metric-folded coefficients (the k1 halo planes stay raw)
@@ -1234,11 +1237,12 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
   auto iteration_m = [&](int k, cudaStream_t is) {
     k_cur = k;
     if (needs_halos(g)) g->comm_global += 1;
-    const int a = (k - 1) & 1;
     const FinRed* fs = (g->comm || sb_s > 4096) ? nullptr : &fin_m;
     int nbs;
-    if (k == 1) nbs = sweep(g, {{H_Z, zb[0], ncomp}}, is, make_m, fs);
-    else nbs = sweep(g, {{H_Z, zb[a], ncomp}, {H_W, wb[a], ncomp}, {H_P, pb[a], ncomp}}, is, make_m, fs);
+    if (k == 1) nbs = sweep(g, {{H_Z, p4[0], ncomp}}, is, make_m, fs);
+    else
+      nbs = sweep(g, {{H_Z, p4[(k - 2) & 3], ncomp}, {H_W, wb[(k - 1) & 1], ncomp}, {H_P, p4[(k - 1) & 3], ncomp}},
+                  is, make_m, fs);
     if (!fs) {
       Timed t(g, STS_K_PCG_REDUCE, is);
       launch_pcg_reduce(partials, pstride, nbs, ncomp, 4, sums, g->comm ? PH_NONE : PH_M, sc, rtol2, is, g->d_red2,
@@ -1301,6 +1305,9 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
 
   auto* hsc = reinterpret_cast<PcgScal*>(g->h_pinned);
   const bool device_loop = g->graphs && !g->timing && g->comm == nullptr;
+  // iterations k >= 4 repeat with this period (the buffer roles): the merged iteration's
+  // p buffers rotate by k % 4, the two-pass iteration's by k % 2
+  const int cycle = merged ? 4 : 2;
   // (cudaGraphExecDestroy synchronizes the device: completed loop graphs are released in
   // bulk, rarely, instead of once per solve)
   if (g->retired_execs.size() >= 64) reap_execs(g, false);
@@ -1340,8 +1347,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
       const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
       STS_CUDA(cudaStreamBeginCaptureToGraph(is, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
       capturing = true;
-      iteration(4, is);
-      iteration(5, is);
+      for (int k = 4; k < 4 + cycle; ++k) iteration(k, is);
       launch_pcg_continue(h, sc, ncomp, body_count, true, is);
       g->launches += 1;
       capturing = false;
@@ -1420,7 +1426,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
       const int nb = std::min(batch, kmax - launched);
       for (int it = 0; it < nb;) {
         const int k = launched + it + 1;
-        if (pair_graph && !pair_failed && k >= 4 && (k % 2) == 0 && it + 2 <= nb) {
+        if (pair_graph && !pair_failed && k >= 4 && (k % cycle) == 0 && it + cycle <= nb) {
           if (!pair_exec) {
             const long long l0 = g->launches, cl0 = g->comm_local, cg0 = g->comm_global;
             cudaGraph_t graph = nullptr;
@@ -1428,8 +1434,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
             try {
               STS_CUDA(cudaStreamBeginCapture(is, cudaStreamCaptureModeThreadLocal));
               capturing = true;
-              iteration(k, is);
-              iteration(k + 1, is);
+              for (int j = 0; j < cycle; ++j) iteration(k + j, is);
               capturing = false;
               STS_CUDA(cudaStreamEndCapture(is, &graph));
               STS_CUDA(cudaGraphInstantiate(&pair_exec, graph, 0));
@@ -1457,7 +1462,7 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
           g->launches += pair_launches;
           g->comm_local += pair_local;
           g->comm_global += pair_global;
-          it += 2;
+          it += cycle;
         } else {
           iteration(k, is);
           it += 1;
@@ -1479,7 +1484,10 @@ static bool pcg_core(sts_grid* g, int mode, int ncomp, const double* un, double*
   }
   {
     Timed t(g, STS_K_PCG_XFINAL, st);
-    launch_pcg_xfinal(ncomp, (long long)N, cs, x, pb[0], pb[1], sc, st);
+    // p_k in pk[k % 4] (the two-pass iteration's p ping-pongs: its pattern repeats)
+    const double* pk[4] = {merged ? p4[0] : pb[0], merged ? p4[1] : pb[1], merged ? p4[2] : pb[0],
+                           merged ? p4[3] : pb[1]};
+    launch_pcg_xfinal(ncomp, (long long)N, cs, x, pk, sc, st);
   }
   launch_publish(reinterpret_cast<const double*>(sc), npub, g->d_pinned, st);
   g->launches += 1;

@@ -41,7 +41,7 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     s.flags = 0;                           // (kmax was set by launch_pcg_init)
     s.xm = X_NORMAL;
     s.xmf = X_FIN_ONE;
-    s.cxp = s.cxz = s.axp = 0.0;
+    s.cxp = s.cxz = s.axp = s.bprev = 0.0;
     s.nskip = s.ncatch = 0;
     s.done = (s.rz <= s.thresh) ? 1 : 0;   // DESIGN R8: already converged -> 0 iterations
     s.beta = 0.0;
@@ -88,7 +88,8 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
     }
     s.pAp = sums[c * nq + 1];
     if (!(s.pAp > 0.0) || !isfinite(s.pAp) || !isfinite(rz)) return pcg_breakdown(s);
-    const double a_prev = s.ax, b_prev = s.beta;   // alpha_{k-1}, beta_k (used by this pass)
+    const double a_prev = s.ax;            // alpha_{k-1} (used by this pass)
+    s.bprev = s.beta;                      // beta_k: the next pass's p_{k-1} coefficient
     s.alpha = rz / s.pAp;
     s.rz_old = rz;
     s.rz = rz - 2.0 * s.alpha * sums[c * nq + 2] + s.alpha * s.alpha * sums[c * nq + 3];
@@ -114,8 +115,8 @@ __device__ inline void pcg_phase(const double* sums, int c, int nq, int phase, P
       }
     } else if (mk == X_SKIP) {
       s.xm = X_CATCHUP;
-      s.cxz = a_prev / b_prev;
-      s.cxp = s.alpha + s.cxz;
+      s.cxp = s.alpha;                     // x_{k+1} = x_{k-1} + alpha_k p_k + alpha_{k-1} p_{k-1}
+      s.cxz = a_prev;
       s.ncatch += 1;
     } else if (s.beta >= X_SKIP_BETA) {
       s.xm = X_SKIP;

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   // 1/g3 of the vertex rows j0-1 .. j0+XJ-1 (row vj of a warp and the one above it)
   // and the PCG scalars beta_k, alpha_{k-1}
   // (merged PCG: the x mode of this pass and its catch-up coefficients, pcg.cuh)
-  __shared__ double sg3[XJ + 1], sbx[4];
+  __shared__ double sg3[XJ + 1], sbx[5];
   __shared__ int sxm;
   if (tid <= XJ) {
     const int r = j0 - 1 + tid;
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
     sbx[1] = kPcg ? c.ea.sc[0].ax : 0.0;
     sbx[2] = (kM && kPcg) ? c.ea.sc[0].cxp : 0.0;
     sbx[3] = (kM && kPcg) ? c.ea.sc[0].cxz : 0.0;
+    sbx[4] = (kM && kPcg) ? c.ea.sc[0].bprev : 0.0;
     sxm = (kM && kPcg) ? c.ea.sc[0].xm : X_NORMAL;
   }
   if (tid == 0) {
@@ -254,8 +255,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   // merged PCG (kM): fields zold, wold, pold; z = zold - ax wold, source p = z + beta pold
   constexpr bool kP = (EPI == EPI_PCG_S);
   constexpr int PF = kM ? 2 * U_FIELD : U_FIELD;    // pold field offset
+  // merged (fields p_{k-2}, w_{k-1}, p_{k-1}): z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1}
   auto zof = [&](const double* S, int o) {
-    if (kM && !first) return fma(-ax, S[U_FIELD + o], S[o]);
+    if (kM && !first) return fma(-ax, S[U_FIELD + o], fma(-sbx[4], S[o], S[PF + o]));
     return S[o];
   };
   auto usums = [&](const double* S, double& Su, double& Tu, double& Fu, double& un, double& pon, double& zn) {
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       if (!first && xm != X_SKIP && own && p >= ib && p < ie) {
         const double* Ox = S + Lay::O + OW_X * O_PART + vj * XK + vk + se;
         double xn = fma(xm == X_CATCHUP ? sbx[2] : ax, H.po, *Ox);
-        if (xm == X_CATCHUP) xn = fma(-sbx[3], S[o11], xn);
+        if (xm == X_CATCHUP) xn = fma(sbx[3], S[o11], xn);   // + alpha_{k-2} p_{k-2} (field 0)
         __stcs(c.ea.x + (long long)p * G.plane + coff, xn);
       }
     }
@@ -415,7 +417,6 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           // streaming stores (evict-first in L2): the outputs are read again only by the
           // next pass, after far more than L2 has streamed through; L2 keeps the input
           // halo rows the neighbouring tiles re-read instead
-          __stcs(c.ea.out + gi, zc);
           __stcs(c.ea.out2 + gi, uc);
           __stcs(c.ea.out3 + gi, wk);
           // (x of this plane was updated when its slot landed, above)

@@ -177,11 +177,12 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 
   // PCG scalars of this iteration, broadcast from shared memory (keeps them out of registers)
   // (merged PCG: each component's x mode of this pass and catch-up coefficients, pcg.cuh)
-  __shared__ double sbeta[NC], sax[NC], scxp[NC], scxz[NC];
+  __shared__ double sbeta[NC], sax[NC], scxp[NC], scxz[NC], sbp[NC];
   __shared__ int sxm[NC];
   if (tid < NC) {
     sbeta[tid] = kP ? c.ea.sc[tid].beta : 0.0;
     sax[tid] = kP ? c.ea.sc[tid].ax : 0.0;
+    sbp[tid] = (kM && kP) ? c.ea.sc[tid].bprev : 0.0;
     scxp[tid] = (kM && kP) ? c.ea.sc[tid].cxp : 0.0;
     scxz[tid] = (kM && kP) ? c.ea.sc[tid].cxz : 0.0;
     sxm[tid] = (kM && kP) ? c.ea.sc[tid].xm : X_NORMAL;
@@ -207,11 +208,11 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
       if constexpr (kF) {
         double* S = ring + slot * Lay::SLOT;
-        // p_k = (zold - alpha wold) + beta pold over wold; zold stays raw (the own cell's
-        // z_k = p_k - beta pold is re-formed by its consumer, and the x catch-up reads the
-        // raw z_{k-1})
+        // fields p_{k-2}, w_{k-1}, p_{k-1}: z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1},
+        // p_k = z_k + beta_k p_{k-1} over w_{k-1}; p_{k-2} stays (the x catch-up reads it), the
+        // own cell's z_k = p_k - beta_k p_{k-1} is re-formed by its consumer
         auto form = [&](int o, int q) {
-          const double z = fma(-sax[q], S[o + Lay::FS], S[o]);
+          const double z = fma(-sax[q], S[o + Lay::FS], fma(-sbp[q], S[o], S[o + 2 * Lay::FS]));
           S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
         };
 #pragma unroll
@@ -325,8 +326,9 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   const int dkm = kmw_box ? Lay::DB + S_MAIN + 0 * S_W + (tj + 1) * 2 + 1 : dc - 1;
   const int dkp = kpw_box ? Lay::DB + S_MAIN + 1 * S_W + (tj + 1) * 2 : dc + 1;
   // merged PCG: z_k at a staged position (field 0 zold, field 1 wold)
+  // (fields p_{k-2}, w_{k-1}, p_{k-1}: z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1})
   auto zm = [&](const double* S, int o, int q) {
-    if constexpr (kP && !kF) return fma(-sax[q], S[o + Lay::FS], S[o]);
+    if constexpr (kP && !kF) return fma(-sax[q], S[o + Lay::FS], fma(-sbp[q], S[o], S[o + 2 * Lay::FS]));
     return S[o];
   };
   // source value at (field-0 offset o, d offset od): PCG S-pass p = r d + beta pold
@@ -360,7 +362,8 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       if constexpr (kP) return fma(sbeta[q], po, z * dd);
       return z * dd;
     } else if constexpr (kM) {
-      if constexpr (kP) return fma(sbeta[q], po, fma(-sax[q], dd, z));
+      // (z: p_{k-2}, po: p_{k-1}, dd: w_{k-1}) -> p_k = z_k + beta_k p_{k-1}
+      if constexpr (kP) return fma(sbeta[q], po, fma(-sax[q], dd, fma(-sbp[q], z, po)));
       return z;
     }
     return z;
@@ -562,15 +565,14 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           C.z[q] = zk;
           if (!skip[q]) {
             const long long go = gi + q * cs;
-            __stcs(o1 + go, zk);
             __stcs(o2 + go, u0);
             if constexpr (kP) {
               // x in pairs (pcg.cuh): x_k = x_{k-1} + alpha_{k-1} p_{k-1}; skipped; or the
-              // catch-up x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (the raw staged z_{k-1})
+              // catch-up x_k = x_{k-2} + alpha_{k-1} p_{k-1} + alpha_{k-2} p_{k-2} (both staged)
               const int m = sxm[q];
               if (m != X_SKIP) {
                 double xn = fma(m == X_CATCHUP ? scxp[q] : sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
-                if (m == X_CATCHUP) xn = fma(-scxz[q], S[oq], xn);
+                if (m == X_CATCHUP) xn = fma(scxz[q], S[oq], xn);   // + alpha_{k-2} p_{k-2} (field 0)
                 __stcs(ox + go, xn);
               }
             }

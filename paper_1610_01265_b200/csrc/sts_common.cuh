@@ -300,11 +300,13 @@ struct PcgScal {
   double rz, rz_old, pAp, alpha, beta, thresh;
   double ax;        // alpha of the last completed iteration, not yet applied to x (deferred x update;
                     // the merged iteration also applies it to z)
-  // merged iteration, x updated every other pass (DESIGN.md §5.3 "x in pairs"): the pass's
-  // x mode xm -- X_NORMAL: x_k = x_{k-1} + ax p_{k-1}; X_SKIP: x not touched;
-  // X_CATCHUP: x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (p_{k-2} = (p_{k-1} - z_{k-1}) / beta_{k-1});
+  // merged iteration: z is not stored -- the pass forms
+  //   p_k = (1 + beta_k) p_{k-1} - bprev p_{k-2} - ax w_{k-1},  bprev = beta_{k-1}
+  // -- and x is updated every other pass ("x in pairs"): the pass's x mode xm --
+  // X_NORMAL: x_k = x_{k-1} + ax p_{k-1}; X_SKIP: x not touched;
+  // X_CATCHUP: x_k = x_{k-2} + cxp p_{k-1} + cxz p_{k-2} (cxp = alpha_{k-1}, cxz = alpha_{k-2});
   // xmf / axp: what the final pass still owes x after the last iteration (X_FIN_*)
-  double cxp, cxz, axp;
+  double cxp, cxz, axp, bprev;
   int done, iters;
   int flags;        // PCG_BREAKDOWN (p.A p <= 0 or a non-finite scalar: A not SPD / NaN input), PCG_KMAX
   int kmax;         // iteration limit (set by launch_pcg_init): reaching it stops the component
@@ -313,10 +315,10 @@ struct PcgScal {
 };
 enum { X_NORMAL = 0, X_SKIP = 1, X_CATCHUP = 2 };
 enum { X_FIN_ONE = 0, X_FIN_TWO = 4, X_FIN_PREV = 5 };   // final x += ax p_k | + axp p_{k-1} | axp p_{k-1} only
-// a pass skips the x update only if the next pass's catch-up divides by a beta at least this
-// large (its rounding is amplified by ~1 + 1/beta; CG's beta is ~0.8-1 in slow convergence)
+// the merged pass skips its x update (then the next one catches up) when beta_{k+1} is at
+// least this (the catch-up reads p_{k-2} staged: no division, any beta >= 0 works)
 #ifndef STS_X_SKIP_BETA   // (A-B: a value > 1 disables the skipped x updates)
-#define STS_X_SKIP_BETA 0.1
+#define STS_X_SKIP_BETA 0.0
 #endif
 constexpr double X_SKIP_BETA = STS_X_SKIP_BETA;
 constexpr int PCG_BREAKDOWN = 1;
@@ -428,8 +430,8 @@ void launch_pcg_pnew(int ncomp, long long n, long long cstride, double* pnew, co
 int launch_pcg_rupdate(int ncomp, long long n, long long cstride, double* r, double* z, const double* y,
                         const double* d, const PcgScal* sc, double* partials, long long pstride,
                         const FinRed& fin, cudaStream_t st);
-// x += ax p[iters % 2] for components with iters > 0
-void launch_pcg_xfinal(int ncomp, long long n, long long cstride, double* x, const double* p0, const double* p1,
+// the final x update (PcgScal::xmf): p_k in pk[k % 4]
+void launch_pcg_xfinal(int ncomp, long long n, long long cstride, double* x, const double* const pk[4],
                        const PcgScal* sc, cudaStream_t st);
 
 // pointwise / auxiliary kernels (aux.cu)
