@@ -32,6 +32,7 @@ def build(force=False, verbose=True, out=None, defines=()):
     """Compile the library (out / defines: A-B variants of the compile-time knobs, e.g.
     defines=("ISO_RASTER_H=0",), out=".../libsts_b200_v.so"; loaded with STS_LIB=path)."""
     OUTP = out or OUT
+    force = force or out is not None   # (a variant always reflects its defines)
     if not force and os.path.exists(OUTP):
         t = os.path.getmtime(OUTP)
         if all(os.path.getmtime(d) <= t for d in DEPS):

@@ -73,8 +73,15 @@ struct IsoTile {
 #ifndef ISO_RASTER_H     // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ISO_RASTER_H 0
 #endif
-__host__ __device__ constexpr int iso_rows(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? ISO_M3_ROWS : 7; }
-__host__ __device__ constexpr int iso_minb(int epi, int nc) { return (epi == EPI_PCG_M && nc == 3) ? 1 : 2; }
+#ifndef ISO_D3_ROWS      // rows of the 3-component RKL2 deviation stage (> 7: one CTA per SM)
+#define ISO_D3_ROWS 7
+#endif
+__host__ __device__ constexpr int iso_rows(int epi, int nc) {
+  return (epi == EPI_PCG_M && nc == 3) ? ISO_M3_ROWS : ((epi == EPI_RKL2_DSTAGE && nc == 3) ? ISO_D3_ROWS : 7);
+}
+__host__ __device__ constexpr int iso_minb(int epi, int nc) {
+  return (epi == EPI_PCG_M && nc == 3) ? 1 : ((epi == EPI_RKL2_DSTAGE && nc == 3 && ISO_D3_ROWS > 7) ? 1 : 2);
+}
 
 template <int EPI, int NC>
 struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
