@@ -544,7 +544,8 @@ def measure_device(G, inp, ratio, args, ws, dev, ncells_local, ncells_total):
 def config_block(args, gg, ratio, ws, info, ncells_total, nvirt):
     return {"workload": args.config, "shape": list(gg.shape), "cells": ncells_total,
             "dt_over_dt_exp": ratio, "pcg_rtol": RTOL,
-            "parallelism": f"r-slab x{ws}" + (f" (x{nvirt} virtual slabs per GPU)" if nvirt > 1 else ""),
+            "parallelism": f"r-slab x{ws}" + (f" (x{nvirt} virtual slabs per GPU)" if nvirt > 1 else "") +
+                           (", halo exchange overlapped with interior planes" if args.halo_overlap else ""),
             "l2": f"inputs larger than L2 ({ncells_total * 8 / 1e9:.2f} GB per field)" if
             ncells_total * 8 > 126e6 else "inputs fit L2 (no flush)",
             "stages_cond": info["s_cond"], "pcg_iters_cond": info["it_cond"],
@@ -567,6 +568,8 @@ def main():
     ap.add_argument("--ratios", default=None,
                     help="comma-separated dt/dt_exp values: one device-timed JSON line each (e.g. the "
                          "configs[3] sweep 10,100,1000); skips the e2e and CPU legs")
+    ap.add_argument("--halo-overlap", action="store_true",
+                    help="decomposed grids: interior planes during the halo exchange, boundary planes after")
     ap.add_argument("--virtual", type=int, default=1,
                     help="emulate an N-way r-slab decomposition on each GPU (halo exchange through halo "
                          "buffers, the multi-GPU schedule) to measure its overhead")
@@ -593,6 +596,7 @@ def main():
     cfg = W.make_config(args.config, device=dev, shape=shape, slab=(i0, nl) if ws > 1 else None)
     gg = cfg["global_grid"]
     G = sts.Grid.from_grid(gg, i0=i0, nl=nl, n_virtual=args.virtual, device=lrank)
+    G.set_halo_overlap(args.halo_overlap)
     if ws > 1:
         import torch.distributed as dist
         obj = [sts.nccl_unique_id() if rank == 0 else None]

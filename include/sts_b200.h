@@ -222,6 +222,14 @@ int sts_grid_set_pcg_merged(sts_grid* g, int enable);
  * three solution-sized arrays instead of four.  0: Fig. 2 as printed.
  */
 int sts_grid_set_rkl2_deviation(sts_grid* g, int enable);
+/*
+ * Halo schedule of decomposed grids (virtual slabs or NCCL ranks).
+ * enable != 0: every stencil pass computes the interior planes while the neighbour
+ * planes are exchanged, then the two boundary planes in their own one-plane launches;
+ * 0 (the default): the pass waits for the exchange and is ONE launch per slab (measured
+ * faster on B200: a one-plane launch of the TMA pipeline costs more than the exchange).
+ */
+int sts_grid_set_halo_overlap(sts_grid* g, int enable);
 int sts_grid_timing_reset(sts_grid* g);
 int sts_grid_timing(sts_grid* g, int kind, long long* count, double* ms);
 

@@ -687,15 +687,21 @@ static std::vector<Range> sweep_ranges(const sts_grid* g, bool overlap) {
 template <class Make>
 static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Make make,
                  const FinRed* fin = nullptr) {
-  const bool overlap = needs_halos(g) && xs.size() > 0;
+  // halo exchange on the communication stream; with halo_overlap the interior planes are
+  // computed meanwhile and the boundary planes after it (one-plane launches), else the
+  // exchange is waited for and each slab is ONE launch (the one-plane
+  // launches cost more than the exchange they hide)
+  const bool exch = needs_halos(g) && xs.size() > 0;
+  const bool overlap = exch && g->halo_overlap;
   cudaStream_t cst = nullptr;
-  if (overlap) {
+  if (exch) {
     g->comm_local += 1;
     cst = comm_stream(g);
     STS_CUDA(cudaEventRecord(g->ev_a, st));
     STS_CUDA(cudaStreamWaitEvent(cst, g->ev_a, 0));
     for (const Xch& x : xs) exchange(g, x.slot, x.arr, x.ncomp, cst);
     STS_CUDA(cudaEventRecord(g->ev_b, cst));
+    if (!overlap) STS_CUDA(cudaStreamWaitEvent(st, g->ev_b, 0));
   }
   const std::vector<Range> ranges = sweep_ranges(g, overlap);
   std::vector<StencilCall> calls;
@@ -728,7 +734,7 @@ static int sweep(sts_grid* g, std::initializer_list<Xch> xs, cudaStream_t st, Ma
 template <class Make>
 static int sweep_blocks(sts_grid* g, bool has_x, Make make) {
   int pb = 0;
-  for (const Range& r : sweep_ranges(g, needs_halos(g) && has_x)) {
+  for (const Range& r : sweep_ranges(g, needs_halos(g) && has_x && g->halo_overlap)) {
     StencilCall c = make(r.si);
     c.ib = r.ib;
     c.ie = r.ie;
@@ -1705,6 +1711,13 @@ int sts_grid_set_pcg_merged(sts_grid* g, int enable) {
   return guard([&] {
     STS_REQUIRE(g, "NULL grid");
     g->pcg_merged = enable != 0;
+  });
+}
+
+int sts_grid_set_halo_overlap(sts_grid* g, int enable) {
+  return guard([&] {
+    STS_REQUIRE(g, "NULL grid");
+    g->halo_overlap = enable != 0;
   });
 }
 

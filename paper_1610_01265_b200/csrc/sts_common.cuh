@@ -183,6 +183,7 @@ struct sts_grid {
   bool graphs = true;                   // CUDA-graph replay of PCG iteration pairs (sts_grid_set_graphs)
   bool pcg_merged = true;               // one-pass PCG iteration where eligible (sts_grid_set_pcg_merged)
   bool rkl2_dev = true;                 // RKL2 stages in deviation form where eligible (sts_grid_set_rkl2_deviation)
+  bool halo_overlap = false;            // interior / boundary split of the passes (sts_grid_set_halo_overlap)
   cudaStream_t graph_stream = nullptr;  // non-blocking stream for capture / replay
   cudaEvent_t ev_c = nullptr;
   // per-kernel-class event timing (sts_grid_set_timing)

@@ -65,6 +65,7 @@ def lib():
         "sts_grid_set_graphs": (I, [P, I]),
         "sts_grid_set_pcg_merged": (I, [P, I]),
         "sts_grid_set_rkl2_deviation": (I, [P, I]),
+        "sts_grid_set_halo_overlap": (I, [P, I]),
         "sts_grid_timing_reset": (I, [P]),
         "sts_grid_timing": (I, [P, I, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(D)]),
         "sts_nccl_unique_id": (I, [P, ctypes.c_size_t]),
@@ -241,6 +242,11 @@ class Grid:
     def set_rkl2_deviation(self, enable=True):
         """RKL2 stages 2..s-1 on the deviation D_j = Y_j - Y0 (default) or on Y_j as Fig. 2 prints them."""
         _check("sts_grid_set_rkl2_deviation", lib().sts_grid_set_rkl2_deviation(self._h, int(bool(enable))))
+
+    def set_halo_overlap(self, enable=True):
+        """Decomposed grids: overlap the halo exchange with the interior planes (one-plane
+        boundary launches) or wait for it and run one launch per slab (default)."""
+        _check("sts_grid_set_halo_overlap", lib().sts_grid_set_halo_overlap(self._h, int(bool(enable))))
 
     def timing_reset(self):
         _check("sts_grid_timing_reset", lib().sts_grid_timing_reset(self._h))

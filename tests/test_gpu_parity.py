@@ -354,15 +354,19 @@ def test_be_pcg_degenerate(dev):
 
 
 # ---------------------------------------------------------------- decomposition emulation
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("nv", [2, 3, 7])
-def test_virtual_slabs_match_single_domain(dev, nv):
+def test_virtual_slabs_match_single_domain(dev, nv, overlap):
     """n_virtual r-slabs exchange boundary planes through halo buffers exactly
-    like the multi-GPU path; per-cell arithmetic is identical -> bitwise equal
-    operator / RKL2, PCG within rounding of its dot products."""
+    like the multi-GPU path -- waited for (one launch per slab, the default) or
+    overlapped with the interior planes (one-plane boundary launches); per-cell
+    arithmetic is identical -> bitwise equal operator / RKL2, PCG within rounding of
+    its dot products."""
     cfg = W.make_config("c1_spitzer64", shape=(21, 19, 70))
     g = cfg["grid"]
     G1 = sts().Grid.from_grid(g)
     Gv = sts().Grid.from_grid(g, n_virtual=nv)
+    Gv.set_halo_overlap(overlap)
     T = cfg["T"].to(dev)
     b = cfg["b"].to(dev)
     k = G1.face_kappa_spitzer(T, cfg["kappa0"], cfg["T_cut"])
@@ -381,6 +385,13 @@ def test_virtual_slabs_match_single_domain(dev, nv):
     kv = [f.to(dev) for f in cv["visc_faces"]]
     rho, v = cv["rho"].to(dev), cv["v"].to(dev)
     assert torch.equal(G1.op_apply("iso", v, kv, None, rho), Gv.op_apply("iso", v, kv, None, rho))
+    dv = G1.dt_euler("iso", kv, None, rho)
+    sv = sts().rkl2_num_stages(300 * dv, dv)
+    assert torch.equal(G1.rkl2_advance("iso", v, kv, None, rho, 300 * dv, sv),
+                       Gv.rkl2_advance("iso", v, kv, None, rho, 300 * dv, sv))
+    y1, j1 = G1.be_pcg_solve("iso", v, kv, None, rho, 300 * dv, 1e-12, 10000)
+    yv, jv = Gv.be_pcg_solve("iso", v, kv, None, rho, 300 * dv, 1e-12, 10000)
+    assert all(abs(a - b) <= 1 for a, b in zip(j1, jv)) and rel_l2(cpu(yv), cpu(y1)) <= 1e-12
 
 
 # ---------------------------------------------------------------- TMA vs cp.async kernels
