@@ -29,8 +29,10 @@
 // Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
 // deviation form D_j = Y_j - Y0), the PCG initial residual with the Jacobi diagonal,
 // the two-pass PCG S-pass  p = z + beta pold, x += ax pold, y = A p, partial p.y, and
-// the merged one-pass PCG iteration (z = zold - ax wold, p = z + beta pold, y = A p,
-// w = d y, four partial sums; Fig. 1 reorganised).
+// the merged one-pass PCG iteration (from staged p_{k-2}, w_{k-1}, p_{k-1}:
+// z = (p_{k-1} - beta_{k-1} p_{k-2}) - ax w_{k-1}, p = z + beta p_{k-1}, y = A p, w = d y,
+// four partial sums, x updated every other pass; Fig. 1 reorganised,
+// DESIGN.md §5.3).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
           if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);   // x_k = x_{k-1} + alpha_{k-1} p_{k-1}
           part += uc * y;
         } else if constexpr (kM) {
-          // y_k = A p_k, w_k = d y_k; z_k, p_k, w_k to the other buffers, x in place;
+          // y_k = A p_k, w_k = d y_k; p_k, w_k to the next buffers (z is not stored);
           // partials r_k.z_k = z_k^2 / d, p_k.y_k, z_k.y_k, w_k.y_k
           const double y = WV * uc - c.ea.dt * Lu;
           // the Jacobi diagonal A_ii = wV - dt L_ii of the R0 pass (same arithmetic), d = 1/A_ii

@@ -21,8 +21,9 @@
 // Epilogues: F, RKL2 first stage / stage recurrence (Fig. 2, also in
 // deviation form D_j = Y_j - Y0), the PCG initial residual (R0), the two-pass PCG
 // S-pass, and the merged one-pass PCG iteration (Fig. 1 reorganised,
-// DESIGN.md §5.3): z = zold - alpha wold, p = z + beta pold, x += alpha pold,
-// y = A p, w = d y and the four partial sums.  Passes other than the merged one take
+// DESIGN.md §5.3): from staged p_{k-2}, w_{k-1}, p_{k-1},
+// z = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha w_{k-1}, p = z + beta p_{k-1}, y = A p,
+// w = d y, the four partial sums, x updated every other pass.  Passes other than the merged one take
 // the own column's r-neighbours from registers prefetched two planes ahead; the
 // merged pass takes the r-up neighbour from the next plane's slot instead.
 #include "sts_common.cuh"
