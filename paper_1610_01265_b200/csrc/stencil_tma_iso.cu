@@ -135,10 +135,10 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
 }  // namespace
 
 struct IsoTmaArgs {
-  CUtensorMap src[3];     // staged sources (u | r, pold | zold, wold, pold), 3D (n3, n2, NC nl), box 36 x 9
-  CUtensorMap srcw[3];    // their wrap columns, box 2 x 9
+  CUtensorMap src[3];     // staged sources (u | r, pold | p_{k-2}, w_{k-1}, p_{k-1}), 3D (n3, n2, NC nl), box 36 x (IJ+2)
+  CUtensorMap srcw[3];    // their wrap columns, box 2 x (IJ+2)
   CUtensorMap k2, k3, k3w, k1, w;   // boxes 32x8, 34x7, 2x7, 32x7, 32x7
-  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x 7 (merged PCG: x, d)
+  CUtensorMap epi[3];     // epilogue operands, 3D (n3, n2, NC nl), box 32 x IJ (merged PCG: x)
   CUtensorMap dm, dmw;    // PCG S-pass: d, box 36 x 9 / its wrap columns 2 x 9
   int has_w;
 };
@@ -235,8 +235,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     }
     return;
   }
-  if (tid >= INT) {
-    if (tid != INT) return;
+  if (tid >= INT) {   // (the whole warp runs the loop; the elected lane issues)
     constexpr int nsrcf_now = ((kS || kM) && FST) ? 1 : Lay::nsrcf;
     const int cpl = (int)(G.cstride / G.plane);   // planes per component of the (whole local) array
     uint32_t bytes = nsrcf_now * NC * SBW * SBH * 8 + (K2W * K2H + K3W * K3H + OWN) * 8;
@@ -258,42 +257,57 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       if (wrapL) bytes += 2 * SBH * 8;
       if (wrapR) bytes += 2 * SBH * 8;
     }
+    // per-plane metrics, loaded one plane ahead (a load at the top of the iteration put
+    // its latency between a slot's release and its TMA issue); F2r == F3r
+    double mf1 = 0.0, mf2 = 0.0, mvr = 0.0;
+    if (ib < ie) {
+      mf1 = M.F1r[G.i0 + ib];
+      mf2 = M.F2r[G.i0 + ib];
+      mvr = M.Vr[G.i0 + ib];
+    }
     for (int p = ib; p < ie; ++p) {
       const int slot = (p - ib) % NS, n = (p - ib) / NS;
       if (n > 0) mbar_wait(empty + slot, (uint32_t)((n - 1) & 1));
       double* S = ring + slot * Lay::SLOT;
       uint64_t* bar = full + slot;
-      {  // per-plane metrics (plain stores, released by the arrive below); F2r == F3r
-        const int ig = G.i0 + p;
-        S[Lay::MT + 0] = M.F1r[ig];
-        S[Lay::MT + 1] = M.F2r[ig];
-        S[Lay::MT + 2] = M.Vr[ig];
+      const double f1 = mf1, f2 = mf2, vr = mvr;
+      if (p + 1 < ie) {
+        mf1 = M.F1r[G.i0 + p + 1];
+        mf2 = M.F2r[G.i0 + p + 1];
+        mvr = M.Vr[G.i0 + p + 1];
       }
-      fence_proxy_async();
-      mbar_expect_tx(bar, bytes);
+      if (elect_one()) {
+        // (plain stores, released by the arrive below)
+        S[Lay::MT + 0] = f1;
+        S[Lay::MT + 1] = f2;
+        S[Lay::MT + 2] = vr;
+        fence_proxy_async();
+        mbar_expect_tx(bar, bytes);
 #pragma unroll
-      for (int f = 0; f < nsrcf_now; ++f)
+        for (int f = 0; f < nsrcf_now; ++f)
 #pragma unroll
-        for (int q = 0; q < NC; ++q) {
-          const int pl = q * cpl + p;
-          double* F = S + f * Lay::FS;
-          tma3(F + q * S_MAIN, &ta.src[f], k0 - 2, j0 - 1, pl, bar);
-          if (wrapL) tma3(F + Lay::WRP + (q * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
-          if (wrapR) tma3(F + Lay::WRP + (q * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
+          for (int q = 0; q < NC; ++q) {
+            const int pl = q * cpl + p;
+            double* F = S + f * Lay::FS;
+            tma3(F + q * S_MAIN, &ta.src[f], k0 - 2, j0 - 1, pl, bar);
+            if (wrapL) tma3(F + Lay::WRP + (q * 2 + 0) * S_W, &ta.srcw[f], G.n3 - 2, j0 - 1, pl, bar);
+            if (wrapR) tma3(F + Lay::WRP + (q * 2 + 1) * S_W, &ta.srcw[f], 0, j0 - 1, pl, bar);
+          }
+        if (Lay::nd) {
+          tma3(S + Lay::DB, &ta.dm, k0 - 2, j0 - 1, p, bar);
+          if (wrapL) tma3(S + Lay::DB + S_MAIN, &ta.dmw, G.n3 - 2, j0 - 1, p, bar);
+          if (wrapR) tma3(S + Lay::DB + S_MAIN + S_W, &ta.dmw, 0, j0 - 1, p, bar);
         }
-      if (Lay::nd) {
-        tma3(S + Lay::DB, &ta.dm, k0 - 2, j0 - 1, p, bar);
-        if (wrapL) tma3(S + Lay::DB + S_MAIN, &ta.dmw, G.n3 - 2, j0 - 1, p, bar);
-        if (wrapR) tma3(S + Lay::DB + S_MAIN + S_W, &ta.dmw, 0, j0 - 1, p, bar);
-      }
-      tma3(S + Lay::K2, &ta.k2, k0, j0 - 1, p, bar);
-      tma3(S + Lay::K3, &ta.k3, k0 - 2, j0, p, bar);
-      if (wrapL) tma3(S + Lay::K3R, &ta.k3w, G.n3 - 2, j0, p, bar);
-      tma3(S + Lay::K1, &ta.k1, k0, j0, p, bar);
-      if (ta.has_w) tma3(S + Lay::WB, &ta.w, k0, j0, p, bar);
+        tma3(S + Lay::K2, &ta.k2, k0, j0 - 1, p, bar);
+        tma3(S + Lay::K3, &ta.k3, k0 - 2, j0, p, bar);
+        if (wrapL) tma3(S + Lay::K3R, &ta.k3w, G.n3 - 2, j0, p, bar);
+        tma3(S + Lay::K1, &ta.k1, k0, j0, p, bar);
+        if (ta.has_w) tma3(S + Lay::WB, &ta.w, k0, j0, p, bar);
 #pragma unroll
-      for (int q = 0; q < Lay::nepi; ++q)
-        if (!(kM && no_x[q % NC])) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+        for (int q = 0; q < Lay::nepi; ++q)
+          if (!(kM && no_x[q % NC])) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+      }
+      __syncwarp();
     }
     return;
   }

@@ -44,6 +44,23 @@ __device__ __forceinline__ void tma3(double* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// one lane of a converged warp (the isotropic producer warp runs its loop warp-wide and
+// issues from the elected lane: the TMA operands then stay in uniform registers -- a
+// single-thread producer made the compiler wrap every cp.async.bulk.tensor in an
+// ELECT / R2UR.BROADCAST loop, ~20 instructions per box, and the producer's issue
+// rate limited the merged isotropic PCG pass; ncu source page, DESIGN.md §5.4.  The
+// anisotropic producer, ~60 % busy, measured no gain from it and keeps one thread.)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
