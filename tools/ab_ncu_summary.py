@@ -4,7 +4,7 @@ import glob
 import io
 import sys
 
-CELLS = float(sys.argv[1]) if len(sys.argv) > 1 else 268435456.0
+CELLS = float(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].endswith(".csv") else 268435456.0
 for f in sorted(glob.glob("gpurun_out/abncu_*.csv")):
     lines = [ln for ln in open(f) if ln.startswith('"')]
     if not lines:
