@@ -550,15 +550,17 @@ __global__ void __launch_bounds__(FNT, (EPI == EPI_RKL2_STAGE ? 3 : 4)) aniso_fa
 constexpr int VCJ = 8, VCK = 32, VCR = VCJ + 1, VCC = VCK + 1, VCN = VCR * VCC;   // 9 x 33 cells
 __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b, FieldV k1, FieldV k2, FieldV k3,
                                                                 double* __restrict__ ev, int ic) {
-  __shared__ double cs[2][6][VCN];
+  __shared__ double cs[3][6][VCN];   // cell planes il, il+1 and the one in flight (cp.async)
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
   const int R0 = blockIdx.y * VCJ, C0 = blockIdx.x * VCK;        // padded row / col origin
   const int vlo = -1 + (int)blockIdx.z * ic;                     // vertex planes [vlo, vhi)
   const int vhi = min(vlo + ic, G.nl);
   const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3), es = (long long)(G.nl + 1) * pp;
-  // stage cell plane il (-1..nl) into ring slot sl: cells rows R0-1+r (r < 9), cols C0-1+c (c < 33)
-  auto stage = [&](int il, int sl) {
+  // stage cell plane il (-1..nl) into ring slot (il + 3) % 3 asynchronously: cells rows R0-1+r
+  // (r < 9), cols C0-1+c (c < 33); missing cells / planes are zero-filled
+  auto stage = [&](int il) {
+    const int sl = (il + 3) % 3;
     const double* src[6] = {plane_ptr(b, G, il, 0), plane_ptr(b, G, il, 1), plane_ptr(b, G, il, 2),
                             plane_ptr(k1, G, il, 0), plane_ptr(k2, G, il, 0), plane_ptr(k3, G, il, 0)};
     for (int e = tid; e < VCN; e += 256) {
@@ -568,10 +570,11 @@ __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b,
       bool ok = j >= 0 && j < G.n2;
       if (G.periodic3) k = (k % G.n3 + G.n3) % G.n3;
       else ok = ok && k >= 0 && k < G.n3;
-      const long long o = (long long)j * G.n3 + k;
+      const long long o = ok ? (long long)j * G.n3 + k : 0;
 #pragma unroll
-      for (int f = 0; f < 6; ++f) cs[sl][f][e] = (ok && src[f]) ? __ldg(src[f] + o) : 0.0;
+      for (int f = 0; f < 6; ++f) cp_async8(&cs[sl][f][e], (ok && src[f]) ? src[f] + o : ev, ok && src[f]);
     }
+    cp_async_commit();
   };
   const int vr = tid >> 5, vc = tid & 31;                        // this thread's padded vertex (R0+vr, C0+vc)
   const int jv = R0 + vr - 1;
@@ -580,18 +583,20 @@ __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b,
   const bool inrange = (R0 + vr) <= G.n2 && (C0 + vc) < (int)row;
   // cells of the vertex in the staged tile: rows vr, vr+1 ; cols vc, vc+1 (tile col c <-> global C0-1+c)
   const int o00 = vr * VCC + vc, o01 = o00 + 1, o10 = o00 + VCC, o11 = o10 + 1;
-  stage(vlo, (vlo + 2) & 1);
+  stage(vlo);
+  stage(vlo + 1);
   for (int il = vlo; il < vhi; ++il) {
-    stage(il + 1, (il + 3) & 1);
-    __syncthreads();
+    cp_async_wait_all();   // cell planes il and il+1 have landed (this thread's copies)
+    __syncthreads();       // ... everyone's; and plane il-1's slot is no longer read
+    if (il + 2 <= vhi) stage(il + 2);   // in flight during this plane's work
     const int iv = G.i0 + il;
     bool ok = inrange && kv >= 0 && kv < G.n3 && iv >= 0 && iv + 1 < G.n1g && jv >= 0 && jv + 1 < G.n2 &&
               (G.periodic3 || kv + 1 < G.n3);
     double er = 0.0, et = 0.0, ep = 0.0;
     if (ok) {
       const int kv1 = (kv + 1 < G.n3) ? kv + 1 : 0;
-      const double(&L)[6][VCN] = cs[(il + 2) & 1];
-      const double(&H)[6][VCN] = cs[(il + 3) & 1];
+      const double(&L)[6][VCN] = cs[(il + 3) % 3];
+      const double(&H)[6][VCN] = cs[(il + 4) % 3];
       const double br = 0.125 * ((L[0][o00] + L[0][o01]) + (L[0][o10] + L[0][o11]) + ((H[0][o00] + H[0][o01]) + (H[0][o10] + H[0][o11])));
       const double bt = 0.125 * ((L[1][o00] + L[1][o01]) + (L[1][o10] + L[1][o11]) + ((H[1][o00] + H[1][o01]) + (H[1][o10] + H[1][o11])));
       const double bp = 0.125 * ((L[2][o00] + L[2][o01]) + (L[2][o10] + L[2][o11]) + ((H[2][o00] + H[2][o01]) + (H[2][o10] + H[2][o11])));
@@ -610,8 +615,8 @@ __global__ void __launch_bounds__(256) vertex_coef_tiled_kernel(Geo G, FieldV b,
       ev[es + e] = et;
       ev[2 * es + e] = ep;
     }
-    __syncthreads();   // the next stage() overwrites the slot of plane il
   }
+  cp_async_wait_all();
 }
 
 void launch_vertex_coef(const Geo& G, FieldV b, FieldV k1, FieldV k2, FieldV k3, double* ev, cudaStream_t st) {
@@ -1075,83 +1080,123 @@ void launch_stencil(const StencilCall& c, cudaStream_t st) {
 //   g_v(sigma) = s1 e_r + s2 e_t / r_i + s3 e_p / (r_i sin th_j),  s_a = 2 sigma_a - 1,
 // (i, j) = the cell's r / theta indices, and E_v = 1/2 (sum_sigma g_v(sigma) u_sigma)^2,
 // so L_cq = -sum over the vertices v shared by c and q of g_v(sigma_c) g_v(sigma_q).
-// A CTA owns 8 x 32 cells and marches along r; per vertex plane its threads compute the
-// 8 weights of every vertex of the tile (+ the low-side ring) once into shared memory
-// (two planes), then each cell sums its 8 vertices' 8 products into its 27 entries and
-// takes sum |L_cq| / (w V).  24 B (e) per cell streamed instead of the 48 B of b and
-// kappa plus the per-entry metric gathers of the generic kernel.  n3 >= 3 (no aliased
-// phi neighbours).
-constexpr int GJ = 8, GK = 32, GVJ = GJ + 1, GVK = GK + 1, GVC = GVJ * GVK;
+// A CTA = 8 warps x 32 lanes = one 8 x 32 block of vertices (vertex row per warp) and
+// its 7 x 31 cells; it marches along r.  Per vertex plane each thread computes the 8
+// weights of ITS vertex once (e prefetched one plane ahead), stores them for the warp
+// below through shared memory (the only CTA barrier of the plane), and takes the
+// right-hand neighbours' weights by shuffle: 8 shared loads + 16 shuffles of doubles per
+// cell and plane instead of 64 shared loads (the previous version computed all weights
+// into shared memory and was shared-memory bound, 0.13 of the copy peak).  A vertex
+// plane completes the row of the cell plane below it (entries with the plane above:
+// dz = 2, and the rest of its own plane) and opens the row of the cell plane above it
+// (entries with the plane below are complete at once, so only their |.| sum and the 9
+// own-plane partials are carried).  24 B of e per cell; bound by the FP64 pipe
+// (~115 FP64 instructions per cell) and the MIO pipe.  n3 >= 3 (no aliased phi
+// neighbours).
+constexpr int GJ = 8, GK = 32, GOJ = GJ - 1, GOK = GK - 1;
 constexpr int GNT = GJ * GK;
 
-__global__ void __launch_bounds__(GNT, 3) gersh_ev_kernel(Geo G, const double* __restrict__ ev,
+__global__ void __launch_bounds__(GNT, 2) gersh_ev_kernel(Geo G, const double* __restrict__ ev,
                                                           const double* __restrict__ w, int ib0, int ie0, int ic,
                                                           unsigned long long* dmax) {
-  __shared__ double gs[2][8][GVC];
+  __shared__ double gsm[2][8][GNT];
   const Metrics& M = G.m;
-  const int tid = threadIdx.x, tj = tid / GK, tk = tid % GK;
-  const int k0 = blockIdx.x * GK, j0 = blockIdx.y * GJ;
+  const int tid = threadIdx.x, tj = tid >> 5, tk = tid & 31;
+  const int k0 = blockIdx.x * GOK, j0 = blockIdx.y * GOJ;
   const int ib = ib0 + blockIdx.z * ic, ie = min(ib + ic, ie0);
   const long long row = ev_row(G.n3), pp = ev_plane(G.n2, G.n3), es = ev_cstride(G.nl, G.n2, G.n3);
-  // weights of the vertices of vertex plane il (between cell planes il and il+1) -> slot
-  auto weights = [&](int il, int slot) {
+  // this thread's vertex (jv, kv) = (j0 - 1 + tj, k0 - 1 + tk) and cell (j, k) = (j0 + tj, k0 + tk)
+  const int jv = j0 - 1 + tj, kv = k0 - 1 + tk;
+  const bool vin = jv >= 0 && jv + 1 < G.n2 && kv + 1 <= G.n3;   // (vertex rows between cell rows only)
+  const long long vo = (long long)(jv + 1) * row + (kv + 1);
+  const double ig3l = vin ? M.iG3[jv] : 0.0, ig3h = vin ? M.iG3[jv + 1] : 0.0;
+  const int j = j0 + tj, k = k0 + tk;
+  const bool own = tj < GOJ && tk < GOK && j < G.n2 && k < G.n3;
+  const double vtp = own ? M.Vt[j] * M.Vp[k] : 0.0;
+  auto load_e = [&](int il, double& er, double& et, double& ep) {
     const int iv = G.i0 + il;
-    for (int e = tid; e < GVC; e += GNT) {
-      const int vj = e / GVK, vk = e - vj * GVK;
-      const int jv = j0 - 1 + vj, kv = k0 - 1 + vk;      // padded entry (jv+1, kv+1)
-      double g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (iv >= 0 && iv + 1 < G.n1g && jv >= 0 && jv + 1 < G.n2 && kv + 1 <= G.n3) {
-        const long long o = (long long)(il + 1) * pp + (long long)(jv + 1) * row + (kv + 1);
-        const double er = __ldg(ev + o), et = __ldg(ev + es + o), ep = __ldg(ev + 2 * es + o);
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const int s1 = (s >> 2) & 1, s2 = (s >> 1) & 1, s3 = s & 1;
-          const double ig2 = M.iG2[iv + s1], ig3 = M.iG3[jv + s2];
-          g[s] = (s1 ? er : -er) + (s2 ? et : -et) * ig2 + (s3 ? ep : -ep) * (ig2 * ig3);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < 8; ++s) gs[slot][s][e] = g[s];
+    er = et = ep = 0.0;
+    if (vin && iv >= 0 && iv + 1 < G.n1g && il + 1 >= 0 && il + 1 <= G.nl) {
+      const long long o = (long long)(il + 1) * pp + vo;
+      er = __ldg(ev + o);
+      et = __ldg(ev + es + o);
+      ep = __ldg(ev + 2 * es + o);
     }
   };
-  const int j = j0 + tj, k = k0 + tk;
-  const bool own = j < G.n2 && k < G.n3;
+  // weights g[s], s = (s1 s2 s3) bits, of this thread's vertex in vertex plane il
+  auto weights = [&](int il, double er, double et, double ep, double g[8]) {
+    const int iv = G.i0 + il;
+    const double g2l = (iv >= 0 && iv < G.n1g) ? M.iG2[iv] : 0.0;
+    const double g2h = (iv + 1 >= 0 && iv + 1 < G.n1g) ? M.iG2[iv + 1] : 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int s1 = (s >> 2) & 1, s2 = (s >> 1) & 1, s3 = s & 1;
+      const double ig2 = s1 ? g2h : g2l, ig3 = s2 ? ig3h : ig3l;
+      g[s] = (s1 ? er : -er) + (s2 ? et : -et) * ig2 + (s3 ? ep : -ep) * (ig2 * ig3);
+    }
+  };
   double rowmax = 0.0;
-  weights(ib - 1, (ib + 1) & 1);
-  for (int il = ib; il < ie; ++il) {
-    weights(il, il & 1);
+  double cmid[9], clow = 0.0;   // the open row of the cell plane above the last vertex plane
+#pragma unroll
+  for (int q = 0; q < 9; ++q) cmid[q] = 0.0;
+  double er, et, ep;
+  load_e(ib - 1, er, et, ep);
+  for (int il = ib - 1; il < ie; ++il) {   // vertex plane il, between cell planes il and il+1
+    double g[8], gn[8];
+    weights(il, er, et, ep, g);
+    if (il + 1 < ie) load_e(il + 1, er, et, ep);   // prefetch the next plane's e
+    double* gp = gsm[il & 1][0];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) gp[s * GNT + tid] = g[s];
     __syncthreads();
-    if (own) {
-      double ent[27];
+    // the cell's 4 vertices: (a, b) = (0, 0) own, (0, 1) right (shuffle), (1, 0) below
+    // (shared memory, the next warp), (1, 1) below-right; the cell sits at octant
+    // (c2, c3) = (1 - a, 1 - b) of vertex (a, b)
+    double top[9], low[9], nmid[9];
 #pragma unroll
-      for (int q = 0; q < 27; ++q) ent[q] = 0.0;
+    for (int q = 0; q < 9; ++q) top[q] = low[q] = nmid[q] = 0.0;
 #pragma unroll
-      for (int up = 0; up < 2; ++up) {          // up = 0: the vertex plane below (cell at sigma_1 = 1)
-        const int slot = up ? (il & 1) : ((il + 1) & 1);
-        const int c1 = up ? 0 : 1;
+    for (int a = 0; a < 2; ++a) {
+      if (a == 1) {
 #pragma unroll
-        for (int a = 0; a < 2; ++a)            // vertex row tj + a: the cell sits at sigma_2 = 1 - a
-#pragma unroll
-          for (int bq = 0; bq < 2; ++bq) {     // vertex col tk + bq: sigma_3 = 1 - bq
-            const int e = (tj + a) * GVK + tk + bq;
-            const int c2 = 1 - a, c3 = 1 - bq;
-            const double gc = gs[slot][(c1 << 2) | (c2 << 1) | c3][e];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int q1 = (q >> 2) & 1, q2 = (q >> 1) & 1, q3 = q & 1;
-              ent[(q1 - c1 + 1) * 9 + (q2 - c2 + 1) * 3 + (q3 - c3 + 1)] += gc * gs[slot][q][e];
-            }
-          }
+        for (int s = 0; s < 8; ++s) g[s] = tj + 1 < GJ ? gp[s * GNT + tid + 32] : 0.0;
       }
-      double sum = 0.0;
 #pragma unroll
-      for (int q = 0; q < 27; ++q) sum += fabs(ent[q]);
+      for (int s = 0; s < 8; ++s) gn[s] = __shfl_down_sync(0xffffffffu, g[s], 1);
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double* gv = b ? gn : g;
+        const int c2 = 1 - a, c3 = 1 - b;
+        const double glo = gv[(0 << 2) | (c2 << 1) | c3];   // cell il (below the vertex plane): s1 = 0
+        const double ghi = gv[(1 << 2) | (c2 << 1) | c3];   // cell il+1 (above): s1 = 1
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int q1 = (q >> 2) & 1, q2 = (q >> 1) & 1, q3 = q & 1;
+          const int e9 = (q2 - c2 + 1) * 3 + (q3 - c3 + 1);
+          if (q1 == 0) {
+            cmid[e9] = fma(glo, gv[q], cmid[e9]);   // cell il, neighbours in plane il
+            low[e9] = fma(ghi, gv[q], low[e9]);     // cell il+1, neighbours in plane il
+          } else {
+            top[e9] = fma(glo, gv[q], top[e9]);     // cell il, neighbours in plane il+1
+            nmid[e9] = fma(ghi, gv[q], nmid[e9]);   // cell il+1, neighbours in plane il+1
+          }
+        }
+      }
+    }
+    if (il >= ib && own) {   // the row of cell (il, j, k) is complete
+      double sum = clow;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) sum += fabs(cmid[q]) + fabs(top[q]);
       const int ig = G.i0 + il;
-      const double WV = (w ? __ldg(w + (long long)il * G.plane + (long long)j * G.n3 + k) : 1.0) * M.Vr[ig] *
-                        M.Vt[j] * M.Vp[k];
+      const double WV = (w ? __ldg(w + (long long)il * G.plane + (long long)j * G.n3 + k) : 1.0) * M.Vr[ig] * vtp;
       rowmax = fmax(rowmax, sum / WV);
     }
-    __syncthreads();   // the next plane's weights overwrite the lower slot
+    clow = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      clow += fabs(low[q]);
+      cmid[q] = nmid[q];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) rowmax = fmax(rowmax, __shfl_xor_sync(0xffffffffu, rowmax, o));
@@ -1161,10 +1206,10 @@ __global__ void __launch_bounds__(GNT, 3) gersh_ev_kernel(Geo G, const double* _
 void launch_gershgorin(const StencilCall& c, unsigned long long* d_max, cudaStream_t st) {
   const Geo& G = c.geo;
   if (c.mode == STS_MODE_ANISO && c.ev && G.n3 >= 3) {
-    const int nbx = (G.n3 + GK - 1) / GK, nby = (G.n2 + GJ - 1) / GJ;
+    const int nbx = (G.n3 + GOK - 1) / GOK, nby = (G.n2 + GOJ - 1) / GOJ;
     const int np = c.ie - c.ib;
     if (np <= 0) return;
-    const int ic = choose_chunk((long long)nbx * nby, np, 148LL * 3, 1.0, 4);
+    const int ic = choose_chunk((long long)nbx * nby, np, 148LL * 2, 1.0, 4);
     gersh_ev_kernel<<<dim3(nbx, nby, (np + ic - 1) / ic), GNT, 0, st>>>(G, c.ev, c.w, c.ib, c.ie, ic, d_max);
     STS_CUDA(cudaGetLastError());
     return;

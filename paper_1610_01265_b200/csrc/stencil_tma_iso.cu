@@ -692,8 +692,15 @@ static dim3 iso_grid(const Geo& G, int ib, int ie, int rows, int minb, int* ic_o
     return dim3(0, 0, 0);
   }
   const long long tiles = (long long)nbx * nby;
-  // (long marches leave a ragged last wave: cap the chunk at 128 planes)
-  const int ic = choose_chunk(tiles, np, 148LL * per_sm, 0.5, 4, 128);
+  // (long marches leave a ragged last wave: cap the chunk at ISO_CHUNK_MAX planes; a chunk
+  // costs ISO_CHUNK_EXTRA planes of pipeline fill and r-boundary reads)
+#ifndef ISO_CHUNK_EXTRA
+#define ISO_CHUNK_EXTRA 0.5
+#endif
+#ifndef ISO_CHUNK_MAX
+#define ISO_CHUNK_MAX 128
+#endif
+  const int ic = choose_chunk(tiles, np, 148LL * per_sm, ISO_CHUNK_EXTRA, 4, ISO_CHUNK_MAX);
   *ic_out = ic;
   return dim3(nbx, nby, (np + ic - 1) / ic);
 }
@@ -708,8 +715,8 @@ template <int EPI, int NC, bool FST, bool FR>
 static void launch_iso_g(const StencilCall& c, dim3 grid, int ic, const IsoTmaArgs& ta, cudaStream_t st) {
   static std::atomic<unsigned long long> attr{0};
   ensure_smem_attr(iso_tma_kernel<EPI, NC, FST, FR>, (int)IsoLay<EPI, NC>::SMEM, attr);
-  iso_tma_kernel<EPI, NC, FST, FR>
-      <<<dim3(grid.x * grid.y * grid.z), IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
+  const unsigned nb = grid.x * grid.y * grid.z;
+  iso_tma_kernel<EPI, NC, FST, FR><<<dim3(nb), IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::SMEM, st>>>(c, ic, ta);
 }
 
 template <int EPI, int NC, bool FST>
