@@ -48,23 +48,36 @@ using namespace tma;
 
 namespace {
 
-constexpr int XJ = 8, XK = 32;              // vertex rows / cols (= consumer warps / lanes)
+// register blocking: each consumer thread owns RB vertex rows of its column (the staged
+// source rows it shares with its own vertex rows are loaded once, the vertical vertex
+// pairs inside the thread are summed in registers; only its first row goes through
+// shared memory to the warp above).  NW consumer warps -> XJ = NW RB vertex rows.
+#ifndef ANISO_RB
+#define ANISO_RB 2
+#endif
+#ifndef ANISO_NW
+#define ANISO_NW 4
+#endif
+constexpr int RB = ANISO_RB, NW = ANISO_NW;
+constexpr int XJ = NW * RB, XK = 32;         // vertex rows / cols
 constexpr int XOJ = XJ - 1, XOK = XK - 1;   // output rows / cols
-constexpr int XNT = XJ * XK;                // consumer threads
+constexpr int XNT = NW * XK;                // consumer threads
 constexpr int XTHREADS = XNT + 32;          // + producer warp
 // ring slots (packages in flight = slots - 1): TmaLay::NS, 4 (3 for the merged PCG pass)
-constexpr int UBW = 36, UBH = 9;            // staged-source box (cols x rows)
+constexpr int UBW = 36, UBH = XJ + 1;       // staged-source box (cols x rows)
 constexpr int EBW = 34;                     // vertex-coefficient box cols
 constexpr int MAXSRC = 3;                   // staged sources (PCG S-pass: z, pold; merged: zold, wold, pold)
 constexpr int MAXOWN = 4;                   // epilogue operand boxes
+constexpr int r16(int n) { return (n + 15) & ~15; }
 // slot parts (doubles); every part starts on a 128 B boundary
-constexpr int U_MAIN = 336;                 // 9 x 36 = 324 -> 336
-constexpr int U_WL = 32, U_WR = 32;         // 9 x 2 = 18 -> 32
+constexpr int U_MAIN = r16(UBH * UBW);
+constexpr int U_WL = r16(2 * UBH), U_WR = r16(2 * UBH);
 constexpr int U_FIELD = U_MAIN + U_WL + U_WR;
-constexpr int E_COMP = XJ * EBW;            // 8 x 34 = 272 (2176 B)
+constexpr int E_COMP = r16(XJ * EBW);
 constexpr int E_PART = 3 * E_COMP;
-constexpr int O_PART = XOJ * XK;            // 7 x 32 = 224
-constexpr int VBUF = 3 * XNT;               // A, B, C of one vertex plane
+constexpr int O_PART = r16(XOJ * XK);
+constexpr int VBUF = 3 * XNT;               // A, B, C of each warp's first vertex row
+static_assert(XNT > XJ + 1, "sg3 is loaded by the first XJ + 1 consumer threads");
 
 }  // namespace
 
@@ -93,7 +106,13 @@ struct TmaArgs {
 #ifndef ANISO_RASTER_H   // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ANISO_RASTER_H 0
 #endif
-constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : 3; }
+#ifndef ANISO_NS         // ring slots of the other passes
+#define ANISO_NS 4
+#endif
+#ifndef ANISO_MINB       // resident CTAs per SM of the other passes
+#define ANISO_MINB 3
+#endif
+constexpr int aniso_minb(int epi) { return epi == EPI_PCG_M ? ANISO_M_MINB : ANISO_MINB; }
 
 // epilogue operand slots
 enum { OW_YM2 = 0, OW_Y0 = 1, OW_M0 = 2 };   // RKL2 stage
@@ -114,7 +133,7 @@ struct TmaLay {
   static constexpr int O = E + E_PART;
   static constexpr int MT = O + nown * O_PART;       // per-plane metrics written by the producer
   static constexpr int SLOT = MT + 16;
-  static constexpr int NS = (EPI == EPI_PCG_M) ? ANISO_M_NS : 4;   // (the merged pass has a larger slot)
+  static constexpr int NS = (EPI == EPI_PCG_M) ? ANISO_M_NS : ANISO_NS;   // (the merged pass has a larger slot)
   static constexpr int MINB = aniso_minb(EPI);
   static constexpr size_t SMEM = (size_t)(NS * SLOT + 2 * VBUF) * sizeof(double) + 2 * NS * sizeof(uint64_t) + 128;
 };
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   if (tid == 0) {
     for (int s = 0; s < XTS; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, XJ);
+      mbar_init(empty + s, NW);
     }
     mbar_fence_init();
   }
@@ -196,7 +215,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       uint32_t bytes = nsrc_now * UBW * UBH * 8;
       if (wrapL) bytes += nsrc_now * 2 * UBH * 8;
       if (wrapR) bytes += nsrc_now * 2 * UBH * 8;
-      if (has_e) bytes += E_PART * 8;
+      if (has_e) bytes += 3 * XJ * EBW * 8;   // (E_COMP is padded to 128 B; the box is not)
       // (merged PCG: the x box is of the package's OWN plane p -- the x update uses only
       // values of plane p's slot -- the other epilogue boxes are of plane p-1)
       const bool x_here = kM && !no_x && p >= ib && p < ie;
@@ -230,202 +249,238 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   }
 
   // ======================= consumer warps =======================
+  // warp vj, lane vk: vertex rows vr = vj RB + t (t < RB) of vertex column vk; the own cell
+  // of vertex row vr is cell row j0 + vr, col k0 + vk (between vertex rows vr, vr + 1)
   const int vj = tid >> 5, vk = tid & 31;
+  const int vr0 = vj * RB;
   // references into shared memory (read where used; they hold no registers)
   const double& beta = sbx[0];
   const double& ax = sbx[1];
-  const double& ig3a = sg3[vj];       // vertex row jv = j0-1+vj
-  const double& ig3b = sg3[vj + 1];   // and jv+1 (= the own cell row j)
-  const double& ig3c = sg3[vj + 1];   // (own cells only)
-  const int j = j0 + vj, k = k0 + vk;
-  const bool own = vj < XOJ && vk < XOK && j < G.n2 && k < G.n3;
-  const long long coff = own ? (long long)j * G.n3 + k : 0;
-  const double vtpc = own ? M.Vt[j] * M.Vp[k] : 0.0;
-  // offset (within a staged field block) of the cell at tile row r (global j0-1+r)
-  // and tile col t (global k0-1+t)
-  auto uoff = [&](int r, int t) {
-    const int gk = k0 - 1 + t;                        // global phi index
-    if (per && gk == -1) return U_MAIN + r * 2 + 1;   // periodic wrap: cell n3-1
-    if (per && gk == G.n3) return U_MAIN + U_WL + r * 2;   // periodic wrap: cell 0
-    return r * UBW + (gk - ou);                       // (non-periodic col -1 / n3: OOB zeros)
+  const int k = k0 + vk;
+  const bool colok = vk < XOK && k < G.n3;
+  auto own_t = [&](int t) { return colok && vr0 + t < XOJ && j0 + vr0 + t < G.n2; };
+  const long long coff0 = (long long)(j0 + vr0) * G.n3 + k;   // own cell of row t: coff0 + t n3
+  double vtpc[RB];
+#pragma unroll
+  for (int t = 0; t < RB; ++t) vtpc[t] = own_t(t) ? M.Vt[j0 + vr0 + t] * M.Vp[k] : 0.0;
+  // offset (within a staged field block) of the cell at tile row r (global j0-1+r) and
+  // tile col c (global k0-1+c): base + r * stride (the wrap columns are stored 2 wide)
+  auto ubase = [&](int c, int& stride) {
+    const int gk = k0 - 1 + c;                        // global phi index
+    if (per && gk == -1) { stride = 2; return U_MAIN + 1; }           // periodic wrap: cell n3-1
+    if (per && gk == G.n3) { stride = 2; return U_MAIN + U_WL; }      // periodic wrap: cell 0
+    stride = UBW;
+    return gk - ou;                                   // (non-periodic col -1 / n3: OOB zeros)
   };
-  const int o00 = uoff(vj, vk), o01 = uoff(vj, vk + 1), o10 = uoff(vj + 1, vk), o11 = uoff(vj + 1, vk + 1);
+  int sa, sb;
+  const int ca = ubase(vk, sa), cb = ubase(vk + 1, sb);
+  const int oa = ca + vr0 * sa, ob = cb + vr0 * sb;   // tile row vr0, cols vk / vk+1
 
-  // in-plane 2x2 box of the source value s (PCG: z + beta pold, else u): each lane
-  // loads its column (rows vj, vj+1) and takes column vk+1 from lane vk+1 by shuffle
-  // (lane 31 loads it), halving the shared-memory loads of the march
-  // merged PCG (kM): fields zold, wold, pold; z = zold - ax wold, source p = z + beta pold
+  // in-plane 2x2 boxes of the source value s (PCG: z + beta pold, else u) of the thread's
+  // RB vertex rows: it loads its column's RB+1 source rows once and takes column vk+1 from
+  // lane vk+1 by shuffle (lane 31 loads it)
+  // merged PCG (kM): fields p_{k-2}, w_{k-1}, p_{k-1}: z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1}
   constexpr bool kP = (EPI == EPI_PCG_S);
   constexpr int PF = kM ? 2 * U_FIELD : U_FIELD;    // pold field offset
-  // merged (fields p_{k-2}, w_{k-1}, p_{k-1}): z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1}
   auto zof = [&](const double* S, int o) {
     if (kM && !first) return fma(-ax, S[U_FIELD + o], fma(-sbx[4], S[o], S[PF + o]));
     return S[o];
   };
-  auto usums = [&](const double* S, double& Su, double& Tu, double& Fu, double& un, double& pon, double& zn) {
-    double z00 = zof(S, o00), z10 = zof(S, o10);
-    double zk10 = z10;
-    double q00 = 0.0, q10 = 0.0;
-    if ((kP || kM) && !first) {
-      q00 = S[PF + o00];
-      q10 = S[PF + o10];
-      z00 = fma(beta, q00, z00);
-      z10 = fma(beta, q10, z10);
-    }
-    double z01 = __shfl_down_sync(0xffffffffu, z00, 1), z11 = __shfl_down_sync(0xffffffffu, z10, 1);
-    double q11 = 0.0, zk11 = 0.0;
-    if ((kP || kM) && !first) q11 = __shfl_down_sync(0xffffffffu, q10, 1);
-    if (kM) zk11 = __shfl_down_sync(0xffffffffu, zk10, 1);
-    if (vk == XK - 1) {
-      z01 = zof(S, o01);
-      z11 = zof(S, o11);
-      zk11 = z11;
+  // state of one cell plane carried to the next, per vertex row t: the 2x2 sums of the
+  // source, the vertex-pair sums of the vertex plane below it, the own cell's source value
+  // (pold, z), and (R0) the L_ii part of the 4 vertices above it.  Two sets, alternated
+  // by an unroll by two, so no register moves between planes.
+  // R0: L_ii = -sum over the cell's 8 vertices of W^2, W = the cell's weight in q_v =
+  // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex)
+  struct St {
+    double Su[RB], Tu[RB], Fu[RB], SA[RB], DB[RB], DC[RB], u[RB], po[RB], z[RB], ld[RB];
+  };
+  auto usums = [&](const double* S, St& H) {
+    double zl[RB + 1], zr[RB + 1], qr[RB + 1], kr[RB + 1];
+#pragma unroll
+    for (int r = 0; r <= RB; ++r) {
+      double z = zof(S, oa + r * sa);
+      const double zk = z;
+      double q = 0.0;
       if ((kP || kM) && !first) {
-        q11 = S[PF + o11];
-        z01 = fma(beta, S[PF + o01], z01);
-        z11 = fma(beta, q11, z11);
+        q = S[PF + oa + r * sa];
+        z = fma(beta, q, z);
+      }
+      zl[r] = z;
+      zr[r] = __shfl_down_sync(0xffffffffu, z, 1);
+      qr[r] = ((kP || kM) && !first) ? __shfl_down_sync(0xffffffffu, q, 1) : 0.0;
+      kr[r] = kM ? __shfl_down_sync(0xffffffffu, zk, 1) : 0.0;
+      if (vk == XK - 1) {
+        double z1 = zof(S, ob + r * sb);
+        kr[r] = z1;
+        if ((kP || kM) && !first) {
+          qr[r] = S[PF + ob + r * sb];
+          z1 = fma(beta, qr[r], z1);
+        }
+        zr[r] = z1;
       }
     }
-    Su = (z00 + z01) + (z10 + z11);
-    Tu = (z10 - z00) + (z11 - z01);
-    Fu = ig3a * (z01 - z00) + ig3b * (z11 - z10);
-    un = z11;     // own cell of this plane
-    pon = q11;    // its pold (PCG)
-    zn = zk11;    // its z (merged PCG)
+#pragma unroll
+    for (int t = 0; t < RB; ++t) {
+      H.Su[t] = (zl[t] + zr[t]) + (zl[t + 1] + zr[t + 1]);
+      H.Tu[t] = (zl[t + 1] - zl[t]) + (zr[t + 1] - zr[t]);
+      H.Fu[t] = sg3[vr0 + t] * (zr[t] - zl[t]) + sg3[vr0 + t + 1] * (zr[t + 1] - zl[t + 1]);
+      H.u[t] = zr[t + 1];    // own cell of this plane
+      H.po[t] = qr[t + 1];   // its pold (PCG)
+      H.z[t] = kr[t + 1];    // its z (merged PCG)
+    }
   };
 
   double part = 0.0, part2 = 0.0, part3 = 0.0, part4 = 0.0;
   constexpr bool kR0 = (EPI == EPI_PCG_R0);
-  // state of one cell plane carried to the next: the 2x2 sums of the source, the
-  // vertex-pair sums of the vertex plane below it, the own cell's source value (pold,
-  // z), and (R0) the L_ii part of the 4 vertices above it.  Two sets, alternated by
-  // an unroll by two, so no register moves between planes.
-  // R0: L_ii = -sum over the cell's 8 vertices of W^2, W = the cell's weight in q_v =
-  // sr er + st et ig2 + sp ep ig2 ig3 (signs from the cell's octant in the vertex)
-  struct St {
-    double Su, Tu, Fu, SA, DB, DC, u, po, z, ld;
-  };
-  St SX = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, SY = SX;
+  St SX, SY;
+#pragma unroll
+  for (int t = 0; t < RB; ++t) {
+    SX.Su[t] = SX.Tu[t] = SX.Fu[t] = SX.SA[t] = SX.DB[t] = SX.DC[t] = SX.u[t] = SX.po[t] = SX.z[t] = SX.ld[t] = 0.0;
+  }
+  SY = SX;
   const int xm = kM ? sxm : X_NORMAL;
   // plane p: Q(p) landed; L = state of cell plane p-1, H receives cell plane p's
   auto body = [&](int p, const St& L, St& H) {
     const int slot = (p - ib + 1) % XTS;
     const double* S = ring + slot * Lay::SLOT;
     mbar_wait(full + slot, (uint32_t)(((p - ib + 1) / XTS) & 1));
-    usums(S, H.Su, H.Tu, H.Fu, H.u, H.po, H.z);
+    usums(S, H);
     if constexpr (kM) {
-      // x of the own cell of plane p, from this slot alone (pcg.cuh "x in pairs"):
+      // x of the own cells of plane p, from this slot alone (pcg.cuh "x in pairs"):
       // x_k = x_{k-1} + alpha_{k-1} p_{k-1}, skipped, or the catch-up
       // x_k = x_{k-2} + cxp p_{k-1} - cxz z_{k-1} (raw staged z_{k-1})
-      if (!first && xm != X_SKIP && own && p >= ib && p < ie) {
-        const double* Ox = S + Lay::O + OW_X * O_PART + vj * XK + vk + se;
-        double xn = fma(xm == X_CATCHUP ? sbx[2] : ax, H.po, *Ox);
-        if (xm == X_CATCHUP) xn = fma(sbx[3], S[o11], xn);   // + alpha_{k-2} p_{k-2} (field 0)
-        __stcs(c.ea.x + (long long)p * G.plane + coff, xn);
+      if (!first && xm != X_SKIP && p >= ib && p < ie) {
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          if (!own_t(t)) continue;
+          const double* Ox = S + Lay::O + OW_X * O_PART + (vr0 + t) * XK + vk + se;
+          double xn = fma(xm == X_CATCHUP ? sbx[2] : ax, H.po[t], *Ox);
+          if (xm == X_CATCHUP) xn = fma(sbx[3], S[ob + (t + 1) * sb], xn);   // + alpha_{k-2} p_{k-2} (field 0)
+          __stcs(c.ea.x + (long long)p * G.plane + coff0 + (long long)t * G.n3, xn);
+        }
       }
     }
     double* vb = vbuf + (p & 1) * VBUF;
-    H.SA = H.DB = H.DC = H.ld = 0.0;
+#pragma unroll
+    for (int t = 0; t < RB; ++t) H.SA[t] = H.DB[t] = H.DC[t] = H.ld[t] = 0.0;
     if (p >= ib) {
       // vertex plane v = p-1, between cell planes p-1 (L) and p (H); e = 0 where a cell is missing
       const double* E = S + Lay::E;
-      const int ei = vj * EBW + vk + se;
-      const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
       const double ig2l = S[Lay::MT + 0], ig2h = S[Lay::MT + 1];
-      const double q = er * (H.Su - L.Su) + et * (ig2l * L.Tu + ig2h * H.Tu) + ep * (ig2l * L.Fu + ig2h * H.Fu);
-      double ldhi = 0.0;
-      if constexpr (kR0 || (kM && !ANISO_M_DREAD)) {
-        if (own) {
-          // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
-          // the own cell (j, k) sits at (st, sp) = (+,+) in vertex (vj,vk), (+,-) in (vj,vk+1),
-          // (-,+) in (vj+1,vk), (-,-) in (vj+1,vk+1)
-          const int e4[4] = {ei, ei + 1, ei + EBW, ei + EBW + 1};
-          const double st4[4] = {1.0, 1.0, -1.0, -1.0}, sp4[4] = {1.0, -1.0, 1.0, -1.0};
+      double hA[RB], hB[RB], dC[RB], ldhi[RB];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const double r_ = E[e4[t]], t_ = E[E_COMP + e4[t]], p_ = E[2 * E_COMP + e4[t]];
-            const double wl = -r_ + st4[t] * t_ * ig2l + sp4[t] * p_ * ig2l * ig3c;
-            const double wh = r_ + st4[t] * t_ * ig2h + sp4[t] * p_ * ig2h * ig3c;
-            ldhi += wl * wl;
-            H.ld += wh * wh;
+      for (int t = 0; t < RB; ++t) {
+        const int ei = (vr0 + t) * EBW + vk + se;
+        const double er = E[ei], et = E[E_COMP + ei], ep = E[2 * E_COMP + ei];
+        const double q =
+            er * (H.Su[t] - L.Su[t]) + et * (ig2l * L.Tu[t] + ig2h * H.Tu[t]) + ep * (ig2l * L.Fu[t] + ig2h * H.Fu[t]);
+        ldhi[t] = 0.0;
+        if constexpr (kR0 || (kM && !ANISO_M_DREAD)) {
+          if (own_t(t)) {
+            // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
+            // the own cell (j, k) sits at (st, sp) = (+,+) in vertex (vr,vk), (+,-) in (vr,vk+1),
+            // (-,+) in (vr+1,vk), (-,-) in (vr+1,vk+1)
+            const double ig3c = sg3[vr0 + t + 1];
+            const int e4[4] = {ei, ei + 1, ei + EBW, ei + EBW + 1};
+            const double st4[4] = {1.0, 1.0, -1.0, -1.0}, sp4[4] = {1.0, -1.0, 1.0, -1.0};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double r_ = E[e4[u]], t_ = E[E_COMP + e4[u]], p_ = E[2 * E_COMP + e4[u]];
+              const double wl = -r_ + st4[u] * t_ * ig2l + sp4[u] * p_ * ig2l * ig3c;
+              const double wh = r_ + st4[u] * t_ * ig2h + sp4[u] * p_ * ig2h * ig3c;
+              ldhi[t] += wl * wl;
+              H.ld[t] += wh * wh;
+            }
           }
         }
+        // vertex values A, B, C = q e; the horizontal pair sums/differences by shuffle
+        const double A = q * er, B = q * et, C = q * ep;
+        hA[t] = A + __shfl_down_sync(0xffffffffu, A, 1);
+        hB[t] = B + __shfl_down_sync(0xffffffffu, B, 1);
+        dC[t] = C - __shfl_down_sync(0xffffffffu, C, 1);
       }
-      // vertex values A, B, C = q e; the horizontal pair sums/differences by shuffle,
-      // the vertical pair through shared memory (the next vertex row is the next warp)
-      const double A = q * er, B = q * et, C = q * ep;
-      const double hA = A + __shfl_down_sync(0xffffffffu, A, 1);
-      const double hB = B + __shfl_down_sync(0xffffffffu, B, 1);
-      const double dC = C - __shfl_down_sync(0xffffffffu, C, 1);
-      vb[tid] = hA;
-      vb[XNT + tid] = hB;
-      vb[2 * XNT + tid] = dC;
+      // the vertical pairs: inside the thread, and through shared memory for the last
+      // row (the next vertex row is the first row of the next warp)
+      vb[tid] = hA[0];
+      vb[XNT + tid] = hB[0];
+      vb[2 * XNT + tid] = dC[0];
       // consumer warps only: the vertex plane is complete
       asm volatile("bar.sync 1, %0;\n" ::"r"(XNT) : "memory");
-      if (own) {
-        H.SA = hA + vb[tid + 32];
-        H.DB = hB - vb[XNT + tid + 32];
-        H.DC = dC + vb[2 * XNT + tid + 32];
+#pragma unroll
+      for (int t = 0; t < RB; ++t) {
+        if (!own_t(t)) continue;
+        const double nA = (t + 1 < RB) ? hA[(t + 1) % RB] : vb[tid + 32];
+        const double nB = (t + 1 < RB) ? hB[(t + 1) % RB] : vb[XNT + tid + 32];
+        const double nC = (t + 1 < RB) ? dC[(t + 1) % RB] : vb[2 * XNT + tid + 32];
+        H.SA[t] = hA[t] + nA;
+        H.DB[t] = hB[t] - nB;
+        H.DC[t] = dC[t] + nC;
       }
-      if (p >= ib + 1 && own) {
+      if (p >= ib + 1) {
         // output cell plane il = p-1 (its own values are L's)
         const int il = p - 1;
-        const double* O = S + Lay::O + vj * XK + vk + se;
         const double ig2c = S[Lay::MT + 0];                   // iG2 of plane p-1
-        const double Lu = -((L.SA - H.SA) + ig2c * (L.DB + H.DB) + ig2c * ig3c * (L.DC + H.DC));
-        const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * S[Lay::MT + 2] * vtpc;
-        const long long gi = (long long)il * G.plane + coff;
-        const double uc = L.u, poc = L.po, zc = L.z;
-        if constexpr (EPI == EPI_F) {
-          c.ea.out[gi] = Lu / WV;
-        } else if constexpr (EPI == EPI_RKL2_FIRST) {
-          const double F = Lu / WV;
-          c.ea.out2[gi] = F;
-          c.ea.out[gi] = c.ea.a0 * uc + c.ea.c0 * F;
-        } else if constexpr (EPI == EPI_RKL2_STAGE) {
-          const double F = Lu / WV;
-          c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_YM2 * O_PART] + c.ea.c2 * O[OW_Y0 * O_PART] + c.ea.c0 * F +
-                         c.ea.c1 * O[OW_M0 * O_PART];
-        } else if constexpr (EPI == EPI_RKL2_DSTAGE) {
-          const double F = Lu / WV;
-          c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_DM2 * O_PART] + c.ea.c0 * F + c.ea.c1 * O[OW_DM0 * O_PART];
-        } else if constexpr (kR0) {
-          // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
-          const double Ld = -(L.ld + ldhi);
-          const double r = c.ea.dt * Lu;
-          const double dinv = rcp_pos(WV - c.ea.dt * Ld);
-          const double z = r * dinv;
-          const double bb = WV * uc;
-          c.ea.out[gi] = r;
-          if (c.ea.out2) c.ea.out2[gi] = uc;
-          if (c.ea.out3) c.ea.out3[gi] = z;
-          c.ea.out4[gi] = dinv;
-          part += r * z;
-          part2 += bb * bb * dinv;
-        } else if constexpr (EPI == EPI_PCG_S) {
-          const double y = WV * uc - c.ea.dt * Lu;
-          c.ea.out[gi] = y;
-          c.ea.out2[gi] = uc;                                   // p_k
-          if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);   // x_k = x_{k-1} + alpha_{k-1} p_{k-1}
-          part += uc * y;
-        } else if constexpr (kM) {
-          // y_k = A p_k, w_k = d y_k; p_k, w_k to the next buffers (z is not stored);
-          // partials r_k.z_k = z_k^2 / d, p_k.y_k, z_k.y_k, w_k.y_k
-          const double y = WV * uc - c.ea.dt * Lu;
-          // the Jacobi diagonal A_ii = wV - dt L_ii of the R0 pass (same arithmetic), d = 1/A_ii
-          const double Aii = ANISO_M_DREAD ? rcp_pos(O[1 * O_PART]) : WV - c.ea.dt * (-(L.ld + ldhi));
-          const double dd = ANISO_M_DREAD ? O[1 * O_PART] : rcp_pos(Aii);
-          const double wk = dd * y;
-          // streaming stores (evict-first in L2): the outputs are read again only by the
-          // next pass, after far more than L2 has streamed through; L2 keeps the input
-          // halo rows the neighbouring tiles re-read instead
-          __stcs(c.ea.out2 + gi, uc);
-          __stcs(c.ea.out3 + gi, wk);
-          // (x of this plane was updated when its slot landed, above)
-          part += zc * zc * Aii;
-          part2 += uc * y;
-          part3 += zc * y;
-          part4 += wk * y;
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          if (!own_t(t)) continue;
+          const double ig3c = sg3[vr0 + t + 1];
+          const double* O = S + Lay::O + (vr0 + t) * XK + vk + se;
+          const double Lu = -((L.SA[t] - H.SA[t]) + ig2c * (L.DB[t] + H.DB[t]) + ig2c * ig3c * (L.DC[t] + H.DC[t]));
+          const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * S[Lay::MT + 2] * vtpc[t];
+          const long long gi = (long long)il * G.plane + coff0 + (long long)t * G.n3;
+          const double uc = L.u[t], poc = L.po[t], zc = L.z[t];
+          if constexpr (EPI == EPI_F) {
+            c.ea.out[gi] = Lu / WV;
+          } else if constexpr (EPI == EPI_RKL2_FIRST) {
+            const double F = Lu / WV;
+            c.ea.out2[gi] = F;
+            c.ea.out[gi] = c.ea.a0 * uc + c.ea.c0 * F;
+          } else if constexpr (EPI == EPI_RKL2_STAGE) {
+            const double F = Lu / WV;
+            c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_YM2 * O_PART] + c.ea.c2 * O[OW_Y0 * O_PART] + c.ea.c0 * F +
+                           c.ea.c1 * O[OW_M0 * O_PART];
+          } else if constexpr (EPI == EPI_RKL2_DSTAGE) {
+            const double F = Lu / WV;
+            c.ea.out[gi] = c.ea.mu * uc + c.ea.nu * O[OW_DM2 * O_PART] + c.ea.c0 * F + c.ea.c1 * O[OW_DM0 * O_PART];
+          } else if constexpr (kR0) {
+            // r0 = dt L u (x0 = u^n), d = 1/(wV - dt L_ii) (PC1), z0 = r0 d
+            const double Ld = -(L.ld[t] + ldhi[t]);
+            const double r = c.ea.dt * Lu;
+            const double dinv = rcp_pos(WV - c.ea.dt * Ld);
+            const double z = r * dinv;
+            const double bb = WV * uc;
+            c.ea.out[gi] = r;
+            if (c.ea.out2) c.ea.out2[gi] = uc;
+            if (c.ea.out3) c.ea.out3[gi] = z;
+            c.ea.out4[gi] = dinv;
+            part += r * z;
+            part2 += bb * bb * dinv;
+          } else if constexpr (EPI == EPI_PCG_S) {
+            const double y = WV * uc - c.ea.dt * Lu;
+            c.ea.out[gi] = y;
+            c.ea.out2[gi] = uc;                                   // p_k
+            if (!first) c.ea.x[gi] = fma(ax, poc, O[OW_X * O_PART]);   // x_k = x_{k-1} + alpha_{k-1} p_{k-1}
+            part += uc * y;
+          } else if constexpr (kM) {
+            // y_k = A p_k, w_k = d y_k; p_k, w_k to the next buffers (z is not stored);
+            // partials r_k.z_k = z_k^2 / d, p_k.y_k, z_k.y_k, w_k.y_k
+            const double y = WV * uc - c.ea.dt * Lu;
+            // the Jacobi diagonal A_ii = wV - dt L_ii of the R0 pass (same arithmetic), d = 1/A_ii
+            const double Aii = ANISO_M_DREAD ? rcp_pos(O[1 * O_PART]) : WV - c.ea.dt * (-(L.ld[t] + ldhi[t]));
+            const double dd = ANISO_M_DREAD ? O[1 * O_PART] : rcp_pos(Aii);
+            const double wk = dd * y;
+            // streaming stores (evict-first in L2): the outputs are read again only by the
+            // next pass, after far more than L2 has streamed through; L2 keeps the input
+            // halo rows the neighbouring tiles re-read instead
+            __stcs(c.ea.out2 + gi, uc);
+            __stcs(c.ea.out3 + gi, wk);
+            // (x of this plane was updated when its slot landed, above)
+            part += zc * zc * Aii;
+            part2 += uc * y;
+            part3 += zc * y;
+            part4 += wk * y;
+          }
         }
       }
     }
