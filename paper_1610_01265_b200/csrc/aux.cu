@@ -66,6 +66,63 @@ __global__ void __launch_bounds__(FK_T) face_kappa_kernel(Geo G, FieldV T, doubl
   }
 }
 
+// The same pass with two phi columns per thread (n3 even, 16 B-aligned arrays): double2
+// loads / streaming stores, the next-but-one plane prefetched (two loads in flight per
+// column pair besides the theta row), f_c evaluated once per plane (warp-uniform); the
+// phi neighbour of the pair's second column is the next lane's first (lane 31 loads it).
+constexpr int FK2_T = 128;
+__global__ void __launch_bounds__(FK2_T) face_kappa2_kernel(Geo G, FieldV T, double* __restrict__ k1,
+                                                            double* __restrict__ k2, double* __restrict__ k3,
+                                                            double kappa0, double T_cut, double fc_r0, double fc_w,
+                                                            const double* __restrict__ x1f,
+                                                            const double* __restrict__ x1c, int ic) {
+  const int k = 2 * (blockIdx.x * FK2_T + threadIdx.x), j = blockIdx.y;
+  const int ib = blockIdx.z * ic, ie = min(ib + ic, G.nl);
+  const bool in = k < G.n3;
+  const bool jp = j + 1 < G.n2, kp = G.periodic3 || k + 2 < G.n3;
+  const int kn = (k + 2 < G.n3) ? k + 2 : 0;    // (wrap to k = 0)
+  const long long col = (long long)j * G.n3 + k;
+  const int lane = threadIdx.x & 31;
+  const bool shfl_ok = lane < 31 && k + 2 < G.n3;
+  auto ld2 = [&](long long e) { return __ldg(reinterpret_cast<const double2*>(T.p + e)); };
+  // T of local plane il (il = nl: the halo plane above, or nothing at r_max)
+  auto plane = [&](int il) -> double2 {
+    if (!in || il >= ie + 1 || G.i0 + il >= G.n1g) return make_double2(0.0, 0.0);
+    if (il < G.nl) return ld2((long long)il * G.plane + col);
+    return T.hi ? *reinterpret_cast<const double2*>(T.hi + col) : make_double2(0.0, 0.0);
+  };
+  double2 Tc = plane(ib), Tn = plane(ib + 1);
+  for (int il = ib; il < ie; ++il) {
+    const double2 Tnn = plane(il + 2);
+    const long long e = (long long)il * G.plane + col;
+    const int ig = G.i0 + il;
+    const double Tk_s = __shfl_down_sync(0xffffffffu, Tc.x, 1);
+    if (in) {
+      const double Tk = shfl_ok ? Tk_s : __ldg(T.p + (long long)il * G.plane + (long long)j * G.n3 + kn);
+      const double fcc = fc_profile(x1c[ig], fc_r0, fc_w);
+      const bool rp = ig + 1 < G.n1g;
+      const double fcf = rp ? fc_profile(x1f[ig + 1], fc_r0, fc_w) : 0.0;
+      double2 v1, v2, v3;
+      v1.x = rp ? spitzer(0.5 * (Tc.x + Tn.x), kappa0, T_cut) * fcf : 0.0;
+      v1.y = rp ? spitzer(0.5 * (Tc.y + Tn.y), kappa0, T_cut) * fcf : 0.0;
+      if (jp) {
+        const double2 Tt = ld2(e + G.n3);
+        v2.x = spitzer(0.5 * (Tc.x + Tt.x), kappa0, T_cut) * fcc;
+        v2.y = spitzer(0.5 * (Tc.y + Tt.y), kappa0, T_cut) * fcc;
+      } else {
+        v2 = make_double2(0.0, 0.0);
+      }
+      v3.x = spitzer(0.5 * (Tc.x + Tc.y), kappa0, T_cut) * fcc;
+      v3.y = kp ? spitzer(0.5 * (Tc.y + Tk), kappa0, T_cut) * fcc : 0.0;
+      __stcs(reinterpret_cast<double2*>(k1 + e), v1);
+      __stcs(reinterpret_cast<double2*>(k2 + e), v2);
+      __stcs(reinterpret_cast<double2*>(k3 + e), v3);
+    }
+    Tc = Tn;
+    Tn = Tnn;
+  }
+}
+
 // Face coefficients of the isotropic operator with the metrics folded in, for the
 // merged PCG pass (once per solve): K1 = k1 F1r F1t F1p (r face i+1/2), K2 = k2 F2r
 // F2t F2p (theta face j+1/2), K3 = k3 F2r F3t F3p (phi face k+1/2, periodic wrap),
@@ -103,15 +160,25 @@ void launch_face_kappa(const Geo& G, FieldV T, double* k1, double* k2, double* k
                        cudaStream_t st) {
   if ((long long)G.nl * G.plane == 0) return;
   STS_REQUIRE(G.n2 <= 65535, "grid too large for the face-kappa pass");
-  const int nbx = (G.n3 + FK_T - 1) / FK_T;
+  auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = G.n3 % 2 == 0 && a16(T.p) && a16(T.hi) && a16(k1) && a16(k2) && a16(k3);
+  const int tpb = vec ? FK2_T : FK_T;
+  const int nbx = (vec ? G.n3 / 2 + FK2_T - 1 : G.n3 + FK_T - 1) / tpb;
   // ~8 resident blocks per SM x 148 SMs x 4 waves of columns, chunks of >= 8 planes
+  // (the vectorised pass: 16 blocks of 128 threads per SM, chunks of >= 16 planes)
   const long long cols = (long long)nbx * G.n2;
-  int nch = (int)std::max(1LL, std::min<long long>((148LL * 8 * 4 + cols - 1) / cols, (G.nl + 7) / 8));
+  const long long want = vec ? 148LL * 16 * 4 : 148LL * 8 * 4;
+  const int minc = vec ? 16 : 8;
+  int nch = (int)std::max(1LL, std::min<long long>((want + cols - 1) / cols, (G.nl + minc - 1) / minc));
   nch = std::min(nch, 65535);
   const int ic = (G.nl + nch - 1) / nch;
   nch = (G.nl + ic - 1) / ic;
-  face_kappa_kernel<<<dim3(nbx, G.n2, nch), FK_T, 0, st>>>(G, T, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, x1f_d,
-                                                           x1c_d, ic);
+  if (vec)
+    face_kappa2_kernel<<<dim3(nbx, G.n2, nch), FK2_T, 0, st>>>(G, T, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, x1f_d,
+                                                               x1c_d, ic);
+  else
+    face_kappa_kernel<<<dim3(nbx, G.n2, nch), FK_T, 0, st>>>(G, T, k1, k2, k3, kappa0, T_cut, fc_r0, fc_w, x1f_d,
+                                                             x1c_d, ic);
   STS_CUDA(cudaGetLastError());
 }
 

@@ -106,6 +106,9 @@ struct TmaArgs {
 #ifndef ANISO_RASTER_H   // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ANISO_RASTER_H 0
 #endif
+#ifndef ANISO_PF         // L2 prefetch distance of the producer in planes (0: none)
+#define ANISO_PF 0
+#endif
 #ifndef ANISO_NS         // ring slots of the other passes
 #define ANISO_NS 4
 #endif
@@ -244,6 +247,19 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
         for (int q = 0; q < Lay::nown; ++q)
           if (!(kM && q == OW_X)) tma3(S + Lay::O + q * O_PART, &ta.own[q], oe, j0, p - 1, bar);
       if (x_here) tma3(S + Lay::O + OW_X * O_PART, &ta.own[OW_X], oe, j0, p, bar);
+      if constexpr (ANISO_PF > 0) {
+        // L2 prefetch of package Q(p + PF) (main-array planes only; the wrap columns and
+        // halo planes are small and left to the loads)
+        const int pf = p + ANISO_PF;
+        if (pf <= ie && pf < G.nl) {
+          for (int f = 0; f < nsrc_now; ++f) tma3_prefetch(&ta.src[f], ou, j0 - 1, pf);
+          for (int a = 0; a < 3; ++a) tma3_prefetch(&ta.e, oe, j0, a * (G.nl + 1) + pf);
+#pragma unroll
+          for (int q = 0; q < Lay::nown; ++q)
+            if (!(kM && q == OW_X)) tma3_prefetch(&ta.own[q], oe, j0, pf - 1);
+          if (kM && !no_x && pf < ie) tma3_prefetch(&ta.own[OW_X], oe, j0, pf);
+        }
+      }
     }
     return;
   }

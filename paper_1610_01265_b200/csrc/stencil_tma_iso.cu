@@ -74,6 +74,9 @@ struct IsoTile {
 #ifndef ISO_RASTER_H     // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ISO_RASTER_H 0
 #endif
+#ifndef ISO_PF           // L2 prefetch distance of the producer in planes (0: none)
+#define ISO_PF 0
+#endif
 #ifndef ISO_D3_ROWS      // rows of the 3-component RKL2 deviation stage (> 7: one CTA per SM)
 #define ISO_D3_ROWS 7
 #endif
@@ -306,6 +309,24 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 #pragma unroll
         for (int q = 0; q < Lay::nepi; ++q)
           if (!(kM && no_x[q % NC])) tma3(S + Lay::EP + q * OWN, &ta.epi[q / NC], k0, j0, (q % NC) * cpl + p, bar);
+        if constexpr (ISO_PF > 0) {
+          // L2 prefetch of the package of plane p + PF (main boxes; wrap boxes left to the loads)
+          const int pf = p + ISO_PF;
+          if (pf < ie) {
+#pragma unroll
+            for (int f = 0; f < nsrcf_now; ++f)
+#pragma unroll
+              for (int q = 0; q < NC; ++q) tma3_prefetch(&ta.src[f], k0 - 2, j0 - 1, q * cpl + pf);
+            if (Lay::nd) tma3_prefetch(&ta.dm, k0 - 2, j0 - 1, pf);
+            tma3_prefetch(&ta.k2, k0, j0 - 1, pf);
+            tma3_prefetch(&ta.k3, k0 - 2, j0, pf);
+            tma3_prefetch(&ta.k1, k0, j0, pf);
+            if (ta.has_w) tma3_prefetch(&ta.w, k0, j0, pf);
+#pragma unroll
+            for (int q = 0; q < Lay::nepi; ++q)
+              if (!(kM && no_x[q % NC])) tma3_prefetch(&ta.epi[q / NC], k0, j0, (q % NC) * cpl + pf);
+          }
+        }
       }
       __syncwarp();
     }

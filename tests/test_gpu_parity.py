@@ -82,12 +82,19 @@ def _inputs(g, rng, bkind):
 
 
 # ---------------------------------------------------------------- A3
+# (shape, periodic, virtual slabs): even n3 takes the two-column vectorised pass (phi
+# wrap, walls, n3 = 2, slab halos), odd n3 the one-column pass
+FK_CASES = [((20, 19, 70), True, 1), ((7, 5, 33), True, 1), ((6, 4, 2), True, 1), ((9, 8, 64), False, 1),
+            ((13, 6, 66), True, 3), ((10, 3, 9), False, 2), ((300, 2, 4), True, 1)]
+
+
 @pytest.mark.parametrize("recipe", ["corona", "tr", "tr_fc"])
-def test_face_kappa_parity(dev, recipe):
-    g = sph((20, 19, 70))
+@pytest.mark.parametrize("shape,periodic,nv", FK_CASES)
+def test_face_kappa_parity(dev, recipe, shape, periodic, nv):
+    g = sph(shape, periodic=periodic)
     T = W.corona_T(g, seed=3) if recipe == "corona" else W.tr_corona_T(g, seed=3)
     fc_w = 0.5 if recipe == "tr_fc" else 0.0
-    G = sts().Grid.from_grid(g)
+    G = sts().Grid.from_grid(g, n_virtual=nv)
     k = G.face_kappa_spitzer(T.to(dev), 1e-9, 5e5, 10.0, fc_w)
     ref = O.spitzer_face_kappa(g, T.numpy(), 1e-9, 5e5, 10.0, fc_w)
     for d in range(3):

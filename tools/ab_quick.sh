@@ -14,13 +14,13 @@ done
 names="prod $(for pair in $VARIANTS; do echo ${pair%%:*}; done)"
 for v in $names; do
   if [ $v = prod ]; then unset STS_LIB; else export STS_LIB=$PWD/paper_1610_01265_b200/libsts_b200_$v.so; fi
-  timeout 400 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "${TESTK:-tma_kernels_match or spitzer or be_pcg or op_apply or virtual or dt_euler}" > gpurun_out/abt_$v.log 2>&1
+  timeout 400 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "${TESTK:-tma_kernels_match or spitzer or be_pcg or op_apply or virtual or dt_euler or face_kappa or iso}" > gpurun_out/abt_$v.log 2>&1
   echo "$v tests: $(tail -1 gpurun_out/abt_$v.log)"
 done
 for cfg in ${CFGS:-c3_spitzer256}; do
   for v in $names; do
     if [ $v = prod ]; then unset STS_LIB; else export STS_LIB=$PWD/paper_1610_01265_b200/libsts_b200_$v.so; fi
-    timeout 300 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ab_${cfg}_$v.log 2>&1
+    timeout 300 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --e2e-steps 0 --no-cpu-baseline ${BARGS:-} > gpurun_out/ab_${cfg}_$v.log 2>&1
   done
 done
 unset STS_LIB
