@@ -106,6 +106,12 @@ struct TmaArgs {
 #ifndef ANISO_RASTER_H   // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ANISO_RASTER_H 0
 #endif
+#ifndef ANISO_LEAN       // own-cell p_{k-1} loaded, z_k re-formed (instead of two more shuffles per row)
+#define ANISO_LEAN 1
+#endif
+#ifndef ANISO_REGS       // PCG scalars and 1/g3 in registers instead of shared-memory operands
+#define ANISO_REGS 1
+#endif
 #ifndef ANISO_PF         // L2 prefetch distance of the producer in planes (0: none)
 #define ANISO_PF 0
 #endif
@@ -270,11 +276,26 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   const int vj = tid >> 5, vk = tid & 31;
   const int vr0 = vj * RB;
   // references into shared memory (read where used; they hold no registers)
+#if ANISO_REGS
+  // (ANISO_REGS: the warp-uniform scalars and the 1/g3 of the thread's RB+1 rows in
+  // registers -- shared-memory operands are re-read after every barrier's memory clobber)
+  const double beta = sbx[0], ax = sbx[1], bprev = sbx[4];
+  double rg3[RB + 1];
+#pragma unroll
+  for (int r = 0; r <= RB; ++r) rg3[r] = sg3[vr0 + r];
+#define G3(r) rg3[r]
+#else
   const double& beta = sbx[0];
   const double& ax = sbx[1];
+  const double& bprev = sbx[4];
+#define G3(r) sg3[vr0 + (r)]
+#endif
   const int k = k0 + vk;
   const bool colok = vk < XOK && k < G.n3;
-  auto own_t = [&](int t) { return colok && vr0 + t < XOJ && j0 + vr0 + t < G.n2; };
+  bool ownr[RB];   // (evaluated once: the march tests it per row and plane)
+#pragma unroll
+  for (int t = 0; t < RB; ++t) ownr[t] = colok && vr0 + t < XOJ && j0 + vr0 + t < G.n2;
+  auto own_t = [&](int t) { return ownr[t]; };
   const long long coff0 = (long long)(j0 + vr0) * G.n3 + k;   // own cell of row t: coff0 + t n3
   double vtpc[RB];
 #pragma unroll
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   constexpr bool kP = (EPI == EPI_PCG_S);
   constexpr int PF = kM ? 2 * U_FIELD : U_FIELD;    // pold field offset
   auto zof = [&](const double* S, int o) {
-    if (kM && !first) return fma(-ax, S[U_FIELD + o], fma(-sbx[4], S[o], S[PF + o]));
+    if (kM && !first) return fma(-ax, S[U_FIELD + o], fma(-bprev, S[o], S[PF + o]));
     return S[o];
   };
   // state of one cell plane carried to the next, per vertex row t: the 2x2 sums of the
@@ -324,6 +345,16 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
       }
       zl[r] = z;
       zr[r] = __shfl_down_sync(0xffffffffu, z, 1);
+      if constexpr (ANISO_LEAN) {
+        // the own cells' p_{k-1} (rows 1..RB, col vk+1) straight from the slot, and their
+        // z_k re-formed below as p_k - beta p_{k-1}: one shuffled field instead of three
+        (void)zk;
+        qr[r] = ((kP || kM) && !first && r > 0) ? S[PF + ob + r * sb] : 0.0;
+        kr[r] = 0.0;
+        if (vk == XK - 1) zr[r] = zof(S, ob + r * sb);
+        if (vk == XK - 1 && (kP || kM) && !first) zr[r] = fma(beta, qr[r] = S[PF + ob + r * sb], zr[r]);
+        continue;
+      }
       qr[r] = ((kP || kM) && !first) ? __shfl_down_sync(0xffffffffu, q, 1) : 0.0;
       kr[r] = kM ? __shfl_down_sync(0xffffffffu, zk, 1) : 0.0;
       if (vk == XK - 1) {
@@ -340,10 +371,11 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
     for (int t = 0; t < RB; ++t) {
       H.Su[t] = (zl[t] + zr[t]) + (zl[t + 1] + zr[t + 1]);
       H.Tu[t] = (zl[t + 1] - zl[t]) + (zr[t + 1] - zr[t]);
-      H.Fu[t] = sg3[vr0 + t] * (zr[t] - zl[t]) + sg3[vr0 + t + 1] * (zr[t + 1] - zl[t + 1]);
+      H.Fu[t] = G3(t) * (zr[t] - zl[t]) + G3(t + 1) * (zr[t + 1] - zl[t + 1]);
       H.u[t] = zr[t + 1];    // own cell of this plane
       H.po[t] = qr[t + 1];   // its pold (PCG)
-      H.z[t] = kr[t + 1];    // its z (merged PCG)
+      H.z[t] = ANISO_LEAN ? (kM && !first ? fma(-beta, qr[t + 1], zr[t + 1]) : zr[t + 1])
+                          : kr[t + 1];    // its z (merged PCG)
     }
   };
 
@@ -397,7 +429,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
             // this vertex plane is above cell plane p-1 (sr = -1, ig2l) and below plane p (sr = +1, ig2h);
             // the own cell (j, k) sits at (st, sp) = (+,+) in vertex (vr,vk), (+,-) in (vr,vk+1),
             // (-,+) in (vr+1,vk), (-,-) in (vr+1,vk+1)
-            const double ig3c = sg3[vr0 + t + 1];
+            const double ig3c = G3(t + 1);
             const int e4[4] = {ei, ei + 1, ei + EBW, ei + EBW + 1};
             const double st4[4] = {1.0, 1.0, -1.0, -1.0}, sp4[4] = {1.0, -1.0, 1.0, -1.0};
 #pragma unroll
@@ -440,7 +472,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
 #pragma unroll
         for (int t = 0; t < RB; ++t) {
           if (!own_t(t)) continue;
-          const double ig3c = sg3[vr0 + t + 1];
+          const double ig3c = G3(t + 1);
           const double* O = S + Lay::O + (vr0 + t) * XK + vk + se;
           const double Lu = -((L.SA[t] - H.SA[t]) + ig2c * (L.DB[t] + H.DB[t]) + ig2c * ig3c * (L.DC[t] + H.DC[t]));
           const double WV = (W ? O[Lay::nepi * O_PART] : 1.0) * S[Lay::MT + 2] * vtpc[t];
@@ -558,6 +590,8 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   }
 }
 
+
+#undef G3
 
 // ============================================================================
 // host side

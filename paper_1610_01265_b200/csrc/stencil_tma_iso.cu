@@ -74,6 +74,9 @@ struct IsoTile {
 #ifndef ISO_RASTER_H     // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ISO_RASTER_H 0
 #endif
+#ifndef ISO_FORM_UNROLL  // the former warps' loop fully unrolled (measured neutral: off)
+#define ISO_FORM_UNROLL 0
+#endif
 #ifndef ISO_PF           // L2 prefetch distance of the producer in planes (0: none)
 #define ISO_PF 0
 #endif
@@ -226,9 +229,22 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           const double z = fma(-sax[q], S[o + Lay::FS], fma(-sbp[q], S[o], S[o + 2 * Lay::FS]));
           S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
         };
+        // (compile-time trip counts, fully unrolled: a component's positions are
+        // independent, so their shared loads are all in flight at once -- the formers
+        // sit on the consumers' critical path)
+        constexpr int NF = 32 * (Lay::NFORM > 0 ? Lay::NFORM : 1);
+        constexpr int NI = (SBW * SBH + NF - 1) / NF;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-          for (int o = fl; o < SBW * SBH; o += fn) form(q * S_MAIN + o, q);
+          if constexpr (ISO_FORM_UNROLL) {
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+              const int o = fl + i * NF;
+              if (o < SBW * SBH) form(q * S_MAIN + o, q);
+            }
+          } else {
+            for (int o = fl; o < SBW * SBH; o += fn) form(q * S_MAIN + o, q);
+          }
           if (wrapL || wrapR)
             for (int o = fl; o < 2 * S_W; o += fn) form(Lay::WRP + q * 2 * S_W + o, q);
         }
@@ -578,7 +594,24 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     auto mbody = [&](int il, const St& P, St& C) {
       const int slot = (il - ib) % NS;
       const double* S = ring + slot * Lay::SLOT;
-      mbar_wait((Lay::FORM ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
+      mbar_wait((Lay::FORM && Lay::NFORM > 0 ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
+      if constexpr (kF && Lay::NFORM == 0) {
+        // consumer forming (ISO_FORMERS = 0): the consumer warps form the landed slot's
+        // p_k at every staged position themselves (the former warps' arithmetic, spread
+        // over all consumer threads), then meet at one consumer-only named barrier
+        double* SF = ring + slot * Lay::SLOT;
+        auto form = [&](int o, int q) {
+          const double z = fma(-sax[q], SF[o + Lay::FS], fma(-sbp[q], SF[o], SF[o + 2 * Lay::FS]));
+          SF[o + Lay::FS] = fma(sbeta[q], SF[o + 2 * Lay::FS], z);
+        };
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          for (int o = tid; o < SBW * SBH; o += INT) form(q * S_MAIN + o, q);
+          if (wrapL || wrapR)
+            for (int o = tid; o < 2 * S_W; o += INT) form(Lay::WRP + q * 2 * S_W + o, q);
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"r"(INT) : "memory");
+      }
       C.K = 0.0;
       if (own) {
         // metric-folded coefficients (launch_iso_premul: zero on wall faces)
