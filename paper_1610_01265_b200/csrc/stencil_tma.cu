@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
 #if ANISO_REGS
   // (ANISO_REGS: the warp-uniform scalars and the 1/g3 of the thread's RB+1 rows in
   // registers -- shared-memory operands are re-read after every barrier's memory clobber)
-  const double beta = sbx[0], ax = sbx[1], bprev = sbx[4];
+  const double beta = sbx[0], ax = sbx[1], bprev = sbx[4], cxp = sbx[2], cxz = sbx[3];
   double rg3[RB + 1];
 #pragma unroll
   for (int r = 0; r <= RB; ++r) rg3[r] = sg3[vr0 + r];
@@ -288,6 +288,8 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   const double& beta = sbx[0];
   const double& ax = sbx[1];
   const double& bprev = sbx[4];
+  const double& cxp = sbx[2];
+  const double& cxz = sbx[3];
 #define G3(r) sg3[vr0 + (r)]
 #endif
   const int k = k0 + vk;
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
   for (int t = 0; t < RB; ++t) ownr[t] = colok && vr0 + t < XOJ && j0 + vr0 + t < G.n2;
   auto own_t = [&](int t) { return ownr[t]; };
   const long long coff0 = (long long)(j0 + vr0) * G.n3 + k;   // own cell of row t: coff0 + t n3
+  double* const xown = kM ? c.ea.x + coff0 : nullptr;          // (merged PCG: x of the own cells)
   double vtpc[RB];
 #pragma unroll
   for (int t = 0; t < RB; ++t) vtpc[t] = own_t(t) ? M.Vt[j0 + vr0 + t] * M.Vp[k] : 0.0;
@@ -403,9 +406,9 @@ __global__ void __launch_bounds__(XTHREADS, TmaLay<EPI, W>::MINB) aniso_tma_kern
         for (int t = 0; t < RB; ++t) {
           if (!own_t(t)) continue;
           const double* Ox = S + Lay::O + OW_X * O_PART + (vr0 + t) * XK + vk + se;
-          double xn = fma(xm == X_CATCHUP ? sbx[2] : ax, H.po[t], *Ox);
-          if (xm == X_CATCHUP) xn = fma(sbx[3], S[ob + (t + 1) * sb], xn);   // + alpha_{k-2} p_{k-2} (field 0)
-          __stcs(c.ea.x + (long long)p * G.plane + coff0 + (long long)t * G.n3, xn);
+          double xn = fma(xm == X_CATCHUP ? cxp : ax, H.po[t], *Ox);
+          if (xm == X_CATCHUP) xn = fma(cxz, S[ob + (t + 1) * sb], xn);   // + alpha_{k-2} p_{k-2} (field 0)
+          __stcs(xown + (long long)p * G.plane + t * G.n3, xn);
         }
       }
     }

@@ -74,6 +74,9 @@ struct IsoTile {
 #ifndef ISO_RASTER_H     // (theta-first bands measured worse for L2: DESIGN.md §5.4)
 #define ISO_RASTER_H 0
 #endif
+#ifndef ISO_FORM_SPLIT   // one formed barrier per component (consumers start on component 0 earlier; measured neutral: off)
+#define ISO_FORM_SPLIT 0
+#endif
 #ifndef ISO_FORM_UNROLL  // the former warps' loop fully unrolled (measured neutral: off)
 #define ISO_FORM_UNROLL 0
 #endif
@@ -134,7 +137,7 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   static constexpr int NS2 = (113 * 1024 - FIX) / (SLOT * 8 + 16);   // two CTAs per SM
   static constexpr int NS = (MINB == 2) ? (NS2 > 4 ? 4 : (NS2 < 2 ? 2 : NS2)) : (NS1 > 6 ? 6 : NS1);
   static constexpr size_t SMEM =
-      (size_t)NS * SLOT * sizeof(double) + 3 * NS * sizeof(uint64_t) + 128;
+      (size_t)NS * SLOT * sizeof(double) + (2 + NC) * NS * sizeof(uint64_t) + 128;
   static_assert(SMEM <= (MINB == 2 ? 113 * 1024 : SMEM_1CTA), "iso TMA slot ring does not fit");
 };
 
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   double* ring = smi;
   uint64_t* full = reinterpret_cast<uint64_t*>(smi + NS * Lay::SLOT);
   uint64_t* empty = full + NS;
-  uint64_t* formed = empty + NS;     // (merged PCG with former warps)
+  uint64_t* formed = empty + NS;     // [NS][NC] (merged PCG with former warps; ISO_FORM_SPLIT: one per component)
   const Geo& G = c.geo;
   const Metrics& M = G.m;
   const int tid = threadIdx.x;
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, IJ);
-      mbar_init(formed + s, Lay::NFORM > 0 ? Lay::NFORM : 1);
+      for (int q = 0; q < NC; ++q) mbar_init(formed + s * NC + q, Lay::NFORM > 0 ? Lay::NFORM : 1);
     }
     mbar_fence_init();
   }
@@ -220,23 +223,21 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     for (int p = ib; p < ie; ++p) {
       const int slot = (p - ib) % NS;
       mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
-      if constexpr (kF) {
-        double* S = ring + slot * Lay::SLOT;
-        // fields p_{k-2}, w_{k-1}, p_{k-1}: z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1},
-        // p_k = z_k + beta_k p_{k-1} over w_{k-1}; p_{k-2} stays (the x catch-up reads it), the
-        // own cell's z_k = p_k - beta_k p_{k-1} is re-formed by its consumer
-        auto form = [&](int o, int q) {
-          const double z = fma(-sax[q], S[o + Lay::FS], fma(-sbp[q], S[o], S[o + 2 * Lay::FS]));
-          S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
-        };
-        // (compile-time trip counts, fully unrolled: a component's positions are
-        // independent, so their shared loads are all in flight at once -- the formers
-        // sit on the consumers' critical path)
-        constexpr int NF = 32 * (Lay::NFORM > 0 ? Lay::NFORM : 1);
-        constexpr int NI = (SBW * SBH + NF - 1) / NF;
+      double* S = ring + slot * Lay::SLOT;
+      // fields p_{k-2}, w_{k-1}, p_{k-1}: z_k = (p_{k-1} - beta_{k-1} p_{k-2}) - alpha_{k-1} w_{k-1},
+      // p_k = z_k + beta_k p_{k-1} over w_{k-1}; p_{k-2} stays (the x catch-up reads it), the
+      // own cell's z_k = p_k - beta_k p_{k-1} is re-formed by its consumer
+      auto form = [&](int o, int q) {
+        const double z = fma(-sax[q], S[o + Lay::FS], fma(-sbp[q], S[o], S[o + 2 * Lay::FS]));
+        S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
+      };
+      // (ISO_FORM_UNROLL: compile-time trip counts, fully unrolled)
+      constexpr int NF = 32 * (Lay::NFORM > 0 ? Lay::NFORM : 1);
 #pragma unroll
-        for (int q = 0; q < NC; ++q) {
+      for (int q = 0; q < NC; ++q) {
+        if constexpr (kF) {
           if constexpr (ISO_FORM_UNROLL) {
+            constexpr int NI = (SBW * SBH + NF - 1) / NF;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
               const int o = fl + i * NF;
@@ -248,9 +249,13 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
           if (wrapL || wrapR)
             for (int o = fl; o < 2 * S_W; o += fn) form(Lay::WRP + q * 2 * S_W + o, q);
         }
+        // release the formed component to the consumers (ISO_FORM_SPLIT: component by
+        // component, so the consumers start on component 0 while 1 and 2 are formed)
+        if (ISO_FORM_SPLIT || q == NC - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(formed + slot * NC + (ISO_FORM_SPLIT ? q : 0));
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(formed + slot);   // release: the formed fields to the consumers
     }
     return;
   }
@@ -594,7 +599,9 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
     auto mbody = [&](int il, const St& P, St& C) {
       const int slot = (il - ib) % NS;
       const double* S = ring + slot * Lay::SLOT;
-      mbar_wait((Lay::FORM && Lay::NFORM > 0 ? formed : full) + slot, (uint32_t)(((il - ib) / NS) & 1));
+      const uint32_t par = (uint32_t)(((il - ib) / NS) & 1);
+      constexpr bool kFW = Lay::FORM && Lay::NFORM > 0;   // consumers wait for the former warps
+      mbar_wait(kFW ? formed + slot * NC : full + slot, par);
       if constexpr (kF && Lay::NFORM == 0) {
         // consumer forming (ISO_FORMERS = 0): the consumer warps form the landed slot's
         // p_k at every staged position themselves (the former warps' arithmetic, spread
@@ -630,6 +637,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         const long long gi = (long long)il * pl + coff;
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
+          if (kFW && ISO_FORM_SPLIT && q > 0) mbar_wait(formed + slot * NC + q, par);
           const int oq = q * S_MAIN + oc;
           // (formed slot: field 1 holds p_k, field 0 the raw z_{k-1}: z_k = p_k - beta p_{k-1})
           const double zk = kF ? fma(-sbeta[q], S[oq + 2 * Lay::FS], S[oq + Lay::FS]) : zm(S, oq, q);

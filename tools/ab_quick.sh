@@ -20,7 +20,7 @@ done
 for cfg in ${CFGS:-c3_spitzer256}; do
   for v in $names; do
     if [ $v = prod ]; then unset STS_LIB; else export STS_LIB=$PWD/paper_1610_01265_b200/libsts_b200_$v.so; fi
-    timeout 300 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --e2e-steps 0 --no-cpu-baseline ${BARGS:-} > gpurun_out/ab_${cfg}_$v.log 2>&1
+    timeout 300 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --e2e-steps 0 --no-cpu-baseline ${BARGS:-} > gpurun_out/ab_${cfg}_$v${SUF:-}.log 2>&1
   done
 done
 unset STS_LIB
