@@ -45,6 +45,14 @@ KMAX = 50000
 CPU_BOX = (12, 40, 64)
 
 
+# classes whose HBM fraction is not their bound (DESIGN.md §5.3 / §5.4)
+KERNEL_NOTES = {
+    "aniso_gersh": "bound by its FP64 / shared-memory work (~115 FP64 instructions per cell for the 27 "
+                   "|L_ij| of a row), not by HBM; once per step",
+    "pcg_reduce": "one 1024-thread block per PCG iteration: launch-latency bound, no HBM traffic",
+}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -516,6 +524,8 @@ def measure_device(G, inp, ratio, args, ws, dev, ncells_local, ncells_total):
         if k in Bytes and kms > 0:
             ent["achieved_gbs"] = round(Bytes[k] / (kms * 1e-3) / 1e9, 1)
             ent["frac"] = round(ent["achieved_gbs"] / peak, 4)
+        if k in KERNEL_NOTES:
+            ent["note"] = KERNEL_NOTES[k]
         kernels[k] = ent
     dom = max((k for k in kernels if "achieved_gbs" in kernels[k]), key=lambda k: kernels[k]["ms"])
     traffic = None
