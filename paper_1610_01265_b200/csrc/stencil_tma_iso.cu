@@ -80,6 +80,9 @@ struct IsoTile {
 #ifndef ISO_FORM_UNROLL  // the former warps' loop fully unrolled (measured neutral: off)
 #define ISO_FORM_UNROLL 0
 #endif
+#ifndef ISO_FORM_TRIM    // the former warps form only the staged positions the stencil reads (1: one position
+#define ISO_FORM_TRIM 0      // per form; 2: 16-byte aligned pairs); measured slower: off
+#endif
 #ifndef ISO_PF           // L2 prefetch distance of the producer in planes (0: none)
 #define ISO_PF 0
 #endif
@@ -220,6 +223,35 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
   if (Lay::FORM && tid >= INT + 32) {
     const int lane = tid & 31;
     const int fl = tid - (INT + 32), fn = 32 * Lay::NFORM;   // this thread among the former warps
+    constexpr int NF = 32 * (Lay::NFORM > 0 ? Lay::NFORM : 1);
+    // ISO_FORM_TRIM: only the staged positions the 7-point stencil reads are formed -- the
+    // own rows 1..IJ at box columns 1..IK+2 (own cells and both phi neighbours) and the two
+    // theta-halo rows at the own columns 2..IK+1 -- not the box corners or the alignment
+    // columns 0 and IK+3 (2 IK + IJ (IK + 2) = 506 of 540 positions at 13 rows: 8 instead
+    // of 9 forms per former thread and component); this thread's offsets, fixed per launch
+    // ISO_FORM_TRIM 2: the same set in 16-byte aligned pairs (double2 shared loads / store):
+    // the halo rows' own columns as IK/2 pairs, the own rows as SBW/2 pairs (their alignment
+    // columns 0 and IK+3 come along), 2 (IK/2) + IJ (SBW/2) = 266 pairs at 13 rows: 5 forms
+    // of two positions per former thread and component
+    constexpr int PW = (ISO_FORM_TRIM == 2) ? 2 : 1;               // positions per form
+    constexpr int HW = IK / PW, OW = (ISO_FORM_TRIM == 2) ? SBW / 2 : IK + 2;
+    constexpr int NEED = 2 * HW + IJ * OW;
+    constexpr int NT = (NEED + NF - 1) / NF;
+    int toff[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const int t = fl + i * NF;
+      int o = -1;
+      if (t < HW) {
+        o = 2 + PW * t;                                              // theta-halo row 0
+      } else if (t < HW + IJ * OW) {
+        const int u = t - HW;
+        o = (1 + u / OW) * SBW + (PW == 2 ? 0 : 1) + PW * (u % OW);  // own rows
+      } else if (t < NEED) {
+        o = (IJ + 1) * SBW + 2 + PW * (t - HW - IJ * OW);            // theta-halo row IJ+1
+      }
+      toff[i] = o;
+    }
     for (int p = ib; p < ie; ++p) {
       const int slot = (p - ib) % NS;
       mbar_wait(full + slot, (uint32_t)(((p - ib) / NS) & 1));
@@ -232,11 +264,28 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
         S[o + Lay::FS] = fma(sbeta[q], S[o + 2 * Lay::FS], z);
       };
       // (ISO_FORM_UNROLL: compile-time trip counts, fully unrolled)
-      constexpr int NF = 32 * (Lay::NFORM > 0 ? Lay::NFORM : 1);
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
         if constexpr (kF) {
-          if constexpr (ISO_FORM_UNROLL) {
+          if constexpr (ISO_FORM_TRIM == 2) {
+            // (S_MAIN, FS and the row pitch SBW are even: an even offset is 16-byte aligned)
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+              if (toff[i] >= 0) {
+                const int o = q * S_MAIN + toff[i];
+                const double2 pm2 = *reinterpret_cast<const double2*>(S + o);
+                const double2 wm1 = *reinterpret_cast<const double2*>(S + o + Lay::FS);
+                const double2 pm1 = *reinterpret_cast<const double2*>(S + o + 2 * Lay::FS);
+                const double z0 = fma(-sax[q], wm1.x, fma(-sbp[q], pm2.x, pm1.x));
+                const double z1 = fma(-sax[q], wm1.y, fma(-sbp[q], pm2.y, pm1.y));
+                *reinterpret_cast<double2*>(S + o + Lay::FS) =
+                    make_double2(fma(sbeta[q], pm1.x, z0), fma(sbeta[q], pm1.y, z1));
+              }
+          } else if constexpr (ISO_FORM_TRIM) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+              if (toff[i] >= 0) form(q * S_MAIN + toff[i], q);
+          } else if constexpr (ISO_FORM_UNROLL) {
             constexpr int NI = (SBW * SBH + NF - 1) / NF;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
