@@ -83,6 +83,9 @@ struct IsoTile {
 #ifndef ISO_FORM_TRIM    // the former warps form only the staged positions the stencil reads (1: one position
 #define ISO_FORM_TRIM 0      // per form; 2: 16-byte aligned pairs); measured slower: off
 #endif
+#ifndef ISO_M_XG         // merged 3-component PCG: x read per thread from global (issued before the slot
+#define ISO_M_XG 0       // wait) instead of staged, so the slot is 1/7 smaller (at 12 rows a 4th slot fits)
+#endif
 #ifndef ISO_PF           // L2 prefetch distance of the producer in planes (0: none)
 #define ISO_PF 0
 #endif
@@ -117,7 +120,8 @@ struct IsoLay : IsoTile<iso_rows(EPI, NC)> {
   // the staged face coefficients: A_ii = wV - dt L_ii, d = 1 / A_ii as in the R0 pass)
   static constexpr int nepi =
       (EPI == EPI_RKL2_STAGE) ? 3 * NC
-                              : (EPI == EPI_RKL2_DSTAGE ? 2 * NC : ((EPI == EPI_PCG_S || EPI == EPI_PCG_M) ? NC : 0));
+                              : (EPI == EPI_RKL2_DSTAGE ? 2 * NC
+                                                        : (EPI == EPI_PCG_S ? NC : (EPI == EPI_PCG_M ? (ISO_M_XG && NC == 3 ? 0 : NC) : 0)));
   // one block per staged field: NC main boxes, then the NC x 2 wrap boxes, so a
   // field's cell at any (main or wrap) offset o has its other-field twin at o + FS
   static constexpr int WRP = NC * T::S_MAIN;                          // wrap boxes within a field block
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
 #pragma unroll
     for (int q = 0; q < NC; ++q) no_x[q] = kM && (!kP || sxm[q] == X_SKIP);
     bytes += Lay::nepi * OWN * 8;
-    if constexpr (kM)
+    if constexpr (kM && Lay::nepi > 0)
 #pragma unroll
       for (int q = 0; q < NC; ++q)
         if (no_x[q]) bytes -= OWN * 8;
@@ -650,6 +654,15 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
       const double* S = ring + slot * Lay::SLOT;
       const uint32_t par = (uint32_t)(((il - ib) / NS) & 1);
       constexpr bool kFW = Lay::FORM && Lay::NFORM > 0;   // consumers wait for the former warps
+      // (ISO_M_XG: this plane's x of the own cell loaded before the wait, which hides its latency)
+      constexpr bool kXG = kP && Lay::nepi == 0;
+      double xg[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        xg[q] = 0.0;
+        if constexpr (kXG)
+          if (own && !skip[q] && sxm[q] != X_SKIP) xg[q] = __ldcs(ox + (long long)il * pl + coff + q * cs);
+      }
       mbar_wait(kFW ? formed + slot * NC : full + slot, par);
       if constexpr (kF && Lay::NFORM == 0) {
         // consumer forming (ISO_FORMERS = 0): the consumer warps form the landed slot's
@@ -704,7 +717,7 @@ __global__ void __launch_bounds__(IsoLay<EPI, NC>::THREADS, IsoLay<EPI, NC>::MIN
               // catch-up x_k = x_{k-2} + alpha_{k-1} p_{k-1} + alpha_{k-2} p_{k-2} (both staged)
               const int m = sxm[q];
               if (m != X_SKIP) {
-                double xn = fma(m == X_CATCHUP ? scxp[q] : sax[q], S[oq + 2 * Lay::FS], S[Lay::EP + q * OWN + o8]);
+                double xn = fma(m == X_CATCHUP ? scxp[q] : sax[q], S[oq + 2 * Lay::FS], kXG ? xg[q] : S[Lay::EP + q * OWN + o8]);
                 if (m == X_CATCHUP) xn = fma(scxz[q], S[oq], xn);   // + alpha_{k-2} p_{k-2} (field 0)
                 __stcs(ox + go, xn);
               }
